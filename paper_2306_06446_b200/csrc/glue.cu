@@ -1,0 +1,182 @@
+// Glue kernels around the hot path: LayerNorm, softmax attention of the
+// exempt (MSA) stage, pooling, cls-token rows.
+#include "common.cuh"
+
+namespace sa {
+
+// LayerNorm over the last axis, biased variance, eps inside the sqrt
+// (ref tensor.py:114-128). One warp per row, d <= 512 held in registers.
+template <int PER>
+__global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict__ x,
+                                                       const float* __restrict__ gain,
+                                                       const float* __restrict__ bias,
+                                                       float* __restrict__ y, int64_t M, int d,
+                                                       float eps) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = int64_t(blockIdx.x) * 8 + warp;
+  if (row >= M) return;
+  const float* xr = x + row * d;
+  float v[PER];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int c = lane + 32 * i;
+    v[i] = c < d ? xr[c] : 0.f;
+    s += v[i];
+  }
+  const float mean = warp_sum(s) / float(d);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int c = lane + 32 * i;
+    v[i] = c < d ? v[i] - mean : 0.f;
+    q += v[i] * v[i];
+  }
+  const float var = warp_sum(q) / float(d);
+  const float inv = 1.0f / sqrtf(var + eps);
+  float* yr = y + row * d;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int c = lane + 32 * i;
+    if (c < d) yr[c] = v[i] * inv * gain[c] + bias[c];
+  }
+}
+
+// softmax attention per (image, head) (ref attention.py:92-97): K (padded) and
+// V of the head in shared memory, one warp per query row, lanes over keys for
+// the scores and over channels for P·V.
+__global__ void __launch_bounds__(256) softmax_attn_kernel(const float* __restrict__ q,
+                                                          const float* __restrict__ k,
+                                                          const float* __restrict__ v,
+                                                          float* __restrict__ out, int n, int d,
+                                                          int heads, int dk, float scale_div) {
+  extern __shared__ __align__(16) float sm[];
+  const int kp = dk + 1;
+  float* sk = sm;                         // [n][dk+1]
+  float* sv = sk + n * kp;                // [n][dk]
+  float* sq = sv + n * dk;                // [8][dk]
+  float* sp = sq + 8 * dk;                // [8][n]
+  const int bh = blockIdx.x, b = bh / heads, h = bh % heads;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t rowbase = size_t(b) * n;
+  for (int idx = threadIdx.x; idx < n * dk; idx += blockDim.x) {
+    const int j = idx / dk, c = idx % dk;
+    sk[j * kp + c] = k[(rowbase + j) * d + h * dk + c];
+    sv[j * dk + c] = v[(rowbase + j) * d + h * dk + c];
+  }
+  __syncthreads();
+  float* myq = sq + warp * dk;
+  float* myp = sp + warp * n;
+  for (int i = warp; i < n; i += 8) {
+    for (int c = lane; c < dk; c += 32) myq[c] = q[(rowbase + i) * d + h * dk + c];
+    __syncwarp();
+    float mx = -INFINITY;
+    for (int j = lane; j < n; j += 32) {
+      float s = 0.f;
+      for (int c = 0; c < dk; ++c) s = fmaf(myq[c], sk[j * kp + c], s);
+      s = s / scale_div;
+      myp[j] = s;
+      mx = fmaxf(mx, s);
+    }
+    mx = warp_max(mx);
+    float tot = 0.f;
+    for (int j = lane; j < n; j += 32) {
+      const float e = expf(myp[j] - mx);
+      myp[j] = e;
+      tot += e;
+    }
+    tot = warp_sum(tot);
+    __syncwarp();
+    for (int c = lane; c < dk; c += 32) {
+      float acc = 0.f;
+      for (int j = 0; j < n; ++j) acc = fmaf(myp[j] / tot, sv[j * dk + c], acc);
+      out[(rowbase + i) * d + h * dk + c] = acc;
+    }
+    __syncwarp();
+  }
+}
+
+// tokens.mean(axis=1) (ref model.py:574): numpy reduces a non-contiguous axis
+// sequentially in float32, so a sequential per-channel sum reproduces it.
+__global__ void pool_kernel(const float* __restrict__ x, float* __restrict__ y, int64_t B, int n,
+                            int d, int mode) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= B * d) return;
+  const int64_t b = i / d;
+  const int c = int(i % d);
+  const float* xb = x + b * n * d;
+  if (mode == 1) {
+    y[i] = xb[c];
+    return;
+  }
+  float s = 0.f;
+  for (int t = 0; t < n; ++t) s += xb[int64_t(t) * d + c];
+  y[i] = s / float(n);
+}
+
+__global__ void cls_rows_kernel(const float* __restrict__ cls, const float* __restrict__ pos,
+                                float* __restrict__ y, int64_t B, int64_t rows, int d) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= B * d) return;
+  const int64_t b = i / d;
+  const int c = int(i % d);
+  y[b * rows * d + c] = pos ? cls[c] + pos[c] : cls[c];
+}
+
+int write_cls_rows(const float* cls, const float* pos, float* y, int64_t B, int64_t rows,
+                   int64_t d, cudaStream_t s) {
+  cls_rows_kernel<<<unsigned(cdiv(B * d, 256)), 256, 0, s>>>(cls, pos, y, B, rows, int(d));
+  count_launch(1);
+  SA_LAUNCH_CHECK("cls_rows_kernel");
+  return SA_OK;
+}
+
+}  // namespace sa
+
+using namespace sa;
+
+extern "C" int sa_layernorm(const float* x, const float* gain, const float* bias, float* y,
+                            int64_t M, int64_t d, float eps, void* stream) {
+  SA_REQUIRE(M >= 0 && d > 0 && d <= 1024, SA_ERR_SHAPE, "sa_layernorm: d=%lld unsupported",
+             (long long)d);
+  if (M == 0) return SA_OK;
+  const unsigned grid = unsigned(cdiv(M, 8));
+  cudaStream_t s = as_stream(stream);
+  const int per = int(cdiv(d, 32));
+  if (per <= 1) layernorm_kernel<1><<<grid, 256, 0, s>>>(x, gain, bias, y, M, int(d), eps);
+  else if (per <= 2) layernorm_kernel<2><<<grid, 256, 0, s>>>(x, gain, bias, y, M, int(d), eps);
+  else if (per <= 4) layernorm_kernel<4><<<grid, 256, 0, s>>>(x, gain, bias, y, M, int(d), eps);
+  else if (per <= 8) layernorm_kernel<8><<<grid, 256, 0, s>>>(x, gain, bias, y, M, int(d), eps);
+  else if (per <= 16) layernorm_kernel<16><<<grid, 256, 0, s>>>(x, gain, bias, y, M, int(d), eps);
+  else layernorm_kernel<32><<<grid, 256, 0, s>>>(x, gain, bias, y, M, int(d), eps);
+  count_launch(1);
+  SA_LAUNCH_CHECK("sa_layernorm");
+  return SA_OK;
+}
+
+extern "C" int sa_softmax_attn(const float* q, const float* k, const float* v, float* out,
+                               int64_t B, int64_t n, int64_t d, int64_t heads, void* stream) {
+  SA_REQUIRE(B > 0 && n > 0 && d > 0 && heads > 0 && d % heads == 0, SA_ERR_SHAPE,
+             "sa_softmax_attn: bad extents");
+  const int64_t dk = d / heads;
+  const size_t smem = size_t(n * (dk + 1) + n * dk + 8 * dk + 8 * n) * sizeof(float);
+  SA_REQUIRE(smem <= 220 * 1024, SA_ERR_SHAPE, "sa_softmax_attn: n=%lld dk=%lld too large",
+             (long long)n, (long long)dk);
+  cudaFuncSetAttribute(softmax_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  const float scale_div = sqrtf(float(dk));  // python float math.sqrt(dk) → f32
+  softmax_attn_kernel<<<unsigned(B * heads), 256, smem, as_stream(stream)>>>(
+      q, k, v, out, int(n), int(d), int(heads), int(dk), scale_div);
+  count_launch(1);
+  SA_LAUNCH_CHECK("sa_softmax_attn");
+  return SA_OK;
+}
+
+extern "C" int sa_pool(const float* x, float* y, int64_t B, int64_t n, int64_t d, int mode,
+                       void* stream) {
+  SA_REQUIRE(B > 0 && n > 0 && d > 0, SA_ERR_SHAPE, "sa_pool: bad extents");
+  pool_kernel<<<unsigned(cdiv(B * d, 256)), 256, 0, as_stream(stream)>>>(x, y, B, int(n), int(d),
+                                                                          mode);
+  count_launch(1);
+  SA_LAUNCH_CHECK("sa_pool");
+  return SA_OK;
+}

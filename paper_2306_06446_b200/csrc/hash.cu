@@ -1,0 +1,164 @@
+// K1 — Q/K sign-hash to bit-packed codes + per-(image, head) mean-|x| scale.
+//
+// Semantics (ref quantize.py:78-80, 123-140 as called at model.py:355-358):
+//   code = !(x < 0)        (so -0.0 and NaN hash to 1; built WITHOUT fast-math/FTZ)
+//   gamma[b, h] = mean |x| over the n tokens x dk channels of head h of image b.
+//
+// Layout: x is the flat projection output (B*n, d); codes are written
+// [B][heads][n][W], W = ceil(dk/32), bit j of word w = channel 32w+j of the head.
+//
+// Each CTA owns a chunk of kTokPerCta tokens of one image: warps walk rows with
+// 128-bit loads (lane = 4 channels), build 32-bit words with an 8-lane OR
+// butterfly, stage them in shared memory and write them out coalesced in the
+// [head][token][word] order. |x| is accumulated per channel in registers,
+// reduced across warps in a fixed order and emitted as float64 partials per
+// (image, chunk, head); a second tiny kernel sums the partials in chunk order,
+// so gamma is deterministic (no atomics).
+#include "common.cuh"
+
+namespace sa {
+
+constexpr int kHashThreads = 256;
+constexpr int kTokPerCta = 64;
+
+template <int NBLK>  // NBLK = ceil(d / 128)
+__global__ void __launch_bounds__(kHashThreads) sign_hash_kernel(
+    const float* __restrict__ x, int n, int d, int heads, int dk, int W, int chunks,
+    uint32_t* __restrict__ codes, double* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int dwords = d >> 5;                                    // words per row
+  uint32_t* sm_codes = reinterpret_cast<uint32_t*>(smem_raw);   // [kTokPerCta][dwords]
+  float* sm_cs = reinterpret_cast<float*>(sm_codes + kTokPerCta * dwords);  // [8][d]
+
+  const int b = blockIdx.y, chunk = blockIdx.x;
+  const int t0 = chunk * kTokPerCta;
+  const int rows = min(kTokPerCta, n - t0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  float acc[NBLK][4];
+#pragma unroll
+  for (int j = 0; j < NBLK; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+
+  for (int r = warp; r < rows; r += kHashThreads / 32) {
+    const float* row = x + (size_t(b) * n + t0 + r) * d;
+#pragma unroll
+    for (int j = 0; j < NBLK; ++j) {
+      const int c0 = j * 128 + lane * 4;
+      const bool act = c0 < d;  // uniform within each 8-lane group (d % 32 == 0)
+      float4 v = act ? __ldg(reinterpret_cast<const float4*>(row + c0)) : make_float4(0, 0, 0, 0);
+      acc[j][0] += fabsf(v.x);
+      acc[j][1] += fabsf(v.y);
+      acc[j][2] += fabsf(v.z);
+      acc[j][3] += fabsf(v.w);
+      uint32_t nib = uint32_t(!(v.x < 0.f)) | (uint32_t(!(v.y < 0.f)) << 1) |
+                     (uint32_t(!(v.z < 0.f)) << 2) | (uint32_t(!(v.w < 0.f)) << 3);
+      uint32_t w = nib << (4 * (lane & 7));
+      w |= __shfl_xor_sync(0xffffffffu, w, 1);
+      w |= __shfl_xor_sync(0xffffffffu, w, 2);
+      w |= __shfl_xor_sync(0xffffffffu, w, 4);
+      if (act && (lane & 7) == 0) sm_codes[r * dwords + (c0 >> 5)] = w;
+    }
+  }
+  // per-channel |x| sums of this warp → smem
+#pragma unroll
+  for (int j = 0; j < NBLK; ++j) {
+    const int c0 = j * 128 + lane * 4;
+    if (c0 < d) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sm_cs[warp * d + c0 + i] = acc[j][i];
+    }
+  }
+  __syncthreads();
+
+  // codes out: [head][token][word] order for coalescing
+  const int total = heads * rows * W;
+  for (int idx = threadIdx.x; idx < total; idx += kHashThreads) {
+    const int wi = idx % W;
+    const int r = (idx / W) % rows;
+    const int h = idx / (W * rows);
+    uint32_t word;
+    if (dk >= 32) {
+      word = sm_codes[r * dwords + h * (dk >> 5) + wi];
+    } else {
+      const int bit0 = h * dk;
+      word = (sm_codes[r * dwords + (bit0 >> 5)] >> (bit0 & 31)) & ((1u << dk) - 1u);
+    }
+    codes[((size_t(b) * heads + h) * n + t0 + r) * W + wi] = word;
+  }
+
+  // per-head partial sums: fixed-order float64 reduction (warps, then channels)
+  for (int h = warp; h < heads; h += kHashThreads / 32) {
+    double s = 0.0;
+    for (int c = h * dk + lane; c < (h + 1) * dk; c += 32) {
+      double cs = 0.0;
+      for (int w8 = 0; w8 < kHashThreads / 32; ++w8) cs += double(sm_cs[w8 * d + c]);
+      s += cs;
+    }
+    s = warp_sum(s);
+    if (lane == 0) partial[(size_t(b) * chunks + chunk) * heads + h] = s;
+  }
+}
+
+__global__ void gamma_finalize_kernel(const double* __restrict__ partial, int BH, int heads,
+                                      int chunks, double inv_count, float* __restrict__ gamma) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= BH) return;
+  const int b = i / heads, h = i % heads;
+  double s = 0.0;
+  for (int c = 0; c < chunks; ++c) s += partial[(size_t(b) * chunks + c) * heads + h];
+  gamma[i] = float(s * inv_count);
+}
+
+}  // namespace sa
+
+using namespace sa;
+
+extern "C" size_t sa_sign_hash_workspace(int64_t B, int64_t n, int64_t d, int64_t heads) {
+  (void)d;
+  return size_t(B) * size_t(cdiv(n, kTokPerCta)) * size_t(heads) * sizeof(double);
+}
+
+extern "C" int sa_sign_hash(const float* x, int64_t B, int64_t n, int64_t d, int64_t heads,
+                            uint32_t* codes, float* gamma, void* ws, size_t ws_bytes,
+                            void* stream) {
+  SA_REQUIRE(B > 0 && n > 0 && d > 0 && heads > 0, SA_ERR_SHAPE,
+             "sa_sign_hash: empty extents B=%lld n=%lld d=%lld", (long long)B, (long long)n,
+             (long long)d);
+  SA_REQUIRE(d % heads == 0, SA_ERR_SHAPE, "sa_sign_hash: d %lld not divisible by heads %lld",
+             (long long)d, (long long)heads);
+  const int64_t dk = d / heads;
+  SA_REQUIRE(d % 32 == 0 && d <= 512 && (dk % 32 == 0 || 32 % dk == 0), SA_ERR_SHAPE,
+             "sa_sign_hash: unsupported d=%lld dk=%lld (need d%%32==0, d<=512, dk|32 or 32|dk)",
+             (long long)d, (long long)dk);
+  SA_REQUIRE(ws_bytes >= sa_sign_hash_workspace(B, n, d, heads), SA_ERR_VALUE,
+             "sa_sign_hash: workspace too small");
+  const int W = int(cdiv(dk, 32));
+  const int chunks = int(cdiv(n, kTokPerCta));
+  const size_t smem = size_t(kTokPerCta) * (d / 32) * 4 + size_t(kHashThreads / 32) * d * 4;
+  dim3 grid(chunks, unsigned(B));
+  double* partial = static_cast<double*>(ws);
+  cudaStream_t s = as_stream(stream);
+  const int nblk = int(cdiv(d, 128));
+  switch (nblk) {
+    case 1:
+      sign_hash_kernel<1><<<grid, kHashThreads, smem, s>>>(x, int(n), int(d), int(heads), int(dk),
+                                                          W, chunks, codes, partial);
+      break;
+    case 2:
+      sign_hash_kernel<2><<<grid, kHashThreads, smem, s>>>(x, int(n), int(d), int(heads), int(dk),
+                                                          W, chunks, codes, partial);
+      break;
+    default:
+      cudaFuncSetAttribute(sign_hash_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(smem));
+      sign_hash_kernel<4><<<grid, kHashThreads, smem, s>>>(x, int(n), int(d), int(heads), int(dk),
+                                                          W, chunks, codes, partial);
+      break;
+  }
+  const int BH = int(B * heads);
+  gamma_finalize_kernel<<<int(cdiv(BH, 256)), 256, 0, s>>>(partial, BH, int(heads), chunks,
+                                                           1.0 / double(n * dk), gamma);
+  count_launch(2);
+  SA_LAUNCH_CHECK("sa_sign_hash");
+  return SA_OK;
+}

@@ -1,0 +1,233 @@
+// K4 — top-1 two-expert router + stable token partition (ref moe.py:81-92).
+//
+//   logits = f32(fp64 x·W_g)        one warp per token, fp64 FMA + fixed shuffle tree;
+//                                   every product of two floats is exact in fp64, so the
+//                                   f32-rounded logits equal the reference's (ref tensor.py:68-75)
+//   winner = argmax(softmax(logits)) with ties → expert 0. For two experts the
+//            softmax argmax differs from the logit argmax only when the deficit is
+//            so small that numpy's f32 exp rounds to 1 (ref moe.py:89):
+//            expert 1 iff l1 > l0 and f32(l0 - l1) < -tie_thresh.
+//   gate   = p[winner] = e_w / (e_0 + e_1) in f32 (e of the max logit is exactly 1).
+//   perm   = stable partition [expert-0 tokens ascending | expert-1 tokens ascending]
+//            = concatenate(index_of) (ref moe.py:91), via block counts → one-CTA
+//            scan → block-local ballot ranks. counts[] stay on the device.
+#include "common.cuh"
+
+namespace sa {
+
+constexpr int kRouteTok = 256;  // tokens per route / partition block
+
+// winner + gate from the two f32 logits (see the file comment)
+__device__ __forceinline__ int decide(float l0, float l1, float tie_thresh, float& gate) {
+  const float m = fmaxf(l0, l1);
+  const float sh0 = l0 - m, sh1 = l1 - m;  // f32 max-shift (ref tensor.py:100)
+  // numpy-exp tie rule decides the winner bit-exactly
+  const int e = (l1 > l0 && sh0 < -tie_thresh) ? 1 : 0;
+  // e of the max is exp(0) = 1 exactly; a deficit inside the tie band has
+  // numpy exp == 1 as well
+  const float e0 = (sh0 >= -tie_thresh) ? 1.f : expf(sh0);
+  const float e1 = (sh1 >= -tie_thresh) ? 1.f : expf(sh1);
+  gate = (e ? e1 : e0) / (e0 + e1);
+  return e;
+}
+
+// dispatch from precomputed logits (M, 2): one thread per token
+__global__ void __launch_bounds__(kRouteTok) dispatch_kernel(const float* __restrict__ logits,
+                                                            int64_t M, float tie_thresh,
+                                                            int32_t* __restrict__ expert_of,
+                                                            float* __restrict__ gate,
+                                                            int32_t* __restrict__ block_cnt1) {
+  __shared__ int wcnt[kRouteTok / 32];
+  const int64_t t = int64_t(blockIdx.x) * kRouteTok + threadIdx.x;
+  int e = 0;
+  if (t < M) {
+    float g;
+    e = decide(logits[2 * t], logits[2 * t + 1], tie_thresh, g);
+    expert_of[t] = e;
+    gate[t] = g;
+  }
+  const unsigned b = __ballot_sync(0xffffffffu, e == 1);
+  if ((threadIdx.x & 31) == 0) wcnt[threadIdx.x >> 5] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int w = 0; w < kRouteTok / 32; ++w) c += wcnt[w];
+    block_cnt1[blockIdx.x] = c;
+  }
+}
+
+__global__ void __launch_bounds__(256) route_kernel(const float* __restrict__ x,
+                                                   const float* __restrict__ wg, int64_t M, int d,
+                                                   float tie_thresh, float* __restrict__ logits,
+                                                   int32_t* __restrict__ expert_of,
+                                                   float* __restrict__ gate,
+                                                   int32_t* __restrict__ block_cnt1) {
+  __shared__ double sw[2 * 512];
+  __shared__ int wcnt[8];
+  for (int i = threadIdx.x; i < 2 * d; i += blockDim.x) sw[i] = double(wg[i]);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t base = int64_t(blockIdx.x) * kRouteTok;
+  int mine = 0;
+  for (int r = warp; r < kRouteTok; r += 8) {
+    const int64_t t = base + r;
+    if (t >= M) break;
+    const float* row = x + t * d;
+    double s0 = 0.0, s1 = 0.0;
+    for (int c = lane; c < d; c += 32) {
+      const double xv = double(row[c]);
+      s0 = fma(xv, sw[2 * c], s0);
+      s1 = fma(xv, sw[2 * c + 1], s1);
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    if (lane == 0) {
+      const float l0 = float(s0), l1 = float(s1);
+      float g;
+      const int e = decide(l0, l1, tie_thresh, g);
+      gate[t] = g;
+      expert_of[t] = e;
+      if (logits) {
+        logits[2 * t] = l0;
+        logits[2 * t + 1] = l1;
+      }
+      mine += e;
+    }
+  }
+  if (lane == 0) wcnt[warp] = mine;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int w = 0; w < 8; ++w) c += wcnt[w];
+    block_cnt1[blockIdx.x] = c;
+  }
+}
+
+// single CTA: exclusive scan of per-block expert-1 counts; counts[0..1]
+__global__ void __launch_bounds__(1024) route_scan_kernel(const int32_t* __restrict__ block_cnt1,
+                                                          int nblocks, int64_t M,
+                                                          int32_t* __restrict__ block_off1,
+                                                          int32_t* __restrict__ counts) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nblocks; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < nblocks ? block_cnt1[i] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int w = warp_tot[lane];
+      int wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      warp_tot[lane] = wi - w;  // exclusive warp offsets
+    }
+    __syncthreads();
+    const int excl = carry + warp_tot[warp] + incl - v;
+    if (i < nblocks) block_off1[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    counts[1] = carry;
+    counts[0] = int32_t(M - carry);
+  }
+}
+
+__global__ void __launch_bounds__(kRouteTok) partition_kernel(const int32_t* __restrict__ expert_of,
+                                                             const int32_t* __restrict__ block_off1,
+                                                             const int32_t* __restrict__ counts,
+                                                             int64_t M, int32_t* __restrict__ perm) {
+  __shared__ int wc[kRouteTok / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t t = int64_t(blockIdx.x) * kRouteTok + threadIdx.x;
+  const int e = t < M ? expert_of[t] : 0;
+  const bool valid = t < M;
+  const unsigned b1 = __ballot_sync(0xffffffffu, valid && e == 1);
+  if (lane == 0) wc[warp] = __popc(b1);
+  __syncthreads();
+  int before1 = 0;
+  for (int w = 0; w < warp; ++w) before1 += wc[w];
+  before1 += __popc(b1 & ((1u << lane) - 1u));
+  if (!valid) return;
+  const int64_t off1 = block_off1[blockIdx.x];
+  const int64_t blk0 = int64_t(blockIdx.x) * kRouteTok;
+  const int64_t local = threadIdx.x;
+  int64_t pos;
+  if (e == 1) {
+    pos = int64_t(counts[0]) + off1 + before1;
+  } else {
+    pos = (blk0 - off1) + (local - before1);
+  }
+  perm[pos] = int32_t(t);
+}
+
+}  // namespace sa
+
+using namespace sa;
+
+extern "C" size_t sa_moe_route_workspace(int64_t M) {
+  const int64_t nb = cdiv(M, kRouteTok);
+  return size_t(2 * nb) * sizeof(int32_t) + 64;
+}
+
+extern "C" int sa_moe_route(const float* x, const float* wg, int64_t M, int64_t d,
+                            float tie_thresh, float* logits, int32_t* expert_of, float* gate,
+                            int32_t* counts, int32_t* perm, void* ws, size_t ws_bytes,
+                            void* stream) {
+  SA_REQUIRE(M >= 0 && d > 0 && d <= 512, SA_ERR_SHAPE, "sa_moe_route: d=%lld unsupported",
+             (long long)d);
+  SA_REQUIRE(M < (int64_t(1) << 31), SA_ERR_SHAPE, "sa_moe_route: too many tokens");
+  SA_REQUIRE(ws_bytes >= sa_moe_route_workspace(M), SA_ERR_VALUE,
+             "sa_moe_route: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  if (M == 0) {
+    cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), s);
+    return SA_OK;
+  }
+  const int nb = int(cdiv(M, kRouteTok));
+  int32_t* block_cnt1 = static_cast<int32_t*>(ws);
+  int32_t* block_off1 = block_cnt1 + nb;
+  route_kernel<<<nb, 256, 0, s>>>(x, wg, M, int(d), tie_thresh, logits, expert_of, gate,
+                                  block_cnt1);
+  route_scan_kernel<<<1, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
+  partition_kernel<<<nb, kRouteTok, 0, s>>>(expert_of, block_off1, counts, M, perm);
+  count_launch(3);
+  SA_LAUNCH_CHECK("sa_moe_route");
+  return SA_OK;
+}
+
+extern "C" int sa_moe_dispatch(const float* logits, int64_t M, float tie_thresh,
+                               int32_t* expert_of, float* gate, int32_t* counts, int32_t* perm,
+                               void* ws, size_t ws_bytes, void* stream) {
+  SA_REQUIRE(M >= 0 && M < (int64_t(1) << 31), SA_ERR_SHAPE, "sa_moe_dispatch: bad token count");
+  SA_REQUIRE(ws_bytes >= sa_moe_route_workspace(M), SA_ERR_VALUE,
+             "sa_moe_dispatch: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  if (M == 0) {
+    cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), s);
+    return SA_OK;
+  }
+  const int nb = int(cdiv(M, kRouteTok));
+  int32_t* block_cnt1 = static_cast<int32_t*>(ws);
+  int32_t* block_off1 = block_cnt1 + nb;
+  dispatch_kernel<<<nb, kRouteTok, 0, s>>>(logits, M, tie_thresh, expert_of, gate, block_cnt1);
+  route_scan_kernel<<<1, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
+  partition_kernel<<<nb, kRouteTok, 0, s>>>(expert_of, block_off1, counts, M, perm);
+  count_launch(3);
+  SA_LAUNCH_CHECK("sa_moe_dispatch");
+  return SA_OK;
+}

@@ -1,0 +1,756 @@
+"""Layers, blocks and model builders on the device, mirroring the reference
+`shiftadd.model` module (ref model.py) for the inference path.
+
+Every layer keeps the reference's constructor signature, `kind` attribute and
+`forward(x, train=False)` entry; forwards take and return CUDA tensors in the
+reference's flat (tokens, channels) layout and run in libshiftadd_b200.so.
+Each forward also accepts `residual=` so a Block fuses its residual add into
+the producing kernel's epilogue. Training (backward, optimizers, balance
+losses) is outside the inference hot path; `train=True` raises.
+
+Weights are drawn on the host with the reference's PCG64 order (ref
+model.py:487-553) and uploaded once, so `Model(cfg)` holds exactly the
+reference `Model(cfg)`'s parameters.
+"""
+
+from __future__ import annotations
+
+from dataclasses import asdict, dataclass
+from typing import List, Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import attention as A
+from . import moe as MOE
+from . import quantize as Q
+from . import specs as SPECS
+from .tensor import GradPair, ShapeError, StateError, make_rng, to_device
+
+ATTN_MODES = ("softmax", "linear", "linear-binary")   # ref model.py:31
+LINEAR_MODES = ("dense", "shift", "moe")              # ref model.py:32
+
+
+@dataclass
+class BlockConfig:
+    """ref model.py:35-53 (+ binary_order: linear K^T V or quadratic Hamming)."""
+
+    d: int
+    h: int
+    mlp_ratio: float = 4.0
+    attn_mode: str = "softmax"
+    mlp_mode: str = "dense"
+    attn_linear_mode: str = "dense"
+    exempt: bool = False
+    binary_order: str = "auto"
+
+    def __post_init__(self):
+        if self.d % self.h != 0:
+            raise ShapeError(f"model dim {self.d} not divisible by heads {self.h}")
+        if self.attn_mode not in ATTN_MODES:
+            raise ValueError(f"unknown attn_mode {self.attn_mode!r}")
+        if self.mlp_mode not in LINEAR_MODES:
+            raise ValueError(f"unknown mlp_mode {self.mlp_mode!r}")
+        if self.attn_linear_mode not in LINEAR_MODES:
+            raise ValueError(f"unknown attn_linear_mode {self.attn_linear_mode!r}")
+        if self.binary_order not in A.ORDERS:
+            raise ValueError(f"unknown binary_order {self.binary_order!r}")
+
+
+@dataclass
+class ModelConfig:
+    """ref model.py:56-81"""
+
+    blocks: List[BlockConfig]
+    patch: int = 4
+    img: int = 16
+    classes: int = 5
+    seed: int = 0
+    channels: int = 3
+
+    def __post_init__(self):
+        if self.img % self.patch != 0:
+            raise ShapeError(f"image side {self.img} not divisible by patch {self.patch}")
+
+    @property
+    def tokens(self) -> int:
+        side = self.img // self.patch
+        return side * side
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+    @classmethod
+    def from_dict(cls, payload: dict) -> "ModelConfig":
+        blocks = [BlockConfig(**b) for b in payload["blocks"]]
+        rest = {k: v for k, v in payload.items() if k != "blocks"}
+        return cls(blocks=blocks, **rest)
+
+
+@dataclass
+class MoeConfig:
+    """ref model.py:84-88"""
+
+    sigma: float = 0.1
+    lam: float = 0.01
+    lat: tuple = (3.0, 1.0)   # (mult expert, shift expert)
+
+
+def _no_train(train):
+    if train:
+        raise NotImplementedError("this package implements the inference path only")
+
+
+def _stream():
+    return _lib.stream()
+
+
+# ---------------------------------------------------------------------------
+# layers
+
+
+class Linear:
+    """Dense y = x @ w, no bias (ref model.py:95-123)."""
+
+    kind = "dense"
+
+    def __init__(self, w):
+        self.w = GradPair(to_device(w))
+
+    @property
+    def in_dim(self):
+        return self.w.value.shape[0]
+
+    @property
+    def out_dim(self):
+        return self.w.value.shape[1]
+
+    def weight_arg(self):
+        return self.w.value, _lib.SA_W_DENSE, Q.P_MIN_DEFAULT
+
+    def forward(self, x, train=False, residual=None, act=0):
+        _no_train(train)
+        return _linear_call(self, x, residual, act)
+
+    def named_params(self, prefix):
+        yield prefix + ".w", self.w
+
+    def extra_blobs(self, prefix):
+        return ()
+
+    def post_step(self):
+        pass
+
+
+class ShiftLinearLayer:
+    """Shift layer: forward uses the quantized sign/exponent pair of the dense
+    shadow (ref model.py:126-166); the packed codes live on the device."""
+
+    kind = "shift"
+
+    def __init__(self, shadow, quant_cfg: Q.QuantConfig = None):
+        self.quant_cfg = quant_cfg or Q.QuantConfig()
+        self.w = GradPair(to_device(shadow))
+        self.quant = Q.quantize_shift(self.w.value, self.quant_cfg)
+
+    def requantize(self):
+        self.quant = Q.quantize_shift(self.w.value, self.quant_cfg)
+
+    @property
+    def in_dim(self):
+        return self.quant.in_dim
+
+    @property
+    def out_dim(self):
+        return self.quant.out_dim
+
+    def weight_arg(self):
+        return self.quant.packed, _lib.SA_W_SHIFT, self.quant.p_min
+
+    def forward(self, x, train=False, residual=None, act=0):
+        _no_train(train)
+        return _linear_call(self, x, residual, act)
+
+    def named_params(self, prefix):
+        yield prefix + ".shadow", self.w
+
+    def extra_blobs(self, prefix):
+        yield prefix + ".quant_s", self.quant.s
+        yield prefix + ".quant_p", self.quant.p
+
+    def post_step(self):
+        self.requantize()
+
+
+def _linear_call(layer, x, residual, act):
+    x = to_device(x)
+    lead = x.shape[:-1]
+    x2 = x.reshape(-1, x.shape[-1])
+    if x2.shape[1] != layer.in_dim:
+        raise ShapeError(f"input extent {x2.shape[1]} != layer in_dim {layer.in_dim}")
+    w, kind, p_min = layer.weight_arg()
+    y = torch.empty((x2.shape[0], layer.out_dim), dtype=torch.float32, device=x.device)
+    res = residual.reshape(y.shape) if residual is not None else None
+    _lib.call("sa_linear", _lib.ptr(x2), _lib.ptr(w), kind, _lib.ptr(y), x2.shape[0],
+              layer.in_dim, layer.out_dim, p_min, _lib.ptr(res), int(act), _stream())
+    return y.reshape(*lead, layer.out_dim)
+
+
+class LayerNorm:
+    """ref model.py:168-193 (eps 1e-5, biased variance)."""
+
+    def __init__(self, dim: int, dtype=np.float32):
+        self.gain = GradPair(to_device(np.ones(dim, np.float32)))
+        self.bias = GradPair(to_device(np.zeros(dim, np.float32)))
+
+    def forward(self, x, train=False):
+        _no_train(train)
+        x = to_device(x)
+        d = x.shape[-1]
+        y = torch.empty_like(x)
+        _lib.call("sa_layernorm", _lib.ptr(x), _lib.ptr(self.gain.value), _lib.ptr(self.bias.value),
+                  _lib.ptr(y), x.numel() // d, d, 1e-5, _stream())
+        return y
+
+    def named_params(self, prefix):
+        yield prefix + ".gain", self.gain
+        yield prefix + ".bias", self.bias
+
+    def post_step(self):
+        pass
+
+
+class Mlp:
+    """fc1 → GELU(tanh) → fc2 (ref model.py:196-228); both linears run in one
+    call with the GELU fused into fc1's epilogue."""
+
+    def __init__(self, fc1, fc2):
+        self.fc1 = fc1
+        self.fc2 = fc2
+
+    def forward(self, x, train=False, residual=None):
+        _no_train(train)
+        x = to_device(x)
+        if not (hasattr(self.fc1, "weight_arg") and hasattr(self.fc2, "weight_arg")):
+            h = self.fc1.forward(x)
+            raise NotImplementedError(f"unsupported MLP layers {type(self.fc1)}, {type(h)}")
+        lead = x.shape[:-1]
+        x2 = x.reshape(-1, x.shape[-1])
+        M, d = x2.shape
+        hidden = self.fc1.out_dim
+        w1, k1, pm1 = self.fc1.weight_arg()
+        w2, k2, pm2 = self.fc2.weight_arg()
+        if k1 == _lib.SA_W_SHIFT and k2 == _lib.SA_W_SHIFT and pm1 != pm2:
+            raise ValueError("fc1/fc2 shift layers must share p_min")
+        p_min = pm1 if k1 == _lib.SA_W_SHIFT else pm2
+        y = torch.empty((M, self.fc2.out_dim), dtype=torch.float32, device=x.device)
+        ws = _lib.Workspace.get(_lib.load().sa_mlp_workspace(M, hidden), slot=3)
+        res = residual.reshape(y.shape) if residual is not None else None
+        _lib.call("sa_mlp", _lib.ptr(x2), _lib.ptr(w1), k1, _lib.ptr(w2), k2, _lib.ptr(y), M, d,
+                  hidden, p_min, _lib.ptr(res), _lib.ptr(ws), ws.numel(), _stream())
+        return y.reshape(*lead, self.fc2.out_dim)
+
+    def named_params(self, prefix):
+        yield from self.fc1.named_params(prefix + ".fc1")
+        yield from self.fc2.named_params(prefix + ".fc2")
+
+    def extra_blobs(self, prefix):
+        yield from self.fc1.extra_blobs(prefix + ".fc1")
+        yield from self.fc2.extra_blobs(prefix + ".fc2")
+
+    def post_step(self):
+        self.fc1.post_step()
+        self.fc2.post_step()
+
+
+def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None):
+    """K5 for the two expert shapes the reference builds (ref model.py:499-502,
+    514-521): (Linear, ShiftLinearLayer) and (Mlp(Linear, Linear),
+    Mlp(Shift, Shift)). Returns None for any other expert set."""
+    if len(experts) != 2:
+        return None
+    e0, e1 = experts
+    M = x.shape[0]
+    res = residual.reshape(M, -1) if residual is not None else None
+    if isinstance(e0, Linear) and isinstance(e1, ShiftLinearLayer):
+        K, N = e0.in_dim, e0.out_dim
+        if (e1.in_dim, e1.out_dim) != (K, N):
+            return None
+        y = torch.empty((M, N), dtype=torch.float32, device=x.device)
+        _lib.call("sa_moe_linear", _lib.ptr(x), _lib.ptr(plan.perm_dev), _lib.ptr(plan.counts_dev),
+                  _lib.ptr(plan.gate_dev), _lib.ptr(e0.w.value), _lib.ptr(e1.quant.packed),
+                  e1.quant.p_min, _lib.ptr(y), _lib.ptr(res), M, K, N, _stream())
+        return y
+    if (isinstance(e0, Mlp) and isinstance(e1, Mlp) and isinstance(e0.fc1, Linear)
+            and isinstance(e0.fc2, Linear) and isinstance(e1.fc1, ShiftLinearLayer)
+            and isinstance(e1.fc2, ShiftLinearLayer)):
+        d, hidden = e0.fc1.in_dim, e0.fc1.out_dim
+        if e1.fc1.quant.p_min != e1.fc2.quant.p_min:
+            return None
+        y = torch.empty((M, d), dtype=torch.float32, device=x.device)
+        ws = _lib.Workspace.get(_lib.load().sa_moe_mlp_workspace(M, hidden), slot=3)
+        _lib.call("sa_moe_mlp", _lib.ptr(x), _lib.ptr(plan.perm_dev), _lib.ptr(plan.counts_dev),
+                  _lib.ptr(plan.gate_dev), _lib.ptr(e0.fc1.w.value), _lib.ptr(e0.fc2.w.value),
+                  _lib.ptr(e1.fc1.quant.packed), _lib.ptr(e1.fc2.quant.packed),
+                  e1.fc1.quant.p_min, _lib.ptr(y), _lib.ptr(res), M, d, hidden, _lib.ptr(ws),
+                  ws.numel(), _stream())
+        return y
+    return None
+
+
+class MoeModule:
+    """Top-1 two-expert mixture (ref model.py:230-314): device routing (K4) and
+    one fused launch for both experts (K5). `last_plan` is set on every forward
+    and materialises on the host only when read."""
+
+    def __init__(self, w_g, experts: list, moe_cfg: MoeConfig):
+        self.wg = GradPair(to_device(w_g))
+        self.experts = experts
+        self.cfg = moe_cfg
+        self.alpha = MOE.latency_coefficients(moe_cfg.lat)
+        self.last_plan: Optional[MOE.DispatchPlan] = None
+
+    @property
+    def kind(self):
+        return "moe"
+
+    @property
+    def out_dim(self):
+        e = self.experts[0]
+        return e.fc2.out_dim if isinstance(e, Mlp) else e.out_dim
+
+    def router(self) -> MOE.Router:
+        return MOE.Router(w_g=self.wg.value, sigma=self.cfg.sigma, lam=self.cfg.lam)
+
+    def forward(self, x, train=False, residual=None):
+        _no_train(train)
+        x = to_device(x)
+        lead = x.shape[:-1]
+        x2 = x.reshape(-1, x.shape[-1])
+        plan, _ = MOE.route_plan(x2, self.wg.value)
+        self.last_plan = plan
+        y = fused_expert_forward(x2, self.experts, plan, residual)
+        if y is None:
+            y = MOE.moe_forward(x2, self.experts, plan)
+            if residual is not None:
+                y = residual.reshape(y.shape) + y
+        return y.reshape(*lead, y.shape[-1])
+
+    def named_params(self, prefix):
+        yield prefix + ".router.wg", self.wg
+        for e, expert in enumerate(self.experts):
+            yield from expert.named_params(f"{prefix}.expert{e}")
+
+    def extra_blobs(self, prefix):
+        for e, expert in enumerate(self.experts):
+            yield from expert.extra_blobs(f"{prefix}.expert{e}")
+
+    def post_step(self):
+        for expert in self.experts:
+            expert.post_step()
+
+
+class AttentionLayer:
+    """Multi-head attention over (batch, tokens, dim) (ref model.py:316-444)."""
+
+    def __init__(self, block_cfg: BlockConfig, projections: dict, dw_kernels: Optional[GradPair]):
+        self.cfg = block_cfg
+        self.proj = projections
+        self.dw = dw_kernels
+        if self.dw is not None and not isinstance(self.dw.value, torch.Tensor):
+            self.dw = GradPair(to_device(self.dw.value))
+
+    @property
+    def heads(self):
+        return self.cfg.h
+
+    def forward(self, x, train=False, residual=None):
+        _no_train(train)
+        x = to_device(x)
+        batch, n, d = x.shape
+        flat = x.reshape(batch * n, d)
+        q = self.proj["q"].forward(flat)
+        k = self.proj["k"].forward(flat)
+        v = self.proj["v"].forward(flat)
+        mode = self.cfg.attn_mode
+        if mode == "softmax":
+            merged = A.softmax_core_flat(q, k, v, batch, self.heads)
+        elif mode == "linear-binary":
+            dw = self.dw.value if self.dw is not None else None
+            order = "linear" if self.cfg.binary_order == "auto" else self.cfg.binary_order
+            merged = A.binary_core(q, k, v, batch, self.heads, dw, A.EPS_NORM, order)
+        else:
+            raise ValueError("the relu-feature 'linear' mode is outside the inference hot path")
+        res = residual.reshape(batch * n, d) if residual is not None else None
+        y = self.proj["o"].forward(merged, residual=res)
+        return y.reshape(batch, n, d)
+
+    def named_params(self, prefix):
+        for key in ("q", "k", "v", "o"):
+            yield from self.proj[key].named_params(f"{prefix}.{key}")
+        if self.dw is not None:
+            yield prefix + ".dw", self.dw
+
+    def extra_blobs(self, prefix):
+        for key in ("q", "k", "v", "o"):
+            yield from self.proj[key].extra_blobs(f"{prefix}.{key}")
+
+    def post_step(self):
+        for key in ("q", "k", "v", "o"):
+            self.proj[key].post_step()
+
+
+class Block:
+    """Pre-norm residual block (ref model.py:446-480); both residual adds are
+    fused into the epilogues of W_O and fc2."""
+
+    def __init__(self, cfg: BlockConfig, attn: AttentionLayer, mlp, dtype=np.float32):
+        self.cfg = cfg
+        self.ln1 = LayerNorm(cfg.d, dtype)
+        self.ln2 = LayerNorm(cfg.d, dtype)
+        self.attn = attn
+        self.mlp = mlp
+
+    def forward(self, x, train=False):
+        _no_train(train)
+        x = to_device(x)
+        batch, n, d = x.shape
+        h = self.attn.forward(self.ln1.forward(x), residual=x)
+        flat = self.ln2.forward(h).reshape(batch * n, d)
+        y = self.mlp.forward(flat, residual=h.reshape(batch * n, d))
+        return y.reshape(batch, n, d)
+
+    def named_params(self, prefix):
+        yield from self.ln1.named_params(prefix + ".ln1")
+        yield from self.attn.named_params(prefix + ".attn")
+        yield from self.ln2.named_params(prefix + ".ln2")
+        yield from self.mlp.named_params(prefix + ".mlp")
+
+    def extra_blobs(self, prefix):
+        yield from self.attn.extra_blobs(prefix + ".attn")
+        yield from self.mlp.extra_blobs(prefix + ".mlp")
+
+    def post_step(self):
+        self.attn.post_step()
+        self.mlp.post_step()
+
+
+# ---------------------------------------------------------------------------
+# builders (draw order = ref model.py:487-522)
+
+
+def _init_linear(rng, fan_in, fan_out, dtype=np.float32, scale=None):
+    """N(0,1)·scale, default 1/√fan_in (ref model.py:487-489). Host numpy."""
+    scale = scale if scale is not None else 1.0 / np.sqrt(fan_in)
+    return (rng.standard_normal((fan_in, fan_out)) * scale).astype(dtype)
+
+
+def _make_linear(mode, rng, fan_in, fan_out, dtype, moe_cfg, quant_cfg):
+    """ref model.py:492-503"""
+    w = _init_linear(rng, fan_in, fan_out, dtype)
+    if mode == "dense":
+        return Linear(w)
+    if mode == "shift":
+        return ShiftLinearLayer(w, quant_cfg)
+    if mode == "moe":
+        wg = _init_linear(rng, fan_in, 2, dtype, scale=0.02)
+        return MoeModule(wg, [Linear(w), ShiftLinearLayer(w.copy(), quant_cfg)], moe_cfg)
+    raise ValueError(f"unknown linear mode {mode!r}")
+
+
+def _make_mlp(cfg: BlockConfig, rng, dtype, moe_cfg, quant_cfg):
+    """ref model.py:506-522 (moe: router drawn before w1, w2)."""
+    hidden = int(cfg.d * cfg.mlp_ratio)
+    if cfg.mlp_mode == "dense":
+        return Mlp(Linear(_init_linear(rng, cfg.d, hidden, dtype)),
+                   Linear(_init_linear(rng, hidden, cfg.d, dtype)))
+    if cfg.mlp_mode == "shift":
+        return Mlp(ShiftLinearLayer(_init_linear(rng, cfg.d, hidden, dtype), quant_cfg),
+                   ShiftLinearLayer(_init_linear(rng, hidden, cfg.d, dtype), quant_cfg))
+    if cfg.mlp_mode == "moe":
+        wg = _init_linear(rng, cfg.d, 2, dtype, scale=0.02)
+        w1 = _init_linear(rng, cfg.d, hidden, dtype)
+        w2 = _init_linear(rng, hidden, cfg.d, dtype)
+        return MoeModule(wg, [Mlp(Linear(w1), Linear(w2)),
+                              Mlp(ShiftLinearLayer(w1.copy(), quant_cfg),
+                                  ShiftLinearLayer(w2.copy(), quant_cfg))], moe_cfg)
+    raise ValueError(f"unknown mlp_mode {cfg.mlp_mode!r}")
+
+
+class Stage:
+    """Patch embedding (+cls, +pos, +LN) → blocks → optional stage LN."""
+
+    def __init__(self, spec_stage, c_in, n_tokens, rng, dtype, moe_cfg, quant_cfg, dw_init):
+        st = spec_stage
+        self.patch = st["patch"]
+        self.d = d = st["d"]
+        self.n = n_tokens
+        self.patch_embed = Linear(_init_linear(rng, self.patch * self.patch * c_in, d, dtype))
+        self.cls = None
+        self.pos = None
+        rows = n_tokens + (1 if st.get("cls_token") else 0)
+        if st.get("cls_token"):
+            self.cls = GradPair(to_device((rng.standard_normal((1, d)) * 0.02).astype(dtype)))
+        if st.get("pos"):
+            self.pos = GradPair(to_device((rng.standard_normal((rows, d)) * 0.02).astype(dtype)))
+        self.rows = rows
+        self.blocks = []
+        for bc in st["blocks"]:
+            cfg = BlockConfig(d=d, h=bc["h"], mlp_ratio=bc["mlp_ratio"], attn_mode=bc["attn_mode"],
+                              mlp_mode=bc["mlp_mode"], attn_linear_mode=bc["attn_linear_mode"],
+                              exempt=bc.get("exempt", False),
+                              binary_order=bc.get("binary_order", "auto"))
+            proj = {k: _make_linear(cfg.attn_linear_mode, rng, d, d, dtype, moe_cfg, quant_cfg)
+                    for k in ("q", "k", "v", "o")}
+            dw = None
+            if cfg.attn_mode != "softmax":
+                if isinstance(dw_init, (int, float)):
+                    dw = GradPair(to_device((rng.standard_normal((3, 3, d)) * float(dw_init))
+                                            .astype(dtype)))
+                else:
+                    dw = GradPair(to_device(np.zeros((3, 3, d), dtype)))
+            mlp = _make_mlp(cfg, rng, dtype, moe_cfg, quant_cfg)
+            self.blocks.append(Block(cfg, AttentionLayer(cfg, proj, dw), mlp, dtype))
+        self.embed_ln = LayerNorm(d, dtype) if st.get("embed_norm") else None
+        self.stage_ln = LayerNorm(d, dtype) if st.get("stage_norm") else None
+
+
+class Network:
+    """A ShiftAddViT built from an architecture spec (see specs.py): the
+    reference toy `Model` (one stage) or a PVT / DeiT composition (several
+    stages chained through their token grids). `forward(images NHWC) →
+    logits (B, classes)` like `Model.forward` (ref model.py:565-577)."""
+
+    def __init__(self, spec: dict, dtype=np.float32, moe_cfg: MoeConfig = None,
+                 quant_cfg: Q.QuantConfig = None):
+        self.spec = spec
+        self.dtype = dtype
+        self.moe_cfg = moe_cfg or MoeConfig()
+        self.quant_cfg = quant_cfg or Q.QuantConfig(p_min=spec.get("p_min", -15),
+                                                    p_max=spec.get("p_max", 15))
+        rng = make_rng(spec["seed"])
+        c_in = spec.get("channels", 3)
+        side = spec["img"]
+        self.stages = []
+        for st in spec["stages"]:
+            if side % st["patch"]:
+                raise ShapeError(f"side {side} not divisible by patch {st['patch']}")
+            side //= st["patch"]
+            self.stages.append(Stage(st, c_in, side * side, rng, dtype, self.moe_cfg,
+                                     self.quant_cfg, spec.get("dw_init", "zeros")))
+            c_in = st["d"]
+        self.head = Linear(_init_linear(rng, spec["stages"][-1]["d"], spec["classes"], dtype,
+                                        scale=0.01))
+        dwi = spec.get("dw_init", "zeros")
+        if isinstance(dwi, dict):   # side stream after all main draws (specs.toy_c1)
+            g2 = make_rng(dwi["seed"])
+            for S in self.stages:
+                for blk in S.blocks:
+                    if blk.attn.dw is not None:
+                        vals = (g2.standard_normal(tuple(blk.attn.dw.value.shape)) * dwi["std"])
+                        blk.attn.dw.value.copy_(torch.from_numpy(vals.astype(dtype)))
+        self.pool_mode = 1 if spec.get("pool", "mean") == "cls" else 0
+
+    # -- introspection ---------------------------------------------------
+    @property
+    def blocks(self):
+        return [b for S in self.stages for b in S.blocks]
+
+    def moe_modules(self):
+        for si, S in enumerate(self.stages):
+            for bi, blk in enumerate(S.blocks):
+                pre = f"s{si}.b{bi}"
+                for key in ("q", "k", "v", "o"):
+                    if isinstance(blk.attn.proj[key], MoeModule):
+                        yield f"{pre}.attn.{key}", blk.attn.proj[key]
+                if isinstance(blk.mlp, MoeModule):
+                    yield f"{pre}.mlp", blk.mlp
+
+    def named_weights(self):
+        """(name, device tensor) in oracle.nets.iter_weights order."""
+        for si, S in enumerate(self.stages):
+            yield f"s{si}.pe", S.patch_embed.w.value
+            if S.cls is not None:
+                yield f"s{si}.cls", S.cls.value
+            if S.pos is not None:
+                yield f"s{si}.pos", S.pos.value
+            for bi, blk in enumerate(S.blocks):
+                pre = f"s{si}.b{bi}"
+                for key in ("q", "k", "v", "o"):
+                    yield from _layer_weights(f"{pre}.attn.{key}", blk.attn.proj[key])
+                if blk.attn.dw is not None:
+                    yield f"{pre}.attn.dw", blk.attn.dw.value
+                yield from _layer_weights(f"{pre}.mlp", blk.mlp)
+        yield "head", self.head.w.value
+
+    # -- forward -----------------------------------------------------------
+    def forward(self, images, train=False) -> torch.Tensor:
+        _no_train(train)
+        x = to_device(images)
+        if x.ndim != 4:
+            raise ShapeError(f"images must be (B, H, W, C), got {tuple(x.shape)}")
+        B, H, W, C = x.shape
+        grid = x
+        sub = 0.5                                   # ref model.py:566
+        tok = None
+        for S in self.stages:
+            tok = torch.empty((B * S.rows, S.d), dtype=torch.float32, device=x.device)
+            _lib.call("sa_patch_embed", _lib.ptr(grid), B, H, W, C, S.patch, sub,
+                      _lib.ptr(S.patch_embed.w.value), S.d,
+                      _lib.ptr(S.cls.value if S.cls is not None else None),
+                      _lib.ptr(S.pos.value if S.pos is not None else None), _lib.ptr(tok),
+                      _stream())
+            if S.embed_ln is not None:
+                tok = S.embed_ln.forward(tok)
+            t3 = tok.reshape(B, S.rows, S.d)
+            for blk in S.blocks:
+                t3 = blk.forward(t3)
+            tok = t3.reshape(B * S.rows, S.d)
+            if S.stage_ln is not None:
+                tok = S.stage_ln.forward(tok)
+            side = H // S.patch
+            grid, H, W, C, sub = tok, side, side, S.d, 0.0
+        last = self.stages[-1]
+        pooled = torch.empty((B, last.d), dtype=torch.float32, device=x.device)
+        _lib.call("sa_pool", _lib.ptr(tok), _lib.ptr(pooled), B, last.rows, last.d,
+                  self.pool_mode, _stream())
+        return self.head.forward(pooled)
+
+    __call__ = forward
+
+
+def _layer_weights(name, L):
+    if isinstance(L, (Linear, ShiftLinearLayer)):
+        yield name + ".w", L.w.value
+    elif isinstance(L, Mlp):
+        yield from _layer_weights(name + ".fc1", L.fc1)
+        yield from _layer_weights(name + ".fc2", L.fc2)
+    else:
+        yield name + ".wg", L.wg.value
+        for e, ex in enumerate(L.experts):
+            yield from _layer_weights(f"{name}.expert{e}", ex)
+
+
+def _model_cfg_to_spec(cfg: ModelConfig, quant_cfg) -> dict:
+    d0 = cfg.blocks[0].d
+    if any(b.d != d0 for b in cfg.blocks):
+        raise ShapeError("all blocks of the toy Model share one width")
+    qc = quant_cfg or Q.QuantConfig()
+    return {"name": "Model", "img": cfg.img, "channels": cfg.channels, "classes": cfg.classes,
+            "seed": cfg.seed, "dw_init": "zeros", "pool": "mean", "p_min": qc.p_min,
+            "p_max": qc.p_max,
+            "stages": [{"patch": cfg.patch, "d": d0, "pos": True, "cls_token": False,
+                        "embed_norm": False, "stage_norm": True,
+                        "blocks": [dict(h=b.h, mlp_ratio=b.mlp_ratio, attn_mode=b.attn_mode,
+                                        mlp_mode=b.mlp_mode, attn_linear_mode=b.attn_linear_mode,
+                                        exempt=b.exempt, binary_order=b.binary_order)
+                                   for b in cfg.blocks]}]}
+
+
+class Model(Network):
+    """The reference toy ViT (ref model.py:525-577): patch embed, learned
+    positions, blocks, final LN, mean pool, head — same constructor and the
+    same PCG64 parameters as the reference `Model(cfg)`."""
+
+    def __init__(self, cfg: ModelConfig, dtype=np.float32, moe_cfg: MoeConfig = None,
+                 quant_cfg: Q.QuantConfig = None):
+        self.cfg = cfg
+        super().__init__(_model_cfg_to_spec(cfg, quant_cfg), dtype, moe_cfg, quant_cfg)
+
+    @property
+    def patch_embed(self):
+        return self.stages[0].patch_embed
+
+    @property
+    def pos(self):
+        return self.stages[0].pos
+
+    @property
+    def final_ln(self):
+        return self.stages[0].stage_ln
+
+
+def build_model(spec: dict, **kw) -> Network:
+    return Network(spec, **kw)
+
+
+def pvt_v2_b0(**kw) -> Network:
+    return Network(SPECS.pvt_v2_b0(**kw))
+
+
+def pvt_v2_b2(**kw) -> Network:
+    return Network(SPECS.pvt_v2_b2(**kw))
+
+
+def pvt_v1_tiny(**kw) -> Network:
+    return Network(SPECS.pvt_v1_tiny(**kw))
+
+
+def deit_tiny(**kw) -> Network:
+    return Network(SPECS.deit_tiny(**kw))
+
+
+def apply_stage(model: Network, stage: int, mlp_target: str = "shift",
+                attn_target: str = "shift", reparam_seed: int = 77) -> Network:
+    """Stage-1/2 conversion (ref model.py:897-930): stage 1 switches non-exempt
+    attention to linear-binary (zero DW kernels if absent); stage 2 converts
+    projections / MLPs to shift or moe, preserving weights, with routers drawn
+    from PCG64(reparam_seed) in the reference's order."""
+    if stage not in (1, 2):
+        raise ValueError(f"stage must be 1 or 2, got {stage}")
+    rng = make_rng(reparam_seed)
+    blocks = model.blocks
+    if stage == 2 and any(b.cfg.attn_mode == "softmax" and not b.cfg.exempt for b in blocks):
+        raise ValueError("stage 2 requires a stage-1 model (linear attention)")
+    for block in blocks:
+        if block.cfg.exempt:
+            continue
+        if stage == 1:
+            block.cfg.attn_mode = "linear-binary"
+            block.attn.cfg = block.cfg
+            if block.attn.dw is None:
+                block.attn.dw = GradPair(to_device(np.zeros((3, 3, block.cfg.d), np.float32)))
+        else:
+            block.cfg.attn_linear_mode = attn_target
+            block.cfg.mlp_mode = mlp_target
+            block.attn.cfg = block.cfg
+            for key in ("q", "k", "v", "o"):
+                block.attn.proj[key] = _convert_linear(block.attn.proj[key], attn_target, rng,
+                                                       model.moe_cfg, model.quant_cfg)
+            block.mlp = _convert_mlp(block.mlp, mlp_target, rng, model.moe_cfg, model.quant_cfg)
+    return model
+
+
+def _convert_linear(layer, target, rng, moe_cfg, quant_cfg):
+    """ref model.py:772-783"""
+    if isinstance(layer, MoeModule) or target == "dense":
+        return layer
+    w = layer.w.value.clone()
+    if target == "shift":
+        return ShiftLinearLayer(w, quant_cfg)
+    if target == "moe":
+        wg = (rng.standard_normal((w.shape[0], 2)) * 0.02).astype(np.float32)
+        return MoeModule(wg, [Linear(w.clone()), ShiftLinearLayer(w.clone(), quant_cfg)], moe_cfg)
+    raise ValueError(f"unknown conversion target {target!r}")
+
+
+def _convert_mlp(mlp, target, rng, moe_cfg, quant_cfg):
+    """ref model.py:786-799"""
+    if isinstance(mlp, MoeModule) or target == "dense":
+        return mlp
+    w1 = mlp.fc1.w.value.clone()
+    w2 = mlp.fc2.w.value.clone()
+    if target == "shift":
+        return Mlp(ShiftLinearLayer(w1, quant_cfg), ShiftLinearLayer(w2, quant_cfg))
+    if target == "moe":
+        wg = (rng.standard_normal((w1.shape[0], 2)) * 0.02).astype(np.float32)
+        return MoeModule(wg, [Mlp(Linear(w1.clone()), Linear(w2.clone())),
+                              Mlp(ShiftLinearLayer(w1.clone(), quant_cfg),
+                                  ShiftLinearLayer(w2.clone(), quant_cfg))], moe_cfg)
+    raise ValueError(f"unknown conversion target {target!r}")
+
+
+__all__ = ["BlockConfig", "ModelConfig", "MoeConfig", "Linear", "ShiftLinearLayer", "LayerNorm",
+           "Mlp", "MoeModule", "AttentionLayer", "Block", "Network", "Model", "build_model",
+           "pvt_v2_b0", "pvt_v2_b2", "pvt_v1_tiny", "deit_tiny", "apply_stage", "StateError"]

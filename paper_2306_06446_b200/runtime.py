@@ -1,0 +1,80 @@
+"""Inference runtime helpers: per-op device timing (CUDA events on the
+launching stream) and CUDA-graph capture of a whole forward.
+
+`OpTimer` hooks the C-ABI dispatcher (`_lib.call`) and brackets every
+library call with a pair of CUDA events on the current stream, so the
+roofline numbers in bench.py are device durations of the hot-path kernels
+measured inside a real forward, not microbenchmarks.
+"""
+
+from __future__ import annotations
+
+import contextlib
+from collections import defaultdict
+
+import torch
+
+from . import _lib
+
+
+class OpTimer:
+    """Accumulates device time and call counts per C-ABI entry point."""
+
+    def __init__(self):
+        self.events = []          # (name, start, end, meta)
+        self._orig = None
+
+    @contextlib.contextmanager
+    def record(self):
+        orig = _lib.call
+        self._orig = orig
+
+        def timed_call(name, *args):
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+            orig(name, *args)
+            e.record()
+            self.events.append((name, s, e, args))
+        _lib.call = timed_call
+        try:
+            yield self
+        finally:
+            _lib.call = orig
+
+    def summary(self):
+        torch.cuda.synchronize()
+        out = defaultdict(lambda: {"calls": 0, "ms": 0.0, "args": []})
+        for name, s, e, args in self.events:
+            r = out[name]
+            r["calls"] += 1
+            r["ms"] += s.elapsed_time(e)
+            r["args"].append(args)
+        return dict(out)
+
+
+class GraphedForward:
+    """Capture `model.forward` on a static input buffer into one CUDA graph
+    (MoE shapes are resolved on the device, so the graph is reusable across
+    inputs). Call with a device tensor of the captured shape."""
+
+    def __init__(self, model, example: torch.Tensor, warmup: int = 2):
+        self.model = model
+        self.static_in = example.clone()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.model.forward(self.static_in)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.static_out = self.model.forward(self.static_in)
+        torch.cuda.synchronize()
+
+    def __call__(self, images: torch.Tensor = None) -> torch.Tensor:
+        if images is not None and images.data_ptr() != self.static_in.data_ptr():
+            self.static_in.copy_(images, non_blocking=True)
+        self.graph.replay()
+        return self.static_out

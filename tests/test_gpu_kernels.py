@@ -1,0 +1,347 @@
+"""Kernel-boundary parity on the GPU: every kernel is fed the oracle's own
+float32 inputs and compared with the oracle (and the golden vectors pinned to
+the real reference).
+
+Bars: bit-exact for codes, popcounts, router winners, permutations and shift
+codes; float results within the tolerances written in each test (the reference
+accumulates in float64, the kernels in float32)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import nets, ops
+
+pytestmark = pytest.mark.gpu
+
+F32 = np.float32
+
+
+def dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+# ---------------------------------------------------------------- K1 sign hash
+
+
+@pytest.mark.parametrize("B,n,d,h", [(2, 196, 64, 4), (3, 3136, 32, 1), (2, 784, 64, 2),
+                                     (2, 196, 160, 5), (2, 197, 192, 3), (1, 5, 32, 2),
+                                     (2, 49, 256, 8)])
+def test_sign_hash_codes_bit_exact(B, n, d, h):
+    from paper_2306_06446_b200 import quantize as Q
+    g = ops.rng(B * 1000 + n)
+    x = g.standard_normal((B * n, d)).astype(F32)
+    x[0, :7] = [-0.0, 0.0, -1e-45, np.nan, -np.inf, np.inf, -1e-40]  # edge values
+    codes, gamma = Q.sign_hash(dev(x), h, B)
+    xh = ops.heads_split(x.reshape(B, n, d), h).reshape(B * h, n, d // h)
+    want = ops.pack_codes(xh).view(np.int32).reshape(B, h, n, -1)
+    assert np.array_equal(host(codes), want)
+    xf = x.copy()
+    xf[0, :7] = 0  # gamma comparison on finite values only
+    codes2, gamma2 = Q.sign_hash(dev(xf), h, B)
+    xh2 = ops.heads_split(xf.reshape(B, n, d), h).reshape(B * h, n, d // h)
+    g_ref = ops.per_head_scale(xh2).reshape(B, h)
+    assert rel_err(host(gamma2), g_ref) < 2e-6
+
+
+def test_sign_hash_golden_edge_values(golden):
+    from paper_2306_06446_b200 import quantize as Q
+    k = golden("kat")
+    x = np.zeros((1, 32), F32)
+    x[0, :8] = k["sign_x"]
+    codes, _ = Q.sign_hash(dev(x), 1, 1)
+    bits = [(int(host(codes).reshape(-1)[0]) >> i) & 1 for i in range(8)]
+    assert bits == [int(v > 0) for v in k["sign_y"]]
+
+
+# ------------------------------------------------------- K2a / K2b binary attn
+
+
+@pytest.mark.parametrize("dk", [16, 32, 64])
+@pytest.mark.parametrize("order", ["linear", "quadratic"])
+def test_binary_core_matches_golden(golden, dk, order):
+    from paper_2306_06446_b200 import attention as A
+    k = golden("kat")
+    pre = f"lc{dk}_"
+    q, kk, v = k[pre + "q"], k[pre + "k"], k[pre + "v"]
+    H, n, _ = q.shape
+    flat = lambda t: dev(t.reshape(H * n, dk))  # noqa: E731  each head = one image
+    out = A.binary_core(flat(q), flat(kk), flat(v), H, 1, None, A.EPS_NORM, order)
+    got = host(out).reshape(H, n, dk)
+    assert rel_err(got, k[pre + "out"]) < 1e-5
+    assert np.all(got[0, 3] == 0)   # all-negative query row → exactly zero
+
+
+@pytest.mark.parametrize("B,n,d,h", [(2, 196, 64, 4), (2, 3136, 32, 1), (2, 784, 64, 2),
+                                     (2, 196, 160, 5)])
+def test_linear_binary_attention_with_dwconv(B, n, d, h):
+    from paper_2306_06446_b200 import attention as A
+    g = ops.rng(7 + n)
+    q, kk, v = (g.standard_normal((B * n, d)).astype(F32) for _ in range(3))
+    dw = (g.standard_normal((3, 3, d)) * 0.1).astype(F32)
+    out = host(A.binary_core(dev(q), dev(kk), dev(v), B, h, dev(dw)))
+    # oracle: the reference AttentionLayer core on the same projections
+    fold = lambda t: ops.heads_split(t.reshape(B, n, d), h).reshape(B * h, n, d // h)  # noqa
+    qf, _ = ops.binary_features(fold(q))
+    kf, _ = ops.binary_features(fold(kk))
+    o = ops.qkv_linear_core(qf, kf, fold(v))
+    merged = ops.heads_merge(o.reshape(B, h, n, d // h)).reshape(B * n, d)
+    merged = merged + np.concatenate([ops.dwconv_tokens(v[i * n:(i + 1) * n], dw) for i in range(B)])
+    assert rel_err(out, merged) < 2e-5
+
+
+def test_hamming_matches_linear_order():
+    from paper_2306_06446_b200 import attention as A
+    g = ops.rng(99)
+    B, n, d, h = 2, 197, 192, 3
+    q, kk, v = (dev(g.standard_normal((B * n, d)).astype(F32)) for _ in range(3))
+    dw = dev((g.standard_normal((3, 3, d)) * 0.1).astype(F32))
+    a = host(A.binary_core(q, kk, v, B, h, dw, order="linear"))
+    b = host(A.binary_core(q, kk, v, B, h, dw, order="quadratic"))
+    assert rel_err(a, b) < 2e-5
+
+
+@pytest.mark.parametrize("dk,n", [(32, 300), (64, 197), (16, 196)])
+def test_popcounts_bit_exact(dk, n):
+    from paper_2306_06446_b200 import attention as A
+    from paper_2306_06446_b200 import quantize as Q
+    g = ops.rng(dk + n)
+    H = 3
+    q = g.standard_normal((H * n, dk)).astype(F32)
+    kk = g.standard_normal((H * n, dk)).astype(F32)
+    cq, _ = Q.sign_hash(dev(q), 1, H)
+    ck, _ = Q.sign_hash(dev(kk), 1, H)
+    cnt, D, S = A.binary_popcounts(cq, ck, dk, with_scores=True)
+    bq = ops.code_bits(q.reshape(H, n, dk)).astype(np.int64)
+    bk = ops.code_bits(kk.reshape(H, n, dk)).astype(np.int64)
+    cnt_ref = bk.sum(axis=1)
+    S_ref = np.einsum("hia,hja->hij", bq, bk)
+    assert np.array_equal(host(cnt), cnt_ref)
+    assert np.array_equal(host(D), np.einsum("hia,ha->hi", bq, cnt_ref))
+    assert np.array_equal(host(S), S_ref)
+    # XOR identity popc(a&b) = (popc a + popc b - popc(a^b)) / 2
+    x = (bq[:, :, None, :] ^ bk[:, None, :, :]).sum(-1)
+    assert np.array_equal(host(S), (bq.sum(-1)[:, :, None] + bk.sum(-1)[:, None, :] - x) // 2)
+
+
+@pytest.mark.parametrize("n", [5, 196, 197])
+def test_dwconv_tokens_golden(golden, n):
+    from paper_2306_06446_b200 import attention as A
+    k = golden("kat")
+    out, side = A._dwconv_tokens(dev(k[f"dw{n}_v"]), dev(k[f"dw{n}_k"]))
+    assert side == int(k[f"dw{n}_side"])
+    assert rel_err(host(out), k[f"dw{n}_y"]) < 1e-6
+
+
+# -------------------------------------------------------------- K3 shift linear
+
+
+def test_quantize_shift_golden_bit_exact(golden):
+    from paper_2306_06446_b200 import quantize as Q
+    k = golden("kat")
+    lay = Q.quantize_shift(dev(k["qs_w"]))
+    assert np.array_equal(host(lay.s), k["qs_s"])
+    assert np.array_equal(host(lay.p), k["qs_p"])
+    rec = host(Q.reconstruct(lay))
+    assert np.array_equal(rec.view(np.uint32), k["qs_rec"].view(np.uint32))
+    packed = ops.pack_shift_codes(k["qs_s"], k["qs_p"])
+    assert np.array_equal(host(lay.packed), packed)
+
+
+@pytest.mark.parametrize("M,K,N", [(37, 48, 24), (802, 32, 256), (1000, 256, 32), (64, 640, 160)])
+@pytest.mark.parametrize("variant", [0, 1])
+def test_shift_linear_vs_oracle(M, K, N, variant):
+    from paper_2306_06446_b200 import quantize as Q
+    g = ops.rng(M + K + N)
+    x = g.uniform(-1, 1, (M, K)).astype(F32)
+    w = (g.standard_normal((K, N)) / np.sqrt(K)).astype(F32)
+    lay = Q.quantize_shift(dev(w))
+    y = host(Q.shift_forward(dev(x), lay, variant=variant))
+    s, p = ops.shift_quantize(w)
+    ref = ops.mm(x, ops.shift_weights(s, p))
+    assert rel_err(y, ref) < 2e-6
+
+
+def test_shift_linear_golden(golden):
+    from paper_2306_06446_b200 import quantize as Q
+    k = golden("kat")
+    lay = Q.ShiftLinear(s=dev(k["sf_s"]), p=dev(k["sf_p"]))
+    for variant in (0, 1):
+        y = host(Q.shift_forward(dev(k["sf_x"]), lay, variant=variant))
+        assert rel_err(y, k["sf_y"]) < 2e-6
+
+
+def test_shift_variants_agree_with_fakeshift_on_device():
+    """Decoded-weight GEMM and literal exponent-add against a dense GEMM on
+    s·exp2(P) built by float multiply (ref tests/test_quantize.py:79-85)."""
+    from paper_2306_06446_b200 import quantize as Q
+    from paper_2306_06446_b200 import tensor as T
+    g = ops.rng(5)
+    x = dev(g.uniform(-1, 1, (256, 64)).astype(F32))
+    lay = Q.quantize_shift(dev(g.uniform(-2, 2, (64, 48)).astype(F32)))
+    fake = (lay.s * torch.exp2(lay.p.float())).contiguous()
+    dense = host(T.matmul(x, fake))
+    assert np.array_equal(host(Q.shift_forward(x, lay, 0)), dense)   # same FFMA core, same order
+    assert rel_err(host(Q.shift_forward(x, lay, 1)), dense) < 2e-6
+
+
+# ------------------------------------------------------------------- K6 GEMM
+
+
+@pytest.mark.parametrize("M,K,N", [(1, 4, 1), (129, 48, 32), (513, 256, 1000), (300, 640, 10)])
+def test_gemm_vs_oracle(M, K, N):
+    from paper_2306_06446_b200 import tensor as T
+    g = ops.rng(M * 7 + N)
+    a = g.standard_normal((M, K)).astype(F32)
+    b = g.standard_normal((K, N)).astype(F32)
+    assert rel_err(host(T.matmul(dev(a), dev(b))), ops.mm(a, b)) < 2e-6
+
+
+# ------------------------------------------------------------ K4 router / plan
+
+
+def test_route_golden_bit_exact(golden):
+    from paper_2306_06446_b200 import moe as MOE
+    k = golden("kat")
+    assert MOE.tie_threshold() == float(k["tie_threshold"])
+    plan, logits = MOE.route_plan(dev(k["rt_x"]), dev(k["rt_wg"]), want_logits=True)
+    assert np.array_equal(host(logits), k["rt_logits"])
+    assert np.array_equal(plan.expert_of, k["rt_expert"])
+    assert np.array_equal(np.concatenate(plan.index_of), k["rt_perm"])
+    assert rel_err(plan.gate_of, k["rt_gate"]) < 1e-6
+
+
+def test_dispatch_ties_golden(golden):
+    from paper_2306_06446_b200 import moe as MOE
+    k = golden("kat")
+    plan = MOE.dispatch(None, dev(k["tie_logits"]))
+    assert np.array_equal(plan.expert_of, k["tie_expert"])
+    assert rel_err(plan.gate_of, k["tie_gate"]) < 1e-6
+
+
+@pytest.mark.parametrize("M,d", [(100_003, 32), (5000, 256), (1, 64), (70_000, 160)])
+def test_route_partition_vs_oracle(M, d):
+    from paper_2306_06446_b200 import moe as MOE
+    g = ops.rng(M + d)
+    x = g.standard_normal((M, d)).astype(F32)
+    wg = (g.standard_normal((d, 2)) * 0.02).astype(F32)
+    plan, logits = MOE.route_plan(dev(x), dev(wg), want_logits=True)
+    p, lg = ops.router_probs(x, wg)
+    e, gate, idx = ops.dispatch_plan(p)
+    assert np.array_equal(host(logits), lg)
+    assert np.array_equal(plan.expert_of, e)
+    assert np.array_equal(np.concatenate(plan.index_of), np.concatenate(idx))
+    assert rel_err(plan.gate_of, gate) < 1e-6
+
+
+def test_route_all_to_one_and_empty_expert():
+    from paper_2306_06446_b200 import moe as MOE
+    x = np.ones((1000, 32), F32)
+    wg = np.zeros((32, 2), F32)
+    wg[:, 1] = 1.0
+    plan, _ = MOE.route_plan(dev(x), dev(wg))
+    assert plan.share(1) == 1.0 and plan.index_of[0].size == 0
+    wg[:, 1] = 0.0   # exact tie everywhere → expert 0
+    plan, _ = MOE.route_plan(dev(x), dev(wg))
+    assert plan.share(0) == 1.0 and np.allclose(plan.gate_of, 0.5)
+
+
+# ----------------------------------------------------------------- K5 experts
+
+
+def _moe_layers(d, out, hidden=None, seed=3):
+    from paper_2306_06446_b200 import model as MD
+    g = ops.rng(seed)
+    wg = (g.standard_normal((d, 2)) * 0.5).astype(F32)   # spread the routes
+    if hidden is None:
+        w = (g.standard_normal((d, out)) / np.sqrt(d)).astype(F32)
+        mod = MD.MoeModule(wg, [MD.Linear(w), MD.ShiftLinearLayer(w.copy())], MD.MoeConfig())
+        s, p = ops.shift_quantize(w)
+        L = {"kind": "moe", "wg": wg, "experts": [{"kind": "dense", "w": w},
+                                                  {"kind": "shift", "w": w, "s": s, "p": p}]}
+    else:
+        w1 = (g.standard_normal((d, hidden)) / np.sqrt(d)).astype(F32)
+        w2 = (g.standard_normal((hidden, d)) / np.sqrt(hidden)).astype(F32)
+        mod = MD.MoeModule(wg, [MD.Mlp(MD.Linear(w1), MD.Linear(w2)),
+                                MD.Mlp(MD.ShiftLinearLayer(w1.copy()),
+                                       MD.ShiftLinearLayer(w2.copy()))], MD.MoeConfig())
+        s1, p1 = ops.shift_quantize(w1)
+        s2, p2 = ops.shift_quantize(w2)
+        L = {"kind": "moe", "wg": wg, "experts": [
+            {"kind": "mlp", "fc1": {"kind": "dense", "w": w1}, "fc2": {"kind": "dense", "w": w2}},
+            {"kind": "mlp", "fc1": {"kind": "shift", "w": w1, "s": s1, "p": p1},
+             "fc2": {"kind": "shift", "w": w2, "s": s2, "p": p2}}]}
+    return mod, L
+
+
+@pytest.mark.parametrize("M,d,hidden", [(3000, 32, None), (3000, 32, 256), (777, 160, 640),
+                                        (4096, 64, 512)])
+def test_moe_module_vs_oracle(M, d, hidden):
+    mod, L = _moe_layers(d, d, hidden)
+    x = ops.rng(M).standard_normal((M, d)).astype(F32)
+    res = ops.rng(M + 1).standard_normal((M, d)).astype(F32)
+    y = host(mod.forward(dev(x), residual=dev(res)))
+    tr = nets.Trace()
+    ref = nets.moe_fwd(L, x, "m", tr)
+    assert np.array_equal(mod.last_plan.expert_of, tr.moe[0]["expert_of"])
+    assert 0.05 < mod.last_plan.share(1) < 0.95
+    assert rel_err(y - res, ref) < 1e-5
+    assert rel_err(y, res + ref) < 1e-5
+
+
+def test_moe_golden(golden):
+    from paper_2306_06446_b200 import model as MD
+    k = golden("kat")
+    w = k["mf_w"]
+    mod = MD.MoeModule(k["mf_wg"], [MD.Linear(w), MD.ShiftLinearLayer(w.copy())], MD.MoeConfig())
+    y = host(mod.forward(dev(k["mf_x"])))
+    assert np.array_equal(mod.last_plan.expert_of, k["mf_expert"])
+    assert rel_err(y, k["mf_y"]) < 1e-5
+
+
+# --------------------------------------------------------------------- glue
+
+
+def test_layernorm_golden(golden):
+    from paper_2306_06446_b200 import tensor as T
+    k = golden("kat")
+    d = k["ln_x"].shape[1]
+    y, _ = T.layernorm(dev(k["ln_x"]), dev(np.ones(d, F32)), dev(np.zeros(d, F32)))
+    assert rel_err(host(y), k["ln_y"]) < 2e-6
+
+
+def test_softmax_core_golden(golden):
+    from paper_2306_06446_b200 import attention as A
+    k = golden("kat")
+    out, _ = A.softmax_core(dev(k["sm_q"]), dev(k["sm_k"]), dev(k["sm_v"]))
+    assert rel_err(host(out), k["sm_out"]) < 2e-6
+
+
+def test_mlp_gelu_vs_oracle(golden):
+    from paper_2306_06446_b200 import model as MD
+    g = ops.rng(1)
+    x = g.standard_normal((999, 64)).astype(F32)
+    w1 = (g.standard_normal((64, 256)) / 8).astype(F32)
+    w2 = (g.standard_normal((256, 64)) / 16).astype(F32)
+    for shift in (False, True):
+        mk = MD.ShiftLinearLayer if shift else MD.Linear
+        mlp = MD.Mlp(mk(w1), mk(w2))
+        y = host(mlp.forward(dev(x)))
+        L1 = {"kind": "dense", "w": w1} if not shift else dict(zip(("kind", "s", "p"), ("shift",) + ops.shift_quantize(w1)))
+        L2 = {"kind": "dense", "w": w2} if not shift else dict(zip(("kind", "s", "p"), ("shift",) + ops.shift_quantize(w2)))
+        ref = nets.linear_fwd({"kind": "mlp", "fc1": L1, "fc2": L2}, x)
+        assert rel_err(y, ref) < 1e-5

@@ -1,0 +1,172 @@
+"""End-to-end parity of the device models against the oracle and the golden
+fixtures produced by the real reference.
+
+fp32 contract: logits within 1e-5 of max|logit|; hash codes and
+router winners bit-exact at every layer when each layer is fed the oracle's
+inputs (teacher forcing), and reported (expected 0) end to end."""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import nets, ops
+from paper_2306_06446_b200 import specs
+
+pytestmark = pytest.mark.gpu
+F32 = np.float32
+LOGIT_TOL = 1e-5
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+def digest(named):
+    h = hashlib.sha256()
+    for name, arr in named:
+        h.update(name.encode())
+        a = arr.detach().cpu().numpy() if isinstance(arr, torch.Tensor) else arr
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+FIXTURES = {
+    "toy_c1": lambda: specs.toy_c1(),
+    "toy_c1_moe": lambda: specs.toy_c1(attn_linear_mode="moe", mlp_mode="moe"),
+    "pvt_small": lambda: specs.pvt_v2_b0(img=64, classes=10),
+    "deit_small": lambda: specs.deit_tiny(img=64, classes=10, depth=3),
+    "pvt_b0_full": lambda: specs.pvt_v2_b0(),
+}
+
+
+def capture_device(model):
+    """Wrap the device model's attention / MoE layers to record codes and plans."""
+    from paper_2306_06446_b200 import attention as A
+    recs = {"codes": {}, "plans": {}}
+    orig = A.binary_core
+
+    def binary_core(q, k, v, batch, heads, dw=None, eps=A.EPS_NORM, order="auto"):
+        from paper_2306_06446_b200 import quantize as Q
+        cq, gq = Q.sign_hash(q, heads, batch)
+        ck, gk = Q.sign_hash(k, heads, batch)
+        recs["codes"].setdefault("q", []).append(q.clone())
+        recs["codes"].setdefault("k", []).append(k.clone())
+        return A.binary_core_codes(cq, ck, gq, gk, v, batch, heads, dw, eps, order)
+    A.binary_core = binary_core
+    return recs, lambda: setattr(A, "binary_core", orig)
+
+
+@pytest.mark.parametrize("name", sorted(FIXTURES))
+def test_model_vs_golden(golden, name):
+    from paper_2306_06446_b200 import model as MD
+    fx = golden(name)
+    spec = FIXTURES[name]()
+    m = MD.Network(spec)
+    assert digest(m.named_weights()) == str(fx["weight_sha256"]), "weights differ from reference"
+    b = int(fx["batch"])
+    images = fx["images"] if "images" in fx else ops.rng(int(fx["images_seed"])).uniform(
+        0, 1, (b, spec["img"], spec["img"], 3)).astype(F32)
+    recs, restore = capture_device(m)
+    try:
+        logits = host(m.forward(dev(images)))
+    finally:
+        restore()
+    assert rel_err(logits, fx["logits"]) < LOGIT_TOL
+    assert np.array_equal(logits.argmax(1), fx["logits"].argmax(1))
+    # end-to-end code / route agreement (fp32 path: expected exact)
+    flips = 0
+    total = 0
+    names = [k[len("codes:"):] for k in fx if k.startswith("codes:")]
+    qs = [n for n in names if n.endswith(".q")]
+    ks = [n for n in names if n.endswith(".k")]
+    for got, key in zip(recs["codes"].get("q", []), qs):
+        bits = np.packbits((~(host(got) < 0)).astype(np.uint8).ravel(), bitorder="little")
+        flips += int(np.unpackbits(bits ^ fx["codes:" + key]).sum())
+        total += bits.size * 8
+    for got, key in zip(recs["codes"].get("k", []), ks):
+        bits = np.packbits((~(host(got) < 0)).astype(np.uint8).ravel(), bitorder="little")
+        flips += int(np.unpackbits(bits ^ fx["codes:" + key]).sum())
+        total += bits.size * 8
+    route_flips = 0
+    for lname, mod in m.moe_modules():
+        bits = np.packbits(mod.last_plan.expert_of.astype(np.uint8), bitorder="little")
+        route_flips += int(np.unpackbits(bits ^ fx["route:" + lname]).sum())
+    assert flips == 0, f"{flips} / {total} code flips"
+    assert route_flips == 0, f"{route_flips} route flips"
+
+
+@pytest.mark.parametrize("name", ["toy_c1_moe", "pvt_small", "deit_small"])
+def test_teacher_forced_layers_bit_exact(golden, name):
+    """Each MoE layer fed the REFERENCE's captured input must reproduce the
+    reference's winners bit-exactly (SURVEY §0.5 tier 1)."""
+    from paper_2306_06446_b200 import moe as MOE
+    fx = golden(name)
+    net = nets.build(FIXTURES[name]())
+    m_inputs = {k[len("moe_x:"):]: v for k, v in fx.items() if k.startswith("moe_x:")}
+    assert m_inputs
+    wg = {}
+    for si, S in enumerate(net["stages"]):
+        for bi, B in enumerate(S["blocks"]):
+            for key in "qkvo":
+                L = B["proj"][key]
+                if L["kind"] == "moe":
+                    wg[f"s{si}.b{bi}.attn.{key}"] = L["wg"]
+            if B["mlp"]["kind"] == "moe":
+                wg[f"s{si}.b{bi}.mlp"] = B["mlp"]["wg"]
+    for lname, x in m_inputs.items():
+        plan, _ = MOE.route_plan(dev(x), dev(wg[lname]))
+        bits = np.packbits(plan.expert_of.astype(np.uint8), bitorder="little")
+        assert np.array_equal(bits, fx["route:" + lname]), lname
+        assert rel_err(plan.gate_of, fx["gate:" + lname]) < 1e-6
+
+
+def test_reference_model_class_api():
+    """`Model(ModelConfig)` holds exactly the reference Model's parameters and
+    runs the same forward (ref model.py:525-577)."""
+    from paper_2306_06446_b200 import model as MD
+    bcs = [MD.BlockConfig(d=64, h=4, mlp_ratio=4.0, attn_mode="linear-binary",
+                          mlp_mode="shift", attn_linear_mode="shift") for _ in range(2)]
+    m = MD.Model(MD.ModelConfig(blocks=bcs, patch=4, img=56, classes=10, seed=0))
+    spec = dict(specs.toy_c1())
+    spec["dw_init"] = "zeros"
+    net = nets.build(spec)
+    assert digest(m.named_weights()) == digest(nets.iter_weights(net))
+    images = ops.rng(1).uniform(0, 1, (4, 56, 56, 3)).astype(F32)
+    assert rel_err(host(m.forward(dev(images))), nets.forward(net, images)) < LOGIT_TOL
+
+
+def test_pvt_b0_full_batch_properties():
+    """PVTv2-B0 at the benchmark batch (256): deterministic, finite, every token
+    routed exactly once, per-image logits independent of batching."""
+    from paper_2306_06446_b200 import model as MD
+    m = MD.pvt_v2_b0()
+    g = ops.rng(11)
+    images = dev(g.uniform(0, 1, (256, 224, 224, 3)).astype(F32))
+    a = m.forward(images)
+    b = m.forward(images)
+    la, lb = host(a), host(b)
+    assert np.isfinite(la).all()
+    assert np.array_equal(la, lb), "forward is not deterministic"
+    for _, mod in m.moe_modules():
+        plan = mod.last_plan
+        seen = np.sort(np.concatenate(plan.index_of))
+        assert np.array_equal(seen, np.arange(plan.expert_of.size))
+    part = host(m.forward(images[:8].contiguous()))
+    assert rel_err(part, la[:8]) < 1e-5
+    # oracle on two of the images
+    net = nets.build(specs.pvt_v2_b0())
+    ref = nets.forward(net, host(images[:2]))
+    assert rel_err(la[:2], ref) < LOGIT_TOL
