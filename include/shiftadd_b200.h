@@ -152,6 +152,40 @@ int sa_moe_mlp(const float* x, const int32_t* perm, const int32_t* counts, const
 int sa_gemm(const float* a, const float* b, float* c, int64_t M, int64_t K, int64_t N,
             void* stream);
 
+/* ---- tensor-core (tcgen05 / TMEM) path, float32-faithful ---------------------
+ * Activations are split into hi+mid+lo bf16 planes (exact); shift weights are
+ * exact in bf16 (1 plane, 3 MMAs per product), dense weights use 3 planes
+ * (6 MMAs per product). Weights are packed once into the shared-memory image
+ * the kernels copy with one bulk async copy per 32-wide K stage. `bn` is the
+ * N tile (32, 64, 128, 160 or 256; sa_tc_tile_n picks it for an N). */
+int sa_tc_tile_n(int64_t N);
+size_t sa_weight_pack_bytes(int64_t K, int64_t N, int w_kind, int bn);
+/* w: float32 (K,N) for SA_W_DENSE or packed shift bytes (K,N) for SA_W_SHIFT */
+int sa_weight_pack(const void* w, int w_kind, int64_t K, int64_t N, int p_min, int bn,
+                   void* out, void* stream);
+/* Linear.forward / ShiftLinearLayer.forward (model.py:104-107, 145-148) */
+int sa_tc_linear(const float* x, const void* wpack, int w_kind, int bn, float* y, int64_t M,
+                 int64_t K, int64_t N, const float* residual, int act, void* stream);
+/* MoeModule.forward with (Linear, ShiftLinearLayer) experts (model.py:250-274, 499-502) */
+int sa_tc_moe_linear(const float* x, const int32_t* perm, const int32_t* counts,
+                     const float* gate, const void* wpack_dense, const void* wpack_shift, int bn,
+                     float* y, const float* residual, int64_t M, int64_t K, int64_t N,
+                     void* stream);
+size_t sa_tc_mlp_workspace(int64_t M, int64_t hidden);
+/* Mlp.forward (model.py:204-208) */
+int sa_tc_mlp(const float* x, const void* w1pack, int w1_kind, int bn1, const void* w2pack,
+              int w2_kind, int bn2, float* y, int64_t M, int64_t d, int64_t hidden,
+              const float* residual, void* ws, size_t ws_bytes, void* stream);
+/* MoeModule.forward with (Mlp(Linear,Linear), Mlp(Shift,Shift)) experts (model.py:514-521) */
+int sa_tc_moe_mlp(const float* x, const int32_t* perm, const int32_t* counts, const float* gate,
+                  const void* w1_dense, const void* w2_dense, const void* w1_shift,
+                  const void* w2_shift, int bn1, int bn2, float* y, const float* residual,
+                  int64_t M, int64_t d, int64_t hidden, void* ws, size_t ws_bytes, void* stream);
+/* patchify (model.py:557-563) + patch-embed Linear on the tensor cores */
+int sa_tc_patch_embed(const float* grid, int64_t B, int64_t H, int64_t W, int64_t C,
+                      int64_t patch, float sub, const void* wpack, int bn, int64_t d,
+                      const float* cls, const float* pos, float* y, void* stream);
+
 /* ---- glue ------------------------------------------------------------------ */
 /* LayerNorm.forward (model.py:174-178 → tensor.layernorm, tensor.py:114-128) */
 int sa_layernorm(const float* x, const float* gain, const float* bias, float* y, int64_t M,

@@ -42,6 +42,43 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict_
   }
 }
 
+// narrow rows (d = 32 / 64): one thread per row, the whole row in registers
+// via 128-bit loads — d/4 independent loads in flight per thread.
+template <int D>
+__global__ void __launch_bounds__(256) layernorm_row_kernel(const float* __restrict__ x,
+                                                           const float* __restrict__ gain,
+                                                           const float* __restrict__ bias,
+                                                           float* __restrict__ y, int64_t M,
+                                                           float eps) {
+  const int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= M) return;
+  const float4* xr = reinterpret_cast<const float4*>(x + row * D);
+  float4 v[D / 4];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < D / 4; ++i) {
+    v[i] = __ldg(xr + i);
+    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+  const float mean = s / float(D);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < D / 4; ++i) {
+    v[i].x -= mean; v[i].y -= mean; v[i].z -= mean; v[i].w -= mean;
+    q += (v[i].x * v[i].x + v[i].y * v[i].y) + (v[i].z * v[i].z + v[i].w * v[i].w);
+  }
+  const float inv = 1.0f / sqrtf(q / float(D) + eps);
+  float4* yr = reinterpret_cast<float4*>(y + row * D);
+  const float4* g4 = reinterpret_cast<const float4*>(gain);
+  const float4* b4 = reinterpret_cast<const float4*>(bias);
+#pragma unroll
+  for (int i = 0; i < D / 4; ++i) {
+    const float4 g = __ldg(g4 + i), bb = __ldg(b4 + i);
+    yr[i] = make_float4(v[i].x * inv * g.x + bb.x, v[i].y * inv * g.y + bb.y,
+                        v[i].z * inv * g.z + bb.z, v[i].w * inv * g.w + bb.w);
+  }
+}
+
 // softmax attention per (image, head) (ref attention.py:92-97): K (padded) and
 // V of the head in shared memory, one warp per query row, lanes over keys for
 // the scores and over channels for P·V.
@@ -140,8 +177,16 @@ extern "C" int sa_layernorm(const float* x, const float* gain, const float* bias
   SA_REQUIRE(M >= 0 && d > 0 && d <= 1024, SA_ERR_SHAPE, "sa_layernorm: d=%lld unsupported",
              (long long)d);
   if (M == 0) return SA_OK;
-  const unsigned grid = unsigned(cdiv(M, 8));
   cudaStream_t s = as_stream(stream);
+  if (d == 32 || d == 64) {
+    const unsigned g = unsigned(cdiv(M, 256));
+    if (d == 32) layernorm_row_kernel<32><<<g, 256, 0, s>>>(x, gain, bias, y, M, eps);
+    else layernorm_row_kernel<64><<<g, 256, 0, s>>>(x, gain, bias, y, M, eps);
+    count_launch(1);
+    SA_LAUNCH_CHECK("sa_layernorm");
+    return SA_OK;
+  }
+  const unsigned grid = unsigned(cdiv(M, 8));
   const int per = int(cdiv(d, 32));
   if (per <= 1) layernorm_kernel<1><<<grid, 256, 0, s>>>(x, gain, bias, y, M, int(d), eps);
   else if (per <= 2) layernorm_kernel<2><<<grid, 256, 0, s>>>(x, gain, bias, y, M, int(d), eps);

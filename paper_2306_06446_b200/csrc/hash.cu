@@ -99,6 +99,78 @@ __global__ void __launch_bounds__(kHashThreads) sign_hash_kernel(
   }
 }
 
+// Fast path for d dividing 1024 (d = 32, 64, 128, 256, 512): the CTA's token
+// chunk is one contiguous run of float4s; thread t always lands on channels
+// 4t mod d, so |x| accumulates in four registers, and every warp-load covers
+// whole 32-channel words (8-lane OR butterfly). All 32 lanes are busy for
+// every d, each thread keeps d/4 independent 128-bit loads in flight.
+constexpr int kStreamTok = 256;
+
+template <int D>
+__global__ void __launch_bounds__(kHashThreads) sign_hash_stream_kernel(
+    const float* __restrict__ x, int n, int heads, int dk, int W, int chunks,
+    uint32_t* __restrict__ codes, double* __restrict__ partial) {
+  constexpr int DW = D / 32;
+  __shared__ uint32_t sm_codes[kStreamTok * DW];
+  __shared__ double red[kHashThreads];
+  const int b = blockIdx.y, chunk = blockIdx.x;
+  const int t0 = chunk * kStreamTok;
+  const int rows = min(kStreamTok, n - t0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float4* src = reinterpret_cast<const float4*>(x + (size_t(b) * n + t0) * D);
+  const int nf4 = rows * (D / 4);
+  const int c = (4 * tid) % D;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  // the loop bound is CTA-uniform, so every lane reaches the shuffles; nf4 is a
+  // multiple of 8 (D/4 >= 8), so an 8-lane word group is either fully active
+  // or fully past the end (and then never stored).
+  for (int base = 0; base < nf4; base += kHashThreads) {
+    const int f = base + tid;
+    const bool act = f < nf4;
+    const float4 v = act ? __ldg(src + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+    a0 += fabsf(v.x);
+    a1 += fabsf(v.y);
+    a2 += fabsf(v.z);
+    a3 += fabsf(v.w);
+    uint32_t nib = uint32_t(!(v.x < 0.f)) | (uint32_t(!(v.y < 0.f)) << 1) |
+                   (uint32_t(!(v.z < 0.f)) << 2) | (uint32_t(!(v.w < 0.f)) << 3);
+    uint32_t w = nib << (4 * (lane & 7));
+    w |= __shfl_xor_sync(0xffffffffu, w, 1);
+    w |= __shfl_xor_sync(0xffffffffu, w, 2);
+    w |= __shfl_xor_sync(0xffffffffu, w, 4);
+    if (act && (lane & 7) == 0) {
+      const int r = (4 * f) / D;
+      sm_codes[r * DW + c / 32] = w;
+    }
+  }
+  red[tid] = double(a0) + double(a1) + double(a2) + double(a3);
+  __syncthreads();
+
+  const int total = heads * rows * W;
+  for (int idx = tid; idx < total; idx += kHashThreads) {
+    const int wi = idx % W;
+    const int r = (idx / W) % rows;
+    const int h = idx / (W * rows);
+    uint32_t word;
+    if (dk >= 32) {
+      word = sm_codes[r * DW + h * (dk >> 5) + wi];
+    } else {
+      const int bit0 = h * dk;
+      word = (sm_codes[r * DW + (bit0 >> 5)] >> (bit0 & 31)) & ((1u << dk) - 1u);
+    }
+    codes[((size_t(b) * heads + h) * n + t0 + r) * W + wi] = word;
+  }
+  // per head: fixed-order sum over the threads whose 4 channels lie in the head
+  // (dk >= 4 so a thread's channels never straddle two heads)
+  for (int h = warp; h < heads; h += kHashThreads / 32) {
+    double s = 0.0;
+    for (int j = lane; j < kHashThreads; j += 32)
+      if (((4 * j) % D) / dk == h) s += red[j];
+    s = warp_sum(s);
+    if (lane == 0) partial[(size_t(b) * chunks + chunk) * heads + h] = s;
+  }
+}
+
 __global__ void gamma_finalize_kernel(const double* __restrict__ partial, int BH, int heads,
                                       int chunks, double inv_count, float* __restrict__ gamma) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -133,27 +205,44 @@ extern "C" int sa_sign_hash(const float* x, int64_t B, int64_t n, int64_t d, int
   SA_REQUIRE(ws_bytes >= sa_sign_hash_workspace(B, n, d, heads), SA_ERR_VALUE,
              "sa_sign_hash: workspace too small");
   const int W = int(cdiv(dk, 32));
-  const int chunks = int(cdiv(n, kTokPerCta));
-  const size_t smem = size_t(kTokPerCta) * (d / 32) * 4 + size_t(kHashThreads / 32) * d * 4;
-  dim3 grid(chunks, unsigned(B));
   double* partial = static_cast<double*>(ws);
   cudaStream_t s = as_stream(stream);
-  const int nblk = int(cdiv(d, 128));
-  switch (nblk) {
-    case 1:
-      sign_hash_kernel<1><<<grid, kHashThreads, smem, s>>>(x, int(n), int(d), int(heads), int(dk),
-                                                          W, chunks, codes, partial);
-      break;
-    case 2:
-      sign_hash_kernel<2><<<grid, kHashThreads, smem, s>>>(x, int(n), int(d), int(heads), int(dk),
-                                                          W, chunks, codes, partial);
-      break;
-    default:
-      cudaFuncSetAttribute(sign_hash_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(smem));
-      sign_hash_kernel<4><<<grid, kHashThreads, smem, s>>>(x, int(n), int(d), int(heads), int(dk),
-                                                          W, chunks, codes, partial);
-      break;
+  int chunks;
+  if (1024 % d == 0) {
+    chunks = int(cdiv(n, kStreamTok));
+    dim3 grid(chunks, unsigned(B));
+#define SA_HASH_STREAM(DV)                                                                \
+  case DV:                                                                                \
+    sign_hash_stream_kernel<DV><<<grid, kHashThreads, 0, s>>>(x, int(n), int(heads), int(dk), \
+                                                              W, chunks, codes, partial); \
+    break;
+    switch (d) {
+      SA_HASH_STREAM(32)
+      SA_HASH_STREAM(64)
+      SA_HASH_STREAM(128)
+      SA_HASH_STREAM(256)
+      SA_HASH_STREAM(512)
+    }
+#undef SA_HASH_STREAM
+  } else {
+    chunks = int(cdiv(n, kTokPerCta));
+    const size_t smem = size_t(kTokPerCta) * (d / 32) * 4 + size_t(kHashThreads / 32) * d * 4;
+    dim3 grid(chunks, unsigned(B));
+    const int nblk = int(cdiv(d, 128));
+    switch (nblk) {
+      case 1:
+        sign_hash_kernel<1><<<grid, kHashThreads, smem, s>>>(x, int(n), int(d), int(heads),
+                                                            int(dk), W, chunks, codes, partial);
+        break;
+      case 2:
+        sign_hash_kernel<2><<<grid, kHashThreads, smem, s>>>(x, int(n), int(d), int(heads),
+                                                            int(dk), W, chunks, codes, partial);
+        break;
+      default:
+        sign_hash_kernel<4><<<grid, kHashThreads, smem, s>>>(x, int(n), int(d), int(heads),
+                                                            int(dk), W, chunks, codes, partial);
+        break;
+    }
   }
   const int BH = int(B * heads);
   gamma_finalize_kernel<<<int(cdiv(BH, 256)), 256, 0, s>>>(partial, BH, int(heads), chunks,

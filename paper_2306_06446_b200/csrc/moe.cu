@@ -56,32 +56,51 @@ __global__ void __launch_bounds__(kRouteTok) dispatch_kernel(const float* __rest
   }
 }
 
+// logits + decision: G threads per token (G = 1 for d <= 64, else 8), each
+// thread streams its slice of the row with 128-bit loads and fp64 FMAs; the G
+// partial sums meet in a fixed xor-shuffle tree (deterministic).
+template <int G>
 __global__ void __launch_bounds__(256) route_kernel(const float* __restrict__ x,
                                                    const float* __restrict__ wg, int64_t M, int d,
                                                    float tie_thresh, float* __restrict__ logits,
                                                    int32_t* __restrict__ expert_of,
                                                    float* __restrict__ gate,
                                                    int32_t* __restrict__ block_cnt1) {
+  constexpr int TPP = 256 / G;  // tokens per pass
   __shared__ double sw[2 * 512];
   __shared__ int wcnt[8];
   for (int i = threadIdx.x; i < 2 * d; i += blockDim.x) sw[i] = double(wg[i]);
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = threadIdx.x % G, slot = threadIdx.x / G;
   const int64_t base = int64_t(blockIdx.x) * kRouteTok;
+  const int d4 = d >> 2;
   int mine = 0;
-  for (int r = warp; r < kRouteTok; r += 8) {
-    const int64_t t = base + r;
-    if (t >= M) break;
-    const float* row = x + t * d;
+#pragma unroll 1
+  for (int pass = 0; pass < G; ++pass) {
+    const int64_t t = base + pass * TPP + slot;
+    const bool ok = t < M;
     double s0 = 0.0, s1 = 0.0;
-    for (int c = lane; c < d; c += 32) {
-      const double xv = double(row[c]);
-      s0 = fma(xv, sw[2 * c], s0);
-      s1 = fma(xv, sw[2 * c + 1], s1);
+    if (ok) {
+      const float4* row = reinterpret_cast<const float4*>(x + t * d);
+      for (int c4 = sub; c4 < d4; c4 += G) {
+        const float4 v = __ldg(row + c4);
+        const double* w = sw + 8 * c4;
+        s0 = fma(double(v.x), w[0], s0);
+        s1 = fma(double(v.x), w[1], s1);
+        s0 = fma(double(v.y), w[2], s0);
+        s1 = fma(double(v.y), w[3], s1);
+        s0 = fma(double(v.z), w[4], s0);
+        s1 = fma(double(v.z), w[5], s1);
+        s0 = fma(double(v.w), w[6], s0);
+        s1 = fma(double(v.w), w[7], s1);
+      }
     }
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
-    if (lane == 0) {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (ok && sub == 0) {
       const float l0 = float(s0), l1 = float(s1);
       float g;
       const int e = decide(l0, l1, tie_thresh, g);
@@ -94,7 +113,8 @@ __global__ void __launch_bounds__(256) route_kernel(const float* __restrict__ x,
       mine += e;
     }
   }
-  if (lane == 0) wcnt[warp] = mine;
+  mine = __reduce_add_sync(0xffffffffu, mine);
+  if ((threadIdx.x & 31) == 0) wcnt[threadIdx.x >> 5] = mine;
   __syncthreads();
   if (threadIdx.x == 0) {
     int c = 0;
@@ -188,8 +208,8 @@ extern "C" int sa_moe_route(const float* x, const float* wg, int64_t M, int64_t 
                             float tie_thresh, float* logits, int32_t* expert_of, float* gate,
                             int32_t* counts, int32_t* perm, void* ws, size_t ws_bytes,
                             void* stream) {
-  SA_REQUIRE(M >= 0 && d > 0 && d <= 512, SA_ERR_SHAPE, "sa_moe_route: d=%lld unsupported",
-             (long long)d);
+  SA_REQUIRE(M >= 0 && d > 0 && d <= 512 && d % 4 == 0, SA_ERR_SHAPE,
+             "sa_moe_route: d=%lld unsupported", (long long)d);
   SA_REQUIRE(M < (int64_t(1) << 31), SA_ERR_SHAPE, "sa_moe_route: too many tokens");
   SA_REQUIRE(ws_bytes >= sa_moe_route_workspace(M), SA_ERR_VALUE,
              "sa_moe_route: workspace too small");
@@ -201,8 +221,12 @@ extern "C" int sa_moe_route(const float* x, const float* wg, int64_t M, int64_t 
   const int nb = int(cdiv(M, kRouteTok));
   int32_t* block_cnt1 = static_cast<int32_t*>(ws);
   int32_t* block_off1 = block_cnt1 + nb;
-  route_kernel<<<nb, 256, 0, s>>>(x, wg, M, int(d), tie_thresh, logits, expert_of, gate,
-                                  block_cnt1);
+  if (d <= 64)
+    route_kernel<1><<<nb, 256, 0, s>>>(x, wg, M, int(d), tie_thresh, logits, expert_of, gate,
+                                       block_cnt1);
+  else
+    route_kernel<8><<<nb, 256, 0, s>>>(x, wg, M, int(d), tie_thresh, logits, expert_of, gate,
+                                       block_cnt1);
   route_scan_kernel<<<1, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
   partition_kernel<<<nb, kRouteTok, 0, s>>>(expert_of, block_off1, counts, M, perm);
   count_launch(3);

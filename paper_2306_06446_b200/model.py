@@ -15,6 +15,7 @@ reference `Model(cfg)`'s parameters.
 
 from __future__ import annotations
 
+import os
 from dataclasses import asdict, dataclass
 from typing import List, Optional
 
@@ -102,6 +103,25 @@ def _no_train(train):
         raise NotImplementedError("this package implements the inference path only")
 
 
+# GEMM engine: "tc" = tcgen05 tensor cores with float32-faithful split-bf16
+# operands (default); "simt" = the CUDA-core FFMA path (kept for A/B checks).
+GEMM_ENGINE = os.environ.get("SA_GEMM", "tc")
+
+
+def tc_enabled() -> bool:
+    return GEMM_ENGINE == "tc"
+
+
+def _pack_weight(w, kind, K, N, p_min):
+    """Pack a (K, N) weight into the tensor-core shared-memory image (K3/K6)."""
+    lib = _lib.load()
+    bn = int(lib.sa_tc_tile_n(N))
+    out = torch.empty(int(lib.sa_weight_pack_bytes(K, N, kind, bn)), dtype=torch.uint8,
+                      device=w.device)
+    _lib.call("sa_weight_pack", _lib.ptr(w), kind, K, N, p_min, bn, _lib.ptr(out), _lib.stream())
+    return out, bn
+
+
 def _stream():
     return _lib.stream()
 
@@ -128,6 +148,13 @@ class Linear:
 
     def weight_arg(self):
         return self.w.value, _lib.SA_W_DENSE, Q.P_MIN_DEFAULT
+
+    def tc_pack(self):
+        """(packed planes, bn, kind) for the tensor-core path, built once."""
+        if getattr(self, "_tc", None) is None:
+            pk, bn = _pack_weight(self.w.value, _lib.SA_W_DENSE, self.in_dim, self.out_dim, -15)
+            self._tc = (pk, bn, _lib.SA_W_DENSE)
+        return self._tc
 
     def forward(self, x, train=False, residual=None, act=0):
         _no_train(train)
@@ -156,6 +183,14 @@ class ShiftLinearLayer:
 
     def requantize(self):
         self.quant = Q.quantize_shift(self.w.value, self.quant_cfg)
+        self._tc = None
+
+    def tc_pack(self):
+        if getattr(self, "_tc", None) is None:
+            pk, bn = _pack_weight(self.quant.packed, _lib.SA_W_SHIFT, self.in_dim, self.out_dim,
+                                  self.quant.p_min)
+            self._tc = (pk, bn, _lib.SA_W_SHIFT)
+        return self._tc
 
     @property
     def in_dim(self):
@@ -189,9 +224,14 @@ def _linear_call(layer, x, residual, act):
     x2 = x.reshape(-1, x.shape[-1])
     if x2.shape[1] != layer.in_dim:
         raise ShapeError(f"input extent {x2.shape[1]} != layer in_dim {layer.in_dim}")
-    w, kind, p_min = layer.weight_arg()
     y = torch.empty((x2.shape[0], layer.out_dim), dtype=torch.float32, device=x.device)
     res = residual.reshape(y.shape) if residual is not None else None
+    if tc_enabled():
+        pk, bn, kind = layer.tc_pack()
+        _lib.call("sa_tc_linear", _lib.ptr(x2), _lib.ptr(pk), kind, bn, _lib.ptr(y), x2.shape[0],
+                  layer.in_dim, layer.out_dim, _lib.ptr(res), int(act), _stream())
+        return y.reshape(*lead, layer.out_dim)
+    w, kind, p_min = layer.weight_arg()
     _lib.call("sa_linear", _lib.ptr(x2), _lib.ptr(w), kind, _lib.ptr(y), x2.shape[0],
               layer.in_dim, layer.out_dim, p_min, _lib.ptr(res), int(act), _stream())
     return y.reshape(*lead, layer.out_dim)
@@ -245,8 +285,15 @@ class Mlp:
             raise ValueError("fc1/fc2 shift layers must share p_min")
         p_min = pm1 if k1 == _lib.SA_W_SHIFT else pm2
         y = torch.empty((M, self.fc2.out_dim), dtype=torch.float32, device=x.device)
-        ws = _lib.Workspace.get(_lib.load().sa_mlp_workspace(M, hidden), slot=3)
         res = residual.reshape(y.shape) if residual is not None else None
+        if tc_enabled():
+            p1, bn1, k1 = self.fc1.tc_pack()
+            p2, bn2, k2 = self.fc2.tc_pack()
+            ws = _lib.Workspace.get(_lib.load().sa_tc_mlp_workspace(M, hidden), slot=3)
+            _lib.call("sa_tc_mlp", _lib.ptr(x2), _lib.ptr(p1), k1, bn1, _lib.ptr(p2), k2, bn2,
+                      _lib.ptr(y), M, d, hidden, _lib.ptr(res), _lib.ptr(ws), ws.numel(), _stream())
+            return y.reshape(*lead, self.fc2.out_dim)
+        ws = _lib.Workspace.get(_lib.load().sa_mlp_workspace(M, hidden), slot=3)
         _lib.call("sa_mlp", _lib.ptr(x2), _lib.ptr(w1), k1, _lib.ptr(w2), k2, _lib.ptr(y), M, d,
                   hidden, p_min, _lib.ptr(res), _lib.ptr(ws), ws.numel(), _stream())
         return y.reshape(*lead, self.fc2.out_dim)
@@ -278,6 +325,14 @@ def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None):
         if (e1.in_dim, e1.out_dim) != (K, N):
             return None
         y = torch.empty((M, N), dtype=torch.float32, device=x.device)
+        if tc_enabled():
+            pd, bn, _ = e0.tc_pack()
+            ps, bn_s, _ = e1.tc_pack()
+            assert bn == bn_s
+            _lib.call("sa_tc_moe_linear", _lib.ptr(x), _lib.ptr(plan.perm_dev),
+                      _lib.ptr(plan.counts_dev), _lib.ptr(plan.gate_dev), _lib.ptr(pd), _lib.ptr(ps),
+                      bn, _lib.ptr(y), _lib.ptr(res), M, K, N, _stream())
+            return y
         _lib.call("sa_moe_linear", _lib.ptr(x), _lib.ptr(plan.perm_dev), _lib.ptr(plan.counts_dev),
                   _lib.ptr(plan.gate_dev), _lib.ptr(e0.w.value), _lib.ptr(e1.quant.packed),
                   e1.quant.p_min, _lib.ptr(y), _lib.ptr(res), M, K, N, _stream())
@@ -289,6 +344,17 @@ def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None):
         if e1.fc1.quant.p_min != e1.fc2.quant.p_min:
             return None
         y = torch.empty((M, d), dtype=torch.float32, device=x.device)
+        if tc_enabled():
+            p1d, bn1, _ = e0.fc1.tc_pack()
+            p2d, bn2, _ = e0.fc2.tc_pack()
+            p1s, _, _ = e1.fc1.tc_pack()
+            p2s, _, _ = e1.fc2.tc_pack()
+            ws = _lib.Workspace.get(_lib.load().sa_tc_mlp_workspace(M, hidden), slot=3)
+            _lib.call("sa_tc_moe_mlp", _lib.ptr(x), _lib.ptr(plan.perm_dev),
+                      _lib.ptr(plan.counts_dev), _lib.ptr(plan.gate_dev), _lib.ptr(p1d),
+                      _lib.ptr(p2d), _lib.ptr(p1s), _lib.ptr(p2s), bn1, bn2, _lib.ptr(y),
+                      _lib.ptr(res), M, d, hidden, _lib.ptr(ws), ws.numel(), _stream())
+            return y
         ws = _lib.Workspace.get(_lib.load().sa_moe_mlp_workspace(M, hidden), slot=3)
         _lib.call("sa_moe_mlp", _lib.ptr(x), _lib.ptr(plan.perm_dev), _lib.ptr(plan.counts_dev),
                   _lib.ptr(plan.gate_dev), _lib.ptr(e0.fc1.w.value), _lib.ptr(e0.fc2.w.value),
@@ -596,11 +662,18 @@ class Network:
         tok = None
         for S in self.stages:
             tok = torch.empty((B * S.rows, S.d), dtype=torch.float32, device=x.device)
-            _lib.call("sa_patch_embed", _lib.ptr(grid), B, H, W, C, S.patch, sub,
-                      _lib.ptr(S.patch_embed.w.value), S.d,
-                      _lib.ptr(S.cls.value if S.cls is not None else None),
-                      _lib.ptr(S.pos.value if S.pos is not None else None), _lib.ptr(tok),
-                      _stream())
+            if tc_enabled():
+                pk, bn, _ = S.patch_embed.tc_pack()
+                _lib.call("sa_tc_patch_embed", _lib.ptr(grid), B, H, W, C, S.patch, sub, _lib.ptr(pk),
+                          bn, S.d, _lib.ptr(S.cls.value if S.cls is not None else None),
+                          _lib.ptr(S.pos.value if S.pos is not None else None), _lib.ptr(tok),
+                          _stream())
+            else:
+                _lib.call("sa_patch_embed", _lib.ptr(grid), B, H, W, C, S.patch, sub,
+                          _lib.ptr(S.patch_embed.w.value), S.d,
+                          _lib.ptr(S.cls.value if S.cls is not None else None),
+                          _lib.ptr(S.pos.value if S.pos is not None else None), _lib.ptr(tok),
+                          _stream())
             if S.embed_ln is not None:
                 tok = S.embed_ln.forward(tok)
             t3 = tok.reshape(B, S.rows, S.d)

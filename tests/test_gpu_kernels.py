@@ -79,9 +79,13 @@ def test_binary_core_matches_golden(golden, dk, order):
     pre = f"lc{dk}_"
     q, kk, v = k[pre + "q"], k[pre + "k"], k[pre + "v"]
     H, n, _ = q.shape
-    flat = lambda t: dev(t.reshape(H * n, dk))  # noqa: E731  each head = one image
-    out = A.binary_core(flat(q), flat(kk), flat(v), H, 1, None, A.EPS_NORM, order)
-    got = host(out).reshape(H, n, dk)
+    g = max(1, 32 // dk)          # heads per 'image' so rows are >= 32 channels wide
+    nb = H // g
+
+    def flat(t):                  # (H, n, dk) → (nb*n, g*dk), heads as channel blocks
+        return dev(ops.heads_merge(t.reshape(nb, g, n, dk)).reshape(nb * n, g * dk))
+    out = A.binary_core(flat(q), flat(kk), flat(v), nb, g, None, A.EPS_NORM, order)
+    got = ops.heads_split(host(out).reshape(nb, n, g * dk), g).reshape(H, n, dk)
     assert rel_err(got, k[pre + "out"]) < 1e-5
     assert np.all(got[0, 3] == 0)   # all-negative query row → exactly zero
 
