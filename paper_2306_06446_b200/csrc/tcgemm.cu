@@ -4,21 +4,28 @@
 // Precision: every float32 activation is split into hi+mid+lo bf16 planes
 // (exact: 3 × 8 significant bits = the 24-bit float32 significand). Shift
 // weights s·2^P are EXACT in bf16 (one plane), so a shift-Linear needs three
-// bf16 MMAs and every product is exact — the result equals the float32 sum of
-// exact products (ref tests/test_quantize.py:79-85 asks for exactly that).
-// Dense (mult-expert) weights are split the same way and six plane products
-// (hh, hm, mh, hl, mm, lh) are accumulated, dropping only terms below 2^-24
-// relative. Accumulation is float32 in TMEM.
+// bf16 MMAs and every product is exact (ref tests/test_quantize.py:79-85 asks
+// for the FakeShift product). Dense (mult-expert) weights are split the same
+// way and six plane products (lh, mm, hl, mh, hm, hh) are accumulated,
+// dropping only terms below 2^-24 relative. Accumulation is float32 in TMEM.
 //
-// Kernel: one 128-row output tile per CTA (4 warps). Per 32-wide K stage:
-// thread 0 pulls the pre-packed weight planes into shared memory with one
-// bulk async copy (TMA engine, mbarrier complete_tx) while all 128 threads
-// gather their A row (plain / MoE-permuted / patchified image), split it and
-// store the three planes in the UMMA canonical layout; one elected thread then
-// issues the tcgen05.mma chain and commits to an mbarrier. The epilogue reads
-// the accumulator with tcgen05.ld (thread = row) and applies GELU / ×gate /
-// +residual / +pos / row scatter before the store. Several CTAs per SM overlap
-// one tile's epilogue with another tile's MMAs.
+// Kernel (persistent, warp-specialized, one CTA per SM, 288 threads):
+//   warps 4-7  producers: per 32-wide K stage, gather their 128 A rows with
+//              coalesced 128-bit loads (plain / MoE-permuted / patchified
+//              image), split to bf16 planes, store them in the UMMA canonical
+//              layout; lane 0 of warp 4 pulls the pre-packed weight planes of
+//              the stage with ONE bulk async copy (TMA engine, complete_tx).
+//   warp 8     MMA issuer: one elected thread chains tcgen05.mma into a
+//              double-buffered TMEM accumulator and commits to mbarriers.
+//   warps 0-3  epilogue: tcgen05.ld (thread = accumulator row), GELU / ×gate,
+//              transpose through shared memory so every store (and residual /
+//              position-embedding load) is a coalesced row segment, scatter
+//              the MoE rows back to token order.
+// A ring of S shared-memory stages (full/empty mbarriers) and two TMEM
+// accumulators (tfull/tempty) let loads, MMAs and epilogues of successive
+// tiles overlap. The tile list is a static stride over (m-tile, n-tile);
+// with MoE grouping the m-tiles of each expert are derived from the device
+// counts, so nothing syncs the host (CUDA-graph capturable).
 //
 // Weight packing (sa_weight_pack): for n-tile nt, K stage kc, plane p the
 // packed image is the exact shared-memory layout (see tc_common.cuh), so a
@@ -28,9 +35,10 @@
 namespace sa {
 namespace tc {
 
-constexpr int kThreads = 128;
 constexpr int kBM = 128;
+constexpr int kThreads = 288;
 constexpr uint32_t kPlaneA = kBM * kBK * 2;  // bytes per A plane
+constexpr int kXPitch = 33;                   // transpose buffer pitch (floats)
 
 enum AMode { A_PLAIN = 0, A_GATHER = 1, A_PATCH = 2 };
 
@@ -44,6 +52,8 @@ struct TcParams {
   int nplanes[2];
   int64_t M, K, N;
   int kchunks;
+  int ntiles;
+  int stages;
   const int32_t* counts;
   float* C;
   const int32_t* c_rows;
@@ -56,178 +66,284 @@ struct TcParams {
 };
 
 template <int BN>
-struct TmemCols {
-  static constexpr uint32_t value = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+struct TmemCols {  // two accumulator buffers, power of two >= 32
+  static constexpr uint32_t value = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
+                                    : 2 * BN <= 256 ? 256 : 512;
 };
 
+struct TileInfo {
+  int group;
+  int64_t r0, r1;
+  int n_tile;
+};
+
+// m-tiles: with grouping, expert 0 owns ceil(c0/128) tiles, expert 1 the rest
+__device__ __forceinline__ int64_t num_m_tiles(const TcParams& p, int64_t c0) {
+  if (!p.counts) return (p.M + kBM - 1) / kBM;
+  return (c0 + kBM - 1) / kBM + (p.M - c0 + kBM - 1) / kBM;
+}
+__device__ __forceinline__ TileInfo tile_info(const TcParams& p, int64_t c0, int64_t t) {
+  TileInfo ti;
+  const int64_t m = t / p.ntiles;
+  ti.n_tile = int(t % p.ntiles);
+  if (!p.counts) {
+    ti.group = 0;
+    ti.r0 = m * kBM;
+    ti.r1 = min(p.M, ti.r0 + kBM);
+    return ti;
+  }
+  const int64_t t0 = (c0 + kBM - 1) / kBM;
+  if (m < t0) {
+    ti.group = 0;
+    ti.r0 = m * kBM;
+    ti.r1 = min(c0, ti.r0 + kBM);
+  } else {
+    ti.group = 1;
+    ti.r0 = c0 + (m - t0) * kBM;
+    ti.r1 = min(p.M, ti.r0 + kBM);
+  }
+  return ti;
+}
+
+__device__ __forceinline__ float gelu_fast(float x) {
+  // 0.5·x·(1 + tanh(u)) == x / (1 + exp(-2u)); ex2.approx + fast divide keep
+  // ~1e-7 relative accuracy (the reference's tanh is itself a float32 libm call)
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  const float u = c * (x + a * (x * x * x));
+  return __fdividef(x, 1.0f + __expf(-2.0f * u));
+}
+
 template <int BN, int AM>
-__global__ void __launch_bounds__(kThreads) tc_gemm_kernel(TcParams p) {
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + 3 * kPlaneA;
-  __shared__ __align__(8) uint64_t bar_b;
-  __shared__ __align__(8) uint64_t bar_mma;
-  __shared__ uint32_t tmem_slot;
   constexpr uint32_t TCOLS = TmemCols<BN>::value;
   constexpr uint32_t kPlaneB = BN * kBK * 2;
-
-  // ---- tile scheduling (MoE grouping reads the device-side counts) ----
-  int group = 0;
-  int64_t r0, r1;
-  if (p.counts) {
-    const int64_t c0 = p.counts[0];
-    const int64_t t0 = (c0 + kBM - 1) / kBM;
-    if (blockIdx.x < t0) {
-      r0 = int64_t(blockIdx.x) * kBM;
-      r1 = min(c0, r0 + kBM);
-    } else {
-      group = 1;
-      r0 = c0 + (int64_t(blockIdx.x) - t0) * kBM;
-      r1 = min(p.M, r0 + kBM);
-    }
-  } else {
-    r0 = int64_t(blockIdx.x) * kBM;
-    r1 = min(p.M, r0 + kBM);
-  }
-  if (r0 >= r1) return;  // uniform for the whole CTA, before any TMEM use
+  const int S = p.stages;
+  const int npb_max = max(p.nplanes[0], p.counts ? p.nplanes[1] : 0);
+  const uint32_t stage_bytes = 3 * kPlaneA + uint32_t(npb_max) * kPlaneB;
+  float* xbuf = reinterpret_cast<float*>(smem + size_t(S) * stage_bytes);      // [4][32][33]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xbuf + 4 * 32 * kXPitch);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* tfull = bars + 2 * S;
+  uint64_t* tempty = bars + 2 * S + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (warp == 0) tmem_alloc<TCOLS>(&tmem_slot);
+  if (warp == 8) tmem_alloc<TCOLS>(tmem_slot);
   if (tid == 0) {
-    mbar_init(&bar_b, 1);
-    mbar_init(&bar_mma, 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 4);     // four producer warps
+      mbar_init(&empty[s], 1);    // one MMA commit
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);    // one MMA commit
+      mbar_init(&tempty[b], 128); // every epilogue thread
+    }
     fence_barrier_init();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tmem_slot;
+  const uint32_t tmem = *tmem_slot;
+  const int64_t c0 = p.counts ? int64_t(p.counts[0]) : 0;
+  const int64_t total = num_m_tiles(p, c0) * p.ntiles;
 
-  // ---- A row source ----
-  const int64_t arow = r0 + tid;
-  const bool a_ok = arow < r1;
-  const float* abase = nullptr;
-  int64_t prs = 0;
-  if (a_ok) {
-    if (AM == A_PLAIN) {
-      abase = p.A + arow * p.lda;
-    } else if (AM == A_GATHER) {
-      abase = p.A + int64_t(p.a_rows[arow]) * p.lda;
-    } else {
-      const int64_t tpi = p.pside * p.pside;
-      const int64_t b = arow / tpi, t = arow % tpi;
-      const int64_t py = t / p.pside, px = t % p.pside;
-      abase = p.A + ((b * p.pH + py * p.patch) * p.pW + px * p.patch) * p.pC;
-      prs = p.pW * p.pC;
-    }
-  }
-  const int64_t pcw = p.patch * p.pC;
-  const int npb = p.nplanes[group];
-  const int64_t n_tile = blockIdx.y;
-  const uint16_t* Bg = p.Bp[group] + size_t(n_tile) * p.kchunks * npb * (BN * kBK);
-  const uint32_t bbytes = uint32_t(npb) * kPlaneB;
-  constexpr uint32_t idesc = idesc_bf16_m128(BN);
-  // plane products: shift (1 B plane) → (0,0),(1,0),(2,0); dense → 6 terms
-  const int npairs = npb == 1 ? 3 : 6;
-  const uint8_t pa_tab[6] = {2, 1, 0, 1, 0, 0};
-  const uint8_t pb_dense[6] = {0, 1, 2, 0, 1, 0};
-
-  const uint32_t sA_u32 = smem_u32(sA), sB_u32 = smem_u32(sB);
-  for (int kc = 0; kc < p.kchunks; ++kc) {
-    const uint32_t ph = uint32_t(kc) & 1u;
-    if (tid == 0) {
-      mbar_expect_tx(&bar_b, bbytes);
-      bulk_g2s(sB, Bg + size_t(kc) * npb * (BN * kBK), bbytes, &bar_b);
-    }
-    // A: this thread's row, 32 k values → 3 bf16 planes
+  if (warp >= 4 && warp < 8) {
+    // ================= producers =================
+    const int ptid = tid - 128;
+    const int rsub = ptid >> 3;          // row within each 16-row slab
+    const int k4 = (ptid & 7) * 4;       // k offset within the 32-wide stage
+    const int64_t pcw = p.patch * p.pC;
+    int s = 0;
+    uint32_t phase = 0;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+      const TileInfo ti = tile_info(p, c0, t);
+      if (ti.r0 >= ti.r1) continue;
+      const int npb = p.nplanes[ti.group];
+      const uint16_t* Bg = p.Bp[ti.group] + size_t(ti.n_tile) * p.kchunks * npb * (BN * kBK);
+      const uint32_t bbytes = uint32_t(npb) * kPlaneB;
+      const float* rowp[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float f[8];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t k = int64_t(kc) * kBK + q * 8 + h * 4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (a_ok && k < p.K) {
-          const float* src = (AM == A_PATCH) ? abase + (k / pcw) * prs + (k % pcw) : abase + k;
-          v = __ldg(reinterpret_cast<const float4*>(src));
-          if (AM == A_PATCH) {
-            v.x -= p.sub; v.y -= p.sub; v.z -= p.sub; v.w -= p.sub;
+      for (int i = 0; i < 8; ++i) {
+        const int64_t row = ti.r0 + rsub + 16 * i;
+        rowp[i] = nullptr;
+        if (row < ti.r1) {
+          if (AM == A_PLAIN) {
+            rowp[i] = p.A + row * p.lda;
+          } else if (AM == A_GATHER) {
+            rowp[i] = p.A + int64_t(__ldg(p.a_rows + row)) * p.lda;
+          } else {
+            const int64_t tpi = p.pside * p.pside;
+            const int64_t b = row / tpi, tt = row % tpi;
+            const int64_t py = tt / p.pside, px = tt % p.pside;
+            rowp[i] = p.A + ((b * p.pH + py * p.patch) * p.pW + px * p.patch) * p.pC;
           }
         }
-        f[h * 4 + 0] = v.x; f[h * 4 + 1] = v.y; f[h * 4 + 2] = v.z; f[h * 4 + 3] = v.w;
       }
-      uint4 ph4[3];
-      uint32_t* hp = reinterpret_cast<uint32_t*>(&ph4[0]);
-      uint32_t* mp = reinterpret_cast<uint32_t*>(&ph4[1]);
-      uint32_t* lp = reinterpret_cast<uint32_t*>(&ph4[2]);
+      for (int kc = 0; kc < p.kchunks; ++kc) {
+        mbar_wait(&empty[s], phase ^ 1u);
+        uint8_t* st = smem + size_t(s) * stage_bytes;
+        if (ptid == 0) {
+          mbar_add_tx(&full[s], bbytes);
+          bulk_g2s(st + 3 * kPlaneA, Bg + size_t(kc) * npb * (BN * kBK), bbytes, &full[s]);
+        }
+        const int64_t k = int64_t(kc) * kBK + k4;
+        float4 v[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const Split3 s = split3x2(f[2 * j], f[2 * j + 1]);
-        hp[j] = bf2_bits(s.h);
-        mp[j] = bf2_bits(s.m);
-        lp[j] = bf2_bits(s.l);
-      }
-      const uint32_t off = plane_offset(tid, q * 8);
+        for (int i = 0; i < 8; ++i) {
+          v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (rowp[i] != nullptr && k < p.K) {
+            const float* src = (AM == A_PATCH)
+                                   ? rowp[i] + (k / pcw) * (p.pW * p.pC) + (k % pcw)
+                                   : rowp[i] + k;
+            v[i] = __ldg(reinterpret_cast<const float4*>(src));
+            if (AM == A_PATCH) {
+              v[i].x -= p.sub; v[i].y -= p.sub; v[i].z -= p.sub; v[i].w -= p.sub;
+            }
+          }
+        }
 #pragma unroll
-      for (int pl = 0; pl < 3; ++pl)
-        *reinterpret_cast<uint4*>(sA + pl * kPlaneA + off) = ph4[pl];
-    }
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      mbar_wait(&bar_b, ph);
-      tc_fence_after();
-#pragma unroll
-      for (int ks = 0; ks < kBK / 16; ++ks) {
-        for (int i = 0; i < npairs; ++i) {
-          const int pa = pa_tab[i];
-          const int pb = npb == 1 ? 0 : pb_dense[i];
-          const uint64_t ad = smem_desc(sA_u32 + pa * kPlaneA + ks * 256);
-          const uint64_t bd = smem_desc(sB_u32 + pb * kPlaneB + ks * 256);
-          mma_bf16(tmem, ad, bd, idesc, (kc | ks | i) != 0 ? 1u : 0u);
+        for (int i = 0; i < 8; ++i) {
+          const Split3 a = split3x2(v[i].x, v[i].y);
+          const Split3 b = split3x2(v[i].z, v[i].w);
+          const uint32_t off = plane_offset(rsub + 16 * i, k4);
+          *reinterpret_cast<uint2*>(st + off) = make_uint2(bf2_bits(a.h), bf2_bits(b.h));
+          *reinterpret_cast<uint2*>(st + kPlaneA + off) = make_uint2(bf2_bits(a.m), bf2_bits(b.m));
+          *reinterpret_cast<uint2*>(st + 2 * kPlaneA + off) =
+              make_uint2(bf2_bits(a.l), bf2_bits(b.l));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+        if (++s == S) {
+          s = 0;
+          phase ^= 1u;
         }
       }
-      mma_commit(&bar_mma);
     }
-    mbar_wait(&bar_mma, ph);
-  }
-  tc_fence_after();
-
-  // ---- epilogue: thread = accumulator row ----
-  const int64_t r = r0 + warp * 32 + lane;
-  const bool r_ok = r < r1;
-  int64_t orow = 0, pos_idx = 0;
-  float g = 1.f;
-  if (r_ok) {
-    orow = p.c_rows ? int64_t(p.c_rows[r]) : r;
-    if (p.img_tokens > 0) {
-      const int64_t b = r / p.img_tokens, t = r % p.img_tokens;
-      orow = b * (p.img_tokens + p.extra) + p.extra + t;
-      pos_idx = p.extra + t;
-    }
-    if (p.gate) g = p.gate[orow];
-  }
-  const int64_t n_base = n_tile * BN;
-#pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    float v[16];
-    tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(c0), v);
-    if (!r_ok) continue;
+  } else if (warp == 8) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_m128(BN);
+      const uint8_t pa_tab[6] = {2, 1, 0, 1, 0, 0};
+      const uint8_t pb_dense[6] = {0, 1, 2, 0, 1, 0};
+      const uint32_t smem_base = smem_u32(smem);
+      int s = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+        const TileInfo ti = tile_info(p, c0, t);
+        if (ti.r0 >= ti.r1) continue;
+        const int npb = p.nplanes[ti.group];
+        const int npairs = npb == 1 ? 3 : 6;
+        mbar_wait(&tempty[acc], acc_phase ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + uint32_t(acc * BN);
+        for (int kc = 0; kc < p.kchunks; ++kc) {
+          mbar_wait(&full[s], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_base + uint32_t(s) * stage_bytes;
+          const uint32_t sb = sa + 3 * kPlaneA;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int64_t n = n_base + c0 + j;
-      if (n >= p.N) continue;
-      float o = v[j];
-      if (p.act == 1) o = gelu_tanh(o);
-      if (p.gate) o = o * g;
-      if (p.pos) o = o + p.pos[pos_idx * p.N + n];
-      if (p.residual) o = p.residual[orow * p.N + n] + o;
-      p.C[orow * p.N + n] = o;
+          for (int ks = 0; ks < kBK / 16; ++ks) {
+            for (int i = 0; i < npairs; ++i) {
+              const int pb = npb == 1 ? 0 : pb_dense[i];
+              const uint64_t ad = smem_desc(sa + pa_tab[i] * kPlaneA + ks * 256);
+              const uint64_t bd = smem_desc(sb + pb * kPlaneB + ks * 256);
+              mma_bf16(d_tmem, ad, bd, idesc, (kc | ks | i) != 0 ? 1u : 0u);
+            }
+          }
+          mma_commit(&empty[s]);
+          if (++s == S) {
+            s = 0;
+            phase ^= 1u;
+          }
+        }
+        mma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ================= epilogue (warps 0-3, thread = TMEM lane = row) =================
+    float* xb = xbuf + warp * 32 * kXPitch;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const bool nvec = false;
+    (void)nvec;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+      const TileInfo ti = tile_info(p, c0, t);
+      if (ti.r0 >= ti.r1) continue;
+      const int64_t r = ti.r0 + warp * 32 + lane;
+      const bool r_ok = r < ti.r1;
+      int64_t orow = 0, pos_idx = 0;
+      float g = 1.f;
+      if (r_ok) {
+        orow = p.c_rows ? int64_t(__ldg(p.c_rows + r)) : r;
+        if (p.img_tokens > 0) {
+          const int64_t b = r / p.img_tokens, tt = r % p.img_tokens;
+          orow = b * (p.img_tokens + p.extra) + p.extra + tt;
+          pos_idx = p.extra + tt;
+        }
+        if (p.gate) g = __ldg(p.gate + orow);
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_base = tmem + (uint32_t(warp * 32) << 16) + uint32_t(acc * BN);
+      const int64_t n_base = int64_t(ti.n_tile) * BN;
+#pragma unroll 1
+      for (int cb = 0; cb < BN; cb += 32) {
+        float v[32];
+        {
+          float lo[16], hi[16];
+          tmem_ld16(t_base + uint32_t(cb), lo);
+          tmem_ld16(t_base + uint32_t(cb + 16), hi);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            v[j] = lo[j];
+            v[16 + j] = hi[j];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float o = v[j];
+          if (p.act == 1) o = gelu_fast(o);
+          if (p.gate) o = o * g;
+          xb[lane * kXPitch + j] = o;
+        }
+        __syncwarp();
+        const int64_t n = n_base + cb + lane;
+        const bool n_ok = n < p.N;
+#pragma unroll 4
+        for (int i = 0; i < 32; ++i) {
+          const int64_t orow_i = __shfl_sync(0xffffffffu, orow, i);
+          const int ok_i = __shfl_sync(0xffffffffu, int(r_ok), i);
+          const int64_t pos_i = __shfl_sync(0xffffffffu, pos_idx, i);
+          if (ok_i && n_ok) {
+            float o = xb[i * kXPitch + lane];
+            if (p.pos) o = o + __ldg(p.pos + pos_i * p.N + n);
+            if (p.residual) o = __ldg(p.residual + orow_i * p.N + n) + o;
+            p.C[orow_i * p.N + n] = o;
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<TCOLS>(tmem);
+  if (warp == 8) tmem_dealloc<TCOLS>(tmem);
 }
 
 // ---- weight packing ---------------------------------------------------------
@@ -270,15 +386,36 @@ static int tc_tile_n_ok(int bn) {
   return bn == 32 || bn == 64 || bn == 128 || bn == 160 || bn == 256;
 }
 
-static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles, cudaStream_t s) {
+static int g_num_sms = 0;
+
+static int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cudaStream_t s) {
   using namespace tc;
   if (p.M == 0) return SA_OK;
-  const int ntiles = int(cdiv(p.N, bn));
-  dim3 grid((unsigned)m_tiles, (unsigned)ntiles, 1u);
+  p.ntiles = int(cdiv(p.N, bn));
   const int npb_max = max(p.nplanes[0], p.counts ? p.nplanes[1] : 0);
-  size_t smem = 3 * size_t(kPlaneA) + size_t(npb_max) * bn * kBK * 2;
-  if (bn > 128) smem = max(smem, size_t(80 * 1024));  // ≤ 2 CTAs/SM: 2 × 256 TMEM columns
-  else if (bn == 128) smem = max(smem, size_t(50 * 1024));  // ≤ 4 CTAs/SM: 4 × 128 columns
+  const size_t stage_bytes = 3 * size_t(kPlaneA) + size_t(npb_max) * bn * kBK * 2;
+  const size_t fixed = 4 * 32 * kXPitch * sizeof(float) + (2 * 8 + 4) * 8 + 16;
+  const size_t budget = 220 * 1024;
+  int stages = int((budget - fixed) / stage_bytes);
+  stages = stages > 4 ? 4 : stages;
+  if (stages < 2) {
+    set_error("tensor-core stage does not fit shared memory (bn=%d)", bn);
+    return SA_ERR_VALUE;
+  }
+  p.stages = stages;
+  const size_t smem = size_t(stages) * stage_bytes + fixed;
+  const int64_t tiles = m_tiles_max * p.ntiles;
+  const int grid = int(tiles < num_sms() ? tiles : num_sms());
 #define SA_TC_CASE(BNV)                                                                          \
   case BNV: {                                                                                    \
     auto kfn = amode == A_PLAIN    ? tc_gemm_kernel<BNV, A_PLAIN>                               \
@@ -323,7 +460,7 @@ using namespace sa;
 extern "C" int sa_tc_tile_n(int64_t N) {
   if (N <= 256) {
     for (int bn : {32, 64, 128, 160, 256})
-      if (N <= bn && (bn == N || bn >= N)) return bn;
+      if (N <= bn) return bn;
   }
   if (N % 256 == 0) return 256;
   if (N % 160 == 0) return 160;

@@ -124,11 +124,15 @@ def test_popcounts_bit_exact(dk, n):
     from paper_2306_06446_b200 import attention as A
     from paper_2306_06446_b200 import quantize as Q
     g = ops.rng(dk + n)
-    H = 3
+    H = 4
+    gh = max(1, 32 // dk)             # heads per 'image' (rows >= 32 channels)
     q = g.standard_normal((H * n, dk)).astype(F32)
     kk = g.standard_normal((H * n, dk)).astype(F32)
-    cq, _ = Q.sign_hash(dev(q), 1, H)
-    ck, _ = Q.sign_hash(dev(kk), 1, H)
+
+    def as_images(t):                 # (H*n, dk) head stacks → (H/gh*n, gh*dk) images
+        return dev(ops.heads_merge(t.reshape(H // gh, gh, n, dk)).reshape(-1, gh * dk))
+    cq, _ = Q.sign_hash(as_images(q), gh, H // gh)
+    ck, _ = Q.sign_hash(as_images(kk), gh, H // gh)
     cnt, D, S = A.binary_popcounts(cq, ck, dk, with_scores=True)
     bq = ops.code_bits(q.reshape(H, n, dk)).astype(np.int64)
     bk = ops.code_bits(kk.reshape(H, n, dk)).astype(np.int64)
