@@ -36,9 +36,9 @@ namespace sa {
 namespace tc {
 
 constexpr int kBM = 128;
-constexpr int kThreads = 288;
+constexpr int kThreads = 416;
 constexpr uint32_t kPlaneA = kBM * kBK * 2;  // bytes per A plane
-constexpr int kXPitch = 33;                   // transpose buffer pitch (floats)
+constexpr int kXPitch = 20;                   // transpose buffer pitch (floats, 16B rows)
 
 enum AMode { A_PLAIN = 0, A_GATHER = 1, A_PATCH = 2 };
 
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
   const int npb_max = max(p.nplanes[0], p.counts ? p.nplanes[1] : 0);
   const uint32_t stage_bytes = 3 * kPlaneA + uint32_t(npb_max) * kPlaneB;
   float* xbuf = reinterpret_cast<float*>(smem + size_t(S) * stage_bytes);      // [4][32][33]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xbuf + 4 * 32 * kXPitch);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<int64_t*>(xbuf + 8 * 32 * kXPitch) + 256);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* tfull = bars + 2 * S;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (warp == 8) tmem_alloc<TCOLS>(tmem_slot);
+  if (warp == 12) tmem_alloc<TCOLS>(tmem_slot);
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 4);     // four producer warps
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);    // one MMA commit
-      mbar_init(&tempty[b], 128); // every epilogue thread
+      mbar_init(&tempty[b], 256); // every epilogue thread
     }
     fence_barrier_init();
   }
@@ -149,9 +149,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
   const int64_t c0 = p.counts ? int64_t(p.counts[0]) : 0;
   const int64_t total = num_m_tiles(p, c0) * p.ntiles;
 
-  if (warp >= 4 && warp < 8) {
+  if (warp >= 8 && warp < 12) {
     // ================= producers =================
-    const int ptid = tid - 128;
+    const int ptid = tid - 256;
     const int rsub = ptid >> 3;          // row within each 16-row slab
     const int k4 = (ptid & 7) * 4;       // k offset within the 32-wide stage
     const int64_t pcw = p.patch * p.pC;
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
         }
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == 12) {
     // ================= MMA issuer =================
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_m128(BN);
@@ -270,18 +270,22 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
     }
     __syncwarp();
   } else {
-    // ================= epilogue (warps 0-3, thread = TMEM lane = row) =================
-    float* xb = xbuf + warp * 32 * kXPitch;
+    // ===== epilogue (warps 0-7): warp e reads TMEM lanes 32*(e%4).. (its rows)
+    // and the column half e/4 of the tile; thread = accumulator row. =====
+    const int quad = warp & 3, half = warp >> 2;
+    float* xb = xbuf + warp * 32 * kXPitch;                 // [32 rows][kXPitch]
+    int64_t* orow_s = reinterpret_cast<int64_t*>(xbuf + 8 * 32 * kXPitch);  // [2][128]
     int acc = 0;
     uint32_t acc_phase = 0;
-    const bool nvec = false;
-    (void)nvec;
+    const bool vec4 = (p.N & 3) == 0;
+    constexpr int HALF = BN / 2;   // columns per warp (multiple of 16)
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
       const TileInfo ti = tile_info(p, c0, t);
       if (ti.r0 >= ti.r1) continue;
-      const int64_t r = ti.r0 + warp * 32 + lane;
+      const int rl = quad * 32 + lane;             // row within the tile
+      const int64_t r = ti.r0 + rl;
       const bool r_ok = r < ti.r1;
-      int64_t orow = 0, pos_idx = 0;
+      int64_t orow = -1, pos_idx = 0;
       float g = 1.f;
       if (r_ok) {
         orow = p.c_rows ? int64_t(__ldg(p.c_rows + r)) : r;
@@ -292,43 +296,63 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
         }
         if (p.gate) g = __ldg(p.gate + orow);
       }
+      int64_t* orow_t = orow_s + acc * 128;
+      if (half == 0) orow_t[rl] = p.pos ? (orow | (pos_idx << 40)) : orow;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t t_base = tmem + (uint32_t(warp * 32) << 16) + uint32_t(acc * BN);
-      const int64_t n_base = int64_t(ti.n_tile) * BN;
+      const uint32_t t_base =
+          tmem + (uint32_t(quad * 32) << 16) + uint32_t(acc * BN + half * HALF);
+      const int64_t n_base = int64_t(ti.n_tile) * BN + half * HALF;
+      // the orow table of this tile is complete once all epilogue warps are here
+      asm volatile("bar.sync 1, 256;" ::: "memory");
 #pragma unroll 1
-      for (int cb = 0; cb < BN; cb += 32) {
-        float v[32];
-        {
-          float lo[16], hi[16];
-          tmem_ld16(t_base + uint32_t(cb), lo);
-          tmem_ld16(t_base + uint32_t(cb + 16), hi);
+      for (int cb = 0; cb < HALF; cb += 16) {
+        float v[16];
+        tmem_ld16(t_base + uint32_t(cb), v);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            v[j] = lo[j];
-            v[16 + j] = hi[j];
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < 16; ++j) {
           float o = v[j];
           if (p.act == 1) o = gelu_fast(o);
           if (p.gate) o = o * g;
-          xb[lane * kXPitch + j] = o;
+          v[j] = o;
         }
+#pragma unroll
+        for (int j = 0; j < 16; j += 4)
+          *reinterpret_cast<float4*>(xb + lane * kXPitch + j) =
+              make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         __syncwarp();
-        const int64_t n = n_base + cb + lane;
-        const bool n_ok = n < p.N;
-#pragma unroll 4
-        for (int i = 0; i < 32; ++i) {
-          const int64_t orow_i = __shfl_sync(0xffffffffu, orow, i);
-          const int ok_i = __shfl_sync(0xffffffffu, int(r_ok), i);
-          const int64_t pos_i = __shfl_sync(0xffffffffu, pos_idx, i);
-          if (ok_i && n_ok) {
-            float o = xb[i * kXPitch + lane];
-            if (p.pos) o = o + __ldg(p.pos + pos_i * p.N + n);
-            if (p.residual) o = __ldg(p.residual + orow_i * p.N + n) + o;
-            p.C[orow_i * p.N + n] = o;
+        // 8 rows x 4 float4 per instruction: each row segment is 64 contiguous bytes
+        const int c4 = (lane & 3) * 4;
+        const int64_t n = n_base + cb + c4;
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int ri = it * 8 + (lane >> 2);
+          const int64_t meta = orow_t[quad * 32 + ri];
+          if (meta < 0) continue;
+          const int64_t orow_i = p.pos ? (meta & ((int64_t(1) << 40) - 1)) : meta;
+          const int64_t pos_i = p.pos ? (meta >> 40) : 0;
+          float4 o = *reinterpret_cast<const float4*>(xb + ri * kXPitch + c4);
+          if (vec4 && n + 3 < p.N) {
+            if (p.pos) {
+              const float4 q = __ldg(reinterpret_cast<const float4*>(p.pos + pos_i * p.N + n));
+              o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+            }
+            if (p.residual) {
+              const float4 q =
+                  __ldg(reinterpret_cast<const float4*>(p.residual + orow_i * p.N + n));
+              o = make_float4(q.x + o.x, q.y + o.y, q.z + o.z, q.w + o.w);
+            }
+            *reinterpret_cast<float4*>(p.C + orow_i * p.N + n) = o;
+          } else {
+            const float ov[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              if (n + j >= p.N) break;
+              float e = ov[j];
+              if (p.pos) e = e + __ldg(p.pos + pos_i * p.N + n + j);
+              if (p.residual) e = __ldg(p.residual + orow_i * p.N + n + j) + e;
+              p.C[orow_i * p.N + n + j] = e;
+            }
           }
         }
         __syncwarp();
@@ -343,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) tmem_dealloc<TCOLS>(tmem);
+  if (warp == 12) tmem_dealloc<TCOLS>(tmem);
 }
 
 // ---- weight packing ---------------------------------------------------------
@@ -404,7 +428,7 @@ static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cu
   p.ntiles = int(cdiv(p.N, bn));
   const int npb_max = max(p.nplanes[0], p.counts ? p.nplanes[1] : 0);
   const size_t stage_bytes = 3 * size_t(kPlaneA) + size_t(npb_max) * bn * kBK * 2;
-  const size_t fixed = 4 * 32 * kXPitch * sizeof(float) + (2 * 8 + 4) * 8 + 16;
+  const size_t fixed = 8 * 32 * kXPitch * sizeof(float) + 256 * 8 + (2 * 8 + 4) * 8 + 16;
   const size_t budget = 220 * 1024;
   int stages = int((budget - fixed) / stage_bytes);
   stages = stages > 4 ? 4 : stages;
