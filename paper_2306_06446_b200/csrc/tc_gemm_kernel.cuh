@@ -1,0 +1,373 @@
+// Persistent warp-specialized tcgen05 GEMM (see tcgemm.cu for the numerics).
+//
+// One CTA per SM, 17 warps, tiles of 128 rows x BN columns processed in a
+// static stride; the CTA's j-th non-empty tile belongs to "lane" g = j & 1:
+//   warps  8-11 / 12-15  producer group g: per 32-wide K stage, gather the
+//                        tile's 128 A rows with coalesced 128-bit loads (plain /
+//                        MoE-permuted / patchified image), split them into
+//                        hi/mid/lo bf16 planes in the UMMA canonical layout; one
+//                        thread pulls the weight planes of the stage with a
+//                        single bulk async copy (TMA engine, complete_tx);
+//   warp  16             MMA issuer: one thread chains tcgen05.mma into TMEM
+//                        accumulator g and commits to the mbarriers;
+//   warps  0-3 / 4-7     epilogue group g: tcgen05.ld (thread = accumulator
+//                        row), GELU / x gate, transpose through shared memory,
+//                        then coalesced 64-byte row segments with residual /
+//                        position add and MoE scatter back to token order.
+// Two producer groups, two TMEM accumulators and two epilogue groups keep
+// two tiles' latency chains in flight; each group owns every other stage of
+// the shared-memory ring (full/empty mbarriers), tfull/tempty hand the
+// accumulators between MMA and epilogue.
+#pragma once
+
+#include "tc_common.cuh"
+
+namespace sa {
+namespace tc {
+
+constexpr int kBM = 128;
+constexpr int kThreads = 544;
+constexpr int kMmaWarp = 16;
+constexpr uint32_t kPlaneA = kBM * kBK * 2;  // bytes per A plane
+constexpr int kXPitch = 20;                   // transpose buffer pitch (floats, 16B rows)
+
+enum AMode { A_PLAIN = 0, A_GATHER = 1, A_PATCH = 2 };
+
+struct TcParams {
+  const float* A;
+  int64_t lda;
+  const int32_t* a_rows;
+  int64_t pH, pW, pC, patch, pside;
+  float sub;
+  const uint16_t* Bp[2];
+  int nplanes[2];
+  int64_t M, K, N;
+  int kchunks;
+  int ntiles;
+  int stages;  // even; group g owns stages g, g+2, ...
+  const int32_t* counts;
+  float* C;
+  const int32_t* c_rows;
+  const float* gate;
+  const float* residual;
+  int act;
+  const float* pos;
+  int64_t img_tokens;
+  int extra;
+};
+
+template <int BN>
+struct TmemCols {  // two accumulator buffers, power of two >= 32
+  static constexpr uint32_t value = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
+                                    : 2 * BN <= 256 ? 256 : 512;
+};
+
+struct TileInfo {
+  int group;  // expert
+  int64_t r0, r1;
+  int n_tile;
+};
+
+__device__ __forceinline__ int64_t num_m_tiles(const TcParams& p, int64_t c0) {
+  if (!p.counts) return (p.M + kBM - 1) / kBM;
+  return (c0 + kBM - 1) / kBM + (p.M - c0 + kBM - 1) / kBM;
+}
+
+// m-tiles: with grouping, expert 0 owns ceil(c0/128) tiles, expert 1 the rest
+__device__ __forceinline__ TileInfo tile_info(const TcParams& p, int64_t c0, int64_t t) {
+  TileInfo ti;
+  const int64_t m = t / p.ntiles;
+  ti.n_tile = int(t % p.ntiles);
+  if (!p.counts) {
+    ti.group = 0;
+    ti.r0 = m * kBM;
+    ti.r1 = min(p.M, ti.r0 + kBM);
+    return ti;
+  }
+  const int64_t t0 = (c0 + kBM - 1) / kBM;
+  if (m < t0) {
+    ti.group = 0;
+    ti.r0 = m * kBM;
+    ti.r1 = min(c0, ti.r0 + kBM);
+  } else {
+    ti.group = 1;
+    ti.r0 = c0 + (m - t0) * kBM;
+    ti.r1 = min(p.M, ti.r0 + kBM);
+  }
+  return ti;
+}
+
+__device__ __forceinline__ float gelu_fast(float x) {
+  // 0.5·x·(1 + tanh(u)) == x / (1 + exp(-2u)); ex2.approx + fast divide keep
+  // ~1e-7 relative accuracy (the reference's tanh is itself a float32 libm call)
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  const float u = c * (x + a * (x * x * x));
+  return __fdividef(x, 1.0f + __expf(-2.0f * u));
+}
+
+__host__ __device__ inline size_t tc_fixed_smem() {
+  return size_t(8) * 32 * kXPitch * sizeof(float)  // transpose buffers
+         + 2 * 128 * sizeof(int64_t)                // per-group row tables
+         + (2 * 8 + 4) * 8 + 16;                    // barriers + TMEM slot
+}
+
+template <int BN, int AM>
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr uint32_t TCOLS = TmemCols<BN>::value;
+  constexpr uint32_t kPlaneB = BN * kBK * 2;
+  const int S = p.stages;
+  const int SG = S / 2;
+  const int npb_max = max(p.nplanes[0], p.counts ? p.nplanes[1] : 0);
+  const uint32_t stage_bytes = 3 * kPlaneA + uint32_t(npb_max) * kPlaneB;
+  float* xbuf = reinterpret_cast<float*>(smem + size_t(S) * stage_bytes);   // [8][32][kXPitch]
+  int64_t* orow_s = reinterpret_cast<int64_t*>(xbuf + 8 * 32 * kXPitch);    // [2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(orow_s + 256);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* tfull = bars + 2 * S;
+  uint64_t* tempty = bars + 2 * S + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == kMmaWarp) tmem_alloc<TCOLS>(tmem_slot);
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 4);     // the four warps of the owning producer group
+      mbar_init(&empty[s], 1);    // one MMA commit
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);    // one MMA commit
+      mbar_init(&tempty[b], 128); // every thread of the epilogue group
+    }
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int64_t c0 = p.counts ? int64_t(p.counts[0]) : 0;
+  const int64_t total = num_m_tiles(p, c0) * p.ntiles;
+
+  if (warp >= 8 && warp < 16) {
+    // ================= producers =================
+    const int g = (warp - 8) >> 2;
+    const int ptid = tid - 256 - 128 * g;
+    const int rsub = ptid >> 3;          // row within each 16-row slab
+    const int k4 = (ptid & 7) * 4;       // k offset within the 32-wide stage
+    const int64_t pcw = p.patch * p.pC;
+    int sg = 0;
+    uint32_t phase = 0;
+    int j = 0;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+      const TileInfo ti = tile_info(p, c0, t);
+      if (ti.r0 >= ti.r1) continue;
+      if ((j++ & 1) != g) continue;
+      const int npb = p.nplanes[ti.group];
+      const uint16_t* Bg = p.Bp[ti.group] + size_t(ti.n_tile) * p.kchunks * npb * (BN * kBK);
+      const uint32_t bbytes = uint32_t(npb) * kPlaneB;
+      const float* rowp[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t row = ti.r0 + rsub + 16 * i;
+        rowp[i] = nullptr;
+        if (row < ti.r1) {
+          if (AM == A_PLAIN) {
+            rowp[i] = p.A + row * p.lda;
+          } else if (AM == A_GATHER) {
+            rowp[i] = p.A + int64_t(__ldg(p.a_rows + row)) * p.lda;
+          } else {
+            const int64_t tpi = p.pside * p.pside;
+            const int64_t b = row / tpi, tt = row % tpi;
+            const int64_t py = tt / p.pside, px = tt % p.pside;
+            rowp[i] = p.A + ((b * p.pH + py * p.patch) * p.pW + px * p.patch) * p.pC;
+          }
+        }
+      }
+      for (int kc = 0; kc < p.kchunks; ++kc) {
+        const int s = g + 2 * sg;
+        const int64_t k = int64_t(kc) * kBK + k4;
+        float4 v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {   // issue the global loads before waiting for the slot
+          v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (rowp[i] != nullptr && k < p.K) {
+            const float* src = (AM == A_PATCH)
+                                   ? rowp[i] + (k / pcw) * (p.pW * p.pC) + (k % pcw)
+                                   : rowp[i] + k;
+            v[i] = __ldg(reinterpret_cast<const float4*>(src));
+          }
+        }
+        mbar_wait(&empty[s], phase ^ 1u);
+        uint8_t* st = smem + size_t(s) * stage_bytes;
+        if (ptid == 0) {
+          mbar_add_tx(&full[s], bbytes);
+          bulk_g2s(st + 3 * kPlaneA, Bg + size_t(kc) * npb * (BN * kBK), bbytes, &full[s]);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (AM == A_PATCH && rowp[i] != nullptr && k < p.K) {
+            v[i].x -= p.sub; v[i].y -= p.sub; v[i].z -= p.sub; v[i].w -= p.sub;
+          }
+          const Split3 a = split3x2(v[i].x, v[i].y);
+          const Split3 b = split3x2(v[i].z, v[i].w);
+          const uint32_t off = plane_offset(rsub + 16 * i, k4);
+          *reinterpret_cast<uint2*>(st + off) = make_uint2(bf2_bits(a.h), bf2_bits(b.h));
+          *reinterpret_cast<uint2*>(st + kPlaneA + off) = make_uint2(bf2_bits(a.m), bf2_bits(b.m));
+          *reinterpret_cast<uint2*>(st + 2 * kPlaneA + off) =
+              make_uint2(bf2_bits(a.l), bf2_bits(b.l));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+        if (++sg == SG) {
+          sg = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_m128(BN);
+      const uint8_t pa_tab[6] = {2, 1, 0, 1, 0, 0};
+      const uint8_t pb_dense[6] = {0, 1, 2, 0, 1, 0};
+      const uint32_t smem_base = smem_u32(smem);
+      int sg[2] = {0, 0};
+      uint32_t phase[2] = {0, 0};
+      uint32_t acc_phase[2] = {0, 0};
+      int j = 0;
+      for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+        const TileInfo ti = tile_info(p, c0, t);
+        if (ti.r0 >= ti.r1) continue;
+        const int g = j++ & 1;
+        const int npb = p.nplanes[ti.group];
+        const int npairs = npb == 1 ? 3 : 6;
+        mbar_wait(&tempty[g], acc_phase[g] ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + uint32_t(g * BN);
+        for (int kc = 0; kc < p.kchunks; ++kc) {
+          const int s = g + 2 * sg[g];
+          mbar_wait(&full[s], phase[g]);
+          tc_fence_after();
+          const uint32_t sa = smem_base + uint32_t(s) * stage_bytes;
+          const uint32_t sb = sa + 3 * kPlaneA;
+#pragma unroll
+          for (int ks = 0; ks < kBK / 16; ++ks) {
+            for (int i = 0; i < npairs; ++i) {
+              const int pb = npb == 1 ? 0 : pb_dense[i];
+              const uint64_t ad = smem_desc(sa + pa_tab[i] * kPlaneA + ks * 256);
+              const uint64_t bd = smem_desc(sb + pb * kPlaneB + ks * 256);
+              mma_bf16(d_tmem, ad, bd, idesc, (kc | ks | i) != 0 ? 1u : 0u);
+            }
+          }
+          mma_commit(&empty[s]);
+          if (++sg[g] == SG) {
+            sg[g] = 0;
+            phase[g] ^= 1u;
+          }
+        }
+        mma_commit(&tfull[g]);
+        acc_phase[g] ^= 1u;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===== epilogue group g (warps 4g..4g+3): warp reads TMEM lanes 32*(warp%4) =====
+    const int g = warp >> 2, quad = warp & 3;
+    float* xb = xbuf + warp * 32 * kXPitch;     // [32 rows][kXPitch]
+    int64_t* orow_t = orow_s + g * 128;
+    uint32_t acc_phase = 0;
+    const bool vec4 = (p.N & 3) == 0;
+    int j = 0;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+      const TileInfo ti = tile_info(p, c0, t);
+      if (ti.r0 >= ti.r1) continue;
+      if ((j++ & 1) != g) continue;
+      const int rl = quad * 32 + lane;             // row within the tile
+      const int64_t r = ti.r0 + rl;
+      const bool r_ok = r < ti.r1;
+      int64_t orow = -1, pos_idx = 0;
+      float gt = 1.f;
+      if (r_ok) {
+        orow = p.c_rows ? int64_t(__ldg(p.c_rows + r)) : r;
+        if (p.img_tokens > 0) {
+          const int64_t b = r / p.img_tokens, tt = r % p.img_tokens;
+          orow = b * (p.img_tokens + p.extra) + p.extra + tt;
+          pos_idx = p.extra + tt;
+        }
+        if (p.gate) gt = __ldg(p.gate + orow);
+      }
+      // the row table of the previous tile of this group has been consumed by
+      // every warp of the group once they all reach this barrier
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+      orow_t[rl] = r_ok ? (p.pos ? (orow | (pos_idx << 40)) : orow) : int64_t(-1);
+      mbar_wait(&tfull[g], acc_phase);
+      acc_phase ^= 1u;
+      tc_fence_after();
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+      const uint32_t t_base = tmem + (uint32_t(quad * 32) << 16) + uint32_t(g * BN);
+      const int64_t n_base = int64_t(ti.n_tile) * BN;
+#pragma unroll 1
+      for (int cb = 0; cb < BN; cb += 16) {
+        float v[16];
+        tmem_ld16(t_base + uint32_t(cb), v);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          float o = v[q];
+          if (p.act == 1) o = gelu_fast(o);
+          if (p.gate) o = o * gt;
+          v[q] = o;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; q += 4)
+          *reinterpret_cast<float4*>(xb + lane * kXPitch + q) =
+              make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+        __syncwarp();
+        // 8 rows x 4 float4 per instruction: each row segment is 64 contiguous bytes
+        const int c4 = (lane & 3) * 4;
+        const int64_t n = n_base + cb + c4;
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int ri = it * 8 + (lane >> 2);
+          const int64_t meta = orow_t[quad * 32 + ri];
+          if (meta < 0) continue;
+          const int64_t orow_i = p.pos ? (meta & ((int64_t(1) << 40) - 1)) : meta;
+          const int64_t pos_i = p.pos ? (meta >> 40) : 0;
+          float4 o = *reinterpret_cast<const float4*>(xb + ri * kXPitch + c4);
+          if (vec4 && n + 3 < p.N) {
+            if (p.pos) {
+              const float4 q = __ldg(reinterpret_cast<const float4*>(p.pos + pos_i * p.N + n));
+              o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+            }
+            if (p.residual) {
+              const float4 q =
+                  __ldg(reinterpret_cast<const float4*>(p.residual + orow_i * p.N + n));
+              o = make_float4(q.x + o.x, q.y + o.y, q.z + o.z, q.w + o.w);
+            }
+            *reinterpret_cast<float4*>(p.C + orow_i * p.N + n) = o;
+          } else {
+            const float ov[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (n + q >= p.N) break;
+              float e = ov[q];
+              if (p.pos) e = e + __ldg(p.pos + pos_i * p.N + n + q);
+              if (p.residual) e = __ldg(p.residual + orow_i * p.N + n + q) + e;
+              p.C[orow_i * p.N + n + q] = e;
+            }
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[g]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) tmem_dealloc<TCOLS>(tmem);
+}
+
+}  // namespace tc
+}  // namespace sa
