@@ -207,6 +207,106 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(
   }
 }
 
+// Output pass for dk <= 32, one CTA per (band of token-grid rows, image):
+//  - the V rows of the band plus one halo row above/below are staged in shared
+//    memory with contiguous 128-bit copies, so the 9 DWConv taps are smem reads;
+//  - per head, kv is folded into Four-Russians nibble tables
+//      T[g][m][c] = sum_{i in m} kv[4g+i][c],  Tc[g][m] = sum_{i in m} cnt[4g+i]
+//    (each entry one addition from a smaller subset), so a token's additive
+//    Q·(K^T V) is dk/4 independent table lookups + adds (no multiplies);
+//  - one warp per token, lane = channel of the head: coalesced 128 B stores.
+template <int DK>
+__global__ void __launch_bounds__(kAttnThreads) attn_out_band_kernel(
+    const uint32_t* __restrict__ codes_q, const float* __restrict__ gamma_q,
+    const float* __restrict__ gamma_k, const float* __restrict__ kv, const int* __restrict__ cnt,
+    const float* __restrict__ v, const float* __restrict__ dw, float* __restrict__ out, int n,
+    int d, int heads, int side, int band_rows, float eps) {
+  constexpr int G = DK / 4;                 // nibble groups
+  extern __shared__ __align__(16) float sm[];
+  float* T = sm;                            // [G][16][DK]
+  int* Tc = reinterpret_cast<int*>(T + G * 16 * DK);     // [G][16]
+  float* Vs = reinterpret_cast<float*>(Tc + G * 16);     // [(rows+2)*side][d]
+  const int b = blockIdx.y;
+  const int r0 = blockIdx.x * band_rows;
+  const int t_lo = r0 * side, t_hi = min(n, (r0 + band_rows) * side);
+  const int h_lo = max(0, (r0 - 1) * side), h_hi = min(n, (r0 + band_rows + 1) * side);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* vb = v + size_t(b) * n * d;
+  if (dw) {  // stage V[h_lo, h_hi) (contiguous rows of the flat token matrix)
+    const float4* src = reinterpret_cast<const float4*>(vb + size_t(h_lo) * d);
+    float4* dst = reinterpret_cast<float4*>(Vs);
+    const int nf4 = (h_hi - h_lo) * d / 4;
+    for (int i = threadIdx.x; i < nf4; i += kAttnThreads) dst[i] = __ldg(src + i);
+  }
+  for (int h = 0; h < heads; ++h) {
+    const int bh = b * heads + h;
+    __syncthreads();  // previous head's tables are no longer read
+    if (threadIdx.x < G * DK) {
+      const int g = threadIdx.x / DK, c = threadIdx.x % DK;
+      const float* kvh = kv + size_t(bh) * DK * DK;
+      float row[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) row[i] = kvh[(4 * g + i) * DK + c];
+      float val[16];
+      val[0] = 0.f;
+#pragma unroll
+      for (int m = 1; m < 16; ++m) val[m] = val[m & (m - 1)] + row[__ffs(m) - 1];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) T[(g * 16 + m) * DK + c] = val[m];
+    }
+    if (threadIdx.x < G) {
+      const int g = threadIdx.x;
+      int cr[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cr[i] = cnt[bh * DK + 4 * g + i];
+      int val[16];
+      val[0] = 0;
+#pragma unroll
+      for (int m = 1; m < 16; ++m) val[m] = val[m & (m - 1)] + cr[__ffs(m) - 1];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) Tc[g * 16 + m] = val[m];
+    }
+    float tap[9];
+    const bool lane_ok = lane < DK;
+    const int ch = h * DK + (lane_ok ? lane : 0);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) tap[q] = dw ? __ldg(dw + q * d + ch) : 0.f;
+    __syncthreads();
+    const float gq = gamma_q[bh], gk = gamma_k[bh];
+    const float gg = gq * gk;
+    const uint32_t* cq = codes_q + size_t(bh) * n;
+    for (int t = t_lo + warp; t < t_hi; t += kAttnThreads / 32) {
+      const uint32_t w = __ldg(cq + t);
+      float acc = 0.f;
+      int D = 0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int m = (w >> (4 * g)) & 15;
+        if (lane_ok) acc += T[(g * 16 + m) * DK + lane];
+        D += Tc[g * 16 + m];
+      }
+      float o = (gq * acc) / (gg * float(D) + eps);
+      if (dw) {
+        const int r = t / side, cc = t % side;
+        float s = 0.f;
+#pragma unroll
+        for (int di = 0; di < 3; ++di) {
+#pragma unroll
+          for (int dj = 0; dj < 3; ++dj) {
+            const int rr = r + di - 1, c2 = cc + dj - 1;
+            if (rr < 0 || rr >= side || c2 < 0 || c2 >= side) continue;
+            const int idx = rr * side + c2;
+            if (idx >= n) continue;
+            s = fmaf(Vs[(idx - h_lo) * d + ch], tap[di * 3 + dj], s);
+          }
+        }
+        o += s;
+      }
+      if (lane_ok) out[(size_t(b) * n + t) * d + ch] = o;
+    }
+  }
+}
+
 // quadratic Hamming form: one CTA per (query chunk, b*heads)
 constexpr int kHamQ = 32;
 template <int DK>
@@ -379,15 +479,32 @@ extern "C" int sa_linear_binary_attn(const uint32_t* codes_q, const uint32_t* co
   dim3 g1(nsplit, unsigned(BH));
   dim3 g3(unsigned(cdiv(n, kOutTok)), unsigned(B));
   const int side = grid_side(n);
+  // band geometry for the dk <= 32 output pass: rows of the token grid per CTA
+  // so that the staged V band (+2 halo rows) stays within ~64 KB
+  const int64_t row_bytes = int64_t(side) * d * 4;
+  int band_rows = int(64 * 1024 / row_bytes) - 2;
+  band_rows = band_rows < 1 ? 1 : (band_rows > side ? side : band_rows);
+  const int nbands = int(cdiv(cdiv(n, side), band_rows));
+  const size_t band_smem = (dk / 4) * 16 * (dk + 1) * 4 +
+                           (dw ? size_t(band_rows + 2) * row_bytes : 0);
 #define SA_ATTN_CASE(DKV)                                                                     \
   case DKV:                                                                                   \
     kv_partial_kernel<DKV><<<g1, kAttnThreads, 0, s>>>(codes_k, v, int(n), int(d), int(heads), \
                                                        nsplit, part, cnt_part);              \
     kv_reduce_kernel<<<unsigned(BH), 256, 0, s>>>(part, cnt_part, gamma_k, DKV, nsplit, kv,  \
                                                   cnt);                                       \
-    attn_out_kernel<DKV><<<g3, kAttnThreads, 0, s>>>(codes_q, gamma_q, gamma_k, kv, cnt, v, dw, \
-                                                     out, int(n), int(d), int(heads), side,   \
-                                                     eps);                                    \
+    if (DKV <= 32) {                                                                          \
+      cudaFuncSetAttribute(attn_out_band_kernel<DKV <= 32 ? DKV : 32>,                        \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(band_smem));      \
+      attn_out_band_kernel<DKV <= 32 ? DKV : 32>                                              \
+          <<<dim3(unsigned(nbands), unsigned(B)), kAttnThreads, band_smem, s>>>(              \
+              codes_q, gamma_q, gamma_k, kv, cnt, v, dw, out, int(n), int(d), int(heads),     \
+              side, band_rows, eps);                                                          \
+    } else {                                                                                  \
+      attn_out_kernel<DKV><<<g3, kAttnThreads, 0, s>>>(codes_q, gamma_q, gamma_k, kv, cnt, v, \
+                                                       dw, out, int(n), int(d), int(heads),   \
+                                                       side, eps);                            \
+    }                                                                                         \
     break;
   switch (dk) {
     SA_ATTN_CASE(16)
