@@ -128,6 +128,17 @@ int sa_moe_route(const float* x, const float* wg, int64_t M, int64_t d, float ti
                  float* logits, int32_t* expert_of, float* gate, int32_t* counts,
                  int32_t* perm, void* ws, size_t ws_bytes, void* stream);
 
+/* LayerNorm.forward (model.py:174-178) fused with 1..3 routers reading its output
+ * (the q/k/v MoE projections share one input, model.py:342-345; the MLP router
+ * reads ln2): y = LN(x); for router r: logits from wg_r (d, 2), then the same
+ * winner / gate / stable partition as sa_moe_route into expert_of[r*M..],
+ * gate[r*M..], counts[2r..], perm[r*M..]. d = 32 or 64. */
+size_t sa_ln_route_workspace(int64_t M, int nr);
+int sa_ln_route(const float* x, const float* gain, const float* bias, float* y, int64_t M,
+                int64_t d, float eps, int nr, const float* wg0, const float* wg1,
+                const float* wg2, float tie_thresh, int32_t* expert_of, float* gate,
+                int32_t* counts, int32_t* perm, void* ws, size_t ws_bytes, void* stream);
+
 /* dispatch only (moe.dispatch, moe.py:87-92) from precomputed logits (M, 2) */
 int sa_moe_dispatch(const float* logits, int64_t M, float tie_thresh, int32_t* expert_of,
                     float* gate, int32_t* counts, int32_t* perm, void* ws, size_t ws_bytes,

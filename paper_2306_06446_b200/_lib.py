@@ -52,6 +52,9 @@ _SIGS = {
     "sa_moe_route_workspace": (_SZ, [_I64]),
     "sa_moe_route": (_I32, [_P, _P, _I64, _I64, _F32, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "sa_moe_dispatch": (_I32, [_P, _I64, _F32, _P, _P, _P, _P, _P, _SZ, _P]),
+    "sa_ln_route_workspace": (_SZ, [_I64, _I32]),
+    "sa_ln_route": (_I32, [_P, _P, _P, _P, _I64, _I64, _F32, _I32, _P, _P, _P, _F32, _P, _P, _P,
+                           _P, _P, _SZ, _P]),
     "sa_moe_linear": (_I32, [_P, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _I64, _I64, _P]),
     "sa_moe_mlp_workspace": (_SZ, [_I64, _I64]),
     "sa_moe_mlp": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _I64, _I64, _P,

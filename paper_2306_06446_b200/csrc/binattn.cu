@@ -225,11 +225,13 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_band_kernel(
   extern __shared__ __align__(16) float sm[];
   float* T = sm;                            // [G][16][DK]
   int* Tc = reinterpret_cast<int*>(T + G * 16 * DK);     // [G][16]
-  float* Vs = reinterpret_cast<float*>(Tc + G * 16);     // [(rows+2)*side][d]
+  uint32_t* Cs = reinterpret_cast<uint32_t*>(Tc + G * 16);  // [heads][band tokens]
   const int b = blockIdx.y;
   const int r0 = blockIdx.x * band_rows;
   const int t_lo = r0 * side, t_hi = min(n, (r0 + band_rows) * side);
   const int h_lo = max(0, (r0 - 1) * side), h_hi = min(n, (r0 + band_rows + 1) * side);
+  const int nt = t_hi - t_lo;
+  float* Vs = reinterpret_cast<float*>(Cs + ((heads * band_rows * side + 3) & ~3));  // [(rows+2)*side][d]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* vb = v + size_t(b) * n * d;
   if (dw) {  // stage V[h_lo, h_hi) (contiguous rows of the flat token matrix)
@@ -237,6 +239,10 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_band_kernel(
     float4* dst = reinterpret_cast<float4*>(Vs);
     const int nf4 = (h_hi - h_lo) * d / 4;
     for (int i = threadIdx.x; i < nf4; i += kAttnThreads) dst[i] = __ldg(src + i);
+  }
+  for (int i = threadIdx.x; i < heads * nt; i += kAttnThreads) {  // query codes of the band
+    const int h = i / nt, t = i % nt;
+    Cs[h * nt + t] = __ldg(codes_q + (size_t(b) * heads + h) * n + t_lo + t);
   }
   for (int h = 0; h < heads; ++h) {
     const int bh = b * heads + h;
@@ -274,9 +280,10 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_band_kernel(
     __syncthreads();
     const float gq = gamma_q[bh], gk = gamma_k[bh];
     const float gg = gq * gk;
-    const uint32_t* cq = codes_q + size_t(bh) * n;
+    const uint32_t* cq = Cs + h * nt - t_lo;
+#pragma unroll 2
     for (int t = t_lo + warp; t < t_hi; t += kAttnThreads / 32) {
-      const uint32_t w = __ldg(cq + t);
+      const uint32_t w = cq[t];
       float acc = 0.f;
       int D = 0;
 #pragma unroll
@@ -486,6 +493,7 @@ extern "C" int sa_linear_binary_attn(const uint32_t* codes_q, const uint32_t* co
   band_rows = band_rows < 1 ? 1 : (band_rows > side ? side : band_rows);
   const int nbands = int(cdiv(cdiv(n, side), band_rows));
   const size_t band_smem = (dk / 4) * 16 * (dk + 1) * 4 +
+                           size_t((heads * band_rows * side + 3) & ~3) * 4 +
                            (dw ? size_t(band_rows + 2) * row_bytes : 0);
 #define SA_ATTN_CASE(DKV)                                                                     \
   case DKV:                                                                                   \

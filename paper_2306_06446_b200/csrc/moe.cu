@@ -123,11 +123,15 @@ __global__ void __launch_bounds__(256) route_kernel(const float* __restrict__ x,
   }
 }
 
-// single CTA: exclusive scan of per-block expert-1 counts; counts[0..1]
+// one CTA per router (blockIdx.x): exclusive scan of per-block expert-1
+// counts; counts[2r..2r+1]
 __global__ void __launch_bounds__(1024) route_scan_kernel(const int32_t* __restrict__ block_cnt1,
                                                           int nblocks, int64_t M,
                                                           int32_t* __restrict__ block_off1,
                                                           int32_t* __restrict__ counts) {
+  block_cnt1 += size_t(blockIdx.x) * nblocks;
+  block_off1 += size_t(blockIdx.x) * nblocks;
+  counts += 2 * blockIdx.x;
   __shared__ int warp_tot[32];
   __shared__ int carry;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -171,6 +175,11 @@ __global__ void __launch_bounds__(kRouteTok) partition_kernel(const int32_t* __r
                                                              const int32_t* __restrict__ block_off1,
                                                              const int32_t* __restrict__ counts,
                                                              int64_t M, int32_t* __restrict__ perm) {
+  // router r = blockIdx.y (stacked plans of a fused multi-router pass)
+  expert_of += size_t(blockIdx.y) * M;
+  perm += size_t(blockIdx.y) * M;
+  block_off1 += size_t(blockIdx.y) * gridDim.x;
+  counts += 2 * blockIdx.y;
   __shared__ int wc[kRouteTok / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t t = int64_t(blockIdx.x) * kRouteTok + threadIdx.x;
@@ -195,9 +204,116 @@ __global__ void __launch_bounds__(kRouteTok) partition_kernel(const int32_t* __r
   perm[pos] = int32_t(t);
 }
 
+// LayerNorm (ref tensor.py:114-128) fused with up to three routers reading the
+// normalized rows (the q/k/v projections of an AttentionLayer share one input,
+// ref model.py:342-345): one thread per row holds the D floats in registers,
+// writes y and, per router, the fp64 logits → winner / gate → block counts.
+constexpr int kMaxRouters = 3;
+
+template <int D>
+__global__ void __launch_bounds__(kRouteTok) ln_route_kernel(
+    const float* __restrict__ x, const float* __restrict__ gain, const float* __restrict__ bias,
+    float* __restrict__ y, int64_t M, float eps, int nr, const float* __restrict__ wg0,
+    const float* __restrict__ wg1, const float* __restrict__ wg2, float tie_thresh,
+    int32_t* __restrict__ expert_of, float* __restrict__ gate, int32_t* __restrict__ block_cnt1) {
+  __shared__ double sw[kMaxRouters][2 * D];
+  __shared__ int wcnt[kMaxRouters][kRouteTok / 32];
+  const float* wgs[kMaxRouters] = {wg0, wg1, wg2};
+  for (int r = 0; r < nr; ++r)
+    for (int i = threadIdx.x; i < 2 * D; i += kRouteTok) sw[r][i] = double(wgs[r][i]);
+  __syncthreads();
+  const int64_t row = int64_t(blockIdx.x) * kRouteTok + threadIdx.x;
+  const bool ok = row < M;
+  float v[D];
+  if (ok) {
+    const float4* xr = reinterpret_cast<const float4*>(x + row * D);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < D / 4; ++i) {
+      const float4 q = __ldg(xr + i);
+      v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
+      s += (q.x + q.y) + (q.z + q.w);
+    }
+    const float mean = s / float(D);
+    float q2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      v[i] -= mean;
+      q2 += v[i] * v[i];
+    }
+    const float inv = 1.0f / sqrtf(q2 / float(D) + eps);
+    float4* yr = reinterpret_cast<float4*>(y + row * D);
+#pragma unroll
+    for (int i = 0; i < D / 4; ++i) {
+      const float4 g = __ldg(reinterpret_cast<const float4*>(gain) + i);
+      const float4 b = __ldg(reinterpret_cast<const float4*>(bias) + i);
+      v[4 * i] = v[4 * i] * inv * g.x + b.x;
+      v[4 * i + 1] = v[4 * i + 1] * inv * g.y + b.y;
+      v[4 * i + 2] = v[4 * i + 2] * inv * g.z + b.z;
+      v[4 * i + 3] = v[4 * i + 3] * inv * g.w + b.w;
+      yr[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+  }
+  for (int r = 0; r < nr; ++r) {
+    int e = 0;
+    if (ok) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        s0 = fma(double(v[c]), sw[r][2 * c], s0);
+        s1 = fma(double(v[c]), sw[r][2 * c + 1], s1);
+      }
+      float g;
+      e = decide(float(s0), float(s1), tie_thresh, g);
+      expert_of[size_t(r) * M + row] = e;
+      gate[size_t(r) * M + row] = g;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, e == 1);
+    if ((threadIdx.x & 31) == 0) wcnt[r][threadIdx.x >> 5] = __popc(bal);
+  }
+  __syncthreads();
+  if (threadIdx.x < nr) {
+    int c = 0;
+    for (int w = 0; w < kRouteTok / 32; ++w) c += wcnt[threadIdx.x][w];
+    block_cnt1[size_t(threadIdx.x) * gridDim.x + blockIdx.x] = c;
+  }
+}
+
 }  // namespace sa
 
 using namespace sa;
+
+extern "C" size_t sa_ln_route_workspace(int64_t M, int nr) {
+  return size_t(2 * cdiv(M, kRouteTok) * nr) * sizeof(int32_t) + 64;
+}
+
+extern "C" int sa_ln_route(const float* x, const float* gain, const float* bias, float* y,
+                           int64_t M, int64_t d, float eps, int nr, const float* wg0,
+                           const float* wg1, const float* wg2, float tie_thresh,
+                           int32_t* expert_of, float* gate, int32_t* counts, int32_t* perm,
+                           void* ws, size_t ws_bytes, void* stream) {
+  SA_REQUIRE(d == 32 || d == 64, SA_ERR_SHAPE, "sa_ln_route: d=%lld unsupported (32 or 64)",
+             (long long)d);
+  SA_REQUIRE(nr >= 1 && nr <= kMaxRouters, SA_ERR_VALUE, "sa_ln_route: 1..3 routers, got %d", nr);
+  SA_REQUIRE(M > 0 && M < (int64_t(1) << 31), SA_ERR_SHAPE, "sa_ln_route: bad token count");
+  SA_REQUIRE(ws_bytes >= sa_ln_route_workspace(M, nr), SA_ERR_VALUE,
+             "sa_ln_route: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  const int nb = int(cdiv(M, kRouteTok));
+  int32_t* block_cnt1 = static_cast<int32_t*>(ws);
+  int32_t* block_off1 = block_cnt1 + size_t(nb) * nr;
+  if (d == 32)
+    ln_route_kernel<32><<<nb, kRouteTok, 0, s>>>(x, gain, bias, y, M, eps, nr, wg0, wg1, wg2,
+                                                 tie_thresh, expert_of, gate, block_cnt1);
+  else
+    ln_route_kernel<64><<<nb, kRouteTok, 0, s>>>(x, gain, bias, y, M, eps, nr, wg0, wg1, wg2,
+                                                 tie_thresh, expert_of, gate, block_cnt1);
+  route_scan_kernel<<<nr, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
+  partition_kernel<<<dim3(nb, nr), kRouteTok, 0, s>>>(expert_of, block_off1, counts, M, perm);
+  count_launch(3);
+  SA_LAUNCH_CHECK("sa_ln_route");
+  return SA_OK;
+}
 
 extern "C" size_t sa_moe_route_workspace(int64_t M) {
   const int64_t nb = cdiv(M, kRouteTok);

@@ -112,6 +112,10 @@ def tc_enabled() -> bool:
     return GEMM_ENGINE == "tc"
 
 
+# LayerNorm fused with the routers that read its output (d = 32 / 64)
+FUSE_LN_ROUTE = os.environ.get("SA_FUSE_LN_ROUTE", "1") == "1"
+
+
 def _pack_weight(w, kind, K, N, p_min):
     """Pack a (K, N) weight into the tensor-core shared-memory image (K3/K6)."""
     lib = _lib.load()
@@ -389,12 +393,15 @@ class MoeModule:
     def router(self) -> MOE.Router:
         return MOE.Router(w_g=self.wg.value, sigma=self.cfg.sigma, lam=self.cfg.lam)
 
-    def forward(self, x, train=False, residual=None):
+    def forward(self, x, train=False, residual=None, plan=None):
+        """`plan` (optional) is a DispatchPlan already computed for x by a fused
+        LayerNorm+router pass (Block.forward); otherwise routing runs here."""
         _no_train(train)
         x = to_device(x)
         lead = x.shape[:-1]
         x2 = x.reshape(-1, x.shape[-1])
-        plan, _ = MOE.route_plan(x2, self.wg.value)
+        if plan is None:
+            plan, _ = MOE.route_plan(x2, self.wg.value)
         self.last_plan = plan
         y = fused_expert_forward(x2, self.experts, plan, residual)
         if y is None:
@@ -431,14 +438,19 @@ class AttentionLayer:
     def heads(self):
         return self.cfg.h
 
-    def forward(self, x, train=False, residual=None):
+    def forward(self, x, train=False, residual=None, plans=None):
         _no_train(train)
         x = to_device(x)
         batch, n, d = x.shape
         flat = x.reshape(batch * n, d)
-        q = self.proj["q"].forward(flat)
-        k = self.proj["k"].forward(flat)
-        v = self.proj["v"].forward(flat)
+        if plans is not None:   # q/k/v routed by the fused LN1+router pass
+            q = self.proj["q"].forward(flat, plan=plans[0])
+            k = self.proj["k"].forward(flat, plan=plans[1])
+            v = self.proj["v"].forward(flat, plan=plans[2])
+        else:
+            q = self.proj["q"].forward(flat)
+            k = self.proj["k"].forward(flat)
+            v = self.proj["v"].forward(flat)
         mode = self.cfg.attn_mode
         if mode == "softmax":
             merged = A.softmax_core_flat(q, k, v, batch, self.heads)
@@ -482,9 +494,23 @@ class Block:
         _no_train(train)
         x = to_device(x)
         batch, n, d = x.shape
-        h = self.attn.forward(self.ln1.forward(x), residual=x)
-        flat = self.ln2.forward(h).reshape(batch * n, d)
-        y = self.mlp.forward(flat, residual=h.reshape(batch * n, d))
+        x2 = x.reshape(batch * n, d)
+        fuse = FUSE_LN_ROUTE and d in (32, 64)
+        qkv = [self.attn.proj[k] for k in ("q", "k", "v")]
+        if fuse and all(isinstance(p, MoeModule) for p in qkv):
+            y, plans = MOE.ln_route_plans(x2, self.ln1.gain.value, self.ln1.bias.value,
+                                          [p.wg.value for p in qkv])
+            h = self.attn.forward(y.reshape(batch, n, d), residual=x, plans=plans)
+        else:
+            h = self.attn.forward(self.ln1.forward(x), residual=x)
+        h2 = h.reshape(batch * n, d)
+        if fuse and isinstance(self.mlp, MoeModule):
+            flat, (plan,) = MOE.ln_route_plans(h2, self.ln2.gain.value, self.ln2.bias.value,
+                                               [self.mlp.wg.value])
+            y = self.mlp.forward(flat, residual=h2, plan=plan)
+        else:
+            flat = self.ln2.forward(h).reshape(batch * n, d)
+            y = self.mlp.forward(flat, residual=h2)
         return y.reshape(batch, n, d)
 
     def named_params(self, prefix):

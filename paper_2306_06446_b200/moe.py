@@ -130,6 +130,27 @@ def route_plan(x: torch.Tensor, w_g: torch.Tensor, want_logits=False):
     return DispatchPlan(expert_of, gate, counts, perm), logits
 
 
+def ln_route_plans(x: torch.Tensor, gain, bias, w_gs, eps: float = 1e-5):
+    """LayerNorm of x fused with 1..3 routers on its output (d = 32 / 64).
+    Returns (y, [DispatchPlan per router]); the plans are views of stacked
+    device buffers, no host synchronisation."""
+    M, d = x.shape
+    nr = len(w_gs)
+    dev = x.device
+    y = torch.empty_like(x)
+    expert_of = torch.empty((nr, M), dtype=torch.int32, device=dev)
+    gate = torch.empty((nr, M), dtype=torch.float32, device=dev)
+    counts = torch.empty((nr, 2), dtype=torch.int32, device=dev)
+    perm = torch.empty((nr, M), dtype=torch.int32, device=dev)
+    ws = _lib.Workspace.get(_lib.load().sa_ln_route_workspace(M, nr), slot=1)
+    wp = [_lib.ptr(w) for w in w_gs] + [None] * (3 - nr)
+    _lib.call("sa_ln_route", _lib.ptr(x), _lib.ptr(gain), _lib.ptr(bias), _lib.ptr(y), M, d,
+              float(eps), nr, wp[0], wp[1], wp[2], tie_threshold(), _lib.ptr(expert_of),
+              _lib.ptr(gate), _lib.ptr(counts), _lib.ptr(perm), _lib.ptr(ws), ws.numel(),
+              _lib.stream())
+    return y, [DispatchPlan(expert_of[r], gate[r], counts[r], perm[r]) for r in range(nr)]
+
+
 def route(x, router: Router):
     """(p, logits): p = softmax(x @ W_g) rowwise (ref moe.py:81-84)."""
     x = to_device(x)

@@ -353,3 +353,25 @@ def test_mlp_gelu_vs_oracle(golden):
         L2 = {"kind": "dense", "w": w2} if not shift else dict(zip(("kind", "s", "p"), ("shift",) + ops.shift_quantize(w2)))
         ref = nets.linear_fwd({"kind": "mlp", "fc1": L1, "fc2": L2}, x)
         assert rel_err(y, ref) < 1e-5
+
+
+@pytest.mark.parametrize("M,d,nr", [(50_000, 32, 3), (777, 64, 1), (4096, 64, 3)])
+def test_ln_route_fused_vs_oracle(M, d, nr):
+    """LayerNorm fused with 1..3 routers: y within fp32 tolerance of the
+    oracle LN, winners / permutations bit-exact against the oracle router
+    evaluated on the device's own y (kernel-boundary parity)."""
+    from paper_2306_06446_b200 import moe as MOE
+    g = ops.rng(M + d + nr)
+    x = (g.standard_normal((M, d)) * 2 + 0.3).astype(F32)
+    wgs = [(g.standard_normal((d, 2)) * 0.3).astype(F32) for _ in range(nr)]
+    gain = np.ones(d, F32)
+    bias = np.zeros(d, F32)
+    y, plans = MOE.ln_route_plans(dev(x), dev(gain), dev(bias), [dev(w) for w in wgs])
+    yh = host(y)
+    assert rel_err(yh, ops.layer_norm(x, gain, bias)) < 2e-6
+    for w, plan in zip(wgs, plans):
+        p, _ = ops.router_probs(yh, w)
+        e, gate, idx = ops.dispatch_plan(p)
+        assert np.array_equal(plan.expert_of, e)
+        assert np.array_equal(np.concatenate(plan.index_of), np.concatenate(idx))
+        assert rel_err(plan.gate_of, gate) < 1e-6
