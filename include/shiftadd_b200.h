@@ -192,6 +192,18 @@ int sa_tc_moe_mlp(const float* x, const int32_t* perm, const int32_t* counts, co
                   const void* w1_dense, const void* w2_dense, const void* w1_shift,
                   const void* w2_shift, int bn1, int bn2, float* y, const float* residual,
                   int64_t M, int64_t d, int64_t hidden, void* ws, size_t ws_bytes, void* stream);
+/* Fused MLP on the tensor cores: fc1 → GELU → fc2 in ONE kernel, the hidden
+ * activations stay on chip (TMEM → registers → shared memory); d = 32 or 64,
+ * hidden % 32 == 0. W1 must be packed with bn = 32, W2 with bn = d. */
+int sa_tc_fused_mlp_ok(int64_t d, int64_t hidden);
+int sa_tc_moe_mlp_fused(const float* x, const int32_t* perm, const int32_t* counts,
+                        const float* gate, const void* w1_dense, const void* w2_dense,
+                        const void* w1_shift, const void* w2_shift, float* y,
+                        const float* residual, int64_t M, int64_t d, int64_t hidden,
+                        void* stream);
+int sa_tc_mlp_fused(const float* x, const void* w1pack, int w1_kind, const void* w2pack,
+                    int w2_kind, float* y, int64_t M, int64_t d, int64_t hidden,
+                    const float* residual, void* stream);
 /* patchify (model.py:557-563) + patch-embed Linear on the tensor cores */
 int sa_tc_patch_embed(const float* grid, int64_t B, int64_t H, int64_t W, int64_t C,
                       int64_t patch, float sub, const void* wpack, int bn, int64_t d,

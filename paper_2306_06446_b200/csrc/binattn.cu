@@ -231,14 +231,27 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_band_kernel(
   const int t_lo = r0 * side, t_hi = min(n, (r0 + band_rows) * side);
   const int h_lo = max(0, (r0 - 1) * side), h_hi = min(n, (r0 + band_rows + 1) * side);
   const int nt = t_hi - t_lo;
-  float* Vs = reinterpret_cast<float*>(Cs + ((heads * band_rows * side + 3) & ~3));  // [(rows+2)*side][d]
+  // V band on a zero-padded grid: (band_rows+2) x (side+2) cells of d floats;
+  // cell (R, C) holds token (r0-1+R)*side + (C-1) when it exists, else zeros
+  float* Vs = reinterpret_cast<float*>(Cs + ((heads * band_rows * side + 3) & ~3));
+  const int pw = side + 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* vb = v + size_t(b) * n * d;
-  if (dw) {  // stage V[h_lo, h_hi) (contiguous rows of the flat token matrix)
-    const float4* src = reinterpret_cast<const float4*>(vb + size_t(h_lo) * d);
+  if (dw) {
+    const int d4 = d / 4;
     float4* dst = reinterpret_cast<float4*>(Vs);
-    const int nf4 = (h_hi - h_lo) * d / 4;
-    for (int i = threadIdx.x; i < nf4; i += kAttnThreads) dst[i] = __ldg(src + i);
+    const int ncell4 = (band_rows + 2) * pw * d4;
+    for (int i = threadIdx.x; i < ncell4; i += kAttnThreads) {
+      const int c4 = i % d4, cell = i / d4;
+      const int R = cell / pw, C = cell % pw;
+      const int rr = r0 - 1 + R, cc = C - 1;
+      float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (rr >= 0 && rr < side && cc >= 0 && cc < side) {
+        const int idx = rr * side + cc;
+        if (idx < n) val = __ldg(reinterpret_cast<const float4*>(vb + size_t(idx) * d) + c4);
+      }
+      dst[i] = val;
+    }
   }
   for (int i = threadIdx.x; i < heads * nt; i += kAttnThreads) {  // query codes of the band
     const int h = i / nt, t = i % nt;
@@ -292,21 +305,17 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_band_kernel(
         if (lane_ok) acc += T[(g * 16 + m) * DK + lane];
         D += Tc[g * 16 + m];
       }
-      float o = (gq * acc) / (gg * float(D) + eps);
+      float o = (gq * acc) * __frcp_rn(gg * float(D) + eps);
       if (dw) {
+        // token (r, c) sits at padded cell (r - r0 + 1, c + 1); taps in the
+        // reference's (row, col) order (tensor.py:191-194), zeros outside
         const int r = t / side, cc = t % side;
+        const float* base = Vs + ((r - r0) * pw + cc) * d + ch;   // cell (R-1, C-1)
         float s = 0.f;
 #pragma unroll
-        for (int di = 0; di < 3; ++di) {
+        for (int di = 0; di < 3; ++di)
 #pragma unroll
-          for (int dj = 0; dj < 3; ++dj) {
-            const int rr = r + di - 1, c2 = cc + dj - 1;
-            if (rr < 0 || rr >= side || c2 < 0 || c2 >= side) continue;
-            const int idx = rr * side + c2;
-            if (idx >= n) continue;
-            s = fmaf(Vs[(idx - h_lo) * d + ch], tap[di * 3 + dj], s);
-          }
-        }
+          for (int dj = 0; dj < 3; ++dj) s = fmaf(base[(di * pw + dj) * d], tap[di * 3 + dj], s);
         o += s;
       }
       if (lane_ok) out[(size_t(b) * n + t) * d + ch] = o;
@@ -488,7 +497,7 @@ extern "C" int sa_linear_binary_attn(const uint32_t* codes_q, const uint32_t* co
   const int side = grid_side(n);
   // band geometry for the dk <= 32 output pass: rows of the token grid per CTA
   // so that the staged V band (+2 halo rows) stays within ~64 KB
-  const int64_t row_bytes = int64_t(side) * d * 4;
+  const int64_t row_bytes = int64_t(side + 2) * d * 4;   // padded grid row
   int band_rows = int(64 * 1024 / row_bytes) - 2;
   band_rows = band_rows < 1 ? 1 : (band_rows > side ? side : band_rows);
   const int nbands = int(cdiv(cdiv(n, side), band_rows));

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kRouteTok) partition_kernel(const int32_t* __r
 constexpr int kMaxRouters = 3;
 
 template <int D>
-__global__ void __launch_bounds__(kRouteTok) ln_route_kernel(
+__global__ void __launch_bounds__(kRouteTok, 3) ln_route_kernel(
     const float* __restrict__ x, const float* __restrict__ gain, const float* __restrict__ bias,
     float* __restrict__ y, int64_t M, float eps, int nr, const float* __restrict__ wg0,
     const float* __restrict__ wg1, const float* __restrict__ wg2, float tie_thresh,

@@ -114,12 +114,18 @@ def tc_enabled() -> bool:
 
 # LayerNorm fused with the routers that read its output (d = 32 / 64)
 FUSE_LN_ROUTE = os.environ.get("SA_FUSE_LN_ROUTE", "1") == "1"
+# fc1 → GELU → fc2 in one tensor-core kernel (d = 32 / 64)
+FUSE_MLP = os.environ.get("SA_FUSE_MLP", "1") == "1"
 
 
-def _pack_weight(w, kind, K, N, p_min):
+def fused_mlp_ok(d, hidden) -> bool:
+    return tc_enabled() and FUSE_MLP and bool(_lib.load().sa_tc_fused_mlp_ok(d, hidden))
+
+
+def _pack_weight(w, kind, K, N, p_min, bn=None):
     """Pack a (K, N) weight into the tensor-core shared-memory image (K3/K6)."""
     lib = _lib.load()
-    bn = int(lib.sa_tc_tile_n(N))
+    bn = int(lib.sa_tc_tile_n(N)) if bn is None else int(bn)
     out = torch.empty(int(lib.sa_weight_pack_bytes(K, N, kind, bn)), dtype=torch.uint8,
                       device=w.device)
     _lib.call("sa_weight_pack", _lib.ptr(w), kind, K, N, p_min, bn, _lib.ptr(out), _lib.stream())
@@ -153,12 +159,13 @@ class Linear:
     def weight_arg(self):
         return self.w.value, _lib.SA_W_DENSE, Q.P_MIN_DEFAULT
 
-    def tc_pack(self):
-        """(packed planes, bn, kind) for the tensor-core path, built once."""
-        if getattr(self, "_tc", None) is None:
-            pk, bn = _pack_weight(self.w.value, _lib.SA_W_DENSE, self.in_dim, self.out_dim, -15)
-            self._tc = (pk, bn, _lib.SA_W_DENSE)
-        return self._tc
+    def tc_pack(self, bn=None):
+        """(packed planes, bn, kind) for the tensor-core path, built once per bn."""
+        cache = self.__dict__.setdefault("_tc", {})
+        if bn not in cache:
+            pk, b = _pack_weight(self.w.value, _lib.SA_W_DENSE, self.in_dim, self.out_dim, -15, bn)
+            cache[bn] = (pk, b, _lib.SA_W_DENSE)
+        return cache[bn]
 
     def forward(self, x, train=False, residual=None, act=0):
         _no_train(train)
@@ -187,14 +194,15 @@ class ShiftLinearLayer:
 
     def requantize(self):
         self.quant = Q.quantize_shift(self.w.value, self.quant_cfg)
-        self._tc = None
+        self._tc = {}
 
-    def tc_pack(self):
-        if getattr(self, "_tc", None) is None:
-            pk, bn = _pack_weight(self.quant.packed, _lib.SA_W_SHIFT, self.in_dim, self.out_dim,
-                                  self.quant.p_min)
-            self._tc = (pk, bn, _lib.SA_W_SHIFT)
-        return self._tc
+    def tc_pack(self, bn=None):
+        cache = self.__dict__.setdefault("_tc", {})
+        if bn not in cache:
+            pk, b = _pack_weight(self.quant.packed, _lib.SA_W_SHIFT, self.in_dim, self.out_dim,
+                                 self.quant.p_min, bn)
+            cache[bn] = (pk, b, _lib.SA_W_SHIFT)
+        return cache[bn]
 
     @property
     def in_dim(self):
@@ -290,6 +298,12 @@ class Mlp:
         p_min = pm1 if k1 == _lib.SA_W_SHIFT else pm2
         y = torch.empty((M, self.fc2.out_dim), dtype=torch.float32, device=x.device)
         res = residual.reshape(y.shape) if residual is not None else None
+        if fused_mlp_ok(d, hidden) and k1 == k2:
+            p1, _, _ = self.fc1.tc_pack(32)
+            p2, _, _ = self.fc2.tc_pack()
+            _lib.call("sa_tc_mlp_fused", _lib.ptr(x2), _lib.ptr(p1), k1, _lib.ptr(p2), k2,
+                      _lib.ptr(y), M, d, hidden, _lib.ptr(res), _stream())
+            return y.reshape(*lead, self.fc2.out_dim)
         if tc_enabled():
             p1, bn1, k1 = self.fc1.tc_pack()
             p2, bn2, k2 = self.fc2.tc_pack()
@@ -348,6 +362,16 @@ def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None):
         if e1.fc1.quant.p_min != e1.fc2.quant.p_min:
             return None
         y = torch.empty((M, d), dtype=torch.float32, device=x.device)
+        if fused_mlp_ok(d, hidden):
+            p1d, _, _ = e0.fc1.tc_pack(32)
+            p2d, _, _ = e0.fc2.tc_pack()
+            p1s, _, _ = e1.fc1.tc_pack(32)
+            p2s, _, _ = e1.fc2.tc_pack()
+            _lib.call("sa_tc_moe_mlp_fused", _lib.ptr(x), _lib.ptr(plan.perm_dev),
+                      _lib.ptr(plan.counts_dev), _lib.ptr(plan.gate_dev), _lib.ptr(p1d),
+                      _lib.ptr(p2d), _lib.ptr(p1s), _lib.ptr(p2s), _lib.ptr(y), _lib.ptr(res),
+                      M, d, hidden, _stream())
+            return y
         if tc_enabled():
             p1d, bn1, _ = e0.fc1.tc_pack()
             p2d, bn2, _ = e0.fc2.tc_pack()
