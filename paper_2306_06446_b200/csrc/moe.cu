@@ -216,21 +216,33 @@ __global__ void __launch_bounds__(kRouteTok, 3) ln_route_kernel(
     float* __restrict__ y, int64_t M, float eps, int nr, const float* __restrict__ wg0,
     const float* __restrict__ wg1, const float* __restrict__ wg2, float tie_thresh,
     int32_t* __restrict__ expert_of, float* __restrict__ gate, int32_t* __restrict__ block_cnt1) {
+  constexpr int PITCH = D + 4;  // floats; keeps the per-thread row reads 4-wavefront
   __shared__ double sw[kMaxRouters][2 * D];
   __shared__ int wcnt[kMaxRouters][kRouteTok / 32];
+  extern __shared__ __align__(16) float tile[];  // [kRouteTok][PITCH]
   const float* wgs[kMaxRouters] = {wg0, wg1, wg2};
   for (int r = 0; r < nr; ++r)
     for (int i = threadIdx.x; i < 2 * D; i += kRouteTok) sw[r][i] = double(wgs[r][i]);
+  // coalesced stage-in of the block's rows (one contiguous run of float4s)
+  const int64_t row0 = int64_t(blockIdx.x) * kRouteTok;
+  const int nrows = int(min(int64_t(kRouteTok), M - row0));
+  {
+    const float4* src = reinterpret_cast<const float4*>(x + row0 * D);
+    for (int i = threadIdx.x; i < nrows * (D / 4); i += kRouteTok) {
+      const int rr = i / (D / 4), c4 = i % (D / 4);
+      *reinterpret_cast<float4*>(tile + rr * PITCH + 4 * c4) = __ldg(src + i);
+    }
+  }
   __syncthreads();
-  const int64_t row = int64_t(blockIdx.x) * kRouteTok + threadIdx.x;
+  const int64_t row = row0 + threadIdx.x;
   const bool ok = row < M;
   float v[D];
+  float* trow = tile + threadIdx.x * PITCH;
   if (ok) {
-    const float4* xr = reinterpret_cast<const float4*>(x + row * D);
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < D / 4; ++i) {
-      const float4 q = __ldg(xr + i);
+      const float4 q = *reinterpret_cast<const float4*>(trow + 4 * i);
       v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
       s += (q.x + q.y) + (q.z + q.w);
     }
@@ -242,7 +254,6 @@ __global__ void __launch_bounds__(kRouteTok, 3) ln_route_kernel(
       q2 += v[i] * v[i];
     }
     const float inv = 1.0f / sqrtf(q2 / float(D) + eps);
-    float4* yr = reinterpret_cast<float4*>(y + row * D);
 #pragma unroll
     for (int i = 0; i < D / 4; ++i) {
       const float4 g = __ldg(reinterpret_cast<const float4*>(gain) + i);
@@ -251,7 +262,16 @@ __global__ void __launch_bounds__(kRouteTok, 3) ln_route_kernel(
       v[4 * i + 1] = v[4 * i + 1] * inv * g.y + b.y;
       v[4 * i + 2] = v[4 * i + 2] * inv * g.z + b.z;
       v[4 * i + 3] = v[4 * i + 3] * inv * g.w + b.w;
-      yr[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      *reinterpret_cast<float4*>(trow + 4 * i) =
+          make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+  }
+  __syncthreads();
+  {  // coalesced write-back of the normalized rows
+    float4* dst = reinterpret_cast<float4*>(y + row0 * D);
+    for (int i = threadIdx.x; i < nrows * (D / 4); i += kRouteTok) {
+      const int rr = i / (D / 4), c4 = i % (D / 4);
+      dst[i] = *reinterpret_cast<const float4*>(tile + rr * PITCH + 4 * c4);
     }
   }
   for (int r = 0; r < nr; ++r) {
@@ -302,12 +322,16 @@ extern "C" int sa_ln_route(const float* x, const float* gain, const float* bias,
   const int nb = int(cdiv(M, kRouteTok));
   int32_t* block_cnt1 = static_cast<int32_t*>(ws);
   int32_t* block_off1 = block_cnt1 + size_t(nb) * nr;
-  if (d == 32)
-    ln_route_kernel<32><<<nb, kRouteTok, 0, s>>>(x, gain, bias, y, M, eps, nr, wg0, wg1, wg2,
-                                                 tie_thresh, expert_of, gate, block_cnt1);
-  else
-    ln_route_kernel<64><<<nb, kRouteTok, 0, s>>>(x, gain, bias, y, M, eps, nr, wg0, wg1, wg2,
-                                                 tie_thresh, expert_of, gate, block_cnt1);
+  if (d == 32) {
+    const int smem = kRouteTok * (32 + 4) * 4;
+    ln_route_kernel<32><<<nb, kRouteTok, smem, s>>>(x, gain, bias, y, M, eps, nr, wg0, wg1,
+                                                    wg2, tie_thresh, expert_of, gate, block_cnt1);
+  } else {
+    const int smem = kRouteTok * (64 + 4) * 4;
+    cudaFuncSetAttribute(ln_route_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    ln_route_kernel<64><<<nb, kRouteTok, smem, s>>>(x, gain, bias, y, M, eps, nr, wg0, wg1,
+                                                    wg2, tie_thresh, expert_of, gate, block_cnt1);
+  }
   route_scan_kernel<<<nr, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
   partition_kernel<<<dim3(nb, nr), kRouteTok, 0, s>>>(expert_of, block_off1, counts, M, perm);
   count_launch(3);
