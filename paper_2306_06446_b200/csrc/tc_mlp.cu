@@ -29,7 +29,7 @@ using namespace tc;
 
 constexpr int HC = 32;                 // hidden chunk (fc1 N, fc2 K)
 constexpr int NB = 4;                  // acc1 / A2 buffers
-constexpr int LOOK = 2;                // fc1 lookahead over fc2
+constexpr int LOOK = 3;                // fc1 lookahead over fc2 (< NB)
 constexpr int kThreads = 480;
 constexpr int kMma = 12, kW1 = 13, kW2 = 14;
 constexpr uint32_t kPlane32 = 128 * 32 * 2;   // one 128-row x 32-k bf16 plane
@@ -228,69 +228,94 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
       const uint8_t pa_tab[6] = {2, 1, 0, 1, 0, 0};
       const uint8_t pb_dense[6] = {0, 1, 2, 0, 1, 0};
       const uint32_t sbase = smem_u32(smem);
-      int64_t q0 = 0;
-      int64_t j = 0;
-      for (int64_t m = blockIdx.x; m < ntile; m += gridDim.x) {
-        int e;
-        int64_t r0, r1;
-        if (!mlp_tile(p, c0, m, e, r0, r1)) continue;
-        const int abuf = int(j % L::NA);
-        const uint32_t aph = par(j / L::NA);
-        const int ob = int(j & 1);
-        const uint32_t oph = par(j >> 1);
-        ++j;
-        const int np = p.np[e];
-        const int npairs = np == 1 ? 3 : 6;
-        const uint32_t a1 = sbase + L::OFF_A1 + abuf * L::A1;
-        const uint32_t d2 = tmem + uint32_t(NB * HC + ob * D);
-        mbar_wait(&a1_full[abuf], aph);
-        tc_fence_after();
-        for (int c = 0; c < nchunk + LOOK; ++c) {
-          if (c < nchunk) {  // ---- fc1(q)
-            const int64_t q = q0 + c;
-            const int b = int(q % NB), ws = int(q % L::NW);
-            mbar_wait(&w1_full[ws], par(q / L::NW));
-            mbar_wait(&h_empty[b], par(q / NB) ^ 1u);   // acc1[b] drained (GELU(q - NB))
-            tc_fence_after();
-            const uint32_t w1 = sbase + L::OFF_W1 + ws * L::W1C;
-            const uint32_t d1 = tmem + uint32_t(b * HC);
-            for (int kc = 0; kc < L::KC1; ++kc)
-#pragma unroll
-              for (int ks = 0; ks < 2; ++ks)
-                for (int i = 0; i < npairs; ++i) {
-                  const int pb = np == 1 ? 0 : pb_dense[i];
-                  const uint64_t ad = smem_desc(a1 + (kc * 3 + pa_tab[i]) * kPlane32 + ks * 256);
-                  const uint64_t bd = smem_desc(w1 + (kc * np + pb) * (HC * 32 * 2) + ks * 256);
-                  mma_bf16(d1, ad, bd, id1, (kc | ks | i) != 0 ? 1u : 0u);
-                }
-            mma_commit(&h_full[b]);
-            mma_commit(&w1_empty[ws]);
-            if (c == nchunk - 1) mma_commit(&a1_empty[abuf]);  // A1 fully consumed
+      // Two cursors walk the CTA's chunk sequence continuously across tiles:
+      // fc1 runs LOOK chunks ahead of fc2, so the next tile's fc1 overlaps the
+      // current tile's GELU / fc2 tail (no per-tile drain).
+      struct Cur {
+        int64_t m, j, q;   // tile index, ordinal of the tile in this CTA, chunk counter
+        int c, e;
+        bool ok;
+      };
+      auto first_tile = [&](Cur& u, int64_t m) {
+        u.ok = false;
+        for (; m < ntile; m += gridDim.x) {
+          int64_t r0, r1;
+          if (mlp_tile(p, c0, m, u.e, r0, r1)) {
+            u.m = m;
+            u.ok = true;
+            return;
           }
-          if (c >= LOOK) {   // ---- fc2(q)
-            const int cc = c - LOOK;
-            const int64_t q = q0 + cc;
-            const int b = int(q % NB), ws = int(q % L::NW);
-            if (cc == 0) mbar_wait(&o_empty[ob], oph ^ 1u);   // acc2[ob] drained (tile j-2)
-            mbar_wait(&w2_full[ws], par(q / L::NW));
-            mbar_wait(&h_empty[b], par(q / NB));            // GELU(q) wrote A2[b]
-            tc_fence_after();
-            const uint32_t a2 = sbase + L::OFF_A2 + b * L::A2;
-            const uint32_t w2 = sbase + L::OFF_W2 + ws * L::W2C;
+        }
+      };
+      auto advance = [&](Cur& u) {
+        ++u.q;
+        if (++u.c == nchunk) {
+          u.c = 0;
+          ++u.j;
+          first_tile(u, u.m + gridDim.x);
+        }
+      };
+      Cur A, B;
+      A.j = B.j = 0;
+      A.q = B.q = 0;
+      A.c = B.c = 0;
+      first_tile(A, blockIdx.x);
+      first_tile(B, blockIdx.x);
+      int lead = 0;
+      while (A.ok || B.ok) {
+        if (A.ok) {  // ---- fc1(A.q)
+          const int np = p.np[A.e];
+          const int npairs = np == 1 ? 3 : 6;
+          const int abuf = int(A.j % L::NA);
+          const uint32_t a1 = sbase + L::OFF_A1 + abuf * L::A1;
+          if (A.c == 0) mbar_wait(&a1_full[abuf], par(A.j / L::NA));
+          const int b = int(A.q % NB), ws = int(A.q % L::NW);
+          mbar_wait(&w1_full[ws], par(A.q / L::NW));
+          mbar_wait(&h_empty[b], par(A.q / NB) ^ 1u);   // acc1[b] drained (GELU(q - NB))
+          tc_fence_after();
+          const uint32_t w1 = sbase + L::OFF_W1 + ws * L::W1C;
+          const uint32_t d1 = tmem + uint32_t(b * HC);
+          for (int kc = 0; kc < L::KC1; ++kc)
 #pragma unroll
             for (int ks = 0; ks < 2; ++ks)
               for (int i = 0; i < npairs; ++i) {
                 const int pb = np == 1 ? 0 : pb_dense[i];
-                const uint64_t ad = smem_desc(a2 + pa_tab[i] * kPlane32 + ks * 256);
-                const uint64_t bd = smem_desc(w2 + pb * (D * 32 * 2) + ks * 256);
-                mma_bf16(d2, ad, bd, id2, (cc | ks | i) != 0 ? 1u : 0u);
+                const uint64_t ad = smem_desc(a1 + (kc * 3 + pa_tab[i]) * kPlane32 + ks * 256);
+                const uint64_t bd = smem_desc(w1 + (kc * np + pb) * (HC * 32 * 2) + ks * 256);
+                mma_bf16(d1, ad, bd, id1, (kc | ks | i) != 0 ? 1u : 0u);
               }
-            mma_commit(&a2_empty[b]);
-            mma_commit(&w2_empty[ws]);
-          }
+          mma_commit(&h_full[b]);
+          mma_commit(&w1_empty[ws]);
+          if (A.c == nchunk - 1) mma_commit(&a1_empty[abuf]);  // A1 fully consumed
+          advance(A);
+          ++lead;
         }
-        mma_commit(&o_full[ob]);
-        q0 += nchunk;
+        if (B.ok && (lead > LOOK || !A.ok)) {   // ---- fc2(B.q)
+          const int np = p.np[B.e];
+          const int npairs = np == 1 ? 3 : 6;
+          const int ob = int(B.j & 1);
+          const uint32_t d2 = tmem + uint32_t(NB * HC + ob * D);
+          if (B.c == 0) mbar_wait(&o_empty[ob], par(B.j >> 1) ^ 1u);   // acc2[ob] drained
+          const int b = int(B.q % NB), ws = int(B.q % L::NW);
+          mbar_wait(&w2_full[ws], par(B.q / L::NW));
+          mbar_wait(&h_empty[b], par(B.q / NB));            // GELU(q) wrote A2[b]
+          tc_fence_after();
+          const uint32_t a2 = sbase + L::OFF_A2 + b * L::A2;
+          const uint32_t w2 = sbase + L::OFF_W2 + ws * L::W2C;
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+            for (int i = 0; i < npairs; ++i) {
+              const int pb = np == 1 ? 0 : pb_dense[i];
+              const uint64_t ad = smem_desc(a2 + pa_tab[i] * kPlane32 + ks * 256);
+              const uint64_t bd = smem_desc(w2 + pb * (D * 32 * 2) + ks * 256);
+              mma_bf16(d2, ad, bd, id2, (B.c | ks | i) != 0 ? 1u : 0u);
+            }
+          mma_commit(&a2_empty[b]);
+          mma_commit(&w2_empty[ws]);
+          if (B.c == nchunk - 1) mma_commit(&o_full[ob]);
+          advance(B);
+          --lead;
+        }
       }
     }
     __syncwarp();
