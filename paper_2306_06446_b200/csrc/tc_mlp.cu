@@ -46,7 +46,12 @@ struct MlpParams {
   int np[2];                 // planes per expert (3 dense, 1 shift)
   int64_t M;
   int hidden;
+  unsigned long long* prof;  // optional: cycles per wait site (debug builds of the timeline)
 };
+
+// wait-site ids for the optional cycle profile
+enum { P_A1E = 0, P_W1E, P_W2E, P_A1F, P_W1F, P_HE1, P_OE, P_W2F, P_HE2, P_HF, P_A2E, P_OF,
+       P_T_PROD, P_T_MMA, P_T_GELU, P_NSITE };
 
 template <int D>
 struct Layout {
@@ -119,6 +124,19 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_BAR + L::NBAR * 8);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ unsigned long long sprof[P_NSITE];
+  if (tid < P_NSITE) sprof[tid] = 0;
+  const long long t_start = clock64();
+#define PWAIT(site, b, par_)                                        \
+  do {                                                              \
+    if (p.prof) {                                                   \
+      const long long t0_ = clock64();                              \
+      mbar_wait(b, par_);                                           \
+      if (lane == 0) atomicAdd(&sprof[site], (unsigned long long)(clock64() - t0_)); \
+    } else {                                                        \
+      mbar_wait(b, par_);                                           \
+    }                                                               \
+  } while (0)
   if (warp == kMma) tmem_alloc<L::TCOLS>(tmem_slot);
   if (tid == 0) {
     for (int i = 0; i < L::NA; ++i) {
@@ -177,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
         for (int i = 0; i < 8; ++i)
           v[kc][i] = rowp[i] ? __ldg(reinterpret_cast<const float4*>(rowp[i] + kc * 32 + k4))
                              : make_float4(0.f, 0.f, 0.f, 0.f);
-      mbar_wait(&a1_empty[buf], ph ^ 1u);
+      PWAIT(P_A1E, &a1_empty[buf], ph ^ 1u);
       uint8_t* a1 = smem + L::OFF_A1 + buf * L::A1;
 #pragma unroll
       for (int kc = 0; kc < L::KC1; ++kc)
@@ -213,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
         const uint16_t* src0 = first ? p.w1[e] : p.w2[e];
         for (int c = 0; c < nchunk; ++c, ++q) {
           const int s = int(q % L::NW);
-          mbar_wait(&empty[s], par(q / L::NW) ^ 1u);
+          PWAIT(first ? P_W1E : P_W2E, &empty[s], par(q / L::NW) ^ 1u);
           mbar_expect_tx(&full[s], bytes);
           bulk_g2s(ring + s * slot_bytes, src0 + size_t(c) * (bytes / 2), bytes, &full[s]);
         }
@@ -268,10 +286,10 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
           const int npairs = np == 1 ? 3 : 6;
           const int abuf = int(A.j % L::NA);
           const uint32_t a1 = sbase + L::OFF_A1 + abuf * L::A1;
-          if (A.c == 0) mbar_wait(&a1_full[abuf], par(A.j / L::NA));
+          if (A.c == 0) PWAIT(P_A1F, &a1_full[abuf], par(A.j / L::NA));
           const int b = int(A.q % NB), ws = int(A.q % L::NW);
-          mbar_wait(&w1_full[ws], par(A.q / L::NW));
-          mbar_wait(&h_empty[b], par(A.q / NB) ^ 1u);   // acc1[b] drained (GELU(q - NB))
+          PWAIT(P_W1F, &w1_full[ws], par(A.q / L::NW));
+          PWAIT(P_HE1, &h_empty[b], par(A.q / NB) ^ 1u);   // acc1[b] drained (GELU(q - NB))
           tc_fence_after();
           const uint32_t w1 = sbase + L::OFF_W1 + ws * L::W1C;
           const uint32_t d1 = tmem + uint32_t(b * HC);
@@ -295,10 +313,10 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
           const int npairs = np == 1 ? 3 : 6;
           const int ob = int(B.j & 1);
           const uint32_t d2 = tmem + uint32_t(NB * HC + ob * D);
-          if (B.c == 0) mbar_wait(&o_empty[ob], par(B.j >> 1) ^ 1u);   // acc2[ob] drained
+          if (B.c == 0) PWAIT(P_OE, &o_empty[ob], par(B.j >> 1) ^ 1u);   // acc2[ob] drained
           const int b = int(B.q % NB), ws = int(B.q % L::NW);
-          mbar_wait(&w2_full[ws], par(B.q / L::NW));
-          mbar_wait(&h_empty[b], par(B.q / NB));            // GELU(q) wrote A2[b]
+          PWAIT(P_W2F, &w2_full[ws], par(B.q / L::NW));
+          PWAIT(P_HE2, &h_empty[b], par(B.q / NB));            // GELU(q) wrote A2[b]
           tc_fence_after();
           const uint32_t a2 = sbase + L::OFF_A2 + b * L::A2;
           const uint32_t w2 = sbase + L::OFF_W2 + ws * L::W2C;
@@ -338,8 +356,8 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
         if (int(q & 1) != g) continue;
         const int b = int(q % NB);
         const uint32_t ph = par(q / NB);
-        mbar_wait(&h_full[b], ph);            // fc1(q) done
-        mbar_wait(&a2_empty[b], ph ^ 1u);     // fc2(q - NB) finished reading A2[b]
+        PWAIT(P_HF, &h_full[b], ph);            // fc1(q) done
+        PWAIT(P_A2E, &a2_empty[b], ph ^ 1u);     // fc2(q - NB) finished reading A2[b]
         tc_fence_after();
         float v[32];
         {
@@ -388,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
       int64_t* rt = rowtab + g * 128;
       asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");   // previous table consumed
       rt[rl] = orow;
-      mbar_wait(&o_full[ob], oph);
+      PWAIT(P_OF, &o_full[ob], oph);
       tc_fence_after();
       asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
 #pragma unroll 1
@@ -420,18 +438,30 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
       mbar_arrive(&o_empty[ob]);
     }
   }
+  if (p.prof && lane == 0) {
+    const int site = warp < 8 ? P_T_GELU : (warp < 12 ? P_T_PROD : (warp == kMma ? P_T_MMA : -1));
+    if (site >= 0) atomicAdd(&sprof[site], (unsigned long long)(clock64() - t_start));
+  }
+#undef PWAIT
   tc_fence_before();
   __syncthreads();
+  if (p.prof && tid < P_NSITE) atomicAdd(p.prof + tid, sprof[tid]);
   if (warp == kMma) tmem_dealloc<L::TCOLS>(tmem);
 }
 
 }  // namespace tcm
+
+static unsigned long long* g_mlp_prof = nullptr;
+extern "C" void sa_debug_mlp_profile(void* dev_buf) {
+  g_mlp_prof = static_cast<unsigned long long*>(dev_buf);
+}
 
 static int g_sms_mlp = 0;
 
 static int mlp_launch(tcm::MlpParams& p, int d, cudaStream_t s) {
   using namespace tcm;
   if (p.M == 0) return SA_OK;
+  p.prof = g_mlp_prof;
   if (g_sms_mlp == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
