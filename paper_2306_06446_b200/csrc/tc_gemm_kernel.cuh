@@ -113,7 +113,9 @@ __host__ __device__ inline size_t tc_fixed_smem() {
 
 template <int BN, int AM>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // the swizzle pattern keys on absolute address bits: align the carve-out to 1 KB
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr uint32_t TCOLS = TmemCols<BN>::value;
   constexpr uint32_t kPlaneB = BN * kBK * 2;
   const int S = p.stages;

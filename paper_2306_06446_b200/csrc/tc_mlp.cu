@@ -73,7 +73,7 @@ struct Layout {
   // barriers: a1 full/empty[NA], w1 full/empty[NW], w2 full/empty[NW],
   //           h_full/h_empty/a2_empty[NB], o_full/o_empty[2]
   static constexpr uint32_t NBAR = 2 * NA + 4 * NW + 3 * NB + 4;
-  static constexpr uint32_t TOTAL = OFF_BAR + NBAR * 8 + 16;
+  static constexpr uint32_t TOTAL = OFF_BAR + NBAR * 8 + 16 + 1024;  // + alignment slack
   static constexpr uint32_t TCOLS = NB * HC + 2 * D <= 256 ? 256 : 512;  // acc1[NB] + acc2[2]
 };
 
@@ -107,7 +107,9 @@ __device__ __forceinline__ uint32_t par(int64_t use) { return uint32_t(use) & 1u
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
   using L = Layout<D>;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // the swizzle pattern keys on absolute address bits: align the carve-out to 1 KB
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* a1_full = bar;
   uint64_t* a1_empty = a1_full + L::NA;

@@ -1,0 +1,62 @@
+// Microbenchmark probe (diagnostics only): issue rate of tcgen05.mma kind::f16
+// M=128 with both operands in shared memory, for a given N and operand layout.
+// One CTA, one issuing thread, `iters` dependent-accumulate MMAs into one TMEM
+// accumulator; reports clock64 cycles per MMA. Used to size the GEMM tiles.
+#include "tc_common.cuh"
+
+namespace sa {
+namespace tcp {
+
+using namespace tc;
+
+__global__ void __launch_bounds__(128, 1) mma_probe_kernel(int n, int iters, int layout,
+                                                           unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < (128 + 256) * 64 / 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  if (tid < 32) tmem_alloc<256>(&slot);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (tid == 0) {
+    const uint32_t a = smem_u32(smem), b = a + 128 * 64;
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) |
+                           (uint32_t(128 >> 4) << 24);
+    auto desc = [&](uint32_t s) -> uint64_t {
+      if (layout == 0)  // interleaved, LBO 128, SBO 512
+        return uint64_t((s >> 4) & 0x3FFFu) | (uint64_t(128 >> 4) << 16) |
+               (uint64_t(512 >> 4) << 32) | (uint64_t(1) << 46);
+      return smem_desc(s);  // SWIZZLE_64B
+    };
+    const uint64_t ad = desc(a), bd = desc(b);
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) mma_bf16(tmem, ad, bd, idesc, i > 0 ? 1u : 0u);
+    const long long t1 = clock64();
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    const long long t2 = clock64();
+    out[0] = (unsigned long long)(t1 - t0);
+    out[1] = (unsigned long long)(t2 - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 32) tmem_dealloc<256>(tmem);
+}
+
+}  // namespace tcp
+}  // namespace sa
+
+extern "C" int sa_probe_mma(int n, int iters, int layout, unsigned long long* out, void* stream) {
+  const int smem = (128 + 256) * 64 + 1024;
+  sa::tcp::mma_probe_kernel<<<1, 128, smem, sa::as_stream(stream)>>>(n, iters, layout, out);
+  return cudaGetLastError() == cudaSuccess ? SA_OK : SA_ERR_CUDA;
+}

@@ -92,7 +92,7 @@ static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cu
     return SA_ERR_VALUE;
   }
   p.stages = stages;
-  const size_t smem = size_t(stages) * stage_bytes + fixed;
+  const size_t smem = size_t(stages) * stage_bytes + fixed + 1024;  // + 1 KB alignment slack
   const int64_t tiles = m_tiles_max * p.ntiles;
   const int grid = int(tiles < num_sms() ? tiles : num_sms());
 #define SA_TC_CASE(BNV)                                                                          \
