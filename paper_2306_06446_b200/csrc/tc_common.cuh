@@ -26,15 +26,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// 64-byte-swizzled K-major layout (UMMA layout type SWIZZLE_64B): each row of
-// a 32-wide K stage is 64 contiguous bytes (four 16-byte chunks), eight rows
-// form a 512-byte atom, and the hardware XORs address bits [4:5] with bits
-// [7:8] — i.e. chunk c of row r is stored at chunk c ^ ((r >> 1) & 3). The
-// non-swizzled "interleaved" layout starves the tensor core on shared-memory
-// reads (measured ~180 cycles per 128x32x16 MMA); buffers are 512 B aligned.
+// Interleaved (SWIZZLE_NONE) K-major layout: core matrices of 8 rows x 16 B.
+// (A probe, scripts/probe_mma.py, measured the same tcgen05.mma rate for this
+// layout and for SWIZZLE_64B: ~46 cycles per 128x32x16 MMA, 64 at N=128,
+// 128 at N=256 — the per-instruction floor, not shared-memory bandwidth.)
 __host__ __device__ __forceinline__ uint32_t plane_offset(int r, int k) {
-  return uint32_t(r) * 64u + ((uint32_t(k >> 3) ^ (uint32_t(r >> 1) & 3u)) << 4) +
-         uint32_t(k & 7) * 2u;
+  return uint32_t(r >> 3) * kSBO + uint32_t(k >> 3) * kLBO + uint32_t(r & 7) * 16 +
+         uint32_t(k & 7) * 2;
 }
 
 // ---- mbarrier -------------------------------------------------------------
@@ -135,14 +133,37 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 
 // ---- descriptors ----------------------------------------------------------
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
-  // start >> 4 | LBO (unused for swizzled K-major, 16 B) | SBO = 512 B between
-  // 8-row groups | version 1 | layout type 4 = SWIZZLE_64B
-  return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(1) << 16) |
-         (uint64_t(kSBO >> 4) << 32) | (uint64_t(1) << 46) | (uint64_t(4) << 61);
+  // start >> 4 | LBO = 128 B (next 8 k) | SBO = 512 B (next 8 rows) | version 1 |
+  // layout type 0 = SWIZZLE_NONE
+  return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(kLBO >> 4) << 16) |
+         (uint64_t(kSBO >> 4) << 32) | (uint64_t(1) << 46);
 }
 // kind::f16, A = B = BF16, D = F32, K-major A and B, M = 128
 __host__ __device__ constexpr uint32_t idesc_bf16_m128(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
+
+// One 16-deep K step of a split-precision product: every (A plane, B plane)
+// pair whose combined weight is >= 2^-16, accumulated into d_tmem.
+// NPB = 1 (shift weights, exact in bf16): lo·w, mid·w, hi·w.
+// NPB = 3 (dense weights): lo·hi, mid·mid, hi·lo, mid·hi, hi·mid, hi·hi.
+// Descriptors are pre-built for plane 0 of A and B; the other planes are
+// constant byte offsets added to the 14-bit start-address field (addr >> 4),
+// so the unrolled chain is just 64-bit adds and UTCHMMA issues.
+template <int NPB>
+__device__ __forceinline__ void mma_split_step(uint32_t d_tmem, uint64_t a0, uint64_t b0,
+                                               uint32_t a_plane_bytes, uint32_t b_plane_bytes,
+                                               uint32_t idesc, bool accumulate) {
+  constexpr int NP = NPB == 1 ? 3 : 6;
+  constexpr int pa[6] = {2, 1, 0, 1, 0, 0};
+  constexpr int pb1[6] = {0, 0, 0, 0, 0, 0};
+  constexpr int pb3[6] = {0, 1, 2, 0, 1, 0};
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const int bpl = NPB == 1 ? pb1[i] : pb3[i];
+    mma_bf16(d_tmem, a0 + uint64_t((pa[i] * a_plane_bytes) >> 4),
+             b0 + uint64_t((bpl * b_plane_bytes) >> 4), idesc, (accumulate || i > 0) ? 1u : 0u);
+  }
 }
 
 // ---- float32 → hi/mid/lo bf16 (hi+mid+lo == x for normal x) ---------------

@@ -232,8 +232,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
     // ================= MMA issuer =================
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_m128(BN);
-      const uint8_t pa_tab[6] = {2, 1, 0, 1, 0, 0};
-      const uint8_t pb_dense[6] = {0, 1, 2, 0, 1, 0};
       const uint32_t smem_base = smem_u32(smem);
       int sg[2] = {0, 0};
       uint32_t phase[2] = {0, 0};
@@ -244,7 +242,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
         if (ti.r0 >= ti.r1) continue;
         const int g = j++ & 1;
         const int npb = p.nplanes[ti.group];
-        const int npairs = npb == 1 ? 3 : 6;
         mbar_wait(&tempty[g], acc_phase[g] ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem + uint32_t(g * BN);
@@ -256,12 +253,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
           const uint32_t sb = sa + 3 * kPlaneA;
 #pragma unroll
           for (int ks = 0; ks < kBK / 16; ++ks) {
-            for (int i = 0; i < npairs; ++i) {
-              const int pb = npb == 1 ? 0 : pb_dense[i];
-              const uint64_t ad = smem_desc(sa + pa_tab[i] * kPlaneA + ks * 256);
-              const uint64_t bd = smem_desc(sb + pb * kPlaneB + ks * 256);
-              mma_bf16(d_tmem, ad, bd, idesc, (kc | ks | i) != 0 ? 1u : 0u);
-            }
+            const uint64_t ad = smem_desc(sa + ks * 256);
+            const uint64_t bd = smem_desc(sb + ks * 256);
+            if (npb == 1)
+              mma_split_step<1>(d_tmem, ad, bd, kPlaneA, kPlaneB, idesc, (kc | ks) != 0);
+            else
+              mma_split_step<3>(d_tmem, ad, bd, kPlaneA, kPlaneB, idesc, (kc | ks) != 0);
           }
           mma_commit(&empty[s]);
           if (++sg[g] == SG) {

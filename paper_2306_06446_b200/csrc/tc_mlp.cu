@@ -245,8 +245,6 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
     if (lane == 0) {
       constexpr uint32_t id1 = idesc_bf16_m128(HC);
       constexpr uint32_t id2 = idesc_bf16_m128(D);
-      const uint8_t pa_tab[6] = {2, 1, 0, 1, 0, 0};
-      const uint8_t pb_dense[6] = {0, 1, 2, 0, 1, 0};
       const uint32_t sbase = smem_u32(smem);
       // Two cursors walk the CTA's chunk sequence continuously across tiles:
       // fc1 runs LOOK chunks ahead of fc2, so the next tile's fc1 overlaps the
@@ -285,7 +283,6 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
       while (A.ok || B.ok) {
         if (A.ok) {  // ---- fc1(A.q)
           const int np = p.np[A.e];
-          const int npairs = np == 1 ? 3 : 6;
           const int abuf = int(A.j % L::NA);
           const uint32_t a1 = sbase + L::OFF_A1 + abuf * L::A1;
           if (A.c == 0) PWAIT(P_A1F, &a1_full[abuf], par(A.j / L::NA));
@@ -295,15 +292,17 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
           tc_fence_after();
           const uint32_t w1 = sbase + L::OFF_W1 + ws * L::W1C;
           const uint32_t d1 = tmem + uint32_t(b * HC);
+#pragma unroll
           for (int kc = 0; kc < L::KC1; ++kc)
 #pragma unroll
-            for (int ks = 0; ks < 2; ++ks)
-              for (int i = 0; i < npairs; ++i) {
-                const int pb = np == 1 ? 0 : pb_dense[i];
-                const uint64_t ad = smem_desc(a1 + (kc * 3 + pa_tab[i]) * kPlane32 + ks * 256);
-                const uint64_t bd = smem_desc(w1 + (kc * np + pb) * (HC * 32 * 2) + ks * 256);
-                mma_bf16(d1, ad, bd, id1, (kc | ks | i) != 0 ? 1u : 0u);
-              }
+            for (int ks = 0; ks < 2; ++ks) {
+              const uint64_t ad = smem_desc(a1 + kc * 3 * kPlane32 + ks * 256);
+              const uint64_t bd = smem_desc(w1 + kc * np * (HC * 32 * 2) + ks * 256);
+              if (np == 1)
+                mma_split_step<1>(d1, ad, bd, kPlane32, HC * 32 * 2, id1, (kc | ks) != 0);
+              else
+                mma_split_step<3>(d1, ad, bd, kPlane32, HC * 32 * 2, id1, (kc | ks) != 0);
+            }
           mma_commit(&h_full[b]);
           mma_commit(&w1_empty[ws]);
           if (A.c == nchunk - 1) mma_commit(&a1_empty[abuf]);  // A1 fully consumed
@@ -312,7 +311,6 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
         }
         if (B.ok && (lead > LOOK || !A.ok)) {   // ---- fc2(B.q)
           const int np = p.np[B.e];
-          const int npairs = np == 1 ? 3 : 6;
           const int ob = int(B.j & 1);
           const uint32_t d2 = tmem + uint32_t(NB * HC + ob * D);
           if (B.c == 0) PWAIT(P_OE, &o_empty[ob], par(B.j >> 1) ^ 1u);   // acc2[ob] drained
@@ -323,13 +321,14 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
           const uint32_t a2 = sbase + L::OFF_A2 + b * L::A2;
           const uint32_t w2 = sbase + L::OFF_W2 + ws * L::W2C;
 #pragma unroll
-          for (int ks = 0; ks < 2; ++ks)
-            for (int i = 0; i < npairs; ++i) {
-              const int pb = np == 1 ? 0 : pb_dense[i];
-              const uint64_t ad = smem_desc(a2 + pa_tab[i] * kPlane32 + ks * 256);
-              const uint64_t bd = smem_desc(w2 + pb * (D * 32 * 2) + ks * 256);
-              mma_bf16(d2, ad, bd, id2, (B.c | ks | i) != 0 ? 1u : 0u);
-            }
+          for (int ks = 0; ks < 2; ++ks) {
+            const uint64_t ad = smem_desc(a2 + ks * 256);
+            const uint64_t bd = smem_desc(w2 + ks * 256);
+            if (np == 1)
+              mma_split_step<1>(d2, ad, bd, kPlane32, D * 32 * 2, id2, (B.c | ks) != 0);
+            else
+              mma_split_step<3>(d2, ad, bd, kPlane32, D * 32 * 2, id2, (B.c | ks) != 0);
+          }
           mma_commit(&a2_empty[b]);
           mma_commit(&w2_empty[ws]);
           if (B.c == nchunk - 1) mma_commit(&o_full[ob]);
