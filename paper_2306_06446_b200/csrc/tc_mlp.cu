@@ -16,7 +16,7 @@
 //                     lane block); group (tile % 2) also runs the final epilogue
 //                     of the tile: tcgen05.ld acc2, x gate, + residual, scatter
 //   warps  8-11       producers: gather x rows (MoE permutation), split → A1
-//   warp  12          MMA issuer (one thread): fc1 runs two chunks ahead of fc2
+//   warp  12          MMA issuer (one thread): fc1 runs LOOK chunks ahead of fc2
 //   warps 13 / 14     weight streamers: W1 / W2 chunk rings (bulk async copy)
 // Every ring carries full/empty mbarriers; parities derive from the running
 // counters, so tiles of the two experts interleave freely.
@@ -33,6 +33,7 @@ constexpr int LOOK = 3;                // fc1 lookahead over fc2 (< NB)
 constexpr int kThreads = 480;
 constexpr int kMma = 12, kW1 = 13, kW2 = 14;
 constexpr uint32_t kPlane32 = 128 * 32 * 2;   // one 128-row x 32-k bf16 plane
+constexpr int kMaxTiles = 1024;               // per-CTA tile table of the MMA issuer
 
 struct MlpParams {
   const float* x;
@@ -51,7 +52,7 @@ struct MlpParams {
 
 // wait-site ids for the optional cycle profile
 enum { P_A1E = 0, P_W1E, P_W2E, P_A1F, P_W1F, P_HE1, P_OE, P_W2F, P_HE2, P_HF, P_A2E, P_OF,
-       P_T_PROD, P_T_MMA, P_T_GELU, P_NSITE };
+       P_T_PROD, P_T_MMA, P_T_GELU, P_ISS1, P_ISS2, P_NSITE };
 
 template <int D>
 struct Layout {
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __shared__ unsigned long long sprof[P_NSITE];
+  __shared__ uint8_t tile_e[kMaxTiles];
   if (tid < P_NSITE) sprof[tid] = 0;
   const long long t_start = clock64();
 #define PWAIT(site, b, par_)                                        \
@@ -246,50 +248,30 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
       constexpr uint32_t id1 = idesc_bf16_m128(HC);
       constexpr uint32_t id2 = idesc_bf16_m128(D);
       const uint32_t sbase = smem_u32(smem);
-      // Two cursors walk the CTA's chunk sequence continuously across tiles:
-      // fc1 runs LOOK chunks ahead of fc2, so the next tile's fc1 overlaps the
-      // current tile's GELU / fc2 tail (no per-tile drain).
-      struct Cur {
-        int64_t m, j, q;   // tile index, ordinal of the tile in this CTA, chunk counter
-        int c, e;
-        bool ok;
-      };
-      auto first_tile = [&](Cur& u, int64_t m) {
-        u.ok = false;
-        for (; m < ntile; m += gridDim.x) {
-          int64_t r0, r1;
-          if (mlp_tile(p, c0, m, u.e, r0, r1)) {
-            u.m = m;
-            u.ok = true;
-            return;
-          }
-        }
-      };
-      auto advance = [&](Cur& u) {
-        ++u.q;
-        if (++u.c == nchunk) {
-          u.c = 0;
-          ++u.j;
-          first_tile(u, u.m + gridDim.x);
-        }
-      };
-      Cur A, B;
-      A.j = B.j = 0;
-      A.q = B.q = 0;
-      A.c = B.c = 0;
-      first_tile(A, blockIdx.x);
-      first_tile(B, blockIdx.x);
-      int lead = 0;
-      while (A.ok || B.ok) {
-        if (A.ok) {  // ---- fc1(A.q)
-          const int np = p.np[A.e];
-          const int abuf = int(A.j % L::NA);
-          const uint32_t a1 = sbase + L::OFF_A1 + abuf * L::A1;
-          if (A.c == 0) PWAIT(P_A1F, &a1_full[abuf], par(A.j / L::NA));
-          const int b = int(A.q % NB), ws = int(A.q % L::NW);
-          PWAIT(P_W1F, &w1_full[ws], par(A.q / L::NW));
-          PWAIT(P_HE1, &h_empty[b], par(A.q / NB) ^ 1u);   // acc1[b] drained (GELU(q - NB))
+      // The CTA's non-empty tiles in order (expert of each); chunk q of the
+      // CTA's sequence belongs to tile q / nchunk. fc1 runs LOOK chunks ahead
+      // of fc2 across tile boundaries, so there is no per-tile drain. All
+      // cursor state stays in registers (32-bit).
+      int nt = 0;
+      for (int64_t m = blockIdx.x; m < ntile && nt < kMaxTiles; m += gridDim.x) {
+        int e;
+        int64_t r0, r1;
+        if (mlp_tile(p, c0, m, e, r0, r1)) tile_e[nt++] = uint8_t(e);
+      }
+      const int np0 = p.np[0], np1 = p.np[1];
+      const int total_q = nt * nchunk;
+      for (int step = 0; step < total_q + LOOK; ++step) {
+        if (step < total_q) {  // ---- fc1(q)
+          const int q = step;
+          const int jt = q / nchunk, c = q - jt * nchunk;
+          const int np = tile_e[jt] ? np1 : np0;
+          const int abuf = jt % L::NA;
+          if (c == 0) PWAIT(P_A1F, &a1_full[abuf], par(jt / L::NA));
+          const int b = q % NB, ws = q % L::NW;
+          PWAIT(P_W1F, &w1_full[ws], par(q / L::NW));
+          PWAIT(P_HE1, &h_empty[b], par(q / NB) ^ 1u);   // acc1[b] drained (GELU(q - NB))
           tc_fence_after();
+          const uint32_t a1 = sbase + L::OFF_A1 + abuf * L::A1;
           const uint32_t w1 = sbase + L::OFF_W1 + ws * L::W1C;
           const uint32_t d1 = tmem + uint32_t(b * HC);
 #pragma unroll
@@ -305,35 +287,33 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
             }
           mma_commit(&h_full[b]);
           mma_commit(&w1_empty[ws]);
-          if (A.c == nchunk - 1) mma_commit(&a1_empty[abuf]);  // A1 fully consumed
-          advance(A);
-          ++lead;
+          if (c == nchunk - 1) mma_commit(&a1_empty[abuf]);  // A1 fully consumed
         }
-        if (B.ok && (lead > LOOK || !A.ok)) {   // ---- fc2(B.q)
-          const int np = p.np[B.e];
-          const int ob = int(B.j & 1);
-          const uint32_t d2 = tmem + uint32_t(NB * HC + ob * D);
-          if (B.c == 0) PWAIT(P_OE, &o_empty[ob], par(B.j >> 1) ^ 1u);   // acc2[ob] drained
-          const int b = int(B.q % NB), ws = int(B.q % L::NW);
-          PWAIT(P_W2F, &w2_full[ws], par(B.q / L::NW));
-          PWAIT(P_HE2, &h_empty[b], par(B.q / NB));            // GELU(q) wrote A2[b]
+        if (step >= LOOK) {   // ---- fc2(q)
+          const int q = step - LOOK;
+          const int jt = q / nchunk, c = q - jt * nchunk;
+          const int np = tile_e[jt] ? np1 : np0;
+          const int ob = jt & 1;
+          if (c == 0) PWAIT(P_OE, &o_empty[ob], par(jt >> 1) ^ 1u);   // acc2[ob] drained
+          const int b = q % NB, ws = q % L::NW;
+          PWAIT(P_W2F, &w2_full[ws], par(q / L::NW));
+          PWAIT(P_HE2, &h_empty[b], par(q / NB));            // GELU(q) wrote A2[b]
           tc_fence_after();
           const uint32_t a2 = sbase + L::OFF_A2 + b * L::A2;
           const uint32_t w2 = sbase + L::OFF_W2 + ws * L::W2C;
+          const uint32_t d2 = tmem + uint32_t(NB * HC + ob * D);
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks) {
             const uint64_t ad = smem_desc(a2 + ks * 256);
             const uint64_t bd = smem_desc(w2 + ks * 256);
             if (np == 1)
-              mma_split_step<1>(d2, ad, bd, kPlane32, D * 32 * 2, id2, (B.c | ks) != 0);
+              mma_split_step<1>(d2, ad, bd, kPlane32, D * 32 * 2, id2, (c | ks) != 0);
             else
-              mma_split_step<3>(d2, ad, bd, kPlane32, D * 32 * 2, id2, (B.c | ks) != 0);
+              mma_split_step<3>(d2, ad, bd, kPlane32, D * 32 * 2, id2, (c | ks) != 0);
           }
           mma_commit(&a2_empty[b]);
           mma_commit(&w2_empty[ws]);
-          if (B.c == nchunk - 1) mma_commit(&o_full[ob]);
-          advance(B);
-          --lead;
+          if (c == nchunk - 1) mma_commit(&o_full[ob]);
         }
       }
     }

@@ -16,7 +16,7 @@ __global__ void __launch_bounds__(128, 1) mma_probe_kernel(int n, int iters, int
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t slot;
   const int tid = threadIdx.x;
-  for (int i = tid; i < (128 + 256) * 64 / 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  for (int i = tid; i < (3 * 8192 + 3 * 256 * 64) / 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0;
   if (tid < 32) tmem_alloc<256>(&slot);
   if (tid == 0) {
     mbar_init(&bar, 1);
@@ -39,7 +39,17 @@ __global__ void __launch_bounds__(128, 1) mma_probe_kernel(int n, int iters, int
     };
     const uint64_t ad = desc(a), bd = desc(b);
     const long long t0 = clock64();
-    for (int i = 0; i < iters; ++i) mma_bf16(tmem, ad, bd, idesc, i > 0 ? 1u : 0u);
+    if (layout < 2) {
+      for (int i = 0; i < iters; ++i) mma_bf16(tmem, ad, bd, idesc, i > 0 ? 1u : 0u);
+    } else {
+      // the GEMM kernels' pattern: 3 A planes (8 KB apart) x 3 B planes, 2 k-steps
+      const uint64_t a2 = desc(smem_u32(smem)), b2 = desc(smem_u32(smem) + 3 * 8192);
+      for (int i = 0; i < iters / 12; ++i)
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+          mma_split_step<3>(tmem, a2 + uint64_t(ks * 16), b2 + uint64_t(ks * 16), 8192,
+                            uint32_t(n) * 64, idesc, (i | ks) != 0);
+    }
     const long long t1 = clock64();
     mma_commit(&bar);
     mbar_wait(&bar, 0);
@@ -56,7 +66,9 @@ __global__ void __launch_bounds__(128, 1) mma_probe_kernel(int n, int iters, int
 }  // namespace sa
 
 extern "C" int sa_probe_mma(int n, int iters, int layout, unsigned long long* out, void* stream) {
-  const int smem = (128 + 256) * 64 + 1024;
+  const int smem = 3 * 8192 + 3 * 256 * 64 + 1024;
+  cudaFuncSetAttribute(sa::tcp::mma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       smem);
   sa::tcp::mma_probe_kernel<<<1, 128, smem, sa::as_stream(stream)>>>(n, iters, layout, out);
   return cudaGetLastError() == cudaSuccess ? SA_OK : SA_ERR_CUDA;
 }

@@ -14,7 +14,7 @@ from oracle import ops  # noqa: E402
 
 SITES = ["prod a1_empty", "w1stream empty", "w2stream empty", "mma a1_full", "mma w1_full",
          "mma h_empty(fc1)", "mma o_empty", "mma w2_full", "mma h_empty(fc2)", "gelu h_full",
-         "gelu a2_empty", "epi o_full", "T prod", "T mma", "T gelu"]
+         "gelu a2_empty", "epi o_full", "T prod", "T mma", "T gelu", "mma issue fc1", "mma issue fc2"]
 lib = _lib.load()
 lib.sa_debug_mlp_profile.argtypes = [ctypes.c_void_p]
 for d, hidden in ((32, 256), (64, 512)):
@@ -28,7 +28,7 @@ for d, hidden in ((32, 256), (64, 512)):
                        MD.MoeConfig())
     x = torch.from_numpy(g.standard_normal((M, d)).astype(np.float32)).cuda()
     mod.forward(x)
-    buf = torch.zeros(16, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(32, dtype=torch.int64, device="cuda")
     lib.sa_debug_mlp_profile(buf.data_ptr())
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
@@ -42,7 +42,7 @@ for d, hidden in ((32, 256), (64, 512)):
     warps = {"prod": 4, "w1": 1, "w2": 1, "mma": 1, "gelu": 8, "epi": 8}
     for i, name in enumerate(SITES):
         key = name.split()[0]
-        w = {"prod": 4, "w1stream": 1, "w2stream": 1, "mma": 1, "gelu": 8, "epi": 4, "T": 1}[key]
+        w = {"prod": 4, "w1stream": 1, "w2stream": 1, "mma": 1, "gelu": 4, "epi": 4, "T": 1}[key]
         if name.startswith("T "):
             w = {"T prod": 4, "T mma": 1, "T gelu": 8}[name]
         print(f"  {name:22s} {v[i] / ncta / w / 1e3:10.1f} kcycles/warp")
