@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-kernels", action="store_true", help="no standalone kernel timings")
     return ap.parse_args()
 
 
@@ -163,11 +164,118 @@ def op_bytes(name, args):
     if name == "sa_layernorm":
         M, d = args[4], args[5]
         return 2 * M * d * A
-    if name == "sa_patch_embed":
-        B, H, W, C, p, _, _, d = args[1:9]
+    if name in ("sa_patch_embed", "sa_tc_patch_embed"):
+        B, H, W, C, p = args[1:6]
+        d = args[8] if name == "sa_patch_embed" else args[9]
         n = (H // p) * (W // p)
         return B * H * W * C * A + B * n * d * A
+    if name == "sa_tc_linear":
+        kind, M, K, N, res = args[2], args[5], args[6], args[7], args[8]
+        return M * K * A + M * N * A + K * N * (2 if kind == 1 else 6) + (M * N * A if res else 0)
+    if name == "sa_tc_moe_linear":
+        M, K, N, res = args[9], args[10], args[11], args[8]
+        return M * K * A + M * N * A + K * N * 8 + (M * N * A if res else 0) + M * 8
+    if name in ("sa_tc_moe_mlp_fused", "sa_tc_moe_mlp"):
+        if name == "sa_tc_moe_mlp_fused":
+            res, M, d, hidden = args[9], args[10], args[11], args[12]
+        else:
+            res, M, d, hidden = args[11], args[12], args[13], args[14]
+        return 2 * M * d * A + (M * d * A if res else 0) + M * 8 + 2 * d * hidden * 8
+    if name in ("sa_tc_mlp_fused", "sa_tc_mlp"):
+        if name == "sa_tc_mlp_fused":
+            M, d, hidden, res = args[6], args[7], args[8], args[9]
+        else:
+            M, d, hidden, res = args[8], args[9], args[10], args[11]
+        return 2 * M * d * A + (M * d * A if res else 0) + 2 * d * hidden * 6
+    if name == "sa_ln_route":
+        M, d, nr = args[4], args[5], args[7]
+        return 2 * M * d * A + nr * M * 12
+    if name == "sa_softmax_attn":
+        B, n, d = args[4], args[5], args[6]
+        return 4 * B * n * d * A
+    if name == "sa_pool":
+        B, n, d = args[2], args[3], args[4]
+        return B * n * d * A
     return None
+
+
+def kernel_microbench(torch, hbm_peak, iters=20):
+    """Standalone timings of the hot-path kernels at the PVTv2-B0 stage-1 shape
+    (B=256, n=3136, d=32; hidden 256): K1 sign-hash, K2a binary attention,
+    K3 shift-Linear (tensor-core variant 0 and literal exponent-add variant 1),
+    K4 route, K5 fused MoE MLP. CUDA events on the launching stream; every
+    kernel streams >= 100 MB of fp32 activations (the 126 MB L2 cannot hold a
+    launch's working set across launches, except K2a's 3 MB of codes); each
+    timing is the mean of `iters` back-to-back launches after one warm-up."""
+    import numpy as np
+    from paper_2306_06446_b200 import _lib, attention as A, model as MD, moe as MOE
+    from paper_2306_06446_b200 import quantize as Q
+    B, n, d, hidden = 256, 3136, 32, 256
+    M = B * n
+    g = np.random.Generator(np.random.PCG64(7))
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    x = dev(g.standard_normal((M, d)).astype(np.float32))
+    v = dev(g.standard_normal((M, d)).astype(np.float32))
+    dw = dev((g.standard_normal((3, 3, d)) * 0.1).astype(np.float32))
+    w1 = (g.standard_normal((d, hidden)) / np.sqrt(d)).astype(np.float32)
+    w2 = (g.standard_normal((hidden, d)) / np.sqrt(hidden)).astype(np.float32)
+    wg = (g.standard_normal((d, 2)) * 0.3).astype(np.float32)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / iters
+
+    rows = []
+
+    def add(kernel, shape, ms, nbytes, bound="hbm", flops=None):
+        ach = nbytes / 1e9 / (ms / 1e3)
+        r = {"kernel": kernel, "shape": shape, "ms": ms, "bytes": nbytes, "bound": bound,
+             "achieved_gbs": ach, "frac_hbm": ach / hbm_peak}
+        if flops:
+            r["gops"] = flops / 1e9 / (ms / 1e3)
+        rows.append(r)
+
+    cq, gq = Q.sign_hash(x, 1, B)
+    ck, gk = Q.sign_hash(v, 1, B)
+    add("K1 sign_hash", f"({M},{d}) h=1", timed(lambda: Q.sign_hash(x, 1, B)), M * d * 4 + M * d // 8)
+    add("K2a linear_binary_attn (+dwconv)", f"B={B} n={n} d={d} h=1",
+        timed(lambda: A.binary_core_codes(cq, ck, gq, gk, v, B, 1, dw, A.EPS_NORM, "linear")),
+        2 * M * d // 8 + 2 * M * d * 4)
+    lay = MD.ShiftLinearLayer(w1)
+    y = torch.empty((M, hidden), dtype=torch.float32, device="cuda")
+    pk, bn, kind = lay.tc_pack()
+
+    def k3():
+        _lib.call("sa_tc_linear", _lib.ptr(x), _lib.ptr(pk), kind, bn, _lib.ptr(y), M, d, hidden,
+                  None, 0, _lib.stream())
+    add("K3 shift_linear (tcgen05, variant 0)", f"({M},{d})x({d},{hidden})", timed(k3),
+        M * d * 4 + M * hidden * 4 + d * hidden)
+    xs = x[: M // 16].contiguous()
+    ys = torch.empty((M // 16, hidden), dtype=torch.float32, device="cuda")
+
+    def k3b():
+        _lib.call("sa_shift_linear", _lib.ptr(xs), _lib.ptr(lay.quant.packed), _lib.ptr(ys),
+                  M // 16, d, hidden, -15, 1, _lib.stream())
+    ms_b = timed(k3b)
+    add("K3 shift_linear (literal exponent-add, variant 1)", f"({M // 16},{d})x({d},{hidden})",
+        ms_b, (M // 16) * (d + hidden) * 4 + d * hidden, bound="alu",
+        flops=(M // 16) * d * hidden)
+    add("K4 moe_route (+stable partition)", f"({M},{d})",
+        timed(lambda: MOE.route_plan(x, dev(wg))), M * d * 4 + M * 12)
+    mod = MD.MoeModule(wg, [MD.Mlp(MD.Linear(w1), MD.Linear(w2)),
+                            MD.Mlp(MD.ShiftLinearLayer(w1.copy()),
+                                   MD.ShiftLinearLayer(w2.copy()))], MD.MoeConfig())
+    plan, _ = MOE.route_plan(x, mod.wg.value)
+    add("K5 fused MoE MLP (mult+shift experts)", f"({M},{d}) hidden {hidden}",
+        timed(lambda: mod.forward(x, plan=plan, residual=v)), 3 * M * d * 4 + M * 8)
+    return rows
 
 
 def main():
@@ -300,11 +408,17 @@ def main():
                          "achieved_gbs": ach, "frac_hbm": (ach / hbm_peak) if ach else None})
     ops_rows.sort(key=lambda r: -r["ms_per_fwd"])
     dom = next(r for r in ops_rows if r["achieved_gbs"] is not None)
+    traffic = None
+    tr_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if os.path.exists(tr_path):   # dram bytes per launch from the committed ncu capture
+        traffic = json.load(open(tr_path)).get(dom["op"])
     roofline = {"bound": "hbm", "kernel": dom["op"], "achieved": dom["achieved_gbs"],
                 "peak": hbm_peak, "unit": "GB/s", "frac": dom["frac_hbm"],
-                "traffic": None, "peak_source": peak_src,
+                "traffic": traffic, "peak_source": peak_src,
                 "per_launch_bytes": dom["bytes_per_fwd"] / max(dom["calls_per_fwd"], 1),
-                "ms_per_fwd": dom["ms_per_fwd"]}
+                "ms_per_fwd": dom["ms_per_fwd"],
+                "timing": "CUDA events around each library call inside 3 eager forwards"}
+    kernels = None if args.skip_kernels else kernel_microbench(torch, hbm_peak)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -312,7 +426,8 @@ def main():
             "data": "synthetic uniform(0,1) 224x224x3 images, PCG64 random-init weights",
             "config": config_dict(args, world), "e2e": e2e, "gpu_launches": int(gpu_launches),
             "launches_per_forward": int(per_fwd), "cuda_graph": not args.no_graph,
-            "roofline": roofline, "clocks": clk.summary(), "ops": ops_rows[:12]}
+            "roofline": roofline, "clocks": clk.summary(), "ops": ops_rows[:14],
+            "kernels": kernels}
 
     if rank == 0 and world == 1 and not args.skip_cpu:
         ips, done, el, cores = cpu_reference(spec, 4, args.cpu_seconds)

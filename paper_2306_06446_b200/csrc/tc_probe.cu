@@ -13,13 +13,14 @@ __global__ void __launch_bounds__(128, 1) mma_probe_kernel(int n, int iters, int
                                                            unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar, bar2;
   __shared__ uint32_t slot;
   const int tid = threadIdx.x;
   for (int i = tid; i < (3 * 8192 + 3 * 256 * 64) / 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0;
   if (tid < 32) tmem_alloc<256>(&slot);
   if (tid == 0) {
     mbar_init(&bar, 1);
+    mbar_init(&bar2, 1);
     fence_barrier_init();
   }
   fence_proxy_async_smem();
@@ -42,13 +43,18 @@ __global__ void __launch_bounds__(128, 1) mma_probe_kernel(int n, int iters, int
     if (layout < 2) {
       for (int i = 0; i < iters; ++i) mma_bf16(tmem, ad, bd, idesc, i > 0 ? 1u : 0u);
     } else {
-      // the GEMM kernels' pattern: 3 A planes (8 KB apart) x 3 B planes, 2 k-steps
+      // the GEMM kernels' pattern: 3 A planes (8 KB apart) x 3 B planes, 2 k-steps;
+      // layout 3: + a tcgen05.commit after every 12 MMAs; layout 4: + alternate
+      // between two accumulators (as fc1 / fc2 do)
       const uint64_t a2 = desc(smem_u32(smem)), b2 = desc(smem_u32(smem) + 3 * 8192);
-      for (int i = 0; i < iters / 12; ++i)
+      for (int i = 0; i < iters / 12; ++i) {
+        const uint32_t dt = (layout == 4 && (i & 1)) ? tmem + 128 : tmem;
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks)
-          mma_split_step<3>(tmem, a2 + uint64_t(ks * 16), b2 + uint64_t(ks * 16), 8192,
+          mma_split_step<3>(dt, a2 + uint64_t(ks * 16), b2 + uint64_t(ks * 16), 8192,
                             uint32_t(n) * 64, idesc, (i | ks) != 0);
+        if (layout >= 3) mma_commit(&bar2);
+      }
     }
     const long long t1 = clock64();
     mma_commit(&bar);

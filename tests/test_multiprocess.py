@@ -1,0 +1,66 @@
+"""Multi-process (world_size 2, gloo, CPU) coverage of the N>1 path: image
+sharding, per-rank forward on the shard, and the single logits all-gather.
+
+The per-rank forward here is the numpy oracle (CPU); the GPU ranks run the
+same sharding/gather code with NCCL. Per-token math is batch independent, so
+the gathered logits must match the unsharded forward (up to BLAS batching
+noise: never require bit equality across batchings)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2306_06446_b200 import dist as D
+from paper_2306_06446_b200 import specs
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, spec, images, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import nets
+        net = nets.build(spec)
+        lo, hi = D.shard_bounds(images.shape[0], rank, world)
+        local = nets.forward(net, images[lo:hi])
+        full = D.gather_logits(torch.from_numpy(local), images.shape[0])
+        if rank == 0:
+            np.save(out_path, full.numpy())
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("batch", [4, 5])
+def test_two_rank_sharded_forward_matches_single(tmp_path, batch):
+    spec = specs.toy_c1(attn_linear_mode="moe", mlp_mode="moe", img=32, d=64, h=4, blocks=1)
+    from oracle import nets, ops
+    images = ops.rng(3).uniform(0, 1, (batch, 32, 32, 3)).astype(np.float32)
+    out = str(tmp_path / "gathered.npy")
+    mp.spawn(_worker, args=(2, _free_port(), spec, images, out), nprocs=2, join=True)
+    gathered = np.load(out)
+    ref = nets.forward(nets.build(spec), images)
+    assert gathered.shape == ref.shape
+    assert np.max(np.abs(gathered - ref)) <= 1e-6 * max(1.0, float(np.max(np.abs(ref))))
+
+
+def test_shard_bounds_cover_exactly():
+    for B in (0, 1, 7, 256, 2048):
+        for N in (1, 2, 3, 4, 8):
+            spans = [D.shard_bounds(B, r, N) for r in range(N)]
+            assert spans[0][0] == 0 and spans[-1][1] == B
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert max(h - l for l, h in spans) - min(h - l for l, h in spans) <= 1
+    with pytest.raises(ValueError):
+        D.shard_bounds(8, 2, 2)
