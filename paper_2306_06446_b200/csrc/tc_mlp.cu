@@ -48,6 +48,7 @@ struct MlpParams {
   int64_t M;
   int hidden;
   unsigned long long* prof;  // optional: cycles per wait site (debug builds of the timeline)
+  int dbg;                   // debug experiments (0 in production)
 };
 
 // wait-site ids for the optional cycle profile
@@ -355,6 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
         uint8_t* a2 = smem + L::OFF_A2 + b * L::A2;
 #pragma unroll
         for (int k8 = 0; k8 < 4; ++k8) {
+          if (p.dbg & 1) break;   // debug experiment: skip GELU + A2 stores
           uint32_t hp[4], mp[4], lp[4];
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
@@ -433,9 +435,11 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
 }  // namespace tcm
 
 static unsigned long long* g_mlp_prof = nullptr;
+static int g_mlp_dbg = 0;
 extern "C" void sa_debug_mlp_profile(void* dev_buf) {
   g_mlp_prof = static_cast<unsigned long long*>(dev_buf);
 }
+extern "C" void sa_debug_mlp_mode(int mode) { g_mlp_dbg = mode; }
 
 static int g_sms_mlp = 0;
 
@@ -443,6 +447,7 @@ static int mlp_launch(tcm::MlpParams& p, int d, cudaStream_t s) {
   using namespace tcm;
   if (p.M == 0) return SA_OK;
   p.prof = g_mlp_prof;
+  p.dbg = g_mlp_dbg;
   if (g_sms_mlp == 0) {
     int dev = 0;
     cudaGetDevice(&dev);

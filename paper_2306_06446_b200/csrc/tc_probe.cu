@@ -54,6 +54,8 @@ __global__ void __launch_bounds__(128, 1) mma_probe_kernel(int n, int iters, int
           mma_split_step<3>(dt, a2 + uint64_t(ks * 16), b2 + uint64_t(ks * 16), 8192,
                             uint32_t(n) * 64, idesc, (i | ks) != 0);
         if (layout >= 3) mma_commit(&bar2);
+        if (layout >= 5) tc_fence_after();      // layout 5: + tcgen05.fence::after_thread_sync
+        if (layout >= 6) tc_fence_before();     // layout 6: + fence::before_thread_sync
       }
     }
     const long long t1 = clock64();
@@ -75,6 +77,8 @@ extern "C" int sa_probe_mma(int n, int iters, int layout, unsigned long long* ou
   const int smem = 3 * 8192 + 3 * 256 * 64 + 1024;
   cudaFuncSetAttribute(sa::tcp::mma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        smem);
-  sa::tcp::mma_probe_kernel<<<1, 128, smem, sa::as_stream(stream)>>>(n, iters, layout, out);
+  // layout >= 10: the same pattern on every SM at once (full-chip contention)
+  const int grid = layout >= 10 ? 148 : 1;
+  sa::tcp::mma_probe_kernel<<<grid, 128, smem, sa::as_stream(stream)>>>(n, iters, layout % 10, out);
   return cudaGetLastError() == cudaSuccess ? SA_OK : SA_ERR_CUDA;
 }

@@ -16,7 +16,8 @@ def main(path):
     rows = load(path)
     agg = collections.OrderedDict()
     tot = 0.0
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+             "second": 1e6, "s": 1e6}
     for r in rows:
         if r.get("Metric Name") != "gpu__time_duration.sum":
             continue

@@ -17,6 +17,9 @@ SITES = ["prod a1_empty", "w1stream empty", "w2stream empty", "mma a1_full", "mm
          "gelu a2_empty", "epi o_full", "T prod", "T mma", "T gelu", "mma issue fc1", "mma issue fc2"]
 lib = _lib.load()
 lib.sa_debug_mlp_profile.argtypes = [ctypes.c_void_p]
+lib.sa_debug_mlp_mode.argtypes = [ctypes.c_int]
+MODE = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+lib.sa_debug_mlp_mode(MODE)
 for d, hidden in ((32, 256), (64, 512)):
     M = 802816 if d == 32 else 200704
     g = ops.rng(0)
