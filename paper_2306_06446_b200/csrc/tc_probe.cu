@@ -82,3 +82,104 @@ extern "C" int sa_probe_mma(int n, int iters, int layout, unsigned long long* ou
   sa::tcp::mma_probe_kernel<<<grid, 128, smem, sa::as_stream(stream)>>>(n, iters, layout % 10, out);
   return cudaGetLastError() == cudaSuccess ? SA_OK : SA_ERR_CUDA;
 }
+
+// ---- A-operand-in-TMEM probe (diagnostics only) ------------------------------
+// 1) correctness: D = A·B^T for M=128, N=n, K=16 with A written to TMEM by
+//    tcgen05.st (lane = row, column c = bf16 pair k = 2c, 2c+1) and B in smem
+//    (interleaved K-major); D copied to `d_out` (128 x n fp32).
+// 2) rate: `iters` chained MMAs with A in TMEM; out[0]/out[1] issue/complete cycles.
+namespace sa {
+namespace tcp {
+using namespace tc;
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(128, 1) mma_ts_probe_kernel(int n, int iters,
+                                                              const uint16_t* a_in,
+                                                              const uint16_t* b_in, float* d_out,
+                                                              unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  // B (n x 16) into the interleaved K-major layout
+  for (int i = tid; i < n * 16; i += 128) {
+    const int r = i / 16, k = i % 16;
+    *reinterpret_cast<uint16_t*>(smem + plane_offset(r, k)) = b_in[i];
+  }
+  if (warp == 0) tmem_alloc<512>(&slot);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  const uint32_t a_col = 256;   // A at columns 256..263, D at 0..n-1
+  {
+    uint32_t r[8];
+    for (int c = 0; c < 8; ++c)
+      r[c] = uint32_t(a_in[tid * 16 + 2 * c]) | (uint32_t(a_in[tid * 16 + 2 * c + 1]) << 16);
+    tmem_st8(tmem + (uint32_t(warp * 32) << 16) + a_col, r);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (tid == 0) {
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) |
+                           (uint32_t(128 >> 4) << 24);
+    const uint64_t bd = smem_desc(smem_u32(smem));
+    mma_bf16_ts(tmem, tmem + a_col, bd, idesc, 0u);
+    const long long t0 = clock64();
+    if (iters > 0) {
+      for (int i = 0; i < iters; ++i) mma_bf16_ts(tmem + 128, tmem + a_col, bd, idesc, i > 0);
+    }
+    const long long t1 = clock64();
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    const long long t2 = clock64();
+    out[0] = (unsigned long long)(t1 - t0);
+    out[1] = (unsigned long long)(t2 - t0);
+  }
+  __syncthreads();
+  tc_fence_after();
+  for (int cb = 0; cb < n; cb += 16) {
+    float v[16];
+    tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(cb), v);
+    for (int q = 0; q < 16; ++q) d_out[tid * n + cb + q] = v[q];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace tcp
+}  // namespace sa
+
+extern "C" int sa_probe_mma_ts(int n, int iters, const void* a_in, const void* b_in, float* d_out,
+                               unsigned long long* out, void* stream) {
+  const int smem = 256 * 16 * 2 + 1024;
+  cudaFuncSetAttribute(sa::tcp::mma_ts_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       smem);
+  sa::tcp::mma_ts_probe_kernel<<<1, 128, smem, sa::as_stream(stream)>>>(
+      n, iters, static_cast<const uint16_t*>(a_in), static_cast<const uint16_t*>(b_in), d_out, out);
+  return cudaGetLastError() == cudaSuccess ? SA_OK : SA_ERR_CUDA;
+}
