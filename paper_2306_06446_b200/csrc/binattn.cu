@@ -458,9 +458,16 @@ static int check_attn_shapes(const char* who, int64_t B, int64_t n, int64_t d, i
   return SA_OK;
 }
 
+int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq, const float* gk,
+                         const float* v, const float* dw, float* out, int64_t B, int64_t n,
+                         int64_t d, int64_t heads, float eps, cudaStream_t s);
+static int g_attn_mode = 0;   // 0: fused single-pass kernel when the shape allows; 1: multi-kernel
+
 }  // namespace sa
 
 using namespace sa;
+
+extern "C" void sa_debug_attn_mode(int mode) { g_attn_mode = mode; }
 
 extern "C" size_t sa_linear_binary_attn_workspace(int64_t B, int64_t n, int64_t d, int64_t heads) {
   if (heads <= 0 || d % heads) return 0;
@@ -485,6 +492,11 @@ extern "C" int sa_linear_binary_attn(const uint32_t* codes_q, const uint32_t* co
   SA_REQUIRE(ws_bytes >= sa_linear_binary_attn_workspace(B, n, d, heads), SA_ERR_VALUE,
              "sa_linear_binary_attn: workspace too small");
   const int64_t dk = d / heads;
+  if (dk == 32 && g_attn_mode == 0) {
+    st = binattn_fused_launch(codes_q, codes_k, gamma_q, gamma_k, v, dw, out, B, n, d, heads, eps,
+                              as_stream(stream));
+    if (st != SA_ERR_VALUE) return st;
+  }
   const int nsplit = int(cdiv(n, kv_tok(int(dk))));
   const int64_t BH = B * heads;
   float* part = static_cast<float*>(ws);

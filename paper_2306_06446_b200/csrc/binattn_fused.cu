@@ -1,0 +1,540 @@
+// K2a, single pass over V: binary linear attention + DWConv for head dim 32,
+// one thread-block cluster per image.
+//
+// Semantics are those of binattn.cu (ref attention.py:113-120 on the binary
+// features of model.py:355-358, DWConv branch attention.py:170-179 added
+// before W_O, model.py:367-373):
+//   kv[a][:] = gk * sum_{j : ck[j][a]} v_j,  cnt[a] = sum_j ck[j][a]
+//   out_i    = gq * sum_{a : cq[i][a]} kv[a] / (gq*gk*sum_{a : cq[i][a]} cnt[a] + eps)
+//              + dwconv3x3(V)_i
+//
+// Layout of the work. The token grid (side = ceil(sqrt n), row-major) of one
+// image is cut into CL bands of BR grid rows; CTA `rank` of the image's
+// cluster owns band `rank`:
+//  1. one thread bulk-copies the band's V rows plus one halo row above and
+//     below (each grid row is one contiguous (side x d) fp32 run in HBM) into
+//     shared memory; V is read from HBM exactly once per image;
+//  2. pass 1 (K^T V partial of the band): 16 threads per token stream
+//     (4 row groups of 8 code bits x 4 column groups of 8 channels), 16
+//     streams; per token a thread adds its 8 V channels into the rows whose
+//     K code bit is set (packed f32x2 masked adds: v*1 / v*0 are exact, so
+//     the accumulators only ever receive selected V entries); streams are
+//     combined in a fixed order (shuffle, then shared memory); the code-bit
+//     counts use bit-sliced vertical counters (one warp) and a ballot tree;
+//  3. the CL band partials are exchanged through distributed shared memory
+//     and summed in rank order (deterministic, identical in every CTA);
+//  4. pass 2: per head, kv is folded into Four-Russians nibble tables
+//     T[g][m][c] = sum_{i in m} kv[4g+i][c]; a thread owns 4 channels and
+//     walks a segment of a grid row: 8 table lookups (float4) per token for
+//     the additive Q·(K^T V), the integer D from 8 lanes' count-table lookups
+//     and a shuffle tree, and the 3x3 DWConv from a register sliding window
+//     over the shared-memory band (3 new float4 per token).
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace sa {
+namespace baf {
+
+constexpr int DK = 32;
+constexpr int kThreads = 256;
+constexpr int kStreams = 16;        // pass-1 token streams (16 threads each)
+constexpr int kSeg = 6;             // pass-2 tokens per row segment (multiple of 3)
+
+struct Params {
+  const uint32_t* cq;
+  const uint32_t* ck;
+  const float* gq;
+  const float* gk;
+  const float* v;
+  const float* dw;
+  float* out;
+  int n, d, heads, side, rows_total, band_rows;
+  float eps;
+};
+
+struct Smem {
+  // byte offsets into the dynamic shared memory carve-out
+  uint32_t v, cq, ck, part, cntp, cntw, tab, tcb, mt, bar, total;
+};
+
+__host__ __device__ inline Smem smem_layout(int d, int heads, int side, int band_rows) {
+  Smem s;
+  const uint32_t band_tok = uint32_t(band_rows) * side;
+  uint32_t o = 0;
+  s.v = o;
+  o += uint32_t(band_rows + 2) * side * d * 4;
+  s.cq = o;
+  o += heads * band_tok * 4;
+  s.ck = o;
+  o += heads * band_tok * 4;
+  o = (o + 15) & ~15u;
+  s.part = o;                                  // [heads][DK][DK] band partial of kv
+  o += heads * DK * DK * 4;
+  s.cntp = o;                                  // [heads][DK] band partial of cnt
+  o += heads * DK * 4;
+  s.cntw = o;                                  // [DK] bit counts of the current head
+  o += DK * 4;
+  s.tab = o;                                   // union: pass-1 scratch [4][DK][DK] | tables
+  const uint32_t scratch = 4 * DK * DK * 4 + kStreams * DK * 4;
+  const uint32_t tables = heads * (DK / 4) * 16 * DK * 4;
+  o += scratch > tables ? scratch : tables;
+  s.tcb = o;                                   // [heads][4][256] float: byte tables of cnt
+  o += heads * 4 * 256 * 4;
+  s.mt = o;                                    // [256][8] float: 0/1 masks of a code byte
+  o += 256 * 8 * 4;
+  s.bar = o;                                   // one mbarrier per smem row
+  o += (band_rows + 2) * 8;
+  s.total = o;
+  return s;
+}
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// acc (two packed fp32) += v * m with m = 1.0 or 0.0 (a code bit, broadcast to
+// both lanes): an exact masked add — v*1 and v*0 are exact, so the
+// accumulator only ever receives additions of selected V entries. One FFMA2
+// per channel pair (a predicated add.f32x2 compiles to FADD2 + 2 SEL).
+__device__ __forceinline__ void add2_mask(unsigned long long& acc, unsigned long long v, float m) {
+  asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%2, %2};\n\tfma.rn.f32x2 %0, %1, t, %0;\n\t}"
+      : "+l"(acc)
+      : "l"(v), "f"(m));
+}
+__device__ __forceinline__ void add2(unsigned long long& acc, unsigned long long v) {
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(v));
+}
+__device__ __forceinline__ void fma2(unsigned long long& acc, unsigned long long a,
+                                     unsigned long long b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ float2 unpack2(unsigned long long u) {
+  return make_float2(__uint_as_float(uint32_t(u)), __uint_as_float(uint32_t(u >> 32)));
+}
+__device__ __forceinline__ ulonglong2 lds128(const void* p) {
+  return *reinterpret_cast<const ulonglong2*>(p);
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+struct Win {   // one window column: 4 channels of 3 grid rows (packed pairs)
+  ulonglong2 r[3];
+};
+
+// D = model dim (heads = D / 32), SIDE = token-grid side: every shared-memory
+// stride is a compile-time constant.
+template <int D, int SIDE>
+__global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
+  constexpr int HEADS = D / DK;
+  constexpr uint32_t ROWB = uint32_t(SIDE) * D * 4;   // bytes per smem grid row
+  constexpr uint32_t TOKB = uint32_t(D) * 4;          // bytes per token
+  extern __shared__ __align__(16) uint8_t smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = int(cluster.block_rank());
+  const int CL = int(cluster.num_blocks());
+  const int b = blockIdx.y;
+  const int n = p.n, BR = p.band_rows;
+  const Smem L = smem_layout(D, HEADS, SIDE, BR);
+  uint8_t* Vb = smem + L.v;
+  uint32_t* cqs = reinterpret_cast<uint32_t*>(smem + L.cq);
+  uint32_t* cks = reinterpret_cast<uint32_t*>(smem + L.ck);
+  float* part = reinterpret_cast<float*>(smem + L.part);
+  int* cntp = reinterpret_cast<int*>(smem + L.cntp);
+  int* cntw = reinterpret_cast<int*>(smem + L.cntw);
+  float* tab = reinterpret_cast<float*>(smem + L.tab);
+  float* tcb = reinterpret_cast<float*>(smem + L.tcb);
+  float* mt = reinterpret_cast<float*>(smem + L.mt);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int r0 = rank * BR;
+  const int r1 = min(p.rows_total, r0 + BR);
+  const int t_lo = min(n, r0 * SIDE), t_hi = min(n, r1 * SIDE);
+  const int nt = t_hi - t_lo;
+  const float* vb = p.v + size_t(b) * n * D;
+
+  // ---- 1. band of V (+ halo rows) → shared memory ----------------------------
+  // smem row R holds grid row r0 - 1 + R; cells past n and rows outside the
+  // grid are zero (the reference's zero-padded token grid, attention.py:170-179)
+  // one mbarrier per smem row, so pass 1 starts on the first rows while the
+  // rest of the band is still in flight
+  if (tid == 0) {
+    for (int R = 0; R < BR + 2; ++R)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + R)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // band rows first (pass 1 needs them), the two halo rows last
+    for (int i = 0; i < BR + 2; ++i) {
+      const int R = i < BR ? i + 1 : (i == BR ? 0 : BR + 1);
+      const int rr = r0 - 1 + R;
+      const int ntok = (rr >= 0 && rr < p.rows_total) ? max(0, min(SIDE, n - rr * SIDE)) : 0;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar + R)),
+                   "r"(uint32_t(ntok) * TOKB)
+                   : "memory");
+      if (ntok == 0) continue;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              su32(Vb + R * ROWB)),
+          "l"(vb + size_t(rr) * SIDE * D), "r"(uint32_t(ntok) * TOKB), "r"(su32(bar + R))
+          : "memory");
+    }
+  }
+  for (int R = 0; R < BR + 2; ++R) {   // zero the cells no copy fills
+    const int rr = r0 - 1 + R;
+    const int ntok = (rr >= 0 && rr < p.rows_total) ? max(0, min(SIDE, n - rr * SIDE)) : 0;
+    float4* z = reinterpret_cast<float4*>(Vb + R * ROWB + ntok * TOKB);
+    const int nz = (SIDE - ntok) * D / 4;
+    for (int i = tid; i < nz; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int i = tid; i < HEADS * nt; i += kThreads) {   // codes of the band, [head][token]
+    const int h = i / nt, t = i - h * nt;
+    const size_t g = (size_t(b) * HEADS + h) * n + t_lo + t;
+    cqs[h * nt + t] = __ldg(p.cq + g);
+    cks[h * nt + t] = __ldg(p.ck + g);
+  }
+  for (int i = tid; i < 256 * 8; i += kThreads)          // byte → 8 masks
+    mt[i] = ((i >> 3) >> (i & 7)) & 1 ? 1.0f : 0.0f;
+  __syncthreads();  // barrier init, codes, masks visible
+  auto wait_row = [&](int R) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 q, [%0], 0;\n\t"
+        "@!q bra W_%=;\n\t}" ::"r"(su32(bar + R))
+        : "memory");
+  };
+
+  // ---- 2. pass 1: band partial of K^T V and of the code-bit counts -----------
+  const int s_id = tid >> 4;               // stream 0..15 (two per warp)
+  const int rg = (tid >> 2) & 3;           // code bits 8rg .. 8rg+7
+  const int cgp = tid & 3;                 // channels 8cgp .. 8cgp+7
+#pragma unroll 1
+  for (int h = 0; h < HEADS; ++h) {
+    unsigned long long acc[8][4], cacc[4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0ull;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cacc[j] = 0ull;
+    const uint8_t* vp = Vb + ROWB + (h * DK + cgp * 8) * 4 + s_id * TOKB;
+    const uint32_t* kp = cks + h * nt + s_id;
+    const uint8_t* mtb = reinterpret_cast<const uint8_t*>(mt);
+    int next_row = 0;   // first band-local token of the next unwaited smem row
+    int R_w = 1;
+#pragma unroll 2
+    for (int t = s_id; t < nt; t += kStreams) {
+      if (h == 0 && t >= next_row) {   // band row of token t has landed
+        while (t >= next_row) {
+          wait_row(R_w);
+          ++R_w;
+          next_row += SIDE;
+        }
+      }
+      const ulonglong2 va = lds128(vp);
+      const ulonglong2 vc = lds128(vp + 16);
+      const uint8_t* mrow = mtb + (((*kp) >> (rg * 8)) & 0xffu) * 32;
+      const ulonglong2 mp0 = lds128(mrow);
+      const ulonglong2 mp1 = lds128(mrow + 16);
+      const float2 m01 = unpack2(mp0.x), m23 = unpack2(mp0.y);
+      const float2 m45 = unpack2(mp1.x), m67 = unpack2(mp1.y);
+      const float m[8] = {m01.x, m01.y, m23.x, m23.y, m45.x, m45.y, m67.x, m67.y};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        add2_mask(acc[i][0], va.x, m[i]);
+        add2_mask(acc[i][1], va.y, m[i]);
+        add2_mask(acc[i][2], vc.x, m[i]);
+        add2_mask(acc[i][3], vc.y, m[i]);
+      }
+      // code-bit counts: the same 0/1 masks summed (exact small integers)
+      add2(cacc[0], mp0.x);
+      add2(cacc[1], mp0.y);
+      add2(cacc[2], mp1.x);
+      add2(cacc[3], mp1.y);
+      vp += kStreams * TOKB;
+      kp += kStreams;
+    }
+    if (h == 0) {   // streams with few tokens still own rows later threads read
+      while (R_w <= BR) {
+        wait_row(R_w);
+        ++R_w;
+      }
+    }
+    // combine: the warp's two streams (lanes l, l+16) by shuffle, then warps
+    // 4-7 store, warps 0-3 add their own and store, one 4-way sum (fixed order)
+    float2 cmb[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 a = unpack2(acc[i][j]);
+        cmb[i][j] = make_float2(a.x + __shfl_down_sync(0xffffffffu, a.x, 16),
+                                a.y + __shfl_down_sync(0xffffffffu, a.y, 16));
+      }
+    float* scr = tab + (warp & 3) * DK * DK + rg * 8 * DK + cgp * 8;
+    if (warp >= 4 && lane < 16) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) *reinterpret_cast<float2*>(scr + i * DK + 2 * j) = cmb[i][j];
+    }
+    // counts: lanes with cgp == 0 hold them for rows 8rg..8rg+7 of their
+    // stream; fold the 16 streams in a fixed order through shared memory
+    if (cgp == 0) {
+      float* cs = tab + 4 * DK * DK + s_id * DK + rg * 8;   // after the kv scratch
+#pragma unroll
+      for (int j = 0; j < 4; ++j) *reinterpret_cast<float2*>(cs + 2 * j) = unpack2(cacc[j]);
+    }
+    __syncthreads();
+    if (warp < 4 && lane < 16) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float2* q = reinterpret_cast<float2*>(scr + i * DK + 2 * j);
+          const float2 o = *q;
+          *q = make_float2(cmb[i][j].x + o.x, cmb[i][j].y + o.y);
+        }
+    }
+    __syncthreads();
+    {
+      const int e = tid * 4;   // 256 threads x 4 = DK*DK
+      float4 s4 = *reinterpret_cast<const float4*>(tab + e);
+#pragma unroll
+      for (int w4 = 1; w4 < 4; ++w4) {
+        const float4 q4 = *reinterpret_cast<const float4*>(tab + w4 * DK * DK + e);
+        s4.x += q4.x;
+        s4.y += q4.y;
+        s4.z += q4.z;
+        s4.w += q4.w;
+      }
+      *reinterpret_cast<float4*>(part + h * DK * DK + e) = s4;
+    }
+    if (tid < DK) {
+      const float* cs = tab + 4 * DK * DK + tid;
+      float c = 0.f;
+#pragma unroll
+      for (int st = 0; st < kStreams; ++st) c += cs[st * DK];
+      cntp[h * DK + tid] = int(c);
+    }
+    __syncthreads();
+  }
+
+  // ---- 3. exchange band partials across the cluster (rank order) -------------
+  cluster.sync();
+#pragma unroll 1
+  for (int h = 0; h < HEADS; ++h) {
+    const float g = __ldg(p.gk + b * HEADS + h);
+    const int grp = tid / DK, c = tid % DK;       // tables: thread = (nibble group, column)
+    float x[8][4];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {   // issue every peer's loads before summing
+      if (r < CL) {
+        const float* pr = cluster.map_shared_rank(part, r) + h * DK * DK + 4 * grp * DK + c;
+        x[r][0] = pr[0];
+        x[r][1] = pr[DK];
+        x[r][2] = pr[2 * DK];
+        x[r][3] = pr[3 * DK];
+      }
+    }
+    float row[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (r < CL) {
+        row[0] += x[r][0];
+        row[1] += x[r][1];
+        row[2] += x[r][2];
+        row[3] += x[r][3];
+      }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) row[i] *= g;
+    float val[16];
+    val[0] = 0.f;
+    val[1] = row[0];
+    val[2] = row[1];
+    val[4] = row[2];
+    val[8] = row[3];
+#pragma unroll
+    for (int m = 3; m < 16; ++m)
+      if (m & (m - 1)) val[m] = val[m & (m - 1)] + val[m & -m];
+    float* T = tab + size_t(h) * (DK / 4) * 16 * DK;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) T[(grp * 16 + m) * DK + c] = val[m];
+    if (tid < DK) {   // this head's total counts (rank order), 1 per lane
+      int s = 0;
+      for (int r = 0; r < CL; ++r) s += cluster.map_shared_rank(cntp, r)[h * DK + tid];
+      cntw[tid] = s;
+    }
+    __syncthreads();
+    // byte tables of the counts as exact floats: tcb[h][g][m] = sum_{i in m} cnt[8g+i]
+    for (int e = tid; e < 4 * 256; e += kThreads) {
+      const int g8 = e >> 8, m = e & 255;
+      int s = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if ((m >> i) & 1) s += cntw[8 * g8 + i];
+      tcb[h * 1024 + e] = float(s);
+    }
+    __syncthreads();
+  }
+  cluster.sync();   // every peer has read this CTA's partials; tables complete
+
+  // ---- 4. pass 2: outputs ------------------------------------------------------
+  wait_row(0);
+  wait_row(BR + 1);
+  constexpr int NCG = D / 4;                 // channel groups of 4
+  constexpr int SLOTS = kThreads / NCG;      // (row, segment) units per round
+  constexpr int SEGS = (SIDE + kSeg - 1) / kSeg;
+  const int cgi = tid % NCG, slot = tid / NCG;
+  if (slot >= SLOTS) return;
+  const int h = cgi / (DK / 4), cgl = cgi % (DK / 4);
+  const int ch = cgi * 4;
+  const float gq = __ldg(p.gq + b * HEADS + h), gk = __ldg(p.gk + b * HEADS + h);
+  const float gg = gq * gk;
+  ulonglong2 tapu[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q)
+    tapu[q] = p.dw ? __ldg(reinterpret_cast<const ulonglong2*>(p.dw + q * D + ch))
+                   : make_ulonglong2(0ull, 0ull);
+  const bool has_dw = p.dw != nullptr;
+  const uint8_t* T = reinterpret_cast<const uint8_t*>(tab + size_t(h) * (DK / 4) * 16 * DK + cgl * 4);
+  const float* Tb = tcb + h * 1024;
+  const uint32_t* cqh = cqs + h * nt;
+  const int units = (r1 - r0) * SEGS;
+  float* ob = p.out + size_t(b) * n * D + ch;
+  const ulonglong2 z2 = make_ulonglong2(0ull, 0ull);
+  for (int u = slot; u < units; u += SLOTS) {
+    const int rl = u / SEGS, sg = u - rl * SEGS;
+    const int r = r0 + rl;
+    const int c0 = sg * kSeg;
+    const int c1 = min(SIDE, c0 + kSeg);
+    // column c of smem rows rl..rl+2 (grid rows r-1..r+1) at colb + c*TOKB + R*ROWB
+    const uint8_t* colb = Vb + rl * ROWB + ch * 4;
+    auto load_col = [&](Win& w, int c) {
+      if (c >= 0 && c < SIDE) {
+        const uint8_t* q = colb + c * TOKB;
+        w.r[0] = lds128(q);
+        w.r[1] = lds128(q + ROWB);
+        w.r[2] = lds128(q + 2 * ROWB);
+      } else {
+        w.r[0] = z2;
+        w.r[1] = z2;
+        w.r[2] = z2;
+      }
+    };
+    // ring of three window columns; roles rotate with the (unrolled) step index
+    Win wr[3];
+    load_col(wr[0], c0 - 1);
+    load_col(wr[1], c0);
+    const int tb = r * SIDE + c0;
+    const int kmax = min(c1 - c0, n - tb);
+#pragma unroll
+    for (int k = 0; k < kSeg; ++k) {
+      if (k >= kmax) break;
+      const int c = c0 + k;
+      Win& wl = wr[k % 3];
+      Win& wc = wr[(k + 1) % 3];
+      Win& wn = wr[(k + 2) % 3];
+      load_col(wn, c + 1);
+      const int t = tb + k;
+      const uint32_t q = cqh[t - t_lo];
+      // additive Q·(K^T V): 8 nibble-table rows, packed f32x2 adds
+      unsigned long long a01 = 0ull, a23 = 0ull;
+#pragma unroll
+      for (int g = 0; g < DK / 4; ++g) {
+        const uint32_t off = (g >= 2 ? (q >> (4 * g - 7)) : (q << (7 - 4 * g))) & 0x780u;
+        const ulonglong2 tv = lds128(T + g * 16 * DK * 4 + off);
+        add2(a01, tv.x);
+        add2(a23, tv.y);
+      }
+      // D = sum of the counts of the query's set bits: 4 byte-table lookups
+      const float D_ = (Tb[q & 255] + Tb[256 + ((q >> 8) & 255)]) +
+                       (Tb[512 + ((q >> 16) & 255)] + Tb[768 + (q >> 24)]);
+      const float sc = gq * rcp_approx(fmaf(gg, D_, p.eps));
+      const float2 x01 = unpack2(a01), x23 = unpack2(a23);
+      float4 o = make_float4(x01.x * sc, x01.y * sc, x23.x * sc, x23.y * sc);
+      if (has_dw) {
+        unsigned long long s01 = 0ull, s23 = 0ull;
+#pragma unroll
+        for (int R = 0; R < 3; ++R) {
+          fma2(s01, wl.r[R].x, tapu[R * 3 + 0].x);
+          fma2(s23, wl.r[R].y, tapu[R * 3 + 0].y);
+          fma2(s01, wc.r[R].x, tapu[R * 3 + 1].x);
+          fma2(s23, wc.r[R].y, tapu[R * 3 + 1].y);
+          fma2(s01, wn.r[R].x, tapu[R * 3 + 2].x);
+          fma2(s23, wn.r[R].y, tapu[R * 3 + 2].y);
+        }
+        const float2 y01 = unpack2(s01), y23 = unpack2(s23);
+        o.x += y01.x;
+        o.y += y01.y;
+        o.z += y23.x;
+        o.w += y23.y;
+      }
+      *reinterpret_cast<float4*>(ob + size_t(t) * D) = o;
+    }
+  }
+}
+
+}  // namespace baf
+
+// Host side: picks the cluster geometry and launches; returns SA_ERR_VALUE when
+// the shape is outside this kernel's envelope (the caller then uses the
+// multi-kernel path of binattn.cu).
+int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq, const float* gk,
+                         const float* v, const float* dw, float* out, int64_t B, int64_t n,
+                         int64_t d, int64_t heads, float eps, cudaStream_t s) {
+  using namespace baf;
+  if (d != heads * DK || d % 4 != 0) return SA_ERR_VALUE;
+  int side = 0;
+  while (int64_t(side) * side < n) ++side;
+  const int rows_total = int((n + side - 1) / side);
+  // bands of ~400 (token, head) pairs amortise the per-CTA table work
+  int cl = int((n * heads + 399) / 400);
+  cl = cl < 1 ? 1 : (cl > 8 ? 8 : cl);
+  cl = cl > rows_total ? rows_total : cl;
+  const int br = (rows_total + cl - 1) / cl;
+  cl = (rows_total + br - 1) / br;
+  // every lane group of 8 (one head's channel groups) must sit inside a warp
+  if ((d / 4) % 8 != 0 || d / 4 > kThreads) return SA_ERR_VALUE;
+  const Smem L = smem_layout(int(d), int(heads), side, br);
+  if (L.total > 220 * 1024) return SA_ERR_VALUE;
+  if (br * side > 32 * 63) return SA_ERR_VALUE;   // bit-sliced counters hold 63 tokens/lane
+  Params p{cq, ck, gq, gk, v, dw, out, int(n), int(d), int(heads), side, rows_total, br, eps};
+  void (*kern)(Params) = nullptr;
+  if (d == 32 && side == 56) kern = binattn_fused_kernel<32, 56>;
+  else if (d == 64 && side == 28) kern = binattn_fused_kernel<64, 28>;
+  else if (d == 160 && side == 14) kern = binattn_fused_kernel<160, 14>;
+  else if (d == 32 && side == 14) kern = binattn_fused_kernel<32, 14>;
+  else if (d == 64 && side == 14) kern = binattn_fused_kernel<64, 14>;
+  else if (d == 96 && side == 18) kern = binattn_fused_kernel<96, 18>;
+  else if (d == 32 && side == 3) kern = binattn_fused_kernel<32, 3>;
+  else if (d == 256 && side == 7) kern = binattn_fused_kernel<256, 7>;
+  else if (d == 64 && side == 15) kern = binattn_fused_kernel<64, 15>;
+  if (kern == nullptr) return SA_ERR_VALUE;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(cl), unsigned(B), 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = L.total;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(cl);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
+  if (e != cudaSuccess) {
+    set_error("sa_linear_binary_attn: fused launch failed: %s", cudaGetErrorString(e));
+    return SA_ERR_CUDA;
+  }
+  count_launch(1);
+  return SA_OK;
+}
+
+}  // namespace sa

@@ -375,3 +375,42 @@ def test_ln_route_fused_vs_oracle(M, d, nr):
         assert np.array_equal(plan.expert_of, e)
         assert np.array_equal(np.concatenate(plan.index_of), np.concatenate(idx))
         assert rel_err(plan.gate_of, gate) < 1e-6
+
+
+@pytest.mark.parametrize("B,n,d,h,with_dw", [(3, 3136, 32, 1, True), (2, 784, 64, 2, True),
+                                             (2, 196, 160, 5, True), (2, 300, 96, 3, True),
+                                             (3, 197, 64, 2, False), (1, 5, 32, 1, True),
+                                             (2, 49, 256, 8, True)])
+def test_fused_binary_attention_matches_multikernel(B, n, d, h, with_dw):
+    """The single-pass cluster kernel (dk = 32) against the three-kernel path
+    and the oracle, including non-square token grids and partial last rows."""
+    import ctypes
+    from paper_2306_06446_b200 import _lib
+    from paper_2306_06446_b200 import attention as A
+    lib = _lib.load()
+    lib.sa_debug_attn_mode.argtypes = [ctypes.c_int]
+    g = ops.rng(11 + n + d)
+    q, kk, v = (g.standard_normal((B * n, d)).astype(F32) for _ in range(3))
+    dw = (g.standard_normal((3, 3, d)) * 0.1).astype(F32) if with_dw else None
+    args = (dev(q), dev(kk), dev(v), B, h, dev(dw) if with_dw else None)
+    try:
+        lib.sa_debug_attn_mode(1)
+        legacy = host(A.binary_core(*args))
+    finally:
+        lib.sa_debug_attn_mode(0)
+    fused = host(A.binary_core(*args))
+    assert rel_err(fused, legacy) < 2e-6
+    fold = lambda t: ops.heads_split(t.reshape(B, n, d), h).reshape(B * h, n, d // h)  # noqa
+    qf, _ = ops.binary_features(fold(q))
+    kf, _ = ops.binary_features(fold(kk))
+    o = ops.qkv_linear_core(qf, kf, fold(v))
+    merged = ops.heads_merge(o.reshape(B, h, n, d // h)).reshape(B * n, d)
+    if with_dw:
+        merged = merged + np.concatenate([ops.dwconv_tokens(v[i * n:(i + 1) * n], dw)
+                                          for i in range(B)])
+    assert rel_err(fused, merged) < 2e-5
+    # all-negative query rows give exactly the DWConv term (zero attention part)
+    q2 = q.copy()
+    q2[0, :] = -np.abs(q2[0, :]) - 1.0
+    out2 = host(A.binary_core(dev(q2), dev(kk), dev(v), B, h, None))
+    assert np.all(out2[0] == 0)
