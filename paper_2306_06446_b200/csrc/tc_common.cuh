@@ -166,6 +166,131 @@ __device__ __forceinline__ void mma_split_step(uint32_t d_tmem, uint64_t a0, uin
   }
 }
 
+// ---- A operand in TMEM ("ts" form) -------------------------------------------
+// D[tmem] (+)= A[tmem] · B[smem]^T. The A tile (M = 128) lives in TMEM with
+// lane = row and 32-bit column c holding the bf16 pair (k = 2c, 2c+1), so one
+// K = 16 step reads 8 columns (layout verified against torch by
+// scripts/probe_mma_ts.py). Only B is read from shared memory.
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// 32 lanes x 16 consecutive 32-bit columns ← 16 registers per thread
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// Split-precision K = 16 step with A planes in TMEM (plane p at a0 + p *
+// a_plane_cols columns) and B planes in shared memory (as mma_split_step).
+template <int NPB>
+__device__ __forceinline__ void mma_split_step_ts(uint32_t d_tmem, uint32_t a0, uint64_t b0,
+                                                  uint32_t a_plane_cols, uint32_t b_plane_bytes,
+                                                  uint32_t idesc, bool accumulate) {
+  constexpr int NP = NPB == 1 ? 3 : 6;
+  constexpr int pa[6] = {2, 1, 0, 1, 0, 0};
+  constexpr int pb1[6] = {0, 0, 0, 0, 0, 0};
+  constexpr int pb3[6] = {0, 1, 2, 0, 1, 0};
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const int bpl = NPB == 1 ? pb1[i] : pb3[i];
+    mma_bf16_ts(d_tmem, a0 + uint32_t(pa[i]) * a_plane_cols,
+                b0 + uint64_t((bpl * b_plane_bytes) >> 4), idesc,
+                (accumulate || i > 0) ? 1u : 0u);
+  }
+}
+
+// ---- warp-uniform issue: the whole warp executes these, one elected lane
+// issues (no compiler-generated per-instruction election loop) ------------
+__device__ __forceinline__ void mma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+template <int NPB>
+__device__ __forceinline__ void mma_split_step_ts_w(uint32_t d_tmem, uint32_t a0, uint64_t b0,
+                                                    uint32_t a_plane_cols, uint32_t b_plane_bytes,
+                                                    uint32_t idesc, bool accumulate) {
+  constexpr int NP = NPB == 1 ? 3 : 6;
+  constexpr int pa[6] = {2, 1, 0, 1, 0, 0};
+  constexpr int pb1[6] = {0, 0, 0, 0, 0, 0};
+  constexpr int pb3[6] = {0, 1, 2, 0, 1, 0};
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const int bpl = NPB == 1 ? pb1[i] : pb3[i];
+    mma_ts_w(d_tmem, a0 + uint32_t(pa[i]) * a_plane_cols, b0 + uint64_t((bpl * b_plane_bytes) >> 4),
+             idesc, (accumulate || i > 0) ? 1u : 0u);
+  }
+}
+
+// One K = 16 split-precision step as a single asm block: one elect.sync, the
+// plane operands derived with PTX adds (uniform datapath), then the 3 (shift
+// weights: lo·w, mid·w, hi·w) or 6 (dense: lo·hi, mid·mid, hi·lo, mid·hi,
+// hi·mid, hi·hi) tcgen05.mma, smallest products first. A planes in TMEM at
+// a0 + {0, 1, 2} * apc columns; B planes at b0 + {0, 1, 2} * (bpb >> 4).
+__device__ __forceinline__ void mma_chain3_ts_w(uint32_t d, uint32_t a0, uint64_t b0, uint32_t apc,
+                                                uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b32 a1, a2;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "setp.eq.u32 t, 0, 0;\n\t"
+      "add.u32 a1, %1, %3;\n\t"
+      "add.u32 a2, a1, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], %2, %4, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], %2, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %4, t;\n\t}" ::"r"(d),
+      "r"(a0), "l"(b0), "r"(apc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_chain6_ts_w(uint32_t d, uint32_t a0, uint64_t b0, uint32_t apc,
+                                                uint64_t bpd, uint32_t idesc, uint32_t acc) {
+  // bpd = B plane stride already in descriptor units (bytes >> 4)
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b32 a1, a2;\n\t.reg .b64 b1, b2;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.u32 t, 0, 0;\n\t"
+      "add.u32 a1, %1, %3;\n\t"
+      "add.u32 a2, a1, %3;\n\t"
+      "add.u64 b1, %2, %4;\n\t"
+      "add.u64 b2, b1, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], %2, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], b2, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], %2, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], b1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %5, t;\n\t}" ::"r"(d),
+      "r"(a0), "l"(b0), "r"(apc), "l"(bpd), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
 // ---- float32 → hi/mid/lo bf16 (hi+mid+lo == x for normal x) ---------------
 struct Split3 {
   __nv_bfloat162 h, m, l;

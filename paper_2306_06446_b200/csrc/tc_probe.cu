@@ -183,3 +183,93 @@ extern "C" int sa_probe_mma_ts(int n, int iters, const void* a_in, const void* b
       n, iters, static_cast<const uint16_t*>(a_in), static_cast<const uint16_t*>(b_in), d_out, out);
   return cudaGetLastError() == cudaSuccess ? SA_OK : SA_ERR_CUDA;
 }
+
+// ---- MLP-pattern probe (diagnostics only) ------------------------------------
+// Replays the fused MLP's MMA issue pattern on one CTA with no other warps:
+// per hidden chunk q, fc1 = 2 k-steps x NP plane products into acc1[q % 4]
+// (A = x planes in TMEM, B = ring slot q % 4 of W1), fc2 = 2 k-steps x NP into
+// acc2 (A = GELU planes A2[q % 4] in TMEM, B = ring slot q % 4 of W2).
+// variant bit 0: B of every MMA from slot 0 (no ring); bit 1: every MMA into
+// one accumulator; bit 2: commit per chunk to an mbarrier (as the kernel).
+namespace sa {
+namespace tcp {
+__global__ void __launch_bounds__(128, 1) mma_mlp_probe_kernel(int chunks, int np, int variant,
+                                                               unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ __align__(8) uint64_t bar, bar2;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  // variant bit 4: pseudo-random bf16 operands (else all ones)
+  for (int i = tid; i < (8 * 6144) / 4; i += 128)
+    reinterpret_cast<uint32_t*>(smem)[i] =
+        (variant & 16) ? ((uint32_t(i) * 2654435761u) & 0xbfffbfffu) | 0x3c003c00u : 0x3f803f80u;
+  if (warp == 0) tmem_alloc<512>(&slot);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&bar2, 1);
+    fence_barrier_init();
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  {  // A planes: ones
+    uint32_t r[16];
+    for (int c = 0; c < 16; ++c)
+      r[c] = (variant & 16) ? ((uint32_t(tid * 16 + c) * 2246822519u) & 0xbfffbfffu) | 0x3c003c00u
+                            : 0x3f803f80u;
+    for (int col = 192; col < 512; col += 16) tmem_st16(tmem + (uint32_t(warp * 32) << 16) + col, r);
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (tid == 0) {
+    const uint32_t idesc = idesc_bf16_m128(32);
+    const uint32_t sb = smem_u32(smem);
+    const long long t0 = clock64();
+    for (int q = 0; q < chunks; ++q) {
+      const int s = (variant & 1) ? 0 : (q & 3);
+      const uint32_t d1 = tmem + ((variant & 2) ? 0u : uint32_t((q & 3) * 32));
+      const uint32_t d2 = tmem + ((variant & 2) ? 0u : 128u);
+      const uint32_t w1 = sb + uint32_t(s) * 6144, w2 = sb + 4 * 6144 + uint32_t(s) * 6144;
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint64_t bd = smem_desc(w1 + ks * 256);
+        if (np == 1) mma_split_step_ts<1>(d1, tmem + 192 + ks * 8, bd, 16, 2048, idesc, ks != 0);
+        else mma_split_step_ts<3>(d1, tmem + 192 + ks * 8, bd, 16, 2048, idesc, ks != 0);
+      }
+      if (variant & 4) mma_commit(&bar2);
+      const uint32_t a2 = tmem + 320 + uint32_t((q & 3) * 48);
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint64_t bd = smem_desc(w2 + ks * 256);
+        if (np == 1) mma_split_step_ts<1>(d2, a2 + ks * 8, bd, 16, 2048, idesc, (q | ks) != 0);
+        else mma_split_step_ts<3>(d2, a2 + ks * 8, bd, 16, 2048, idesc, (q | ks) != 0);
+      }
+      if (variant & 4) mma_commit(&bar2);
+    }
+    const long long t1 = clock64();
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    const long long t2 = clock64();
+    out[0] = (unsigned long long)(t1 - t0);
+    out[1] = (unsigned long long)(t2 - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+}  // namespace tcp
+}  // namespace sa
+
+extern "C" int sa_probe_mma_mlp(int chunks, int np, int variant, unsigned long long* out,
+                                void* stream) {
+  const int smem = 8 * 6144 + 1024;
+  cudaFuncSetAttribute(sa::tcp::mma_mlp_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       smem);
+  // variant bit 3: one CTA per SM (full chip)
+  sa::tcp::mma_mlp_probe_kernel<<<(variant & 8) ? 148 : 1, 128, smem, sa::as_stream(stream)>>>(
+      chunks, np, variant, out);
+  return cudaGetLastError() == cudaSuccess ? SA_OK : SA_ERR_CUDA;
+}
