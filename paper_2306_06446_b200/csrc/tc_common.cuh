@@ -291,6 +291,44 @@ __device__ __forceinline__ void mma_chain6_ts_w(uint32_t d, uint32_t a0, uint64_
       : "memory");
 }
 
+// Same chains with A in shared memory (descriptor a0, plane stride apd in
+// descriptor units).
+__device__ __forceinline__ void mma_chain3_ss_w(uint32_t d, uint64_t a0, uint64_t b0, uint64_t apd,
+                                                uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a1, a2;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "setp.eq.u32 t, 0, 0;\n\t"
+      "add.u64 a1, %1, %3;\n\t"
+      "add.u64 a2, a1, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, %2, %4, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, %2, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, t;\n\t}" ::"r"(d),
+      "l"(a0), "l"(b0), "l"(apd), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_chain6_ss_w(uint32_t d, uint64_t a0, uint64_t b0, uint64_t apd,
+                                                uint64_t bpd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a1, a2, b1, b2;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.u32 t, 0, 0;\n\t"
+      "add.u64 a1, %1, %3;\n\t"
+      "add.u64 a2, a1, %3;\n\t"
+      "add.u64 b1, %2, %4;\n\t"
+      "add.u64 b2, b1, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, %2, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, b2, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, %2, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, b1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %5, t;\n\t}" ::"r"(d),
+      "l"(a0), "l"(b0), "l"(apd), "l"(bpd), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
 // ---- float32 → hi/mid/lo bf16 (hi+mid+lo == x for normal x) ---------------
 struct Split3 {
   __nv_bfloat162 h, m, l;

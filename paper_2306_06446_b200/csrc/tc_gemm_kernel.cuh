@@ -73,25 +73,30 @@ __device__ __forceinline__ int64_t num_m_tiles(const TcParams& p, int64_t c0) {
   return (c0 + kBM - 1) / kBM + (p.M - c0 + kBM - 1) / kBM;
 }
 
-// m-tiles: with grouping, expert 0 owns ceil(c0/128) tiles, expert 1 the rest
-__device__ __forceinline__ TileInfo tile_info(const TcParams& p, int64_t c0, int64_t t) {
+// m-tiles: with grouping, expert 0 owns ceil(c0/128) tiles, expert 1 the rest.
+// t < 2^31 (checked on the host); ntiles == 1 (N <= BN) avoids the division.
+__device__ __forceinline__ TileInfo tile_info(const TcParams& p, int64_t c0, int t) {
   TileInfo ti;
-  const int64_t m = t / p.ntiles;
-  ti.n_tile = int(t % p.ntiles);
+  int m = t;
+  ti.n_tile = 0;
+  if (p.ntiles != 1) {
+    m = t / p.ntiles;
+    ti.n_tile = t - m * p.ntiles;
+  }
   if (!p.counts) {
     ti.group = 0;
-    ti.r0 = m * kBM;
+    ti.r0 = int64_t(m) * kBM;
     ti.r1 = min(p.M, ti.r0 + kBM);
     return ti;
   }
   const int64_t t0 = (c0 + kBM - 1) / kBM;
   if (m < t0) {
     ti.group = 0;
-    ti.r0 = m * kBM;
+    ti.r0 = int64_t(m) * kBM;
     ti.r1 = min(c0, ti.r0 + kBM);
   } else {
     ti.group = 1;
-    ti.r0 = c0 + (m - t0) * kBM;
+    ti.r0 = c0 + (int64_t(m) - t0) * kBM;
     ti.r1 = min(p.M, ti.r0 + kBM);
   }
   return ti;
@@ -149,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int64_t c0 = p.counts ? int64_t(p.counts[0]) : 0;
-  const int64_t total = num_m_tiles(p, c0) * p.ntiles;
+  const int total = int(num_m_tiles(p, c0) * p.ntiles);
 
   if (warp >= 8 && warp < 16) {
     // ================= producers =================
@@ -161,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
     int sg = 0;
     uint32_t phase = 0;
     int j = 0;
-    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const TileInfo ti = tile_info(p, c0, t);
       if (ti.r0 >= ti.r1) continue;
       if ((j++ & 1) != g) continue;
@@ -229,48 +234,46 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
       }
     }
   } else if (warp == kMmaWarp) {
-    // ================= MMA issuer =================
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_m128(BN);
-      const uint32_t smem_base = smem_u32(smem);
-      int sg[2] = {0, 0};
-      uint32_t phase[2] = {0, 0};
-      uint32_t acc_phase[2] = {0, 0};
-      int j = 0;
-      for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileInfo ti = tile_info(p, c0, t);
-        if (ti.r0 >= ti.r1) continue;
-        const int g = j++ & 1;
-        const int npb = p.nplanes[ti.group];
-        mbar_wait(&tempty[g], acc_phase[g] ^ 1u);
+    // ================= MMA issuer (whole warp; one elected lane issues) =================
+    constexpr uint32_t idesc = idesc_bf16_m128(BN);
+    const uint32_t smem_base = smem_u32(smem);
+    int sg[2] = {0, 0};
+    uint32_t phase[2] = {0, 0};
+    uint32_t acc_phase[2] = {0, 0};
+    int j = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const TileInfo ti = tile_info(p, c0, t);
+      if (ti.r0 >= ti.r1) continue;
+      const int g = j++ & 1;
+      const int npb = p.nplanes[ti.group];
+      mbar_wait(&tempty[g], acc_phase[g] ^ 1u);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem + uint32_t(g * BN);
+      for (int kc = 0; kc < p.kchunks; ++kc) {
+        const int s = g + 2 * sg[g];
+        mbar_wait(&full[s], phase[g]);
         tc_fence_after();
-        const uint32_t d_tmem = tmem + uint32_t(g * BN);
-        for (int kc = 0; kc < p.kchunks; ++kc) {
-          const int s = g + 2 * sg[g];
-          mbar_wait(&full[s], phase[g]);
-          tc_fence_after();
-          const uint32_t sa = smem_base + uint32_t(s) * stage_bytes;
-          const uint32_t sb = sa + 3 * kPlaneA;
+        const uint32_t sa = smem_base + uint32_t(s) * stage_bytes;
+        const uint32_t sb = sa + 3 * kPlaneA;
 #pragma unroll
-          for (int ks = 0; ks < kBK / 16; ++ks) {
-            const uint64_t ad = smem_desc(sa + ks * 256);
-            const uint64_t bd = smem_desc(sb + ks * 256);
-            if (npb == 1)
-              mma_split_step<1>(d_tmem, ad, bd, kPlaneA, kPlaneB, idesc, (kc | ks) != 0);
-            else
-              mma_split_step<3>(d_tmem, ad, bd, kPlaneA, kPlaneB, idesc, (kc | ks) != 0);
-          }
-          mma_commit(&empty[s]);
-          if (++sg[g] == SG) {
-            sg[g] = 0;
-            phase[g] ^= 1u;
-          }
+        for (int ks = 0; ks < kBK / 16; ++ks) {
+          const uint64_t ad = smem_desc(sa + ks * 256);
+          const uint64_t bd = smem_desc(sb + ks * 256);
+          const uint32_t acc = (kc | ks) != 0;
+          if (npb == 1)
+            mma_chain3_ss_w(d_tmem, ad, bd, kPlaneA >> 4, idesc, acc);
+          else
+            mma_chain6_ss_w(d_tmem, ad, bd, kPlaneA >> 4, kPlaneB >> 4, idesc, acc);
         }
-        mma_commit(&tfull[g]);
-        acc_phase[g] ^= 1u;
+        commit_w(&empty[s]);
+        if (++sg[g] == SG) {
+          sg[g] = 0;
+          phase[g] ^= 1u;
+        }
       }
+      commit_w(&tfull[g]);
+      acc_phase[g] ^= 1u;
     }
-    __syncwarp();
   } else {
     // ===== epilogue group g (warps 4g..4g+3): warp reads TMEM lanes 32*(warp%4) =====
     const int g = warp >> 2, quad = warp & 3;
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
     uint32_t acc_phase = 0;
     const bool vec4 = (p.N & 3) == 0;
     int j = 0;
-    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const TileInfo ti = tile_info(p, c0, t);
       if (ti.r0 >= ti.r1) continue;
       if ((j++ & 1) != g) continue;

@@ -94,6 +94,10 @@ static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cu
   p.stages = stages;
   const size_t smem = size_t(stages) * stage_bytes + fixed + 1024;  // + 1 KB alignment slack
   const int64_t tiles = m_tiles_max * p.ntiles;
+  if (tiles >= (int64_t(1) << 31)) {
+    set_error("tensor-core GEMM: %lld tiles exceed the 32-bit tile index", (long long)tiles);
+    return SA_ERR_SHAPE;
+  }
   const int grid = int(tiles < num_sms() ? tiles : num_sms());
 #define SA_TC_CASE(BNV)                                                                          \
   case BNV: {                                                                                    \
