@@ -10,6 +10,14 @@
 //                        single bulk async copy (TMA engine, complete_tx);
 //   warp  16             MMA issuer: one thread chains tcgen05.mma into TMEM
 //                        accumulator g and commits to the mbarriers;
+//   warp  17             A loader (plain / MoE-gathered rows): bulk-copies the
+//                        tile's fp32 row segments (TMA engine, 128 B per row and
+//                        K stage) into staging slots several stages ahead, one
+//                        ring per producer group (a ring has exactly one in-order
+//                        consumer, so an mbarrier parity can never alias a fill
+//                        two phases old), so the producers read A from shared
+//                        memory and HBM latency stays off their critical path
+//                        (p.nst = 0: producers load A themselves — patchify);
 //   warps  0-3 / 4-7     epilogue group g: tcgen05.ld (thread = accumulator
 //                        row), GELU / x gate, transpose through shared memory,
 //                        then coalesced 64-byte row segments with residual /
@@ -26,8 +34,10 @@ namespace sa {
 namespace tc {
 
 constexpr int kBM = 128;
-constexpr int kThreads = 544;
+constexpr int kThreads = 576;
 constexpr int kMmaWarp = 16;
+constexpr int kLoadWarp = 17;
+constexpr uint32_t kStgBytes = kBM * kBK * 4;   // one fp32 staging slot (128 rows x 32 k)
 constexpr uint32_t kPlaneA = kBM * kBK * 2;  // bytes per A plane
 constexpr int kXPitch = 20;                   // transpose buffer pitch (floats, 16B rows)
 
@@ -54,6 +64,7 @@ struct TcParams {
   const float* pos;
   int64_t img_tokens;
   int extra;
+  int nst;     // A staging slots over both rings (2, 4 or 8; 0 = producers load A directly)
 };
 
 template <int BN>
@@ -113,7 +124,7 @@ __device__ __forceinline__ float gelu_fast(float x) {
 __host__ __device__ inline size_t tc_fixed_smem() {
   return size_t(8) * 32 * kXPitch * sizeof(float)  // transpose buffers
          + 2 * 128 * sizeof(int64_t)                // per-group row tables
-         + (2 * 8 + 4) * 8 + 16;                    // barriers + TMEM slot
+         + (2 * 8 + 4 + 2 * 8) * 8 + 16;            // barriers (+ staging) + TMEM slot
 }
 
 template <int BN, int AM>
@@ -127,14 +138,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
   const int SG = S / 2;
   const int npb_max = max(p.nplanes[0], p.counts ? p.nplanes[1] : 0);
   const uint32_t stage_bytes = 3 * kPlaneA + uint32_t(npb_max) * kPlaneB;
-  float* xbuf = reinterpret_cast<float*>(smem + size_t(S) * stage_bytes);   // [8][32][kXPitch]
+  const int NST = p.nst;
+  uint8_t* stg = smem + size_t(S) * stage_bytes;                             // [NST][128][32] f32
+  float* xbuf = reinterpret_cast<float*>(stg + size_t(NST) * kStgBytes);     // [8][32][kXPitch]
   int64_t* orow_s = reinterpret_cast<int64_t*>(xbuf + 8 * 32 * kXPitch);    // [2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(orow_s + 256);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* tfull = bars + 2 * S;
   uint64_t* tempty = bars + 2 * S + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+  const int NSG = NST / 2;                        // staging slots per producer group
+  uint64_t* sfull = bars + 2 * S + 4;             // [2][NSG] staging slot loaded
+  uint64_t* sempty = sfull + NST;                 // [2][NSG] staging slot consumed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + NST);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == kMmaWarp) tmem_alloc<TCOLS>(tmem_slot);
@@ -146,6 +162,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);    // one MMA commit
       mbar_init(&tempty[b], 128); // every thread of the epilogue group
+    }
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&sfull[i], 32);   // one cp.async completion arrival per loader lane
+      mbar_init(&sempty[i], 4);   // the four warps of the consuming producer group
     }
     fence_barrier_init();
   }
@@ -166,6 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
     int sg = 0;
     uint32_t phase = 0;
     int j = 0;
+    int sidx = 0;   // stages this group has taken from its staging ring
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const TileInfo ti = tile_info(p, c0, t);
       if (ti.r0 >= ti.r1) continue;
@@ -179,8 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
         const int64_t row = ti.r0 + rsub + 16 * i;
         rowp[i] = nullptr;
         if (row < ti.r1) {
-          if (AM == A_PLAIN) {
-            rowp[i] = p.A + row * p.lda;
+          if (AM == A_PLAIN || NST > 0) {
+            rowp[i] = p.A + row * p.lda;   // (staged: only the non-null flag is used)
           } else if (AM == A_GATHER) {
             rowp[i] = p.A + int64_t(__ldg(p.a_rows + row)) * p.lda;
           } else {
@@ -195,14 +216,29 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
         const int s = g + 2 * sg;
         const int64_t k = int64_t(kc) * kBK + k4;
         float4 v[8];
+        if (NST > 0) {   // A rows from the loader's staging slot
+          const int ss = g * NSG + (sidx % NSG);
+          mbar_wait(&sfull[ss], uint32_t(sidx / NSG) & 1u);
+          ++sidx;
+          const float* sp = reinterpret_cast<const float*>(stg + size_t(ss) * kStgBytes);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {   // issue the global loads before waiting for the slot
-          v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (rowp[i] != nullptr && k < p.K) {
-            const float* src = (AM == A_PATCH)
-                                   ? rowp[i] + (k / pcw) * (p.pW * p.pC) + (k % pcw)
-                                   : rowp[i] + k;
-            v[i] = __ldg(reinterpret_cast<const float4*>(src));
+          for (int i = 0; i < 8; ++i) {
+            v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (rowp[i] != nullptr && k < p.K)
+              v[i] = *reinterpret_cast<const float4*>(sp + (rsub + 16 * i) * kBK + k4);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sempty[ss]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {   // issue the global loads before waiting for the slot
+            v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (rowp[i] != nullptr && k < p.K) {
+              const float* src = (AM == A_PATCH)
+                                     ? rowp[i] + (k / pcw) * (p.pW * p.pC) + (k % pcw)
+                                     : rowp[i] + k;
+              v[i] = __ldg(reinterpret_cast<const float4*>(src));
+            }
           }
         }
         mbar_wait(&empty[s], phase ^ 1u);
@@ -232,6 +268,68 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
           phase ^= 1u;
         }
       }
+    }
+  } else if (warp == kLoadWarp) {
+    // ================= A loader (staged mode) =================
+    if (NST > 0 && AM != A_PATCH) {
+      // lane = (16-byte chunk c, row sub-slab rs): one warp instruction copies
+      // four full 128-byte row segments (coalesced cp.async); completion is
+      // tracked per lane by cp.async.mbarrier.arrive.noinc (32 arrivals). The
+      // row indices (MoE gather) of the next tile are loaded one tile ahead.
+      const int c = lane & 7, rs = lane >> 3;
+      auto next_tile = [&](int t) {
+        for (; t < total; t += gridDim.x) {
+          const TileInfo ti = tile_info(p, c0, t);
+          if (ti.r0 < ti.r1) break;
+        }
+        return t;
+      };
+      auto rows_of = [&](int t, int (&src)[32], int& nrows) {
+        nrows = 0;
+        if (t >= total) return;
+        const TileInfo ti = tile_info(p, c0, t);
+        nrows = int(ti.r1 - ti.r0);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int r = rs + 4 * i;
+          const int64_t row = ti.r0 + r;
+          src[i] = r < nrows ? (AM == A_GATHER ? __ldg(p.a_rows + row) : int(row)) : -1;
+        }
+      };
+      int t = next_tile(blockIdx.x);
+      int cur[32], nxt[32];
+      int ncur = 0, nnxt = 0;
+      rows_of(t, cur, ncur);
+      int fills[2] = {0, 0};   // stages loaded into each group's ring
+      int jt = 0;              // non-empty tiles so far (group = jt & 1)
+      while (t < total) {
+        const int tn = next_tile(t + gridDim.x);
+        rows_of(tn, nxt, nnxt);
+        const int gg = jt++ & 1;
+        for (int kc = 0; kc < p.kchunks; ++kc) {
+          const int fi = fills[gg]++;
+          const int ss = gg * NSG + (fi % NSG);
+          mbar_wait(&sempty[ss], (uint32_t(fi / NSG) & 1u) ^ 1u);
+          const bool c_ok = int64_t(kc) * kBK + c * 4 < p.K;
+          const uint32_t dst = smem_u32(stg + size_t(ss) * kStgBytes) + uint32_t(rs * kBK * 4 + c * 16);
+          const float* base = p.A + int64_t(kc) * kBK + c * 4;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (cur[i] >= 0 && c_ok) {
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + uint32_t(i * 4 * kBK * 4)),
+                           "l"(base + int64_t(cur[i]) * p.lda)
+                           : "memory");
+            }
+          }
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&sfull[ss]))
+                       : "memory");
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) cur[i] = nxt[i];
+        ncur = nnxt;
+        t = tn;
+      }
+      (void)ncur;
     }
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer (whole warp; one elected lane issues) =================

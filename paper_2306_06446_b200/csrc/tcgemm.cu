@@ -77,22 +77,41 @@ static int num_sms() {
   return g_num_sms;
 }
 
+static int g_tc_stage = 0;   // A staging: 0 = direct A path (default), 1 = auto, 2/4/8 = force slots
+extern "C" void sa_debug_tc_stage(int on) { g_tc_stage = on; }
+
 static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cudaStream_t s) {
   using namespace tc;
   if (p.M == 0) return SA_OK;
   p.ntiles = int(cdiv(p.N, bn));
   const int npb_max = max(p.nplanes[0], p.counts ? p.nplanes[1] : 0);
   const size_t stage_bytes = 3 * size_t(kPlaneA) + size_t(npb_max) * bn * kBK * 2;
-  const size_t fixed = tc_fixed_smem();
+  const size_t fixed = tc_fixed_smem() + 1024;   // + 1 KB alignment slack
   const size_t budget = 220 * 1024;
-  int stages = int((budget - fixed) / stage_bytes);
-  stages = stages > 4 ? 4 : (stages & ~1);  // even: the two producer groups alternate
+  // A staging (loader warp + bulk copies) for plain / gathered rows whose 16-byte
+  // segments the TMA engine can copy; patchify keeps the direct loads
+  const bool stageable = g_tc_stage && amode != A_PATCH && (p.K % 4) == 0 && (p.lda % 4) == 0 &&
+                         (reinterpret_cast<uintptr_t>(p.A) & 15) == 0;
+  int stages = 0, nst = 0;
+  for (int cand_nst : {8, 4, 2, 0}) {
+    if (cand_nst > 0 && !stageable) continue;
+    if (g_tc_stage >= 2 && cand_nst > g_tc_stage) continue;
+    const size_t room = budget - fixed - size_t(cand_nst) * kStgBytes;
+    int st = int(room / stage_bytes);
+    st = st > 4 ? 4 : (st & ~1);  // even: the two producer groups alternate
+    if (st >= 2) {
+      stages = st;
+      nst = cand_nst;
+      break;
+    }
+  }
   if (stages < 2) {
     set_error("tensor-core stage does not fit shared memory (bn=%d)", bn);
     return SA_ERR_VALUE;
   }
   p.stages = stages;
-  const size_t smem = size_t(stages) * stage_bytes + fixed + 1024;  // + 1 KB alignment slack
+  p.nst = nst;
+  const size_t smem = size_t(stages) * stage_bytes + size_t(nst) * kStgBytes + fixed;
   const int64_t tiles = m_tiles_max * p.ntiles;
   if (tiles >= (int64_t(1) << 31)) {
     set_error("tensor-core GEMM: %lld tiles exceed the 32-bit tile index", (long long)tiles);
