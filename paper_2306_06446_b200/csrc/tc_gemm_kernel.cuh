@@ -67,10 +67,14 @@ struct TcParams {
   int nst;     // A staging slots over both rings (2, 4 or 8; 0 = producers load A directly)
 };
 
+// TMEM accumulators: four buffers when they fit (BN <= 128), so the MMA can run
+// two tiles ahead of each epilogue group; else two.
 template <int BN>
-struct TmemCols {  // two accumulator buffers, power of two >= 32
-  static constexpr uint32_t value = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
-                                    : 2 * BN <= 256 ? 256 : 512;
+struct Acc {
+  static constexpr int N = 4 * BN <= 512 ? 4 : 2;
+  static constexpr uint32_t COLS = N * BN;
+  static constexpr uint32_t TCOLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128
+                                    : COLS <= 256 ? 256 : 512;   // power of two >= 32
 };
 
 struct TileInfo {
@@ -113,6 +117,20 @@ __device__ __forceinline__ TileInfo tile_info(const TcParams& p, int64_t c0, int
   return ti;
 }
 
+// The next non-empty tile at or after t whose ordinal among the CTA's non-empty
+// tiles has parity g (the tiles a producer / epilogue group owns); j counts
+// the ordinals. Returns total when there is none.
+__device__ __forceinline__ int next_group_tile(const TcParams& p, int64_t c0, int total, int g,
+                                               int t, int& j, int& jj, TileInfo& ti) {
+  for (; t < total; t += gridDim.x) {
+    ti = tile_info(p, c0, t);
+    if (ti.r0 >= ti.r1) continue;
+    jj = j++;
+    if ((jj & 1) == g) return t;
+  }
+  return total;
+}
+
 __device__ __forceinline__ float gelu_fast(float x) {
   // 0.5·x·(1 + tanh(u)) == x / (1 + exp(-2u)); ex2.approx + fast divide keep
   // ~1e-7 relative accuracy (the reference's tanh is itself a float32 libm call)
@@ -132,7 +150,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // the swizzle pattern keys on absolute address bits: align the carve-out to 1 KB
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  constexpr uint32_t TCOLS = TmemCols<BN>::value;
+  constexpr uint32_t TCOLS = Acc<BN>::TCOLS;
+  constexpr int NACC = Acc<BN>::N;
   constexpr uint32_t kPlaneB = BN * kBK * 2;
   const int S = p.stages;
   const int SG = S / 2;
@@ -145,10 +164,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(orow_s + 256);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
-  uint64_t* tfull = bars + 2 * S;
-  uint64_t* tempty = bars + 2 * S + 2;
+  uint64_t* tfull = bars + 2 * S;                 // [NACC] accumulator ready
+  uint64_t* tempty = tfull + NACC;                // [NACC] accumulator drained
   const int NSG = NST / 2;                        // staging slots per producer group
-  uint64_t* sfull = bars + 2 * S + 4;             // [2][NSG] staging slot loaded
+  uint64_t* sfull = tempty + NACC;                // [2][NSG] staging slot loaded
   uint64_t* sempty = sfull + NST;                 // [2][NSG] staging slot consumed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + NST);
 
@@ -159,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
       mbar_init(&full[s], 4);     // the four warps of the owning producer group
       mbar_init(&empty[s], 1);    // one MMA commit
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NACC; ++b) {
       mbar_init(&tfull[b], 1);    // one MMA commit
       mbar_init(&tempty[b], 128); // every thread of the epilogue group
     }
@@ -187,10 +206,28 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
     uint32_t phase = 0;
     int j = 0;
     int sidx = 0;   // stages this group has taken from its staging ring
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const TileInfo ti = tile_info(p, c0, t);
-      if (ti.r0 >= ti.r1) continue;
-      if ((j++ & 1) != g) continue;
+    // MoE gather indices of the group's NEXT tile are loaded while the current
+    // tile is processed (their HBM latency would otherwise precede every tile)
+    constexpr bool PF = AM == A_GATHER;
+    int jj_unused;
+    TileInfo ti_n;
+    int t_n = next_group_tile(p, c0, total, g, blockIdx.x, j, jj_unused, ti_n);
+    int idx_n[8];
+    auto load_idx = [&](const TileInfo& tq, int (&ix)[8]) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t row = tq.r0 + rsub + 16 * i;
+        ix[i] = (PF && NST == 0 && row < tq.r1) ? __ldg(p.a_rows + row) : 0;
+      }
+    };
+    if (t_n < total) load_idx(ti_n, idx_n);
+    while (t_n < total) {
+      const TileInfo ti = ti_n;
+      int idx[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) idx[i] = idx_n[i];
+      t_n = next_group_tile(p, c0, total, g, t_n + gridDim.x, j, jj_unused, ti_n);
+      if (t_n < total) load_idx(ti_n, idx_n);
       const int npb = p.nplanes[ti.group];
       const uint16_t* Bg = p.Bp[ti.group] + size_t(ti.n_tile) * p.kchunks * npb * (BN * kBK);
       const uint32_t bbytes = uint32_t(npb) * kPlaneB;
@@ -203,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
           if (AM == A_PLAIN || NST > 0) {
             rowp[i] = p.A + row * p.lda;   // (staged: only the non-null flag is used)
           } else if (AM == A_GATHER) {
-            rowp[i] = p.A + int64_t(__ldg(p.a_rows + row)) * p.lda;
+            rowp[i] = p.A + int64_t(idx[i]) * p.lda;
           } else {
             const int64_t tpi = p.pside * p.pside;
             const int64_t b = row / tpi, tt = row % tpi;
@@ -337,16 +374,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
     const uint32_t smem_base = smem_u32(smem);
     int sg[2] = {0, 0};
     uint32_t phase[2] = {0, 0};
-    uint32_t acc_phase[2] = {0, 0};
+    uint32_t acc_phase[NACC];
+#pragma unroll
+    for (int a = 0; a < NACC; ++a) acc_phase[a] = 0u;
     int j = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const TileInfo ti = tile_info(p, c0, t);
       if (ti.r0 >= ti.r1) continue;
-      const int g = j++ & 1;
+      const int jj = j++;
+      const int g = jj & 1;                 // producer group / smem stage owner
+      const int acc = jj & (NACC - 1);      // TMEM accumulator
       const int npb = p.nplanes[ti.group];
-      mbar_wait(&tempty[g], acc_phase[g] ^ 1u);
+      mbar_wait(&tempty[acc], acc_phase[acc] ^ 1u);
       tc_fence_after();
-      const uint32_t d_tmem = tmem + uint32_t(g * BN);
+      const uint32_t d_tmem = tmem + uint32_t(acc * BN);
       for (int kc = 0; kc < p.kchunks; ++kc) {
         const int s = g + 2 * sg[g];
         mbar_wait(&full[s], phase[g]);
@@ -369,44 +410,67 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
           phase[g] ^= 1u;
         }
       }
-      commit_w(&tfull[g]);
-      acc_phase[g] ^= 1u;
+      commit_w(&tfull[acc]);
+      acc_phase[acc] ^= 1u;
     }
   } else {
     // ===== epilogue group g (warps 4g..4g+3): warp reads TMEM lanes 32*(warp%4) =====
     const int g = warp >> 2, quad = warp & 3;
     float* xb = xbuf + warp * 32 * kXPitch;     // [32 rows][kXPitch]
     int64_t* orow_t = orow_s + g * 128;
-    uint32_t acc_phase = 0;
+    uint32_t acc_phase[NACC / 2];   // this group owns accumulators g, g + 2, ...
+#pragma unroll
+    for (int a = 0; a < NACC / 2; ++a) acc_phase[a] = 0u;
     const bool vec4 = (p.N & 3) == 0;
     int j = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const TileInfo ti = tile_info(p, c0, t);
-      if (ti.r0 >= ti.r1) continue;
-      if ((j++ & 1) != g) continue;
-      const int rl = quad * 32 + lane;             // row within the tile
+    const int rl = quad * 32 + lane;             // row within the tile
+    // Row metadata is software-pipelined over the group's tiles: the scatter
+    // row of tile B (next) and its gate, and the scatter row of tile C (after
+    // next), are in flight while tile A is drained (dependent HBM loads).
+    auto scatter_row = [&](const TileInfo& tq) -> int64_t {
+      const int64_t r = tq.r0 + rl;
+      if (r >= tq.r1) return -1;
+      return p.c_rows ? int64_t(__ldg(p.c_rows + r)) : r;
+    };
+    TileInfo tiA, tiB, tiC;
+    int jjA = 0, jjB = 0, jjC = 0;
+    int tA = next_group_tile(p, c0, total, g, blockIdx.x, j, jjA, tiA);
+    int tB = tA < total ? next_group_tile(p, c0, total, g, tA + gridDim.x, j, jjB, tiB) : total;
+    int64_t crA = tA < total ? scatter_row(tiA) : -1;
+    int64_t crB = tB < total ? scatter_row(tiB) : -1;
+    float gA = (p.gate && crA >= 0 && p.img_tokens == 0) ? __ldg(p.gate + crA) : 1.f;
+    while (tA < total) {
+      const int tC = tB < total ? next_group_tile(p, c0, total, g, tB + gridDim.x, j, jjC, tiC)
+                                : total;
+      const int64_t crC = tC < total ? scatter_row(tiC) : -1;
+      const float gB = (p.gate && crB >= 0 && p.img_tokens == 0) ? __ldg(p.gate + crB) : 1.f;
+      const TileInfo ti = tiA;
+      const int jj = jjA;
+      const int acc = jj & (NACC - 1), ah = acc >> 1;
       const int64_t r = ti.r0 + rl;
       const bool r_ok = r < ti.r1;
       int64_t orow = -1, pos_idx = 0;
       float gt = 1.f;
       if (r_ok) {
-        orow = p.c_rows ? int64_t(__ldg(p.c_rows + r)) : r;
+        orow = crA;
         if (p.img_tokens > 0) {
           const int64_t b = r / p.img_tokens, tt = r % p.img_tokens;
           orow = b * (p.img_tokens + p.extra) + p.extra + tt;
           pos_idx = p.extra + tt;
+          if (p.gate) gt = __ldg(p.gate + orow);
+        } else if (p.gate) {
+          gt = gA;
         }
-        if (p.gate) gt = __ldg(p.gate + orow);
       }
       // the row table of the previous tile of this group has been consumed by
       // every warp of the group once they all reach this barrier
       asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
       orow_t[rl] = r_ok ? (p.pos ? (orow | (pos_idx << 40)) : orow) : int64_t(-1);
-      mbar_wait(&tfull[g], acc_phase);
-      acc_phase ^= 1u;
+      mbar_wait(&tfull[acc], acc_phase[ah]);
+      acc_phase[ah] ^= 1u;
       tc_fence_after();
       asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
-      const uint32_t t_base = tmem + (uint32_t(quad * 32) << 16) + uint32_t(g * BN);
+      const uint32_t t_base = tmem + (uint32_t(quad * 32) << 16) + uint32_t(acc * BN);
       const int64_t n_base = int64_t(ti.n_tile) * BN;
 #pragma unroll 1
       for (int cb = 0; cb < BN; cb += 16) {
@@ -461,7 +525,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
         __syncwarp();
       }
       tc_fence_before();
-      mbar_arrive(&tempty[g]);
+      mbar_arrive(&tempty[acc]);
+      tA = tB;
+      tiA = tiB;
+      jjA = jjB;
+      crA = crB;
+      gA = gB;
+      tB = tC;
+      tiB = tiC;
+      jjB = jjC;
+      crB = crC;
     }
   }
   tc_fence_before();
