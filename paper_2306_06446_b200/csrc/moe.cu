@@ -82,8 +82,21 @@ __global__ void __launch_bounds__(256) route_kernel(const float* __restrict__ x,
     double s0 = 0.0, s1 = 0.0;
     if (ok) {
       const float4* row = reinterpret_cast<const float4*>(x + t * d);
-      for (int c4 = sub; c4 < d4; c4 += G) {
-        const float4 v = __ldg(row + c4);
+      // the row slice in chunks of 16 float4: each chunk's loads are all in
+      // flight before its first FMA (one memory latency per 64 channels)
+      constexpr int PF = 16;
+      for (int cb = 0; cb < d4; cb += PF * G) {
+      float4 pre[PF];
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int c4 = cb + sub + u * G;
+        pre[u] = c4 < d4 ? __ldg(row + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int c4 = cb + sub + u * G;
+        if (c4 >= d4) break;
+        const float4 v = pre[u];
         const double* w = sw + 8 * c4;
         s0 = fma(double(v.x), w[0], s0);
         s1 = fma(double(v.x), w[1], s1);
@@ -93,6 +106,7 @@ __global__ void __launch_bounds__(256) route_kernel(const float* __restrict__ x,
         s1 = fma(double(v.z), w[5], s1);
         s0 = fma(double(v.w), w[6], s0);
         s1 = fma(double(v.w), w[7], s1);
+      }
       }
     }
 #pragma unroll
@@ -227,10 +241,25 @@ __global__ void __launch_bounds__(kRouteTok, 3) ln_route_kernel(
   const int64_t row0 = int64_t(blockIdx.x) * kRouteTok;
   const int nrows = int(min(int64_t(kRouteTok), M - row0));
   {
+    // all of a thread's 128-bit loads are issued before the first store, so
+    // the row block costs one memory latency, not D/4 of them
     const float4* src = reinterpret_cast<const float4*>(x + row0 * D);
-    for (int i = threadIdx.x; i < nrows * (D / 4); i += kRouteTok) {
-      const int rr = i / (D / 4), c4 = i % (D / 4);
-      *reinterpret_cast<float4*>(tile + rr * PITCH + 4 * c4) = __ldg(src + i);
+    constexpr int PER = D / 4;   // float4 per thread (kRouteTok rows x D/4 / kRouteTok)
+    constexpr int CH = PER < 8 ? PER : 8;   // loads in flight per batch (register budget)
+#pragma unroll
+    for (int u0 = 0; u0 < PER; u0 += CH) {
+      float4 buf[CH];
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const int i = threadIdx.x + (u0 + u) * kRouteTok;
+        buf[u] = i < nrows * (D / 4) ? __ldg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const int i = threadIdx.x + (u0 + u) * kRouteTok;
+        const int rr = i / (D / 4), c4 = i % (D / 4);
+        if (i < nrows * (D / 4)) *reinterpret_cast<float4*>(tile + rr * PITCH + 4 * c4) = buf[u];
+      }
     }
   }
   __syncthreads();
@@ -277,11 +306,21 @@ __global__ void __launch_bounds__(kRouteTok, 3) ln_route_kernel(
   for (int r = 0; r < nr; ++r) {
     int e = 0;
     if (ok) {
+      // router dot on the normalized row, re-read from the tile (keeps the
+      // register footprint small: no spills at 3 CTAs / SM)
       double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int c = 0; c < D; ++c) {
-        s0 = fma(double(v[c]), sw[r][2 * c], s0);
-        s1 = fma(double(v[c]), sw[r][2 * c + 1], s1);
+#pragma unroll 4
+      for (int c4 = 0; c4 < D / 4; ++c4) {
+        const float4 q = *reinterpret_cast<const float4*>(trow + 4 * c4);
+        const double* w = &sw[r][8 * c4];
+        s0 = fma(double(q.x), w[0], s0);
+        s1 = fma(double(q.x), w[1], s1);
+        s0 = fma(double(q.y), w[2], s0);
+        s1 = fma(double(q.y), w[3], s1);
+        s0 = fma(double(q.z), w[4], s0);
+        s1 = fma(double(q.z), w[5], s1);
+        s0 = fma(double(q.w), w[6], s0);
+        s1 = fma(double(q.w), w[7], s1);
       }
       float g;
       e = decide(float(s0), float(s1), tie_thresh, g);
@@ -361,12 +400,11 @@ extern "C" int sa_moe_route(const float* x, const float* wg, int64_t M, int64_t 
   const int nb = int(cdiv(M, kRouteTok));
   int32_t* block_cnt1 = static_cast<int32_t*>(ws);
   int32_t* block_off1 = block_cnt1 + nb;
-  if (d <= 64)
-    route_kernel<1><<<nb, 256, 0, s>>>(x, wg, M, int(d), tie_thresh, logits, expert_of, gate,
-                                       block_cnt1);
-  else
-    route_kernel<8><<<nb, 256, 0, s>>>(x, wg, M, int(d), tie_thresh, logits, expert_of, gate,
-                                       block_cnt1);
+  // one thread per token for every width: the row streams in 64-channel
+  // chunks with all loads of a chunk in flight (8 lanes per token with a
+  // per-pass loop serialised 8 passes of latency per block)
+  route_kernel<1><<<nb, 256, 0, s>>>(x, wg, M, int(d), tie_thresh, logits, expert_of, gate,
+                                     block_cnt1);
   route_scan_kernel<<<1, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
   partition_kernel<<<nb, kRouteTok, 0, s>>>(expert_of, block_off1, counts, M, perm);
   count_launch(3);
