@@ -34,7 +34,12 @@ namespace sa {
 namespace tc {
 
 constexpr int kBM = 128;
-constexpr int kThreads = 576;
+// The A-staging loader (warp 17) measured slower than direct producer loads on
+// every projection shape (per-row bulk copies saturate the TMA unit; cp.async
+// staging adds a hop without shortening the per-tile latency chain), so it is
+// compiled out; the code is kept for reference and A/B runs.
+constexpr bool kStaging = false;
+constexpr int kThreads = kStaging ? 576 : 544;
 constexpr int kMmaWarp = 16;
 constexpr int kLoadWarp = 17;
 constexpr uint32_t kStgBytes = kBM * kBK * 4;   // one fp32 staging slot (128 rows x 32 k)
@@ -65,6 +70,9 @@ struct TcParams {
   int64_t img_tokens;
   int extra;
   int nst;     // A staging slots over both rings (2, 4 or 8; 0 = producers load A directly)
+  int rb;      // 1: every weight tile resident in shared memory for the whole kernel
+  uint32_t rb_bytes[2];   // resident bytes per expert (packed planes, [n_tile][kc][plane])
+  int dbg;     // debug role isolation (0 in production): 1 no A loads, 2 no C stores, 4 no MMAs
 };
 
 // TMEM accumulators: four buffers when they fit (BN <= 128), so the MMA can run
@@ -156,9 +164,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
   const int S = p.stages;
   const int SG = S / 2;
   const int npb_max = max(p.nplanes[0], p.counts ? p.nplanes[1] : 0);
-  const uint32_t stage_bytes = 3 * kPlaneA + uint32_t(npb_max) * kPlaneB;
+  // resident weights: B lives in one region loaded at kernel start; stages hold A only
+  const uint32_t stage_bytes = 3 * kPlaneA + (p.rb ? 0u : uint32_t(npb_max) * kPlaneB);
   const int NST = p.nst;
-  uint8_t* stg = smem + size_t(S) * stage_bytes;                             // [NST][128][32] f32
+  uint8_t* resb = smem + size_t(S) * stage_bytes;                            // resident B
+  const uint32_t rb_total = p.rb ? ((p.rb_bytes[0] + p.rb_bytes[1] + 1023u) & ~1023u) : 0u;
+  uint8_t* stg = resb + rb_total;                                            // [NST][128][32] f32
   float* xbuf = reinterpret_cast<float*>(stg + size_t(NST) * kStgBytes);     // [8][32][kXPitch]
   int64_t* orow_s = reinterpret_cast<int64_t*>(xbuf + 8 * 32 * kXPitch);    // [2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(orow_s + 256);
@@ -169,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
   const int NSG = NST / 2;                        // staging slots per producer group
   uint64_t* sfull = tempty + NACC;                // [2][NSG] staging slot loaded
   uint64_t* sempty = sfull + NST;                 // [2][NSG] staging slot consumed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + NST);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + NST + 1);   // (+ resident-B barrier)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == kMmaWarp) tmem_alloc<TCOLS>(tmem_slot);
@@ -187,10 +198,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
       mbar_init(&sempty[i], 4);   // the four warps of the consuming producer group
     }
     fence_barrier_init();
+    if (p.rb) {   // every weight tile of both experts, once (TMA bulk copies)
+      uint64_t* rbar = sempty + NST;
+      mbar_init(rbar, 1);
+      fence_barrier_init();
+      mbar_expect_tx(rbar, p.rb_bytes[0] + p.rb_bytes[1]);
+      bulk_g2s(resb, p.Bp[0], p.rb_bytes[0], rbar);
+      if (p.rb_bytes[1]) bulk_g2s(resb + p.rb_bytes[0], p.Bp[1], p.rb_bytes[1], rbar);
+    }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (p.rb) mbar_wait(sempty + NST, 0);
   const uint32_t tmem = *tmem_slot;
   const int64_t c0 = p.counts ? int64_t(p.counts[0]) : 0;
   const int total = int(num_m_tiles(p, c0) * p.ntiles);
@@ -253,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
         const int s = g + 2 * sg;
         const int64_t k = int64_t(kc) * kBK + k4;
         float4 v[8];
-        if (NST > 0) {   // A rows from the loader's staging slot
+        if (kStaging && NST > 0) {   // A rows from the loader's staging slot
           const int ss = g * NSG + (sidx % NSG);
           mbar_wait(&sfull[ss], uint32_t(sidx / NSG) & 1u);
           ++sidx;
@@ -274,13 +294,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
               const float* src = (AM == A_PATCH)
                                      ? rowp[i] + (k / pcw) * (p.pW * p.pC) + (k % pcw)
                                      : rowp[i] + k;
-              v[i] = __ldg(reinterpret_cast<const float4*>(src));
+              if (!(p.dbg & 1)) v[i] = __ldg(reinterpret_cast<const float4*>(src));
             }
           }
         }
         mbar_wait(&empty[s], phase ^ 1u);
         uint8_t* st = smem + size_t(s) * stage_bytes;
-        if (ptid == 0) {
+        if (ptid == 0 && !p.rb) {
           mbar_add_tx(&full[s], bbytes);
           bulk_g2s(st + 3 * kPlaneA, Bg + size_t(kc) * npb * (BN * kBK), bbytes, &full[s]);
         }
@@ -297,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
           *reinterpret_cast<uint2*>(st + 2 * kPlaneA + off) =
               make_uint2(bf2_bits(a.l), bf2_bits(b.l));
         }
-        fence_proxy_async_smem();
+        if (!(p.dbg & 8)) fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[s]);
         if (++sg == SG) {
@@ -308,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
     }
   } else if (warp == kLoadWarp) {
     // ================= A loader (staged mode) =================
-    if (NST > 0 && AM != A_PATCH) {
+    if (kStaging && NST > 0 && AM != A_PATCH) {
       // lane = (16-byte chunk c, row sub-slab rs): one warp instruction copies
       // four full 128-byte row segments (coalesced cp.async); completion is
       // tracked per lane by cp.async.mbarrier.arrive.noinc (32 arrivals). The
@@ -393,12 +413,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
         mbar_wait(&full[s], phase[g]);
         tc_fence_after();
         const uint32_t sa = smem_base + uint32_t(s) * stage_bytes;
-        const uint32_t sb = sa + 3 * kPlaneA;
+        const uint32_t sb = p.rb ? smem_u32(resb) + (ti.group ? p.rb_bytes[0] : 0u) +
+                                       uint32_t((ti.n_tile * p.kchunks + kc) * npb) * kPlaneB
+                                 : sa + 3 * kPlaneA;
 #pragma unroll
         for (int ks = 0; ks < kBK / 16; ++ks) {
           const uint64_t ad = smem_desc(sa + ks * 256);
           const uint64_t bd = smem_desc(sb + ks * 256);
           const uint32_t acc = (kc | ks) != 0;
+          if (p.dbg & 4) continue;
           if (npb == 1)
             mma_chain3_ss_w(d_tmem, ad, bd, kPlaneA >> 4, idesc, acc);
           else
@@ -509,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
                   __ldg(reinterpret_cast<const float4*>(p.residual + orow_i * p.N + n));
               o = make_float4(q.x + o.x, q.y + o.y, q.z + o.z, q.w + o.w);
             }
-            *reinterpret_cast<float4*>(p.C + orow_i * p.N + n) = o;
+            if (!(p.dbg & 2)) *reinterpret_cast<float4*>(p.C + orow_i * p.N + n) = o;
           } else {
             const float ov[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll

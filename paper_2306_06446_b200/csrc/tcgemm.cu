@@ -77,6 +77,10 @@ static int num_sms() {
   return g_num_sms;
 }
 
+static int g_tc_dbg = 0;
+extern "C" void sa_debug_tc_mode(int m) { g_tc_dbg = m; }
+static int g_tc_resident = 1;   // weights resident in shared memory when they fit
+extern "C" void sa_debug_tc_resident(int on) { g_tc_resident = on; }
 static int g_tc_stage = 0;   // A staging: 0 = direct A path (default), 1 = auto, 2/4/8 = force slots
 extern "C" void sa_debug_tc_stage(int on) { g_tc_stage = on; }
 
@@ -85,18 +89,27 @@ static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cu
   if (p.M == 0) return SA_OK;
   p.ntiles = int(cdiv(p.N, bn));
   const int npb_max = max(p.nplanes[0], p.counts ? p.nplanes[1] : 0);
-  const size_t stage_bytes = 3 * size_t(kPlaneA) + size_t(npb_max) * bn * kBK * 2;
+  // resident weights when both experts' packed tiles fit in 48 KB
+  p.ntiles = int(cdiv(p.N, bn));
+  const size_t wb0 = size_t(p.ntiles) * p.kchunks * p.nplanes[0] * bn * kBK * 2;
+  const size_t wb1 = p.counts ? size_t(p.ntiles) * p.kchunks * p.nplanes[1] * bn * kBK * 2 : 0;
+  p.rb = (g_tc_resident && wb0 + wb1 <= 48 * 1024) ? 1 : 0;
+  p.dbg = g_tc_dbg;
+  p.rb_bytes[0] = p.rb ? uint32_t(wb0) : 0u;
+  p.rb_bytes[1] = p.rb ? uint32_t(wb1) : 0u;
+  const size_t rb_total = p.rb ? ((wb0 + wb1 + 1023) & ~size_t(1023)) : 0;
+  const size_t stage_bytes = 3 * size_t(kPlaneA) + (p.rb ? 0 : size_t(npb_max) * bn * kBK * 2);
   const size_t fixed = tc_fixed_smem() + 1024;   // + 1 KB alignment slack
   const size_t budget = 220 * 1024;
   // A staging (loader warp + bulk copies) for plain / gathered rows whose 16-byte
   // segments the TMA engine can copy; patchify keeps the direct loads
-  const bool stageable = g_tc_stage && amode != A_PATCH && (p.K % 4) == 0 && (p.lda % 4) == 0 &&
+  const bool stageable = tc::kStaging && g_tc_stage && amode != A_PATCH && (p.K % 4) == 0 && (p.lda % 4) == 0 &&
                          (reinterpret_cast<uintptr_t>(p.A) & 15) == 0;
   int stages = 0, nst = 0;
   for (int cand_nst : {8, 4, 2, 0}) {
     if (cand_nst > 0 && !stageable) continue;
     if (g_tc_stage >= 2 && cand_nst > g_tc_stage) continue;
-    const size_t room = budget - fixed - size_t(cand_nst) * kStgBytes;
+    const size_t room = budget - fixed - rb_total - size_t(cand_nst) * kStgBytes;
     int st = int(room / stage_bytes);
     st = st > 4 ? 4 : (st & ~1);  // even: the two producer groups alternate
     if (st >= 2) {
@@ -111,7 +124,7 @@ static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cu
   }
   p.stages = stages;
   p.nst = nst;
-  const size_t smem = size_t(stages) * stage_bytes + size_t(nst) * kStgBytes + fixed;
+  const size_t smem = size_t(stages) * stage_bytes + rb_total + size_t(nst) * kStgBytes + fixed;
   const int64_t tiles = m_tiles_max * p.ntiles;
   if (tiles >= (int64_t(1) << 31)) {
     set_error("tensor-core GEMM: %lld tiles exceed the 32-bit tile index", (long long)tiles);
