@@ -41,6 +41,7 @@ namespace baf {
 constexpr int DK = 32;
 constexpr int kThreads = 256;
 constexpr int kStreams = 16;        // pass-1 token streams (16 threads each)
+constexpr int kMaxCluster = 8;
 constexpr int kSeg = 6;             // pass-2 tokens per row segment (multiple of 3)
 
 struct Params {
@@ -330,9 +331,9 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
   for (int h = 0; h < HEADS; ++h) {
     const float g = __ldg(p.gk + b * HEADS + h);
     const int grp = tid / DK, c = tid % DK;       // tables: thread = (nibble group, column)
-    float x[8][4];
+    float x[kMaxCluster][4];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {   // issue every peer's loads before summing
+    for (int r = 0; r < kMaxCluster; ++r) {   // issue every peer's loads before summing
       if (r < CL) {
         const float* pr = cluster.map_shared_rank(part, r) + h * DK * DK + 4 * grp * DK + c;
         x[r][0] = pr[0];
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
     }
     float row[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
+    for (int r = 0; r < kMaxCluster; ++r)
       if (r < CL) {
         row[0] += x[r][0];
         row[1] += x[r][1];
@@ -493,8 +494,9 @@ int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
   while (int64_t(side) * side < n) ++side;
   const int rows_total = int((n + side - 1) / side);
   // bands of ~400 (token, head) pairs amortise the per-CTA table work
+  // (16-CTA non-portable clusters measured 1.8x slower: GPC packing)
   int cl = int((n * heads + 399) / 400);
-  cl = cl < 1 ? 1 : (cl > 8 ? 8 : cl);
+  cl = cl < 1 ? 1 : (cl > kMaxCluster ? kMaxCluster : cl);
   cl = cl > rows_total ? rows_total : cl;
   const int br = (rows_total + cl - 1) / cl;
   cl = (rows_total + br - 1) / br;
@@ -516,6 +518,7 @@ int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
   else if (d == 64 && side == 15) kern = binattn_fused_kernel<64, 15>;
   if (kern == nullptr) return SA_ERR_VALUE;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total));
+  if (cl > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(cl), unsigned(B), 1);
   cfg.blockDim = dim3(kThreads, 1, 1);

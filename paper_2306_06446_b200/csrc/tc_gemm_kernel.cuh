@@ -155,6 +155,10 @@ __host__ __device__ inline size_t tc_fixed_smem() {
 
 template <int BN, int AM>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
+  // direct epilogue (thread = row, no shared-memory transpose) for wide tiles
+  // (measured: removes the transpose cost but its per-row 16-byte stores halve
+  // DRAM write efficiency — 391 vs 283 us on K3 — so the transposed path stays)
+  constexpr bool DIRECT = false;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // the swizzle pattern keys on absolute address bits: align the carve-out to 1 KB
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -495,6 +499,57 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
       asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
       const uint32_t t_base = tmem + (uint32_t(quad * 32) << 16) + uint32_t(acc * BN);
       const int64_t n_base = int64_t(ti.n_tile) * BN;
+      if (DIRECT) {
+        // thread = output row: 16 columns per TMEM load (issued one chunk
+        // ahead), then four 16-byte stores of the row's contiguous 64-byte
+        // segment (no shared-memory transpose)
+        const bool full4 = vec4 && n_base + BN <= p.N;
+        float* crow = (r_ok && orow >= 0) ? p.C + orow * p.N + n_base : nullptr;
+        const float* rrow = (crow && p.residual) ? p.residual + orow * p.N + n_base : nullptr;
+        const float* prow = (crow && p.pos) ? p.pos + pos_idx * p.N + n_base : nullptr;
+        float v[16];
+        tmem_ld16(t_base, v);
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += 16) {
+          float o[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) o[q] = v[q];
+          if (cb + 16 < BN) tmem_ld16(t_base + uint32_t(cb + 16), v);
+          if (crow == nullptr) continue;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            float e = o[q];
+            if (p.act == 1) e = gelu_fast(e);
+            if (p.gate) e = e * gt;
+            o[q] = e;
+          }
+          if (full4) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float4 w = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+              if (prow) {
+                const float4 pp = __ldg(reinterpret_cast<const float4*>(prow + cb) + q);
+                w.x += pp.x; w.y += pp.y; w.z += pp.z; w.w += pp.w;
+              }
+              if (rrow) {
+                const float4 rq = __ldg(reinterpret_cast<const float4*>(rrow + cb) + q);
+                w = make_float4(rq.x + w.x, rq.y + w.y, rq.z + w.z, rq.w + w.w);
+              }
+              if (!(p.dbg & 2)) *reinterpret_cast<float4*>(crow + cb + 4 * q) = w;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const int64_t n = n_base + cb + q;
+              if (n >= p.N) break;
+              float e = o[q];
+              if (prow) e = e + __ldg(prow + cb + q);
+              if (rrow) e = __ldg(rrow + cb + q) + e;
+              crow[cb + q] = e;
+            }
+          }
+        }
+      } else
 #pragma unroll 1
       for (int cb = 0; cb < BN; cb += 16) {
         float v[16];
