@@ -410,8 +410,9 @@ def main():
     dom = next(r for r in ops_rows if r["achieved_gbs"] is not None)
     traffic = None
     tr_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
-    if os.path.exists(tr_path):   # dram bytes per launch from the committed ncu capture
-        traffic = json.load(open(tr_path)).get(dom["op"])
+    if os.path.exists(tr_path):   # DRAM bytes per call of the op from the committed ncu capture
+        tr = json.load(open(tr_path)).get(dom["op"])
+        traffic = tr["dram_bytes_per_call"] if isinstance(tr, dict) else tr
     roofline = {"bound": "hbm", "kernel": dom["op"], "achieved": dom["achieved_gbs"],
                 "peak": hbm_peak, "unit": "GB/s", "frac": dom["frac_hbm"],
                 "traffic": traffic, "peak_source": peak_src,
