@@ -124,9 +124,13 @@ __global__ void __launch_bounds__(256) softmax_attn_kernel(const float* __restri
     }
     tot = warp_sum(tot);
     __syncwarp();
+    // p_j = e_j / sum (the reference's float32 division, once per key)
+    for (int j = lane; j < n; j += 32) myp[j] = myp[j] / tot;
+    __syncwarp();
     for (int c = lane; c < dk; c += 32) {
       float acc = 0.f;
-      for (int j = 0; j < n; ++j) acc = fmaf(myp[j] / tot, sv[j * dk + c], acc);
+#pragma unroll 4
+      for (int j = 0; j < n; ++j) acc = fmaf(myp[j], sv[j * dk + c], acc);
       out[(rowbase + i) * d + h * dk + c] = acc;
     }
     __syncwarp();

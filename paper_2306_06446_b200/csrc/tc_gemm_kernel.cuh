@@ -126,15 +126,15 @@ __device__ __forceinline__ TileInfo tile_info(const TcParams& p, int64_t c0, int
 }
 
 // The next non-empty tile at or after t whose ordinal among the CTA's non-empty
-// tiles has parity g (the tiles a producer / epilogue group owns); j counts
-// the ordinals. Returns total when there is none.
+// tiles has parity g (the tiles a producer / epilogue group owns; g < 0: any);
+// j counts the ordinals. Returns total when there is none.
 __device__ __forceinline__ int next_group_tile(const TcParams& p, int64_t c0, int total, int g,
                                                int t, int& j, int& jj, TileInfo& ti) {
   for (; t < total; t += gridDim.x) {
     ti = tile_info(p, c0, t);
     if (ti.r0 >= ti.r1) continue;
     jj = j++;
-    if ((jj & 1) == g) return t;
+    if (g < 0 || (jj & 1) == g) return t;   // g < 0: every non-empty tile
   }
   return total;
 }
@@ -235,7 +235,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
     constexpr bool PF = AM == A_GATHER;
     int jj_unused;
     TileInfo ti_n;
-    int t_n = next_group_tile(p, c0, total, g, blockIdx.x, j, jj_unused, ti_n);
+    // K stages: with one stage per tile the two groups alternate tiles; with
+    // several, consecutive stages of the CTA's whole sequence alternate between
+    // the groups, so both keep loads in flight within a deep-K tile
+    const bool kq = p.kchunks > 1;
+    const int gsel = kq ? -1 : g;
+    int q = 0;
+    int t_n = next_group_tile(p, c0, total, gsel, blockIdx.x, j, jj_unused, ti_n);
     int idx_n[8];
     auto load_idx = [&](const TileInfo& tq, int (&ix)[8]) {
 #pragma unroll
@@ -250,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
       int idx[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) idx[i] = idx_n[i];
-      t_n = next_group_tile(p, c0, total, g, t_n + gridDim.x, j, jj_unused, ti_n);
+      t_n = next_group_tile(p, c0, total, gsel, t_n + gridDim.x, j, jj_unused, ti_n);
       if (t_n < total) load_idx(ti_n, idx_n);
       const int npb = p.nplanes[ti.group];
       const uint16_t* Bg = p.Bp[ti.group] + size_t(ti.n_tile) * p.kchunks * npb * (BN * kBK);
@@ -274,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
         }
       }
       for (int kc = 0; kc < p.kchunks; ++kc) {
+        if (kq && ((q++ & 1) != g)) continue;
         const int s = g + 2 * sg;
         const int64_t k = int64_t(kc) * kBK + k4;
         float4 v[8];
@@ -401,18 +408,22 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
     uint32_t acc_phase[NACC];
 #pragma unroll
     for (int a = 0; a < NACC; ++a) acc_phase[a] = 0u;
+    const bool kq_mma = p.kchunks > 1;
+    int qm = 0;
     int j = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const TileInfo ti = tile_info(p, c0, t);
       if (ti.r0 >= ti.r1) continue;
       const int jj = j++;
-      const int g = jj & 1;                 // producer group / smem stage owner
       const int acc = jj & (NACC - 1);      // TMEM accumulator
       const int npb = p.nplanes[ti.group];
       mbar_wait(&tempty[acc], acc_phase[acc] ^ 1u);
       tc_fence_after();
       const uint32_t d_tmem = tmem + uint32_t(acc * BN);
       for (int kc = 0; kc < p.kchunks; ++kc) {
+        // producer group of this stage (alternating tiles, or alternating
+        // stages when the tile has several)
+        const int g = kq_mma ? (qm++ & 1) : (jj & 1);
         const int s = g + 2 * sg[g];
         mbar_wait(&full[s], phase[g]);
         tc_fence_after();
