@@ -45,6 +45,8 @@ constexpr int kLoadWarp = 17;
 constexpr uint32_t kStgBytes = kBM * kBK * 4;   // one fp32 staging slot (128 rows x 32 k)
 constexpr uint32_t kPlaneA = kBM * kBK * 2;  // bytes per A plane
 constexpr int kXPitch = 20;                   // transpose buffer pitch (floats, 16B rows)
+constexpr int kXPitchW = 36;                  // 32-column transpose pitch (wide tiles)
+constexpr uint32_t kWarpSlot = 5120;          // per-epilogue-warp smem slot (>= 32*36*4, 1 KB multiple)
 
 enum AMode { A_PLAIN = 0, A_GATHER = 1, A_PATCH = 2 };
 
@@ -73,6 +75,7 @@ struct TcParams {
   int rb;      // 1: every weight tile resident in shared memory for the whole kernel
   uint32_t rb_bytes[2];   // resident bytes per expert (packed planes, [n_tile][kc][plane])
   int dbg;     // debug role isolation (0 in production): 1 no A loads, 2 no C stores, 4 no MMAs
+  int tma_c;   // 1: C rows are the tile rows (no scatter / residual / position): TMA-store epilogue
 };
 
 // TMEM accumulators: four buffers when they fit (BN <= 128), so the MMA can run
@@ -148,17 +151,21 @@ __device__ __forceinline__ float gelu_fast(float x) {
 }
 
 __host__ __device__ inline size_t tc_fixed_smem() {
-  return size_t(8) * 32 * kXPitch * sizeof(float)  // transpose buffers
+  return size_t(8) * kWarpSlot + 1024             // epilogue slots (+ 1 KB alignment)
          + 2 * 128 * sizeof(int64_t)                // per-group row tables
          + (2 * 8 + 4 + 2 * 8) * 8 + 16;            // barriers (+ staging) + TMEM slot
 }
 
 template <int BN, int AM>
-__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
+                                                              const __grid_constant__ CUtensorMap tmC) {
   // direct epilogue (thread = row, no shared-memory transpose) for wide tiles
   // (measured: removes the transpose cost but its per-row 16-byte stores halve
   // DRAM write efficiency — 391 vs 283 us on K3 — so the transposed path stays)
   constexpr bool DIRECT = false;
+  // (32-column transposes measured slower on the scattered MoE outputs)
+  constexpr bool WIDE = false;
+  constexpr bool TMA_OK = (BN % 32) == 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // the swizzle pattern keys on absolute address bits: align the carve-out to 1 KB
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -174,8 +181,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
   uint8_t* resb = smem + size_t(S) * stage_bytes;                            // resident B
   const uint32_t rb_total = p.rb ? ((p.rb_bytes[0] + p.rb_bytes[1] + 1023u) & ~1023u) : 0u;
   uint8_t* stg = resb + rb_total;                                            // [NST][128][32] f32
-  float* xbuf = reinterpret_cast<float*>(stg + size_t(NST) * kStgBytes);     // [8][32][kXPitch]
-  int64_t* orow_s = reinterpret_cast<int64_t*>(xbuf + 8 * 32 * kXPitch);    // [2][128]
+  // per-epilogue-warp slot (kWarpSlot bytes, 1 KB aligned): the warp's
+  // transpose buffer [32][kXPitch(W)] OR its 4 KB TMA-store box (128-byte
+  // swizzle needs the 1 KB alignment); a warp only ever touches its own slot
+  uint8_t* slots = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(stg + size_t(NST) * kStgBytes) + 1023) & ~uintptr_t(1023));
+  float* xbuf = reinterpret_cast<float*>(slots);
+  int64_t* orow_s = reinterpret_cast<int64_t*>(slots + 8 * kWarpSlot);    // [2][128]
+  uint8_t* tma_box = slots;
   uint64_t* bars = reinterpret_cast<uint64_t*>(orow_s + 256);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
@@ -317,6 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
+          if (p.dbg & 32) break;   // debug: no conversion / stage stores
           if (AM == A_PATCH && rowp[i] != nullptr && k < p.K) {
             v[i].x -= p.sub; v[i].y -= p.sub; v[i].z -= p.sub; v[i].w -= p.sub;
           }
@@ -454,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
   } else {
     // ===== epilogue group g (warps 4g..4g+3): warp reads TMEM lanes 32*(warp%4) =====
     const int g = warp >> 2, quad = warp & 3;
-    float* xb = xbuf + warp * 32 * kXPitch;     // [32 rows][kXPitch]
+    float* xb = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(xbuf) + warp * kWarpSlot);
     int64_t* orow_t = orow_s + g * 128;
     uint32_t acc_phase[NACC / 2];   // this group owns accumulators g, g + 2, ...
 #pragma unroll
@@ -510,7 +524,54 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
       asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
       const uint32_t t_base = tmem + (uint32_t(quad * 32) << 16) + uint32_t(acc * BN);
       const int64_t n_base = int64_t(ti.n_tile) * BN;
-      if (DIRECT) {
+      // a TMA box writes whole 32-row slabs: only tiles that end at a 128-row
+      // boundary or at M (not the partial tile before an expert boundary)
+      const bool tma_tile = TMA_OK && p.tma_c && !(p.dbg & 16) &&
+                            (ti.r1 - ti.r0 == kBM || ti.r1 == p.M);
+      if (TMA_OK && p.tma_c && !tma_tile) {   // the slot may still feed a TMA store
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+      }
+      if (p.dbg & 16) {
+        // debug: epilogue reduced to the accumulator handshake
+      } else if (tma_tile) {
+        // TMA-store epilogue: 32 accumulator columns per TMEM load, written by
+        // the thread (= row) into a 32 x 32 fp32 box in shared memory with the
+        // 128-byte swizzle (16-byte chunk c of row r at c ^ (r & 7): the eight
+        // lanes of a bank group hit distinct banks), then one elected lane
+        // stores the box with cp.async.bulk.tensor (full-line writes, rows past
+        // M clipped by the tensor map).
+        uint8_t* box = tma_box + warp * kWarpSlot;
+        const int row0 = int(ti.r0) + quad * 32;
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += 32) {
+          uint32_t raw[32];
+          tmem_ld32_nowait(t_base + uint32_t(cb), raw);
+          tmem_ld_wait();
+          if (cb + 32 >= BN) {   // accumulator fully in registers: hand it back
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+          }
+          if (lane == 0) bulk_wait_read0();   // the box's previous store has read it
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            float4 o = make_float4(__uint_as_float(raw[4 * c]), __uint_as_float(raw[4 * c + 1]),
+                                   __uint_as_float(raw[4 * c + 2]), __uint_as_float(raw[4 * c + 3]));
+            if (p.act == 1) {
+              o.x = gelu_fast(o.x); o.y = gelu_fast(o.y); o.z = gelu_fast(o.z); o.w = gelu_fast(o.w);
+            }
+            if (p.gate) { o.x *= gt; o.y *= gt; o.z *= gt; o.w *= gt; }
+            *reinterpret_cast<float4*>(box + lane * 128 + ((c ^ (lane & 7)) * 16)) = o;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && !(p.dbg & 2)) {
+            tma_store_2d(&tmC, box, int(n_base) + cb, row0);
+            bulk_commit();
+          }
+        }
+      } else if (DIRECT && false) {
         // thread = output row: 16 columns per TMEM load (issued one chunk
         // ahead), then four 16-byte stores of the row's contiguous 64-byte
         // segment (no shared-memory transpose)
@@ -559,6 +620,61 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
               crow[cb + q] = e;
             }
           }
+        }
+      } else if (WIDE) {
+        // 32 columns per TMEM load; the warp's 32 x 32 block is transposed in
+        // shared memory and written as four full 128-byte row segments per
+        // store instruction (8 lanes per row)
+        const int rq = lane >> 3, c4 = (lane & 7) * 4;
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += 32) {
+          uint32_t raw[32];
+          tmem_ld32_nowait(t_base + uint32_t(cb), raw);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 32; q += 4) {
+            float4 o = make_float4(__uint_as_float(raw[q]), __uint_as_float(raw[q + 1]),
+                                   __uint_as_float(raw[q + 2]), __uint_as_float(raw[q + 3]));
+            if (p.act == 1) {
+              o.x = gelu_fast(o.x); o.y = gelu_fast(o.y); o.z = gelu_fast(o.z); o.w = gelu_fast(o.w);
+            }
+            if (p.gate) { o.x *= gt; o.y *= gt; o.z *= gt; o.w *= gt; }
+            *reinterpret_cast<float4*>(xb + lane * kXPitchW + q) = o;
+          }
+          __syncwarp();
+          const int64_t n = n_base + cb + c4;
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int ri = it * 4 + rq;
+            const int64_t meta = orow_t[quad * 32 + ri];
+            if (meta < 0) continue;
+            const int64_t orow_i = p.pos ? (meta & ((int64_t(1) << 40) - 1)) : meta;
+            const int64_t pos_i = p.pos ? (meta >> 40) : 0;
+            float4 o = *reinterpret_cast<const float4*>(xb + ri * kXPitchW + c4);
+            if (vec4 && n + 3 < p.N) {
+              if (p.pos) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(p.pos + pos_i * p.N + n));
+                o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+              }
+              if (p.residual) {
+                const float4 q =
+                    __ldg(reinterpret_cast<const float4*>(p.residual + orow_i * p.N + n));
+                o = make_float4(q.x + o.x, q.y + o.y, q.z + o.z, q.w + o.w);
+              }
+              if (!(p.dbg & 2)) *reinterpret_cast<float4*>(p.C + orow_i * p.N + n) = o;
+            } else {
+              const float ov[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                if (n + q >= p.N) break;
+                float e = ov[q];
+                if (p.pos) e = e + __ldg(p.pos + pos_i * p.N + n + q);
+                if (p.residual) e = __ldg(p.residual + orow_i * p.N + n + q) + e;
+                p.C[orow_i * p.N + n + q] = e;
+              }
+            }
+          }
+          __syncwarp();
         }
       } else
 #pragma unroll 1
@@ -613,8 +729,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
         }
         __syncwarp();
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if (!tma_tile) {
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+      }
       tA = tB;
       tiA = tiB;
       jjA = jjB;
@@ -626,6 +744,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p) {
       crB = crC;
     }
   }
+  if (warp < 8 && lane == 0) bulk_wait0();   // TMA stores of this warp retired
   tc_fence_before();
   __syncthreads();
   if (warp == kMmaWarp) tmem_dealloc<TCOLS>(tmem);

@@ -78,6 +78,8 @@ static int num_sms() {
 }
 
 static int g_tc_dbg = 0;
+static int g_tc_tma = 1;   // TMA-store epilogue for plain outputs
+extern "C" void sa_debug_tc_tma(int on) { g_tc_tma = on; }
 extern "C" void sa_debug_tc_mode(int m) { g_tc_dbg = m; }
 static int g_tc_resident = 1;   // weights resident in shared memory when they fit
 extern "C" void sa_debug_tc_resident(int on) { g_tc_resident = on; }
@@ -131,13 +133,30 @@ static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cu
     return SA_ERR_SHAPE;
   }
   const int grid = int(tiles < num_sms() ? tiles : num_sms());
+  // TMA-store epilogue when C's rows are exactly the tile rows
+  CUtensorMap tmC;
+  memset(&tmC, 0, sizeof(tmC));
+  p.tma_c = 0;
+  if (g_tc_tma && bn % 32 == 0 && p.c_rows == nullptr && p.residual == nullptr &&
+      p.pos == nullptr && (p.img_tokens == 0 || p.extra == 0) && (p.N % 4) == 0 &&
+      (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && p.M < (int64_t(1) << 31)) {
+    const cuuint64_t dims[2] = {cuuint64_t(p.N), cuuint64_t(p.M)};
+    const cuuint64_t strides[1] = {cuuint64_t(p.N) * 4};
+    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = cuTensorMapEncodeTiled(
+        &tmC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, p.C, dims, strides, box, estr,
+        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS) p.tma_c = 1;
+  }
 #define SA_TC_CASE(BNV)                                                                          \
   case BNV: {                                                                                    \
     auto kfn = amode == A_PLAIN    ? tc_gemm_kernel<BNV, A_PLAIN>                               \
                : amode == A_GATHER ? tc_gemm_kernel<BNV, A_GATHER>                              \
                                    : tc_gemm_kernel<BNV, A_PATCH>;                              \
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));          \
-    kfn<<<grid, kThreads, smem, s>>>(p);                                                         \
+    kfn<<<grid, kThreads, smem, s>>>(p, tmC);                                                    \
   } break;
   switch (bn) {
     SA_TC_CASE(32)
