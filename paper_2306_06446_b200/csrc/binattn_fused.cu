@@ -54,6 +54,7 @@ struct Params {
   float* out;
   int n, d, heads, side, rows_total, band_rows;
   float eps;
+  int ld;     // global row stride of V / out in floats (= model dim); head = blockIdx.z
 };
 
 struct Smem {
@@ -140,6 +141,8 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
   const int rank = int(cluster.block_rank());
   const int CL = int(cluster.num_blocks());
   const int b = blockIdx.y;
+  const int hz = blockIdx.z, H = p.heads;    // this CTA's head of the image
+  const int ld = p.ld;
   const int n = p.n, BR = p.band_rows;
   const Smem L = smem_layout(D, HEADS, SIDE, BR);
   uint8_t* Vb = smem + L.v;
@@ -158,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
   const int r1 = min(p.rows_total, r0 + BR);
   const int t_lo = min(n, r0 * SIDE), t_hi = min(n, r1 * SIDE);
   const int nt = t_hi - t_lo;
-  const float* vb = p.v + size_t(b) * n * D;
+  const float* vb = p.v + size_t(b) * n * ld + hz * DK;
 
   // ---- 1. band of V (+ halo rows) → shared memory ----------------------------
   // smem row R holds grid row r0 - 1 + R; cells past n and rows outside the
@@ -174,16 +177,32 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
       const int R = i < BR ? i + 1 : (i == BR ? 0 : BR + 1);
       const int rr = r0 - 1 + R;
       const int ntok = (rr >= 0 && rr < p.rows_total) ? max(0, min(SIDE, n - rr * SIDE)) : 0;
+      // single-head images: a grid row is one contiguous run (bulk copy);
+      // head slices of a wider model are strided and come in by cp.async below
+      const uint32_t bytes = ld == D ? uint32_t(ntok) * TOKB : 0u;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar + R)),
-                   "r"(uint32_t(ntok) * TOKB)
+                   "r"(bytes)
                    : "memory");
-      if (ntok == 0) continue;
+      if (bytes == 0) continue;
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
               su32(Vb + R * ROWB)),
-          "l"(vb + size_t(rr) * SIDE * D), "r"(uint32_t(ntok) * TOKB), "r"(su32(bar + R))
+          "l"(vb + size_t(rr) * SIDE * D), "r"(bytes), "r"(su32(bar + R))
           : "memory");
     }
+  }
+  if (ld != D) {   // strided head slice: 16-byte cp.async per (token, chunk)
+    const int tok_lo = max(0, (r0 - 1) * SIDE);
+    const int tok_hi = min(n, (r0 + BR + 1) * SIDE);
+    const int smem_tok0 = (r0 - 1) * SIDE;          // token of smem row 0, column 0
+    for (int i = tid; i < (tok_hi - tok_lo) * (D / 4); i += kThreads) {
+      const int t = tok_lo + i / (D / 4), c4 = i % (D / 4);
+      const uint32_t dst = su32(Vb) + uint32_t(t - smem_tok0) * TOKB + c4 * 16;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                   "l"(vb + size_t(t) * ld + c4 * 4)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
   for (int R = 0; R < BR + 2; ++R) {   // zero the cells no copy fills
     const int rr = r0 - 1 + R;
@@ -194,13 +213,14 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
   }
   for (int i = tid; i < HEADS * nt; i += kThreads) {   // codes of the band, [head][token]
     const int h = i / nt, t = i - h * nt;
-    const size_t g = (size_t(b) * HEADS + h) * n + t_lo + t;
+    const size_t g = (size_t(b) * H + hz + h) * n + t_lo + t;
     cqs[h * nt + t] = __ldg(p.cq + g);
     cks[h * nt + t] = __ldg(p.ck + g);
   }
   for (int i = tid; i < 256 * 8; i += kThreads)          // byte → 8 masks
     mt[i] = ((i >> 3) >> (i & 7)) & 1 ? 1.0f : 0.0f;
-  __syncthreads();  // barrier init, codes, masks visible
+  if (ld != D) asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();  // barrier init, codes, masks (and strided V) visible
   auto wait_row = [&](int R) {
     asm volatile(
         "{\n\t.reg .pred q;\n\tW_%=:\n\t"
@@ -329,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
   cluster.sync();
 #pragma unroll 1
   for (int h = 0; h < HEADS; ++h) {
-    const float g = __ldg(p.gk + b * HEADS + h);
+    const float g = __ldg(p.gk + b * H + hz + h);
     const int grp = tid / DK, c = tid % DK;       // tables: thread = (nibble group, column)
     float x[kMaxCluster][4];
 #pragma unroll
@@ -394,19 +414,19 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
   if (slot >= SLOTS) return;
   const int h = cgi / (DK / 4), cgl = cgi % (DK / 4);
   const int ch = cgi * 4;
-  const float gq = __ldg(p.gq + b * HEADS + h), gk = __ldg(p.gk + b * HEADS + h);
+  const float gq = __ldg(p.gq + b * H + hz + h), gk = __ldg(p.gk + b * H + hz + h);
   const float gg = gq * gk;
   ulonglong2 tapu[9];
 #pragma unroll
   for (int q = 0; q < 9; ++q)
-    tapu[q] = p.dw ? __ldg(reinterpret_cast<const ulonglong2*>(p.dw + q * D + ch))
+    tapu[q] = p.dw ? __ldg(reinterpret_cast<const ulonglong2*>(p.dw + q * ld + hz * DK + ch))
                    : make_ulonglong2(0ull, 0ull);
   const bool has_dw = p.dw != nullptr;
   const uint8_t* T = reinterpret_cast<const uint8_t*>(tab + size_t(h) * (DK / 4) * 16 * DK + cgl * 4);
   const float* Tb = tcb + h * 1024;
   const uint32_t* cqh = cqs + h * nt;
   const int units = (r1 - r0) * SEGS;
-  float* ob = p.out + size_t(b) * n * D + ch;
+  float* ob = p.out + size_t(b) * n * ld + hz * DK + ch;
   const ulonglong2 z2 = make_ulonglong2(0ull, 0ull);
   for (int u = slot; u < units; u += SLOTS) {
     const int rl = u / SEGS, sg = u - rl * SEGS;
@@ -475,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
         o.z += y23.x;
         o.w += y23.y;
       }
-      *reinterpret_cast<float4*>(ob + size_t(t) * D) = o;
+      *reinterpret_cast<float4*>(ob + size_t(t) * ld) = o;
     }
   }
 }
@@ -493,34 +513,33 @@ int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
   int side = 0;
   while (int64_t(side) * side < n) ++side;
   const int rows_total = int((n + side - 1) / side);
-  // bands of ~400 (token, head) pairs amortise the per-CTA table work
+  // one CTA per (band, image, head): bands of ~400 tokens amortise the table
+  // work; a head slice of a wider model is a strided view (row stride d)
   // (16-CTA non-portable clusters measured 1.8x slower: GPC packing)
-  int cl = int((n * heads + 399) / 400);
+  int cl = int((n + 399) / 400);
   cl = cl < 1 ? 1 : (cl > kMaxCluster ? kMaxCluster : cl);
   cl = cl > rows_total ? rows_total : cl;
   const int br = (rows_total + cl - 1) / cl;
   cl = (rows_total + br - 1) / br;
-  // every lane group of 8 (one head's channel groups) must sit inside a warp
-  if ((d / 4) % 8 != 0 || d / 4 > kThreads) return SA_ERR_VALUE;
-  const Smem L = smem_layout(int(d), int(heads), side, br);
+  const Smem L = smem_layout(DK, 1, side, br);
   if (L.total > 220 * 1024) return SA_ERR_VALUE;
   if (br * side > 32 * 63) return SA_ERR_VALUE;   // bit-sliced counters hold 63 tokens/lane
-  Params p{cq, ck, gq, gk, v, dw, out, int(n), int(d), int(heads), side, rows_total, br, eps};
+  Params p{cq, ck, gq, gk, v, dw, out, int(n), DK, int(heads), side, rows_total, br, eps, int(d)};
   void (*kern)(Params) = nullptr;
-  if (d == 32 && side == 56) kern = binattn_fused_kernel<32, 56>;
-  else if (d == 64 && side == 28) kern = binattn_fused_kernel<64, 28>;
-  else if (d == 160 && side == 14) kern = binattn_fused_kernel<160, 14>;
-  else if (d == 32 && side == 14) kern = binattn_fused_kernel<32, 14>;
-  else if (d == 64 && side == 14) kern = binattn_fused_kernel<64, 14>;
-  else if (d == 96 && side == 18) kern = binattn_fused_kernel<96, 18>;
-  else if (d == 32 && side == 3) kern = binattn_fused_kernel<32, 3>;
-  else if (d == 256 && side == 7) kern = binattn_fused_kernel<256, 7>;
-  else if (d == 64 && side == 15) kern = binattn_fused_kernel<64, 15>;
-  if (kern == nullptr) return SA_ERR_VALUE;
+  switch (side) {
+    case 56: kern = binattn_fused_kernel<DK, 56>; break;
+    case 28: kern = binattn_fused_kernel<DK, 28>; break;
+    case 14: kern = binattn_fused_kernel<DK, 14>; break;
+    case 7: kern = binattn_fused_kernel<DK, 7>; break;
+    case 15: kern = binattn_fused_kernel<DK, 15>; break;
+    case 18: kern = binattn_fused_kernel<DK, 18>; break;
+    case 3: kern = binattn_fused_kernel<DK, 3>; break;
+    default: return SA_ERR_VALUE;
+  }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total));
   if (cl > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(cl), unsigned(B), 1);
+  cfg.gridDim = dim3(unsigned(cl), unsigned(B), unsigned(heads));
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = L.total;
   cfg.stream = s;
