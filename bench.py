@@ -193,6 +193,11 @@ def op_bytes(name, args):
     if name == "sa_softmax_attn":
         B, n, d = args[4], args[5], args[6]
         return 4 * B * n * d * A
+    if name == "sa_ln_qkv_hash":
+        # x in, v out, q/k codes, three (expert, gate) dispatch arrays
+        B, n, d = args[14], args[15], args[16]
+        M = B * n
+        return 2 * M * d * A + 2 * M * d // 8 + 3 * M * 8
     if name == "sa_pool":
         B, n, d = args[2], args[3], args[4]
         return B * n * d * A

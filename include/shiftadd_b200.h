@@ -139,6 +139,13 @@ int sa_ln_route(const float* x, const float* gain, const float* bias, float* y, 
                 const float* wg2, float tie_thresh, int32_t* expert_of, float* gate,
                 int32_t* counts, int32_t* perm, void* ws, size_t ws_bytes, void* stream);
 
+/* the stable partition only (moe.dispatch's index_of, moe.py:91) from winners
+ * already on the device: counts[2], perm = [expert-0 ascending | expert-1
+ * ascending]. Used to materialise dispatch plans lazily. */
+size_t sa_moe_partition_workspace(int64_t M);
+int sa_moe_partition(const int32_t* expert_of, int64_t M, int32_t* counts, int32_t* perm,
+                     void* ws, size_t ws_bytes, void* stream);
+
 /* dispatch only (moe.dispatch, moe.py:87-92) from precomputed logits (M, 2) */
 int sa_moe_dispatch(const float* logits, int64_t M, float tie_thresh, int32_t* expert_of,
                     float* gate, int32_t* counts, int32_t* perm, void* ws, size_t ws_bytes,
@@ -204,6 +211,24 @@ int sa_tc_moe_mlp_fused(const float* x, const int32_t* perm, const int32_t* coun
 int sa_tc_mlp_fused(const float* x, const void* w1pack, int w1_kind, const void* w2pack,
                     int w2_kind, float* y, int64_t M, int64_t d, int64_t hidden,
                     const float* residual, void* stream);
+/* Fused attention input for d = 32 / 64 (head dim 32), n >= 32:
+ * LayerNorm.forward (model.py:174-178) → the q, k, v routers (moe.py:81-92) →
+ * MoeModule.forward of the three (Linear, ShiftLinearLayer) projections
+ * (model.py:250-274, 499-502; both experts computed, the routed one kept) →
+ * quantize.binarize per (image, head) of q and k (quantize.py:123-140 via
+ * model.py:355-358). Writes expert_of / gate [3][M] (q, k, v), codes_q / codes_k
+ * [B][d/32][n], gamma_q / gamma_k [B*d/32] and v (M, d). Weights packed with
+ * sa_weight_pack (bn = d): dense (3 planes) and shift (1 plane) per projection. */
+int sa_ln_qkv_hash_ok(int64_t d, int64_t n);
+size_t sa_ln_qkv_hash_workspace(int64_t B, int64_t n, int64_t d);
+int sa_ln_qkv_hash(const float* x, const float* gain, const float* bias, float eps,
+                   const float* wg_q, const float* wg_k, const float* wg_v, const void* wq_dense,
+                   const void* wq_shift, const void* wk_dense, const void* wk_shift,
+                   const void* wv_dense, const void* wv_shift, float tie_thresh, int64_t B,
+                   int64_t n, int64_t d, int32_t* expert_of, float* gate, uint32_t* codes_q,
+                   uint32_t* codes_k, float* gamma_q, float* gamma_k, float* v, void* ws,
+                   size_t ws_bytes, void* stream);
+
 /* patchify (model.py:557-563) + patch-embed Linear on the tensor cores */
 int sa_tc_patch_embed(const float* grid, int64_t B, int64_t H, int64_t W, int64_t C,
                       int64_t patch, float sub, const void* wpack, int bn, int64_t d,

@@ -433,3 +433,42 @@ extern "C" int sa_moe_dispatch(const float* logits, int64_t M, float tie_thresh,
   SA_LAUNCH_CHECK("sa_moe_dispatch");
   return SA_OK;
 }
+
+// per-block expert-1 counts from winners already on the device
+__global__ void __launch_bounds__(kRouteTok) count_kernel(const int32_t* __restrict__ expert_of,
+                                                         int64_t M, int32_t* __restrict__ block_cnt1) {
+  __shared__ int wcnt[kRouteTok / 32];
+  const int64_t t = int64_t(blockIdx.x) * kRouteTok + threadIdx.x;
+  const int e = t < M ? expert_of[t] : 0;
+  const unsigned b = __ballot_sync(0xffffffffu, e == 1);
+  if ((threadIdx.x & 31) == 0) wcnt[threadIdx.x >> 5] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int w = 0; w < kRouteTok / 32; ++w) c += wcnt[w];
+    block_cnt1[blockIdx.x] = c;
+  }
+}
+
+extern "C" size_t sa_moe_partition_workspace(int64_t M) { return sa_moe_route_workspace(M); }
+
+extern "C" int sa_moe_partition(const int32_t* expert_of, int64_t M, int32_t* counts,
+                                int32_t* perm, void* ws, size_t ws_bytes, void* stream) {
+  SA_REQUIRE(M >= 0 && M < (int64_t(1) << 31), SA_ERR_SHAPE, "sa_moe_partition: bad token count");
+  SA_REQUIRE(ws_bytes >= sa_moe_partition_workspace(M), SA_ERR_VALUE,
+             "sa_moe_partition: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  if (M == 0) {
+    cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), s);
+    return SA_OK;
+  }
+  const int nb = int(cdiv(M, kRouteTok));
+  int32_t* block_cnt1 = static_cast<int32_t*>(ws);
+  int32_t* block_off1 = block_cnt1 + nb;
+  count_kernel<<<nb, kRouteTok, 0, s>>>(expert_of, M, block_cnt1);
+  route_scan_kernel<<<1, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
+  partition_kernel<<<nb, kRouteTok, 0, s>>>(expert_of, block_off1, counts, M, perm);
+  count_launch(3);
+  SA_LAUNCH_CHECK("sa_moe_partition");
+  return SA_OK;
+}

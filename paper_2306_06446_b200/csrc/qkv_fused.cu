@@ -1,0 +1,472 @@
+// Fused attention input: LayerNorm + the three q/k/v routers +
+// both experts of each q/k/v MoE projection on the tensor cores + the sign-hash
+// epilogue, for model dims 32 and 64 (head dim 32).
+//
+// Reference composition (Block.forward → AttentionLayer.forward,
+// model.py:454-459, 340-358): y = LN1(x) (tensor.py:114-128); for r in q,k,v:
+// route(y, W_g^r) (moe.py:81-92), proj_r(y) = gate · expert_e(y) with experts
+// Linear / ShiftLinearLayer (model.py:250-274, 499-502); q, k are then binarised
+// per (image, head) (quantize.py:123-140 via model.py:355-358).
+//
+// One persistent CTA per SM walks 128-token tiles of the flat (B·n, d) input:
+//   warps 4-7  producers (thread = token row): the x row, LayerNorm in fp32
+//              (the exact arithmetic of sa_ln_route), three fp64 router dots →
+//              winner / gate (numpy-exp tie rule), written to the dispatch
+//              arrays and to a shared route table; the normalised row split
+//              into hi/mid/lo bf16 planes and stored to TMEM (A operand);
+//   warp 8     MMA issuer: per projection the dense expert (6 plane products)
+//              and the shift expert (3, exact bf16 weights) into TMEM
+//              accumulators — both experts for every token, so no
+//              permutation / gather / scatter exists (the selection is a per-row
+//              choice in the epilogue); all weights resident in shared memory;
+//   warps 0-3  epilogue (thread = row): picks its expert's accumulator, × gate;
+//              q and k → 32-bit sign codes (!(y < 0)) and fp64 |y| partials per
+//              32-row segment (→ γ by sa_gamma_finalize), v → a 32 x 32 box in
+//              128-byte-swizzled shared memory stored by TMA.
+// Products per row are computed by the same split-precision MMA chains as the
+// unfused path (sa_tc_moe_linear), so the projections agree bit for bit.
+#include "tc_gemm_kernel.cuh"
+
+namespace sa {
+namespace qkv {
+
+using namespace tc;
+
+constexpr int kEpi = 0, kProd = 4, kMma = 8;
+constexpr int kThreads = 288;   // 9 warps
+constexpr uint32_t kPlaneCols = 16;
+constexpr int kRT = 4;           // route-table ring slots
+
+template <int D>
+struct Cfg {
+  static constexpr int KC1 = D / 32;                // K stages of 32
+  static constexpr int H = D / 32;                  // heads (dk = 32)
+  static constexpr int NA = D == 32 ? 2 : 1;        // A buffers in TMEM
+  static constexpr int NACC = D == 32 ? 2 : 1;      // accumulator buffers
+  static constexpr uint32_t A_COLS = KC1 * 3 * kPlaneCols;
+  static constexpr uint32_t T_A = 0;
+  static constexpr uint32_t T_ACC = 128;            // 6 parts of D columns per buffer
+  static constexpr uint32_t ACC_COLS = 6 * D;
+  static_assert(T_A + NA * A_COLS <= T_ACC, "A region");
+  static_assert(T_ACC + NACC * ACC_COLS <= 512, "TMEM budget");
+  // resident weights: per projection dense (3 planes) then shift (1 plane)
+  static constexpr uint32_t WD = uint32_t(D) * D * 2 * 3;
+  static constexpr uint32_t WS = uint32_t(D) * D * 2;
+  static constexpr uint32_t W_BYTES = 3 * (WD + WS);
+};
+
+struct Params {
+  const float* x;
+  const float* gain;
+  const float* bias;
+  float eps;
+  const float* wg[3];
+  const uint16_t* wd[3];      // dense packed planes (bn = d)
+  const uint16_t* wsh[3];     // shift packed plane (bn = d)
+  float tie;
+  int64_t M;
+  int n;
+  int32_t* expert_of;         // [3][M]
+  float* gate;                // [3][M]
+  uint32_t* codes[2];         // q, k: [B][H][n]
+  double* gpart;              // [2][M/32 segments][H][2]
+  int nseg;
+};
+
+// smem layout (bytes)
+template <int D>
+struct Smem {
+  static constexpr uint32_t W = 0;
+  static constexpr uint32_t WG = Cfg<D>::W_BYTES;                  // [3][2D] double
+  static constexpr uint32_t RT_E = WG + 3 * 2 * D * 8;             // [kRT][3][128] int
+  static constexpr uint32_t RT_G = RT_E + kRT * 3 * 128 * 4;       // [kRT][3][128] float
+  static constexpr uint32_t BOX = (RT_G + kRT * 3 * 128 * 4 + 1023) & ~1023u;   // [4 warps][H][4 KB]
+  static constexpr uint32_t BAR = BOX + 4 * Cfg<D>::H * 4096;
+  static constexpr uint32_t NBAR = 2 * Cfg<D>::NA + 2 * Cfg<D>::NACC + 2 * kRT + 1;
+  static constexpr uint32_t TOTAL = BAR + NBAR * 8 + 16 + 1024;    // + alignment slack
+};
+
+__device__ __forceinline__ int decide2(float l0, float l1, float tie_thresh, float& gate) {
+  // same rule as moe.cu decide() (ref moe.py:81-92)
+  const float m = fmaxf(l0, l1);
+  const float sh0 = l0 - m, sh1 = l1 - m;
+  const int e = (l1 > l0 && sh0 < -tie_thresh) ? 1 : 0;
+  const float e0 = (sh0 >= -tie_thresh) ? 1.f : expf(sh0);
+  const float e1 = (sh1 >= -tie_thresh) ? 1.f : expf(sh1);
+  gate = (e ? e1 : e0) / (e0 + e1);
+  return e;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid_constant__ CUtensorMap tmV) {
+  using C = Cfg<D>;
+  using S = Smem<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  double* swg = reinterpret_cast<double*>(smem + S::WG);
+  int* rt_e = reinterpret_cast<int*>(smem + S::RT_E);
+  float* rt_g = reinterpret_cast<float*>(smem + S::RT_G);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::BAR);
+  uint64_t* a_full = bar;
+  uint64_t* a_empty = a_full + C::NA;
+  uint64_t* acc_full = a_empty + C::NA;
+  uint64_t* acc_empty = acc_full + C::NACC;
+  uint64_t* rt_full = acc_empty + C::NACC;
+  uint64_t* rt_empty = rt_full + kRT;
+  uint64_t* wbar = rt_empty + kRT;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wbar + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == kMma) tmem_alloc<512>(tmem_slot);
+  if (tid == 0) {
+    for (int i = 0; i < C::NA; ++i) {
+      mbar_init(&a_full[i], 4);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < C::NACC; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 128);
+    }
+    for (int i = 0; i < kRT; ++i) {
+      mbar_init(&rt_full[i], 4);
+      mbar_init(&rt_empty[i], 4);
+    }
+    mbar_init(wbar, 1);
+    fence_barrier_init();
+    // every weight tile, once: per projection dense (3 planes) then shift
+    mbar_expect_tx(wbar, C::W_BYTES);
+    for (int r = 0; r < 3; ++r) {
+      bulk_g2s(smem + S::W + r * (C::WD + C::WS), p.wd[r], C::WD, wbar);
+      bulk_g2s(smem + S::W + r * (C::WD + C::WS) + C::WD, p.wsh[r], C::WS, wbar);
+    }
+  }
+  for (int i = tid; i < 3 * 2 * D; i += kThreads) swg[i] = double(p.wg[i / (2 * D)][i % (2 * D)]);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int ntile = int((p.M + 127) / 128);
+
+  if (warp >= kProd && warp < kProd + 4) {
+    // ---------------- producers: LN + routers + A planes ----------------
+    const int rl = (warp - kProd) * 32 + lane;
+    const uint32_t lane_base = uint32_t((warp - kProd) * 32) << 16;
+    int j = 0;
+    for (int m = blockIdx.x; m < ntile; m += gridDim.x, ++j) {
+      const int64_t row = int64_t(m) * 128 + rl;
+      const bool ok = row < p.M;
+      float v[D];
+      if (ok) {
+        const float4* xr = reinterpret_cast<const float4*>(p.x + row * D);
+#pragma unroll
+        for (int i = 0; i < D / 4; ++i) {
+          const float4 q = __ldg(xr + i);
+          v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
+        }
+        // LayerNorm: the exact operation sequence of ln_route_kernel (moe.cu)
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < D / 4; ++i) s += (v[4 * i] + v[4 * i + 1]) + (v[4 * i + 2] + v[4 * i + 3]);
+        const float mean = s / float(D);
+        float q2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          v[i] -= mean;
+          q2 += v[i] * v[i];
+        }
+        const float inv = 1.0f / sqrtf(q2 / float(D) + p.eps);
+#pragma unroll
+        for (int i = 0; i < D / 4; ++i) {
+          const float4 g = __ldg(reinterpret_cast<const float4*>(p.gain) + i);
+          const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias) + i);
+          v[4 * i] = v[4 * i] * inv * g.x + b.x;
+          v[4 * i + 1] = v[4 * i + 1] * inv * g.y + b.y;
+          v[4 * i + 2] = v[4 * i + 2] * inv * g.z + b.z;
+          v[4 * i + 3] = v[4 * i + 3] * inv * g.w + b.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < D; ++i) v[i] = 0.f;
+      }
+      // routers (fp64 dots in channel order, as ln_route_kernel)
+      const int rs = j % kRT;
+      mbar_wait(&rt_empty[rs], (uint32_t(j / kRT) & 1u) ^ 1u);
+#pragma unroll 1
+      for (int r = 0; r < 3; ++r) {
+        double s0 = 0.0, s1 = 0.0;
+        const double* w = swg + r * 2 * D;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          s0 = fma(double(v[c]), w[2 * c], s0);
+          s1 = fma(double(v[c]), w[2 * c + 1], s1);
+        }
+        float g = 1.f;
+        int e = 0;
+        if (ok) {
+          e = decide2(float(s0), float(s1), p.tie, g);
+          p.expert_of[r * p.M + row] = e;
+          p.gate[r * p.M + row] = g;
+        }
+        rt_e[(rs * 3 + r) * 128 + rl] = e;
+        rt_g[(rs * 3 + r) * 128 + rl] = g;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rt_full[rs]);
+      // A planes → TMEM
+      const int ab = j % C::NA;
+      mbar_wait(&a_empty[ab], (uint32_t(j / C::NA) & 1u) ^ 1u);
+      tc_fence_after();
+      const uint32_t a1 = tmem + lane_base + C::T_A + uint32_t(ab) * C::A_COLS;
+#pragma unroll
+      for (int kc = 0; kc < C::KC1; ++kc) {
+        uint32_t hp[16], mp[16], lp[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          const Split3 sp = split3x2(v[kc * 32 + 2 * t], v[kc * 32 + 2 * t + 1]);
+          hp[t] = bf2_bits(sp.h);
+          mp[t] = bf2_bits(sp.m);
+          lp[t] = bf2_bits(sp.l);
+        }
+        tmem_st16(a1 + kc * 3 * kPlaneCols, hp);
+        tmem_st16(a1 + kc * 3 * kPlaneCols + kPlaneCols, mp);
+        tmem_st16(a1 + kc * 3 * kPlaneCols + 2 * kPlaneCols, lp);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_full[ab]);
+    }
+  } else if (warp == kMma) {
+    // ---------------- MMA issuer (whole warp; one elected lane issues) ----------------
+    mbar_wait(wbar, 0);   // resident weights landed
+    constexpr uint32_t idesc = idesc_bf16_m128(D);
+    const uint32_t wbase = smem_u32(smem + S::W);
+    int j = 0;
+    for (int m = blockIdx.x; m < ntile; m += gridDim.x, ++j) {
+      const int ab = j % C::NA, cb = j % C::NACC;
+      mbar_wait(&a_full[ab], uint32_t(j / C::NA) & 1u);
+      mbar_wait(&acc_empty[cb], (uint32_t(j / C::NACC) & 1u) ^ 1u);
+      tc_fence_after();
+      const uint32_t a0 = tmem + C::T_A + uint32_t(ab) * C::A_COLS;
+      const uint32_t acc = tmem + C::T_ACC + uint32_t(cb) * C::ACC_COLS;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const uint32_t wd = wbase + r * (C::WD + C::WS);
+        const uint32_t ws = wd + C::WD;
+#pragma unroll
+        for (int kc = 0; kc < C::KC1; ++kc)
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const uint32_t ad = a0 + kc * 3 * kPlaneCols + ks * 8;
+            const uint32_t accf = (kc | ks) != 0;
+            mma_chain6_ts_w(acc + uint32_t(2 * r) * D, ad,
+                            smem_desc(wd + kc * 3 * (D * 32 * 2) + ks * 256), kPlaneCols,
+                            (D * 32 * 2) >> 4, idesc, accf);
+            mma_chain3_ts_w(acc + uint32_t(2 * r + 1) * D, ad,
+                            smem_desc(ws + kc * (D * 32 * 2) + ks * 256), kPlaneCols, idesc, accf);
+          }
+      }
+      commit_w(&a_empty[ab]);
+      commit_w(&acc_full[cb]);
+    }
+  } else if (warp < kEpi + 4) {
+    // ---------------- epilogue (thread = row) ----------------
+    const int quad = warp - kEpi;
+    const int rl = quad * 32 + lane;
+    const uint32_t lane_base = uint32_t(quad * 32) << 16;
+    uint8_t* box = smem + S::BOX + quad * C::H * 4096;
+    int j = 0;
+    for (int m = blockIdx.x; m < ntile; m += gridDim.x, ++j) {
+      const int64_t row = int64_t(m) * 128 + rl;
+      const bool ok = row < p.M;
+      const int rs = j % kRT, cb = j % C::NACC;
+      mbar_wait(&rt_full[rs], uint32_t(j / kRT) & 1u);
+      int e[3];
+      float g[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        e[r] = rt_e[(rs * 3 + r) * 128 + rl];
+        g[r] = rt_g[(rs * 3 + r) * 128 + rl];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rt_empty[rs]);
+      mbar_wait(&acc_full[cb], uint32_t(j / C::NACC) & 1u);
+      tc_fence_after();
+      const uint32_t acc = tmem + lane_base + C::T_ACC + uint32_t(cb) * C::ACC_COLS;
+      // image / segment bookkeeping of this warp's 32 rows
+      const int64_t wrow0 = int64_t(m) * 128 + quad * 32;
+      const int b = int(row / p.n), t = int(row - int64_t(b) * p.n);
+      const int b0 = int(wrow0 / p.n);
+      const int seg = int(wrow0 >> 5);
+#pragma unroll 1
+      for (int r = 0; r < 3; ++r) {
+#pragma unroll
+        for (int hh = 0; hh < C::H; ++hh) {
+          uint32_t rd[32], rsft[32];
+          tmem_ld32_nowait(acc + uint32_t(2 * r) * D + hh * 32, rd);
+          tmem_ld32_nowait(acc + uint32_t(2 * r + 1) * D + hh * 32, rsft);
+          tmem_ld_wait();
+          float y[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            y[c] = g[r] * __uint_as_float(e[r] ? rsft[c] : rd[c]);
+          if (r < 2) {
+            uint32_t code = 0u;
+            double asum = 0.0;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              code |= (y[c] < 0.f ? 0u : 1u) << c;
+              asum += double(fabsf(y[c]));
+            }
+            if (!ok) asum = 0.0;
+            if (ok) p.codes[r][(int64_t(b) * C::H + hh) * p.n + t] = code;
+            // fp64 |y| partials of this 32-row segment, split by image (the
+            // segment may straddle one image boundary; n >= 32 is required)
+            double s0 = (ok && b == b0) ? asum : 0.0;
+            double s1 = (ok && b != b0) ? asum : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+              s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            }
+            if (lane == 0 && wrow0 < p.M) {
+              double* gp = p.gpart + ((int64_t(r) * p.nseg + seg) * C::H + hh) * 2;
+              gp[0] = s0;
+              gp[1] = s1;
+            }
+          } else {
+            // v: 32 x 32 box (128-byte swizzle) → TMA store
+            uint8_t* bx = box + hh * 4096;
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              *reinterpret_cast<float4*>(bx + lane * 128 + ((c ^ (lane & 7)) * 16)) =
+                  make_float4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmV, bx, hh * 32, int(wrow0));
+              bulk_commit();
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[cb]);
+    }
+    if (lane == 0) bulk_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMma) tmem_dealloc<512>(tmem);
+}
+
+// γ[r][b·H + h] = Σ |y| over image b's rows of head h / (n · 32), summing the
+// 32-row segment partials in segment order (deterministic).
+__global__ void gamma_finalize_qkv(const double* __restrict__ gpart, int nseg, int H, int64_t B,
+                                   int n, float* __restrict__ gq, float* __restrict__ gk) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= 2 * B * H) return;
+  const int r = int(i / (B * H));
+  const int64_t bh = i % (B * H);
+  const int64_t b = bh / H;
+  const int h = int(bh % H);
+  const int64_t lo = b * n, hi = (b + 1) * n;   // rows of image b
+  double s = 0.0;
+  for (int64_t sg = lo >> 5; sg <= (hi - 1) >> 5; ++sg) {
+    const int64_t b0 = (sg * 32) / n;             // image of the segment's first row
+    const double* gp = gpart + ((int64_t(r) * nseg + sg) * H + h) * 2;
+    s += (b0 == b) ? gp[0] : gp[1];
+  }
+  const float gv = float(s / (double(n) * 32.0));
+  (r == 0 ? gq : gk)[bh] = gv;
+}
+
+}  // namespace qkv
+}  // namespace sa
+
+using namespace sa;
+
+extern "C" int sa_ln_qkv_hash_ok(int64_t d, int64_t n) {
+  return (d == 32 || d == 64) && n >= 32;
+}
+
+extern "C" size_t sa_ln_qkv_hash_workspace(int64_t B, int64_t n, int64_t d) {
+  const int64_t M = B * n;
+  const int64_t nseg = (M + 31) / 32;
+  return size_t(2 * nseg * (d / 32) * 2) * sizeof(double) + 256;
+}
+
+extern "C" int sa_ln_qkv_hash(const float* x, const float* gain, const float* bias, float eps,
+                              const float* wg_q, const float* wg_k, const float* wg_v,
+                              const void* wq_dense, const void* wq_shift, const void* wk_dense,
+                              const void* wk_shift, const void* wv_dense, const void* wv_shift,
+                              float tie_thresh, int64_t B, int64_t n, int64_t d,
+                              int32_t* expert_of, float* gate, uint32_t* codes_q,
+                              uint32_t* codes_k, float* gamma_q, float* gamma_k, float* v,
+                              void* ws, size_t ws_bytes, void* stream) {
+  using namespace qkv;
+  SA_REQUIRE(sa_ln_qkv_hash_ok(d, n), SA_ERR_SHAPE, "sa_ln_qkv_hash: d=%lld n=%lld unsupported",
+             (long long)d, (long long)n);
+  SA_REQUIRE(B > 0 && B * n < (int64_t(1) << 31), SA_ERR_SHAPE, "sa_ln_qkv_hash: bad batch");
+  SA_REQUIRE(ws_bytes >= sa_ln_qkv_hash_workspace(B, n, d), SA_ERR_VALUE,
+             "sa_ln_qkv_hash: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  const int64_t M = B * n;
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.x = x;
+  p.gain = gain;
+  p.bias = bias;
+  p.eps = eps;
+  p.wg[0] = wg_q; p.wg[1] = wg_k; p.wg[2] = wg_v;
+  p.wd[0] = static_cast<const uint16_t*>(wq_dense);
+  p.wd[1] = static_cast<const uint16_t*>(wk_dense);
+  p.wd[2] = static_cast<const uint16_t*>(wv_dense);
+  p.wsh[0] = static_cast<const uint16_t*>(wq_shift);
+  p.wsh[1] = static_cast<const uint16_t*>(wk_shift);
+  p.wsh[2] = static_cast<const uint16_t*>(wv_shift);
+  p.tie = tie_thresh;
+  p.M = M;
+  p.n = int(n);
+  p.expert_of = expert_of;
+  p.gate = gate;
+  p.codes[0] = codes_q;
+  p.codes[1] = codes_k;
+  p.gpart = static_cast<double*>(ws);
+  p.nseg = int((M + 31) / 32);
+  CUtensorMap tmV;
+  memset(&tmV, 0, sizeof(tmV));
+  {
+    const cuuint64_t dims[2] = {cuuint64_t(d), cuuint64_t(M)};
+    const cuuint64_t strides[1] = {cuuint64_t(d) * 4};
+    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_tmap_tiled(
+        &tmV, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, v, dims, strides, box, estr,
+        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    SA_REQUIRE(r == CUDA_SUCCESS, SA_ERR_CUDA, "sa_ln_qkv_hash: tensor map for v failed (%d)", int(r));
+  }
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (M + 127) / 128;
+  const int grid = int(tiles < sms ? tiles : sms);
+  if (d == 32) {
+    const int smem = int(Smem<32>::TOTAL);
+    cudaFuncSetAttribute(qkv_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    qkv_kernel<32><<<grid, qkv::kThreads, smem, s>>>(p, tmV);
+  } else {
+    const int smem = int(Smem<64>::TOTAL);
+    cudaFuncSetAttribute(qkv_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    qkv_kernel<64><<<grid, qkv::kThreads, smem, s>>>(p, tmV);
+  }
+  const int64_t H = d / 32;
+  gamma_finalize_qkv<<<unsigned(cdiv(2 * B * H, 256)), 256, 0, s>>>(p.gpart, p.nseg, int(H), B,
+                                                                   int(n), gamma_q, gamma_k);
+  count_launch(2);
+  SA_LAUNCH_CHECK("sa_ln_qkv_hash");
+  return SA_OK;
+}

@@ -13,10 +13,32 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cudaTypedefs.h>
 
 #include "common.cuh"
 
 namespace sa {
+
+// cuTensorMapEncodeTiled resolved through the runtime's driver entry point, so
+// the library has no link-time dependency on libcuda (it loads on machines
+// without a driver; the call itself needs one).
+inline CUresult encode_tmap_tiled(CUtensorMap* map, CUtensorMapDataType dt, cuuint32_t rank,
+                                  void* gaddr, const cuuint64_t* dims, const cuuint64_t* strides,
+                                  const cuuint32_t* box, const cuuint32_t* estr,
+                                  CUtensorMapInterleave il, CUtensorMapSwizzle sw,
+                                  CUtensorMapL2promotion l2, CUtensorMapFloatOOBfill oob) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || f == nullptr)
+      return CUDA_ERROR_NOT_FOUND;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn(map, dt, rank, gaddr, dims, strides, box, estr, il, sw, l2, oob);
+}
+
 namespace tc {
 
 constexpr int kBK = 32;            // K per shared-memory stage

@@ -116,6 +116,14 @@ def tc_enabled() -> bool:
 FUSE_LN_ROUTE = os.environ.get("SA_FUSE_LN_ROUTE", "1") == "1"
 # fc1 → GELU → fc2 in one tensor-core kernel (d = 32 / 64)
 FUSE_MLP = os.environ.get("SA_FUSE_MLP", "1") == "1"
+# LN1 + q/k/v routers + both experts of q/k/v + sign-hash in one kernel (d = 32 / 64)
+FUSE_QKV = os.environ.get("SA_FUSE_QKV", "1") == "1"
+
+
+def _dual_expert_linear(m) -> bool:
+    return (isinstance(m, MoeModule) and len(m.experts) == 2 and isinstance(m.experts[0], Linear)
+            and isinstance(m.experts[1], ShiftLinearLayer)
+            and m.experts[0].in_dim == m.experts[0].out_dim)
 
 
 def fused_mlp_ok(d, hidden) -> bool:
@@ -521,7 +529,9 @@ class Block:
         x2 = x.reshape(batch * n, d)
         fuse = FUSE_LN_ROUTE and d in (32, 64)
         qkv = [self.attn.proj[k] for k in ("q", "k", "v")]
-        if fuse and all(isinstance(p, MoeModule) for p in qkv):
+        if self._fused_qkv_ok(d, n, qkv):
+            h = self._fused_attention(x2, batch, n, d, qkv).reshape(batch, n, d)
+        elif fuse and all(isinstance(p, MoeModule) for p in qkv):
             y, plans = MOE.ln_route_plans(x2, self.ln1.gain.value, self.ln1.bias.value,
                                           [p.wg.value for p in qkv])
             h = self.attn.forward(y.reshape(batch, n, d), residual=x, plans=plans)
@@ -536,6 +546,43 @@ class Block:
             flat = self.ln2.forward(h).reshape(batch * n, d)
             y = self.mlp.forward(flat, residual=h2)
         return y.reshape(batch, n, d)
+
+    def _fused_qkv_ok(self, d, n, qkv) -> bool:
+        cfg = self.cfg
+        return (FUSE_QKV and tc_enabled() and cfg.attn_mode == "linear-binary"
+                and cfg.binary_order in ("auto", "linear") and d == 32 * cfg.h
+                and all(_dual_expert_linear(p) for p in qkv)
+                and bool(_lib.load().sa_ln_qkv_hash_ok(d, n)))
+
+    def _fused_attention(self, x2, batch, n, d, qkv):
+        """sa_ln_qkv_hash (LN1 + routers + q/k/v + sign-hash) → binary core →
+        W_O with the residual; the q/k/v plans are set lazily (their stable
+        partitions are only computed if read)."""
+        M = batch * n
+        H = self.cfg.h
+        dev = x2.device
+        expert_of = torch.empty((3, M), dtype=torch.int32, device=dev)
+        gate = torch.empty((3, M), dtype=torch.float32, device=dev)
+        cq = torch.empty((batch, H, n, 1), dtype=torch.int32, device=dev)
+        ck = torch.empty_like(cq)
+        gq = torch.empty((batch, H), dtype=torch.float32, device=dev)
+        gk = torch.empty_like(gq)
+        v = torch.empty((M, d), dtype=torch.float32, device=dev)
+        ws = _lib.Workspace.get(_lib.load().sa_ln_qkv_hash_workspace(batch, n, d), slot=4)
+        packs = []
+        for proj in qkv:
+            packs.append(_lib.ptr(proj.experts[0].tc_pack(d)[0]))
+            packs.append(_lib.ptr(proj.experts[1].tc_pack(d)[0]))
+        _lib.call("sa_ln_qkv_hash", _lib.ptr(x2), _lib.ptr(self.ln1.gain.value),
+                  _lib.ptr(self.ln1.bias.value), 1e-5, *[_lib.ptr(p.wg.value) for p in qkv], *packs,
+                  MOE.tie_threshold(), batch, n, d, _lib.ptr(expert_of), _lib.ptr(gate),
+                  _lib.ptr(cq), _lib.ptr(ck), _lib.ptr(gq), _lib.ptr(gk), _lib.ptr(v),
+                  _lib.ptr(ws), ws.numel(), _stream())
+        for r, proj in enumerate(qkv):
+            proj.last_plan = MOE.LazyDispatchPlan(expert_of[r], gate[r])
+        dw = self.attn.dw.value if self.attn.dw is not None else None
+        merged = A.binary_core_codes(cq, ck, gq, gk, v, batch, H, dw, A.EPS_NORM, "linear")
+        return self.attn.proj["o"].forward(merged, residual=x2)
 
     def named_params(self, prefix):
         yield from self.ln1.named_params(prefix + ".ln1")

@@ -108,6 +108,45 @@ class DispatchPlan:
         return float(self.index_of[expert].size) / max(e.size, 1)
 
 
+class LazyDispatchPlan(DispatchPlan):
+    """A plan whose winners / gates were produced on the device by a fused
+    kernel (sa_ln_qkv_hash); the stable partition (counts, perm) is computed
+    by sa_moe_partition on first use, on the then-current stream."""
+
+    def __init__(self, expert_of_dev, gate_dev):
+        super().__init__(expert_of_dev, gate_dev, None, None)
+
+    def _partition(self):
+        if self._counts is None:
+            M = self.expert_of_dev.shape[0]
+            dev = self.expert_of_dev.device
+            counts = torch.empty(2, dtype=torch.int32, device=dev)
+            perm = torch.empty(M, dtype=torch.int32, device=dev)
+            nbytes = int(_lib.load().sa_moe_partition_workspace(M))
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
+            _lib.call("sa_moe_partition", _lib.ptr(self.expert_of_dev), M, _lib.ptr(counts),
+                      _lib.ptr(perm), _lib.ptr(ws), ws.numel(), _lib.stream())
+            self._counts, self._perm = counts, perm
+
+    @property
+    def counts_dev(self):
+        self._partition()
+        return self._counts
+
+    @counts_dev.setter
+    def counts_dev(self, v):
+        self._counts = v
+
+    @property
+    def perm_dev(self):
+        self._partition()
+        return self._perm
+
+    @perm_dev.setter
+    def perm_dev(self, v):
+        self._perm = v
+
+
 def _check_two(router: Router):
     if router.num_experts != 2:
         raise ShapeError("the device router implements the two-expert (mult, shift) mixture")

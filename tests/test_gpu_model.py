@@ -53,20 +53,30 @@ FIXTURES = {
 
 
 def capture_device(model):
-    """Wrap the device model's attention / MoE layers to record codes and plans."""
+    """Wrap the binary core to record the packed q / k codes it is given (the
+    fused attention-input kernel and the unfused sign-hash both feed it)."""
     from paper_2306_06446_b200 import attention as A
     recs = {"codes": {}, "plans": {}}
-    orig = A.binary_core
+    orig = A.binary_core_codes
 
-    def binary_core(q, k, v, batch, heads, dw=None, eps=A.EPS_NORM, order="auto"):
-        from paper_2306_06446_b200 import quantize as Q
-        cq, gq = Q.sign_hash(q, heads, batch)
-        ck, gk = Q.sign_hash(k, heads, batch)
-        recs["codes"].setdefault("q", []).append(q.clone())
-        recs["codes"].setdefault("k", []).append(k.clone())
-        return A.binary_core_codes(cq, ck, gq, gk, v, batch, heads, dw, eps, order)
-    A.binary_core = binary_core
-    return recs, lambda: setattr(A, "binary_core", orig)
+    def binary_core_codes(cq, ck, gq, gk, v, batch, heads, dw=None, eps=A.EPS_NORM, order="auto"):
+        dk = v.shape[1] // heads
+        recs["codes"].setdefault("q", []).append((cq.clone(), dk))
+        recs["codes"].setdefault("k", []).append((ck.clone(), dk))
+        return orig(cq, ck, gq, gk, v, batch, heads, dw, eps, order)
+    A.binary_core_codes = binary_core_codes
+    return recs, lambda: setattr(A, "binary_core_codes", orig)
+
+
+def code_bits(rec):
+    """([B, H, n, W] packed words, dk) → the reference's sign bits of the flat
+    (B·n, d) projection, packed little-endian (the golden 'codes:' layout)."""
+    codes, dk = rec
+    c = host(codes).view(np.uint32)
+    B, H, n, W = c.shape
+    bits = ((c[..., None] >> np.arange(32, dtype=np.uint32)) & 1).astype(np.uint8)   # B,H,n,W,32
+    bits = bits.reshape(B, H, n, W * 32)[..., :dk].transpose(0, 2, 1, 3).reshape(-1)
+    return np.packbits(bits, bitorder="little")
 
 
 @pytest.mark.parametrize("name", sorted(FIXTURES))
@@ -93,13 +103,14 @@ def test_model_vs_golden(golden, name):
     qs = [n for n in names if n.endswith(".q")]
     ks = [n for n in names if n.endswith(".k")]
     for got, key in zip(recs["codes"].get("q", []), qs):
-        bits = np.packbits((~(host(got) < 0)).astype(np.uint8).ravel(), bitorder="little")
+        bits = code_bits(got)
         flips += int(np.unpackbits(bits ^ fx["codes:" + key]).sum())
         total += bits.size * 8
     for got, key in zip(recs["codes"].get("k", []), ks):
-        bits = np.packbits((~(host(got) < 0)).astype(np.uint8).ravel(), bitorder="little")
+        bits = code_bits(got)
         flips += int(np.unpackbits(bits ^ fx["codes:" + key]).sum())
         total += bits.size * 8
+    assert len(recs["codes"].get("q", [])) == len(qs), "codes of every binary layer recorded"
     route_flips = 0
     for lname, mod in m.moe_modules():
         bits = np.packbits(mod.last_plan.expert_of.astype(np.uint8), bitorder="little")
@@ -170,3 +181,43 @@ def test_pvt_b0_full_batch_properties():
     net = nets.build(specs.pvt_v2_b0())
     ref = nets.forward(net, host(images[:2]))
     assert rel_err(la[:2], ref) < LOGIT_TOL
+
+
+@pytest.mark.parametrize("name", ["toy_c1_moe", "pvt_small", "pvt_b0_full"])
+def test_fused_qkv_matches_unfused(golden, name):
+    """sa_ln_qkv_hash (LN1 + routers + q/k/v + sign-hash in one kernel) against
+    the unfused chain (LN+routers, three MoE projections, two sign-hash calls):
+    identical routes and codes, logits within fp32 summation noise."""
+    from paper_2306_06446_b200 import model as MD
+    fx = golden(name)
+    spec = FIXTURES[name]()
+    m = MD.Network(spec)
+    b = int(fx["batch"])
+    images = fx["images"] if "images" in fx else ops.rng(int(fx["images_seed"])).uniform(
+        0, 1, (b, spec["img"], spec["img"], 3)).astype(F32)
+    x = dev(images)
+    old = MD.FUSE_QKV
+    try:
+        MD.FUSE_QKV = False
+        recs0, restore = capture_device(m)
+        ref = host(m.forward(x))
+        restore()
+        plans_ref = [mod.last_plan.expert_of.copy() for _, mod in m.moe_modules()]
+        MD.FUSE_QKV = True
+        recs1, restore = capture_device(m)
+        got = host(m.forward(x))
+        restore()
+        plans = [mod.last_plan.expert_of.copy() for _, mod in m.moe_modules()]
+        idx = [mod.last_plan.index_of for _, mod in m.moe_modules()]
+    finally:
+        MD.FUSE_QKV = old
+    for a, c in zip(plans, plans_ref):
+        assert np.array_equal(a, c)
+    for e, ix in zip(plans, idx):   # lazily materialised stable partition
+        assert np.array_equal(ix[0], np.flatnonzero(e == 0))
+        assert np.array_equal(ix[1], np.flatnonzero(e == 1))
+    for key in ("q", "k"):
+        for (c0, _), (c1, _) in zip(recs0["codes"][key], recs1["codes"][key]):
+            assert np.array_equal(host(c0), host(c1))
+    assert rel_err(got, ref) < 1e-6
+    assert rel_err(got, fx["logits"]) < LOGIT_TOL
