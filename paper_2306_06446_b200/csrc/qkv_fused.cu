@@ -152,17 +152,26 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid
     const int rl = (warp - kProd) * 32 + lane;
     const uint32_t lane_base = uint32_t((warp - kProd) * 32) << 16;
     int j = 0;
+    // the next tile's row is loaded while this tile is normalised / routed
+    float4 xn[D / 4];
+    auto load_row = [&](int mm) {
+      const int64_t rr = int64_t(mm) * 128 + rl;
+      const float4* xr = reinterpret_cast<const float4*>(p.x + rr * D);
+#pragma unroll
+      for (int i = 0; i < D / 4; ++i)
+        xn[i] = (mm < ntile && rr < p.M) ? __ldg(xr + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    load_row(blockIdx.x);
     for (int m = blockIdx.x; m < ntile; m += gridDim.x, ++j) {
       const int64_t row = int64_t(m) * 128 + rl;
       const bool ok = row < p.M;
       float v[D];
-      if (ok) {
-        const float4* xr = reinterpret_cast<const float4*>(p.x + row * D);
 #pragma unroll
-        for (int i = 0; i < D / 4; ++i) {
-          const float4 q = __ldg(xr + i);
-          v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
-        }
+      for (int i = 0; i < D / 4; ++i) {
+        v[4 * i] = xn[i].x; v[4 * i + 1] = xn[i].y; v[4 * i + 2] = xn[i].z; v[4 * i + 3] = xn[i].w;
+      }
+      load_row(m + gridDim.x);
+      if (ok) {
         // LayerNorm: the exact operation sequence of ln_route_kernel (moe.cu)
         float s = 0.f;
 #pragma unroll

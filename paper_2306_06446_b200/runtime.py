@@ -78,3 +78,44 @@ class GraphedForward:
             self.static_in.copy_(images, non_blocking=True)
         self.graph.replay()
         return self.static_out
+
+
+class PipelinedForward:
+    """Serving loop with host↔device copies overlapped with compute: two
+    captured forwards on two device input buffers, a host→device copy stream,
+    a compute stream and a device→host stream. Batch i is uploaded while batch
+    i-1 is computed and batch i-2's logits are read back; replays stay
+    serialised on the compute stream (the library's workspaces are shared)."""
+
+    def __init__(self, model, example: torch.Tensor):
+        self.fwd = [GraphedForward(model, example), GraphedForward(model, example)]
+        self.h2d = torch.cuda.Stream()
+        self.comp = torch.cuda.Stream()
+        self.d2h = torch.cuda.Stream()
+        self.in_ready = [torch.cuda.Event(), torch.cuda.Event()]
+        self.done = [torch.cuda.Event(), torch.cuda.Event()]
+        self.read = [torch.cuda.Event(), torch.cuda.Event()]
+        for e in self.done + self.read:
+            e.record(torch.cuda.current_stream())
+
+    def run(self, host_batches, host_outs):
+        """host_batches: pinned host image tensors; host_outs: pinned host
+        logits buffers (len >= 2, reused round robin). Returns the number of
+        batches issued; completion is on the d2h stream (self.d2h)."""
+        for i, hb in enumerate(host_batches):
+            k = i & 1
+            f = self.fwd[k]
+            with torch.cuda.stream(self.h2d):
+                self.h2d.wait_event(self.done[k])          # buffer k no longer read
+                f.static_in.copy_(hb, non_blocking=True)
+                self.in_ready[k].record(self.h2d)
+            with torch.cuda.stream(self.comp):
+                self.comp.wait_event(self.in_ready[k])
+                self.comp.wait_event(self.read[k])         # logits k already read back
+                f.graph.replay()
+                self.done[k].record(self.comp)
+            with torch.cuda.stream(self.d2h):
+                self.d2h.wait_event(self.done[k])
+                host_outs[i % len(host_outs)].copy_(f.static_out, non_blocking=True)
+                self.read[k].record(self.d2h)
+        return len(host_batches)
