@@ -198,6 +198,10 @@ def op_bytes(name, args):
         B, n, d = args[14], args[15], args[16]
         M = B * n
         return 2 * M * d * A + 2 * M * d // 8 + 3 * M * 8
+    if name == "sa_fused_moe_linear":
+        # x, residual in; y out; (expert, gate) dispatch array
+        M, d = args[6], args[7]
+        return 3 * M * d * A + M * 8
     if name == "sa_pool":
         B, n, d = args[2], args[3], args[4]
         return B * n * d * A

@@ -229,6 +229,17 @@ int sa_ln_qkv_hash(const float* x, const float* gain, const float* bias, float e
                    uint32_t* codes_k, float* gamma_q, float* gamma_k, float* v, void* ws,
                    size_t ws_bytes, void* stream);
 
+/* MoeModule.forward of a (Linear, ShiftLinearLayer) d -> d projection plus the
+ * block residual (the attention output projection, model.py:250-274, 374,
+ * 454-459) in one kernel, d = 32 / 64: router (moe.py:81-92) in the producer,
+ * both experts on the tensor cores, y = residual + gate · expert(x). Writes
+ * expert_of / gate [M] (the plan's partition is computed on demand with
+ * sa_moe_partition). Weights packed with bn = d. */
+int sa_fused_moe_linear_ok(int64_t d);
+int sa_fused_moe_linear(const float* x, const float* wg, const void* w_dense, const void* w_shift,
+                        const float* residual, float tie_thresh, int64_t M, int64_t d,
+                        int32_t* expert_of, float* gate, float* y, void* stream);
+
 /* patchify (model.py:557-563) + patch-embed Linear on the tensor cores */
 int sa_tc_patch_embed(const float* grid, int64_t B, int64_t H, int64_t W, int64_t C,
                       int64_t patch, float sub, const void* wpack, int bn, int64_t d,

@@ -25,6 +25,11 @@
 //              128-byte-swizzled shared memory stored by TMA.
 // Products per row are computed by the same split-precision MMA chains as the
 // unfused path (sa_tc_moe_linear), so the projections agree bit for bit.
+//
+// The same kernel in its one-projection form (NP = 1) is the attention output
+// projection W_O (AttentionLayer.forward, model.py:374, with the residual of
+// Block.forward, model.py:454-459): no LayerNorm, one router on the merged
+// heads, out = residual + gate · expert(merged), stored by TMA.
 #include "tc_gemm_kernel.cuh"
 
 namespace sa {
@@ -37,22 +42,21 @@ constexpr int kThreads = 288;   // 9 warps
 constexpr uint32_t kPlaneCols = 16;
 constexpr int kRT = 4;           // route-table ring slots
 
-template <int D>
+template <int D, int NP>   // NP projections: 3 (q, k, v with LN1 + hash) or 1 (W_O)
 struct Cfg {
   static constexpr int KC1 = D / 32;                // K stages of 32
   static constexpr int H = D / 32;                  // heads (dk = 32)
-  static constexpr int NA = D == 32 ? 2 : 1;        // A buffers in TMEM
-  static constexpr int NACC = D == 32 ? 2 : 1;      // accumulator buffers
+  static constexpr int NA = (NP == 3 && D == 64) ? 1 : 2;          // A buffers in TMEM
+  static constexpr int NACC = NP == 3 ? (D == 32 ? 2 : 1) : (D == 32 ? 4 : 2);
   static constexpr uint32_t A_COLS = KC1 * 3 * kPlaneCols;
   static constexpr uint32_t T_A = 0;
-  static constexpr uint32_t T_ACC = 128;            // 6 parts of D columns per buffer
-  static constexpr uint32_t ACC_COLS = 6 * D;
-  static_assert(T_A + NA * A_COLS <= T_ACC, "A region");
+  static constexpr uint32_t T_ACC = (NA * A_COLS + 31) / 32 * 32;  // 2·NP parts of D columns
+  static constexpr uint32_t ACC_COLS = 2 * NP * D;
   static_assert(T_ACC + NACC * ACC_COLS <= 512, "TMEM budget");
   // resident weights: per projection dense (3 planes) then shift (1 plane)
   static constexpr uint32_t WD = uint32_t(D) * D * 2 * 3;
   static constexpr uint32_t WS = uint32_t(D) * D * 2;
-  static constexpr uint32_t W_BYTES = 3 * (WD + WS);
+  static constexpr uint32_t W_BYTES = NP * (WD + WS);
 };
 
 struct Params {
@@ -71,18 +75,19 @@ struct Params {
   uint32_t* codes[2];         // q, k: [B][H][n]
   double* gpart;              // [2][M/32 segments][H][2]
   int nseg;
+  const float* residual;      // NP = 1: out = residual + gate · expert(x)
 };
 
 // smem layout (bytes)
-template <int D>
+template <int D, int NP>
 struct Smem {
   static constexpr uint32_t W = 0;
-  static constexpr uint32_t WG = Cfg<D>::W_BYTES;                  // [3][2D] double
-  static constexpr uint32_t RT_E = WG + 3 * 2 * D * 8;             // [kRT][3][128] int
-  static constexpr uint32_t RT_G = RT_E + kRT * 3 * 128 * 4;       // [kRT][3][128] float
-  static constexpr uint32_t BOX = (RT_G + kRT * 3 * 128 * 4 + 1023) & ~1023u;   // [4 warps][H][4 KB]
-  static constexpr uint32_t BAR = BOX + 4 * Cfg<D>::H * 4096;
-  static constexpr uint32_t NBAR = 2 * Cfg<D>::NA + 2 * Cfg<D>::NACC + 2 * kRT + 1;
+  static constexpr uint32_t WG = Cfg<D, NP>::W_BYTES;              // [NP][2D] double
+  static constexpr uint32_t RT_E = WG + NP * 2 * D * 8;            // [kRT][NP][128] int
+  static constexpr uint32_t RT_G = RT_E + kRT * NP * 128 * 4;      // [kRT][NP][128] float
+  static constexpr uint32_t BOX = (RT_G + kRT * NP * 128 * 4 + 1023) & ~1023u;  // [4 warps][H][4 KB]
+  static constexpr uint32_t BAR = BOX + 4 * Cfg<D, NP>::H * 4096;
+  static constexpr uint32_t NBAR = 2 * Cfg<D, NP>::NA + 2 * Cfg<D, NP>::NACC + 2 * kRT + 1;
   static constexpr uint32_t TOTAL = BAR + NBAR * 8 + 16 + 1024;    // + alignment slack
 };
 
@@ -97,10 +102,10 @@ __device__ __forceinline__ int decide2(float l0, float l1, float tie_thresh, flo
   return e;
 }
 
-template <int D>
+template <int D, int NP>
 __global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid_constant__ CUtensorMap tmV) {
-  using C = Cfg<D>;
-  using S = Smem<D>;
+  using C = Cfg<D, NP>;
+  using S = Smem<D, NP>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   double* swg = reinterpret_cast<double*>(smem + S::WG);
@@ -135,12 +140,12 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid
     fence_barrier_init();
     // every weight tile, once: per projection dense (3 planes) then shift
     mbar_expect_tx(wbar, C::W_BYTES);
-    for (int r = 0; r < 3; ++r) {
+    for (int r = 0; r < NP; ++r) {
       bulk_g2s(smem + S::W + r * (C::WD + C::WS), p.wd[r], C::WD, wbar);
       bulk_g2s(smem + S::W + r * (C::WD + C::WS) + C::WD, p.wsh[r], C::WS, wbar);
     }
   }
-  for (int i = tid; i < 3 * 2 * D; i += kThreads) swg[i] = double(p.wg[i / (2 * D)][i % (2 * D)]);
+  for (int i = tid; i < NP * 2 * D; i += kThreads) swg[i] = double(p.wg[i / (2 * D)][i % (2 * D)]);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -171,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid
         v[4 * i] = xn[i].x; v[4 * i + 1] = xn[i].y; v[4 * i + 2] = xn[i].z; v[4 * i + 3] = xn[i].w;
       }
       load_row(m + gridDim.x);
-      if (ok) {
+      if (NP == 3 && ok) {
         // LayerNorm: the exact operation sequence of ln_route_kernel (moe.cu)
         float s = 0.f;
 #pragma unroll
@@ -193,15 +198,12 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid
           v[4 * i + 2] = v[4 * i + 2] * inv * g.z + b.z;
           v[4 * i + 3] = v[4 * i + 3] * inv * g.w + b.w;
         }
-      } else {
-#pragma unroll
-        for (int i = 0; i < D; ++i) v[i] = 0.f;
       }
-      // routers (fp64 dots in channel order, as ln_route_kernel)
+      // routers (fp64 dots in channel order, as ln_route_kernel / route_kernel)
       const int rs = j % kRT;
       mbar_wait(&rt_empty[rs], (uint32_t(j / kRT) & 1u) ^ 1u);
 #pragma unroll 1
-      for (int r = 0; r < 3; ++r) {
+      for (int r = 0; r < NP; ++r) {
         double s0 = 0.0, s1 = 0.0;
         const double* w = swg + r * 2 * D;
 #pragma unroll
@@ -216,8 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid
           p.expert_of[r * p.M + row] = e;
           p.gate[r * p.M + row] = g;
         }
-        rt_e[(rs * 3 + r) * 128 + rl] = e;
-        rt_g[(rs * 3 + r) * 128 + rl] = g;
+        rt_e[(rs * NP + r) * 128 + rl] = e;
+        rt_g[(rs * NP + r) * 128 + rl] = g;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&rt_full[rs]);
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid
       const uint32_t a0 = tmem + C::T_A + uint32_t(ab) * C::A_COLS;
       const uint32_t acc = tmem + C::T_ACC + uint32_t(cb) * C::ACC_COLS;
 #pragma unroll
-      for (int r = 0; r < 3; ++r) {
+      for (int r = 0; r < NP; ++r) {
         const uint32_t wd = wbase + r * (C::WD + C::WS);
         const uint32_t ws = wd + C::WD;
 #pragma unroll
@@ -290,12 +292,20 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid
       const bool ok = row < p.M;
       const int rs = j % kRT, cb = j % C::NACC;
       mbar_wait(&rt_full[rs], uint32_t(j / kRT) & 1u);
-      int e[3];
-      float g[3];
+      int e[NP];
+      float g[NP];
 #pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        e[r] = rt_e[(rs * 3 + r) * 128 + rl];
-        g[r] = rt_g[(rs * 3 + r) * 128 + rl];
+      for (int r = 0; r < NP; ++r) {
+        e[r] = rt_e[(rs * NP + r) * 128 + rl];
+        g[r] = rt_g[(rs * NP + r) * 128 + rl];
+      }
+      // W_O: the residual row is loaded before the accumulator wait
+      float4 res[NP == 1 ? D / 4 : 1];
+      if (NP == 1) {
+#pragma unroll
+        for (int i = 0; i < (NP == 1 ? D / 4 : 0); ++i)
+          res[i] = ok ? __ldg(reinterpret_cast<const float4*>(p.residual + row * D) + i)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&rt_empty[rs]);
@@ -308,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid
       const int b0 = int(wrow0 / p.n);
       const int seg = int(wrow0 >> 5);
 #pragma unroll 1
-      for (int r = 0; r < 3; ++r) {
+      for (int r = 0; r < NP; ++r) {
 #pragma unroll
         for (int hh = 0; hh < C::H; ++hh) {
           uint32_t rd[32], rsft[32];
@@ -316,10 +326,20 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid
           tmem_ld32_nowait(acc + uint32_t(2 * r + 1) * D + hh * 32, rsft);
           tmem_ld_wait();
           float y[32];
+          // gate and residual are two float32 roundings, as the reference's
+          // y * gate then residual + y (no FMA contraction)
 #pragma unroll
           for (int c = 0; c < 32; ++c)
-            y[c] = g[r] * __uint_as_float(e[r] ? rsft[c] : rd[c]);
-          if (r < 2) {
+            y[c] = __fmul_rn(g[r], __uint_as_float(e[r] ? rsft[c] : rd[c]));
+          if (NP == 1) {   // W_O: + residual
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              const float4 q4 = res[(NP == 1 ? (hh * 32 + c) / 4 : 0)];
+              const float rv = (c & 3) == 0 ? q4.x : (c & 3) == 1 ? q4.y : (c & 3) == 2 ? q4.z : q4.w;
+              y[c] = __fadd_rn(rv, y[c]);
+            }
+          }
+          if (NP == 3 && r < 2) {
             uint32_t code = 0u;
             double asum = 0.0;
 #pragma unroll
@@ -464,18 +484,78 @@ extern "C" int sa_ln_qkv_hash(const float* x, const float* gain, const float* bi
   const int64_t tiles = (M + 127) / 128;
   const int grid = int(tiles < sms ? tiles : sms);
   if (d == 32) {
-    const int smem = int(Smem<32>::TOTAL);
-    cudaFuncSetAttribute(qkv_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    qkv_kernel<32><<<grid, qkv::kThreads, smem, s>>>(p, tmV);
+    const int smem = int(Smem<32, 3>::TOTAL);
+    cudaFuncSetAttribute(qkv_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    qkv_kernel<32, 3><<<grid, qkv::kThreads, smem, s>>>(p, tmV);
   } else {
-    const int smem = int(Smem<64>::TOTAL);
-    cudaFuncSetAttribute(qkv_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    qkv_kernel<64><<<grid, qkv::kThreads, smem, s>>>(p, tmV);
+    const int smem = int(Smem<64, 3>::TOTAL);
+    cudaFuncSetAttribute(qkv_kernel<64, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    qkv_kernel<64, 3><<<grid, qkv::kThreads, smem, s>>>(p, tmV);
   }
   const int64_t H = d / 32;
   gamma_finalize_qkv<<<unsigned(cdiv(2 * B * H, 256)), 256, 0, s>>>(p.gpart, p.nseg, int(H), B,
                                                                    int(n), gamma_q, gamma_k);
   count_launch(2);
   SA_LAUNCH_CHECK("sa_ln_qkv_hash");
+  return SA_OK;
+}
+
+/* MoeModule.forward of a (Linear, ShiftLinearLayer) projection with d -> d and
+ * the block residual (the attention output projection, model.py:250-274, 374,
+ * 454-459): route (fp64 dot, numpy tie rule), both experts on the tensor cores,
+ * out = residual + gate · expert(x); expert_of / gate [M] for the lazy plan. */
+extern "C" int sa_fused_moe_linear_ok(int64_t d) { return d == 32 || d == 64; }
+
+extern "C" int sa_fused_moe_linear(const float* x, const float* wg, const void* w_dense,
+                                   const void* w_shift, const float* residual, float tie_thresh,
+                                   int64_t M, int64_t d, int32_t* expert_of, float* gate,
+                                   float* y, void* stream) {
+  using namespace qkv;
+  SA_REQUIRE(sa_fused_moe_linear_ok(d), SA_ERR_SHAPE, "sa_fused_moe_linear: d=%lld unsupported",
+             (long long)d);
+  SA_REQUIRE(M > 0 && M < (int64_t(1) << 31), SA_ERR_SHAPE, "sa_fused_moe_linear: bad M");
+  SA_REQUIRE(residual != nullptr, SA_ERR_VALUE, "sa_fused_moe_linear: residual required");
+  cudaStream_t s = as_stream(stream);
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.x = x;
+  p.wg[0] = wg;
+  p.wd[0] = static_cast<const uint16_t*>(w_dense);
+  p.wsh[0] = static_cast<const uint16_t*>(w_shift);
+  p.tie = tie_thresh;
+  p.M = M;
+  p.n = int(M);   // (no image structure needed: no hashing)
+  p.expert_of = expert_of;
+  p.gate = gate;
+  p.residual = residual;
+  CUtensorMap tmY;
+  memset(&tmY, 0, sizeof(tmY));
+  {
+    const cuuint64_t dims[2] = {cuuint64_t(d), cuuint64_t(M)};
+    const cuuint64_t strides[1] = {cuuint64_t(d) * 4};
+    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_tmap_tiled(
+        &tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, y, dims, strides, box, estr,
+        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    SA_REQUIRE(r == CUDA_SUCCESS, SA_ERR_CUDA, "sa_fused_moe_linear: tensor map failed (%d)", int(r));
+  }
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (M + 127) / 128;
+  const int grid = int(tiles < sms ? tiles : sms);
+  if (d == 32) {
+    const int smem = int(Smem<32, 1>::TOTAL);
+    cudaFuncSetAttribute(qkv_kernel<32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    qkv_kernel<32, 1><<<grid, qkv::kThreads, smem, s>>>(p, tmY);
+  } else {
+    const int smem = int(Smem<64, 1>::TOTAL);
+    cudaFuncSetAttribute(qkv_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    qkv_kernel<64, 1><<<grid, qkv::kThreads, smem, s>>>(p, tmY);
+  }
+  count_launch(1);
+  SA_LAUNCH_CHECK("sa_fused_moe_linear");
   return SA_OK;
 }

@@ -120,6 +120,15 @@ FUSE_MLP = os.environ.get("SA_FUSE_MLP", "1") == "1"
 FUSE_QKV = os.environ.get("SA_FUSE_QKV", "1") == "1"
 
 
+FUSE_O = os.environ.get("SA_FUSE_O", "1") == "1"
+
+
+def _fused_o_ok(mod, x2) -> bool:
+    return (FUSE_O and tc_enabled() and _dual_expert_linear(mod) and x2.dim() == 2
+            and x2.shape[1] == mod.experts[0].in_dim
+            and bool(_lib.load().sa_fused_moe_linear_ok(x2.shape[1])))
+
+
 def _dual_expert_linear(m) -> bool:
     return (isinstance(m, MoeModule) and len(m.experts) == 2 and isinstance(m.experts[0], Linear)
             and isinstance(m.experts[1], ShiftLinearLayer)
@@ -432,6 +441,18 @@ class MoeModule:
         x = to_device(x)
         lead = x.shape[:-1]
         x2 = x.reshape(-1, x.shape[-1])
+        if plan is None and residual is not None and _fused_o_ok(self, x2):
+            # route + both experts + residual in one kernel (sa_fused_moe_linear)
+            M, d = x2.shape
+            expert_of = torch.empty(M, dtype=torch.int32, device=x2.device)
+            gate = torch.empty(M, dtype=torch.float32, device=x2.device)
+            y = torch.empty_like(x2)
+            _lib.call("sa_fused_moe_linear", _lib.ptr(x2), _lib.ptr(self.wg.value),
+                      _lib.ptr(self.experts[0].tc_pack(d)[0]), _lib.ptr(self.experts[1].tc_pack(d)[0]),
+                      _lib.ptr(residual.reshape(M, d)), MOE.tie_threshold(), M, d,
+                      _lib.ptr(expert_of), _lib.ptr(gate), _lib.ptr(y), _stream())
+            self.last_plan = MOE.LazyDispatchPlan(expert_of, gate)
+            return y.reshape(*lead, d)
         if plan is None:
             plan, _ = MOE.route_plan(x2, self.wg.value)
         self.last_plan = plan

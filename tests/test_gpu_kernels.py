@@ -414,3 +414,32 @@ def test_fused_binary_attention_matches_multikernel(B, n, d, h, with_dw):
     q2[0, :] = -np.abs(q2[0, :]) - 1.0
     out2 = host(A.binary_core(dev(q2), dev(kk), dev(v), B, h, None))
     assert np.all(out2[0] == 0)
+
+
+@pytest.mark.parametrize("M,d", [(777, 32), (20000, 64), (802816 // 64, 32)])
+def test_fused_moe_linear_matches_unfused(M, d):
+    """sa_fused_moe_linear (router + both experts + residual in one kernel, the
+    W_O path) against route_plan + sa_tc_moe_linear: identical winners, gates
+    and outputs (the same split-precision MMA chains), and the oracle."""
+    from paper_2306_06446_b200 import model as MD
+    mod, L = _moe_layers(d, d, None)
+    g = ops.rng(M + d)
+    x = g.standard_normal((M, d)).astype(F32)
+    res = g.standard_normal((M, d)).astype(F32)
+    old = MD.FUSE_O
+    try:
+        MD.FUSE_O = False
+        y0 = host(mod.forward(dev(x), residual=dev(res)))
+        e0, g0, i0 = mod.last_plan.expert_of, mod.last_plan.gate_of, mod.last_plan.index_of
+        MD.FUSE_O = True
+        y1 = host(mod.forward(dev(x), residual=dev(res)))
+        e1, g1, i1 = mod.last_plan.expert_of, mod.last_plan.gate_of, mod.last_plan.index_of
+    finally:
+        MD.FUSE_O = old
+    assert np.array_equal(e0, e1) and np.array_equal(g0, g1)
+    assert np.array_equal(i0[0], i1[0]) and np.array_equal(i0[1], i1[1])
+    assert np.array_equal(y0, y1)
+    tr = nets.Trace()
+    ref = nets.moe_fwd(L, x, "m", tr)
+    assert np.array_equal(e1, tr.moe[0]["expert_of"])
+    assert rel_err(y1, res + ref) < 1e-5
