@@ -76,6 +76,7 @@ struct TcParams {
   uint32_t rb_bytes[2];   // resident bytes per expert (packed planes, [n_tile][kc][plane])
   int dbg;     // debug role isolation (0 in production): 1 no A loads, 2 no C stores, 4 no MMAs
   int tma_c;   // 1: C rows are the tile rows (no scatter / residual / position): TMA-store epilogue
+  int kq_min;  // K stages alternate between producer groups when kchunks > kq_min (else whole tiles)
 };
 
 // TMEM accumulators: four buffers when they fit (BN <= 128), so the MMA can run
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
     // K stages: with one stage per tile the two groups alternate tiles; with
     // several, consecutive stages of the CTA's whole sequence alternate between
     // the groups, so both keep loads in flight within a deep-K tile
-    const bool kq = p.kchunks > 1;
+    const bool kq = p.kchunks > p.kq_min;
     const int gsel = kq ? -1 : g;
     int q = 0;
     int t_n = next_group_tile(p, c0, total, gsel, blockIdx.x, j, jj_unused, ti_n);
@@ -275,6 +276,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
       const uint16_t* Bg = p.Bp[ti.group] + size_t(ti.n_tile) * p.kchunks * npb * (BN * kBK);
       const uint32_t bbytes = uint32_t(npb) * kPlaneB;
       const float* rowp[8];
+      // patchify: (image, patch row, patch col) of this thread's first row by one
+      // division set; the other seven rows (16 apart) step it with carries
+      int pb = 0, py = 0, px = 0;
+      if (AM == A_PATCH && NST == 0) {
+        const int tpi = int(p.pside * p.pside), ps = int(p.pside);
+        const int r32 = int(ti.r0) + rsub;
+        pb = r32 / tpi;
+        const int tt = r32 - pb * tpi;
+        py = tt / ps;
+        px = tt - py * ps;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int64_t row = ti.r0 + rsub + 16 * i;
@@ -285,10 +297,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
           } else if (AM == A_GATHER) {
             rowp[i] = p.A + int64_t(idx[i]) * p.lda;
           } else {
-            const int64_t tpi = p.pside * p.pside;
-            const int64_t b = row / tpi, tt = row % tpi;
-            const int64_t py = tt / p.pside, px = tt % p.pside;
-            rowp[i] = p.A + ((b * p.pH + py * p.patch) * p.pW + px * p.patch) * p.pC;
+            rowp[i] = p.A + ((int64_t(pb) * p.pH + int64_t(py) * p.patch) * p.pW +
+                             int64_t(px) * p.patch) * p.pC;
+          }
+        }
+        if (AM == A_PATCH && NST == 0) {   // next row: 16 tokens on
+          const int ps = int(p.pside);
+          px += 16;
+          while (px >= ps) {
+            px -= ps;
+            if (++py == ps) {
+              py = 0;
+              ++pb;
+            }
           }
         }
       }
@@ -311,13 +332,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
           __syncwarp();
           if (lane == 0) mbar_arrive(&sempty[ss]);
         } else {
+          // patch offset of this thread's k: one division per stage, not per row
+          int64_t koff = k;
+          if (AM == A_PATCH) {
+            const int kq = int(k) / int(pcw);
+            koff = int64_t(kq) * (p.pW * p.pC) + (int(k) - kq * int(pcw));
+          }
 #pragma unroll
           for (int i = 0; i < 8; ++i) {   // issue the global loads before waiting for the slot
             v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (rowp[i] != nullptr && k < p.K) {
-              const float* src = (AM == A_PATCH)
-                                     ? rowp[i] + (k / pcw) * (p.pW * p.pC) + (k % pcw)
-                                     : rowp[i] + k;
+              const float* src = rowp[i] + koff;
               if (!(p.dbg & 1)) v[i] = __ldg(reinterpret_cast<const float4*>(src));
             }
           }
@@ -422,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
     uint32_t acc_phase[NACC];
 #pragma unroll
     for (int a = 0; a < NACC; ++a) acc_phase[a] = 0u;
-    const bool kq_mma = p.kchunks > 1;
+    const bool kq_mma = p.kchunks > p.kq_min;
     int qm = 0;
     int j = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -505,8 +530,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
       float gt = 1.f;
       if (r_ok) {
         orow = crA;
-        if (p.img_tokens > 0) {
-          const int64_t b = r / p.img_tokens, tt = r % p.img_tokens;
+        if (p.img_tokens > 0 && (p.extra != 0 || p.pos != nullptr)) {
+          const int b = int(r) / int(p.img_tokens), tt = int(r) - b * int(p.img_tokens);
           orow = b * (p.img_tokens + p.extra) + p.extra + tt;
           pos_idx = p.extra + tt;
           if (p.gate) gt = __ldg(p.gate + orow);

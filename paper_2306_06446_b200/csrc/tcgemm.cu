@@ -83,6 +83,8 @@ extern "C" void sa_debug_tc_tma(int on) { g_tc_tma = on; }
 extern "C" void sa_debug_tc_mode(int m) { g_tc_dbg = m; }
 static int g_tc_resident = 1;   // weights resident in shared memory when they fit
 extern "C" void sa_debug_tc_resident(int on) { g_tc_resident = on; }
+static int g_tc_kq = 4;   // stage alternation when kchunks > 4 (measured: whole tiles per group win below)
+extern "C" void sa_debug_tc_kq(int v) { g_tc_kq = v; }
 static int g_tc_stage = 0;   // A staging: 0 = direct A path (default), 1 = auto, 2/4/8 = force slots
 extern "C" void sa_debug_tc_stage(int on) { g_tc_stage = on; }
 
@@ -97,6 +99,7 @@ static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cu
   const size_t wb1 = p.counts ? size_t(p.ntiles) * p.kchunks * p.nplanes[1] * bn * kBK * 2 : 0;
   p.rb = (g_tc_resident && wb0 + wb1 <= 48 * 1024) ? 1 : 0;
   p.dbg = g_tc_dbg;
+  p.kq_min = g_tc_kq;
   p.rb_bytes[0] = p.rb ? uint32_t(wb0) : 0u;
   p.rb_bytes[1] = p.rb ? uint32_t(wb1) : 0u;
   const size_t rb_total = p.rb ? ((wb0 + wb1 + 1023) & ~size_t(1023)) : 0;
@@ -330,6 +333,8 @@ extern "C" int sa_tc_patch_embed(const float* grid, int64_t B, int64_t H, int64_
   const int64_t side = H / patch;
   const int64_t n = side * side;
   const int64_t K = patch * patch * C;
+  SA_REQUIRE(B * n < (int64_t(1) << 31), SA_ERR_SHAPE,
+             "sa_tc_patch_embed: %lld tokens exceed the 32-bit token index", (long long)(B * n));
   if (int st = tc_check("sa_tc_patch_embed", B * n, K, d, bn)) return st;
   tc::TcParams p = tc_base(B * n, K, d);
   p.A = grid;
