@@ -137,6 +137,128 @@ __global__ void __launch_bounds__(256) softmax_attn_kernel(const float* __restri
   }
 }
 
+// dk = 32, n <= 32*NJ (PVT stage 4: n = 49): the same arithmetic as
+// softmax_attn_kernel, re-laid for instruction-level parallelism — lane =
+// key (NJ keys per lane) for the scores and lane = channel for P·V, the query
+// rows and probabilities are smem broadcasts, and each warp carries QB queries
+// at once (independent FMA chains); key rows and V are read from shared memory
+// per 4-channel chunk, so registers stay ~72 (seven CTAs per SM).
+// Per key the score is the same fma chain over c = 0..31, the softmax the same
+// warp reductions, and P·V the same fma chain over j (zero-padded keys add
+// exact zeros), so the output is bit-identical to the generic kernel.
+template <int NJ, int QB>
+__global__ void __launch_bounds__(128) softmax_attn32_kernel(const float* __restrict__ q,
+                                                            const float* __restrict__ k,
+                                                            const float* __restrict__ v,
+                                                            float* __restrict__ out, int n, int d,
+                                                            int heads, float scale_div) {
+  constexpr int NK = 32 * NJ;
+  __shared__ __align__(16) float sk[NK][36];   // pitch 36: conflict-free 128-bit row reads
+  __shared__ __align__(16) float sv[NK][32];
+  __shared__ __align__(16) float sq[NK][32];
+  __shared__ __align__(16) float sp[4][QB][NK];
+  const int bh = blockIdx.x, b = bh / heads, h = bh % heads;
+  const size_t rowbase = size_t(b) * n;
+  for (int idx = threadIdx.x; idx < NK * 8; idx += 128) {
+    const int j = idx >> 3, c4 = (idx & 7) * 4;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), bk = a, cv = a;
+    if (j < n) {
+      const size_t off = (rowbase + j) * d + h * 32 + c4;
+      a = __ldg(reinterpret_cast<const float4*>(q + off));
+      bk = __ldg(reinterpret_cast<const float4*>(k + off));
+      cv = __ldg(reinterpret_cast<const float4*>(v + off));
+    }
+    *reinterpret_cast<float4*>(&sq[j][c4]) = a;
+    *reinterpret_cast<float4*>(&sk[j][c4]) = bk;
+    *reinterpret_cast<float4*>(&sv[j][c4]) = cv;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // queries i0 + 4r (r < QB) per warp iteration; a missing query recomputes i0
+  for (int i0 = warp; i0 < n; i0 += 4 * QB) {
+    float s[QB][NJ];
+#pragma unroll
+    for (int r = 0; r < QB; ++r)
+#pragma unroll
+      for (int u = 0; u < NJ; ++u) s[r][u] = 0.f;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      float4 kk[NJ];   // the lane's key rows, 4 channels at a time (shared by the QB queries)
+#pragma unroll
+      for (int u = 0; u < NJ; ++u)
+        kk[u] = *reinterpret_cast<const float4*>(&sk[lane + 32 * u][4 * m]);
+#pragma unroll
+      for (int r = 0; r < QB; ++r) {
+        const int i = i0 + 4 * r < n ? i0 + 4 * r : i0;
+        const float4 qq = *reinterpret_cast<const float4*>(&sq[i][4 * m]);
+#pragma unroll
+        for (int u = 0; u < NJ; ++u) {
+          s[r][u] = fmaf(qq.x, kk[u].x, s[r][u]);
+          s[r][u] = fmaf(qq.y, kk[u].y, s[r][u]);
+          s[r][u] = fmaf(qq.z, kk[u].z, s[r][u]);
+          s[r][u] = fmaf(qq.w, kk[u].w, s[r][u]);
+        }
+      }
+    }
+    float mx[QB], tot[QB];
+#pragma unroll
+    for (int r = 0; r < QB; ++r) {
+      mx[r] = -INFINITY;
+#pragma unroll
+      for (int u = 0; u < NJ; ++u) {
+        s[r][u] = s[r][u] / scale_div;
+        if (lane + 32 * u < n) mx[r] = fmaxf(mx[r], s[r][u]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int r = 0; r < QB; ++r) mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], o));
+#pragma unroll
+    for (int r = 0; r < QB; ++r) {
+      tot[r] = 0.f;
+#pragma unroll
+      for (int u = 0; u < NJ; ++u) {
+        if (lane + 32 * u < n) {
+          s[r][u] = expf(s[r][u] - mx[r]);
+          tot[r] += s[r][u];
+        } else {
+          s[r][u] = 0.f;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int r = 0; r < QB; ++r) tot[r] += __shfl_xor_sync(0xffffffffu, tot[r], o);
+#pragma unroll
+    for (int r = 0; r < QB; ++r)
+#pragma unroll
+      for (int u = 0; u < NJ; ++u) sp[warp][r][lane + 32 * u] = s[r][u] / tot[r];   // padded keys: 0
+    __syncwarp();
+    float acc[QB];
+#pragma unroll
+    for (int r = 0; r < QB; ++r) acc[r] = 0.f;
+#pragma unroll
+    for (int j4 = 0; j4 < NK; j4 += 4) {
+      const float v0 = sv[j4][lane], v1 = sv[j4 + 1][lane], v2 = sv[j4 + 2][lane],
+                  v3 = sv[j4 + 3][lane];
+#pragma unroll
+      for (int r = 0; r < QB; ++r) {
+        const float4 pp = *reinterpret_cast<const float4*>(&sp[warp][r][j4]);
+        acc[r] = fmaf(pp.x, v0, acc[r]);
+        acc[r] = fmaf(pp.y, v1, acc[r]);
+        acc[r] = fmaf(pp.z, v2, acc[r]);
+        acc[r] = fmaf(pp.w, v3, acc[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < QB; ++r)
+      if (i0 + 4 * r < n) out[(rowbase + i0 + 4 * r) * d + h * 32 + lane] = acc[r];
+    __syncwarp();
+  }
+}
+
 // tokens.mean(axis=1) (ref model.py:574): numpy reduces a non-contiguous axis
 // sequentially in float32, so a sequential per-channel sum reproduces it.
 __global__ void pool_kernel(const float* __restrict__ x, float* __restrict__ y, int64_t B, int n,
@@ -203,11 +325,37 @@ extern "C" int sa_layernorm(const float* x, const float* gain, const float* bias
   return SA_OK;
 }
 
+static int g_softmax_generic = 0;
+static int g_softmax_qb = 4;   // queries per warp iteration (debug sweep)
+extern "C" void sa_debug_softmax_qb(int qb) { g_softmax_qb = qb; }
+extern "C" void sa_debug_softmax_generic(int on) { g_softmax_generic = on; }
+
 extern "C" int sa_softmax_attn(const float* q, const float* k, const float* v, float* out,
                                int64_t B, int64_t n, int64_t d, int64_t heads, void* stream) {
   SA_REQUIRE(B > 0 && n > 0 && d > 0 && heads > 0 && d % heads == 0, SA_ERR_SHAPE,
              "sa_softmax_attn: bad extents");
   const int64_t dk = d / heads;
+  const float scale_div0 = sqrtf(float(dk));  // python float math.sqrt(dk) → f32
+  if (!g_softmax_generic && dk == 32 && n <= 64 && (d % 4) == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(k) & 15) == 0 && (reinterpret_cast<uintptr_t>(v) & 15) == 0) {
+    const unsigned grid = unsigned(B * heads);
+    cudaStream_t st = as_stream(stream);
+#define SA_SM32(NJ, QB) \
+  softmax_attn32_kernel<NJ, QB><<<grid, 128, 0, st>>>(q, k, v, out, int(n), int(d), int(heads), scale_div0)
+    if (n <= 32) {
+      if (g_softmax_qb == 2) SA_SM32(1, 2);
+      else if (g_softmax_qb == 8) SA_SM32(1, 8);
+      else SA_SM32(1, 4);
+    } else {
+      if (g_softmax_qb == 2) SA_SM32(2, 2);
+      else if (g_softmax_qb == 8) SA_SM32(2, 8);
+      else SA_SM32(2, 4);
+    }
+#undef SA_SM32
+    count_launch(1);
+    SA_LAUNCH_CHECK("sa_softmax_attn");
+    return SA_OK;
+  }
   const size_t smem = size_t(n * (dk + 1) + n * dk + 8 * dk + 8 * n) * sizeof(float);
   SA_REQUIRE(smem <= 220 * 1024, SA_ERR_SHAPE, "sa_softmax_attn: n=%lld dk=%lld too large",
              (long long)n, (long long)dk);

@@ -339,6 +339,37 @@ def test_softmax_core_golden(golden):
     assert rel_err(host(out), k["sm_out"]) < 2e-6
 
 
+@pytest.mark.parametrize("n", [7, 32, 33, 49, 64])
+def test_softmax_attn32_bit_identical_to_generic(n):
+    """The register-blocked dk=32 softmax kernel computes the generic kernel's
+    arithmetic in the same order: bit-identical outputs, and the oracle's
+    softmax core within fp32 tolerance."""
+    from paper_2306_06446_b200 import _lib
+    from paper_2306_06446_b200 import attention as A
+    lib = _lib.load()
+    g = ops.rng(n)
+    B, heads, dk = 5, 3, 32
+    q, k, v = (g.standard_normal((B * n, heads * dk)).astype(F32) for _ in range(3))
+    fast = host(A.softmax_core_flat(dev(q), dev(k), dev(v), B, heads))
+    for qb in (2, 8):   # queries per warp iteration: same arithmetic per query
+        lib.sa_debug_softmax_qb(qb)
+        try:
+            assert np.array_equal(host(A.softmax_core_flat(dev(q), dev(k), dev(v), B, heads)), fast)
+        finally:
+            lib.sa_debug_softmax_qb(4)
+    lib.sa_debug_softmax_generic(1)
+    try:
+        slow = host(A.softmax_core_flat(dev(q), dev(k), dev(v), B, heads))
+    finally:
+        lib.sa_debug_softmax_generic(0)
+    assert np.array_equal(fast, slow)
+    for b in range(B):
+        for h in range(heads):
+            sl = (slice(b * n, (b + 1) * n), slice(h * dk, (h + 1) * dk))
+            ref = ops.softmax_core(q[sl][None], k[sl][None], v[sl][None])[0]
+            assert rel_err(fast[sl], ref) < 2e-6
+
+
 def test_mlp_gelu_vs_oracle(golden):
     from paper_2306_06446_b200 import model as MD
     g = ops.rng(1)
