@@ -338,6 +338,135 @@ __global__ void __launch_bounds__(kRouteTok, 3) ln_route_kernel(
   }
 }
 
+// Wide rows (d = 32·PER, e.g. 160): one warp per row, lane l holds channels
+// l + 32i. The LayerNorm is layernorm_kernel's arithmetic (lane partials in
+// channel order, the same xor-shuffle reductions), so y is bit-identical to
+// sa_layernorm; each router's fp64 dot is a per-lane chain over the lane's
+// channels followed by a fixed xor tree (deterministic; the f32-rounded
+// logits match route_kernel's sequential fp64 chain unless the two fp64 sums
+// straddle an f32 rounding boundary). A CTA covers kRouteTok tokens (the block
+// counts feed the shared scan / partition kernels); each warp carries RB rows
+// at once so their loads are in flight together.
+template <int PER>
+__global__ void __launch_bounds__(1024, 1) ln_route_warp_kernel(
+    const float* __restrict__ x, const float* __restrict__ gain, const float* __restrict__ bias,
+    float* __restrict__ y, int64_t M, float eps, int nr, const float* __restrict__ wg0,
+    const float* __restrict__ wg1, const float* __restrict__ wg2, float tie_thresh,
+    int32_t* __restrict__ expert_of, float* __restrict__ gate, int32_t* __restrict__ block_cnt1) {
+  constexpr int D = 32 * PER;
+  constexpr int RB = 2;                      // rows per warp step (64-register cap)
+  constexpr int kWarps = 32;                 // 1024 threads: 8 rows per warp
+  constexpr int ROWS_PER_WARP = kRouteTok / kWarps;
+  __shared__ int wcnt[kMaxRouters][kWarps];
+  __shared__ double sw[kMaxRouters][2][D];   // [router][expert][channel]: lane reads are contiguous
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* wgs[kMaxRouters] = {wg0, wg1, wg2};
+  for (int r = 0; r < nr; ++r)
+    for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) sw[r][i & 1][i >> 1] = double(wgs[r][i]);
+  float g[PER], bb[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    g[i] = __ldg(gain + lane + 32 * i);
+    bb[i] = __ldg(bias + lane + 32 * i);
+  }
+  __syncthreads();
+  const int64_t row0 = int64_t(blockIdx.x) * kRouteTok + int64_t(warp) * ROWS_PER_WARP;
+  int cnt[kMaxRouters] = {0, 0, 0};
+#pragma unroll 1
+  for (int rb = 0; rb < ROWS_PER_WARP; rb += RB) {
+    // the RB rows' reductions are interleaved (independent shuffle chains)
+    float v[RB][PER];
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+      const int64_t row = row0 + rb + k;
+#pragma unroll
+      for (int i = 0; i < PER; ++i)
+        v[k][i] = row < M ? __ldg(x + row * D + lane + 32 * i) : 0.f;
+    }
+    float st[RB];
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) s += v[k][i];
+      st[k] = s;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int k = 0; k < RB; ++k) st[k] += __shfl_xor_sync(0xffffffffu, st[k], o);
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+      const float mean = st[k] / float(D);
+      float q = 0.f;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        v[k][i] = v[k][i] - mean;
+        q += v[k][i] * v[k][i];
+      }
+      st[k] = q;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int k = 0; k < RB; ++k) st[k] += __shfl_xor_sync(0xffffffffu, st[k], o);
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+      const int64_t row = row0 + rb + k;
+      const float var = st[k] / float(D);
+      const float inv = 1.0f / sqrtf(var + eps);
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        v[k][i] = v[k][i] * inv * g[i] + bb[i];
+        if (row < M) y[row * D + lane + 32 * i] = v[k][i];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kMaxRouters; ++r) {
+      if (r >= nr) break;   // uniform
+      double s0[RB], s1[RB];
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        s0[k] = 0.0;
+        s1[k] = 0.0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          s0[k] = fma(double(v[k][i]), sw[r][0][lane + 32 * i], s0[k]);
+          s1[k] = fma(double(v[k][i]), sw[r][1][lane + 32 * i], s1[k]);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+          s0[k] += __shfl_xor_sync(0xffffffffu, s0[k], o);
+          s1[k] += __shfl_xor_sync(0xffffffffu, s1[k], o);
+        }
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const int64_t row = row0 + rb + k;
+        float gt;
+        const int e = decide(float(s0[k]), float(s1[k]), tie_thresh, gt);
+        if (row < M) {
+          if (lane == 0) {
+            expert_of[size_t(r) * M + row] = e;
+            gate[size_t(r) * M + row] = gt;
+          }
+          cnt[r] += e;
+        }
+      }
+    }
+  }
+  if (lane == 0)
+    for (int r = 0; r < nr; ++r) wcnt[r][warp] = cnt[r];
+  __syncthreads();
+  if (threadIdx.x < nr) {
+    int c = 0;
+    for (int ww = 0; ww < kWarps; ++ww) c += wcnt[threadIdx.x][ww];
+    block_cnt1[size_t(threadIdx.x) * gridDim.x + blockIdx.x] = c;
+  }
+}
+
 }  // namespace sa
 
 using namespace sa;
@@ -351,8 +480,8 @@ extern "C" int sa_ln_route(const float* x, const float* gain, const float* bias,
                            const float* wg1, const float* wg2, float tie_thresh,
                            int32_t* expert_of, float* gate, int32_t* counts, int32_t* perm,
                            void* ws, size_t ws_bytes, void* stream) {
-  SA_REQUIRE(d == 32 || d == 64, SA_ERR_SHAPE, "sa_ln_route: d=%lld unsupported (32 or 64)",
-             (long long)d);
+  SA_REQUIRE(d > 0 && d % 32 == 0 && d <= 256, SA_ERR_SHAPE,
+             "sa_ln_route: d=%lld unsupported (a multiple of 32 up to 256)", (long long)d);
   SA_REQUIRE(nr >= 1 && nr <= kMaxRouters, SA_ERR_VALUE, "sa_ln_route: 1..3 routers, got %d", nr);
   SA_REQUIRE(M > 0 && M < (int64_t(1) << 31), SA_ERR_SHAPE, "sa_ln_route: bad token count");
   SA_REQUIRE(ws_bytes >= sa_ln_route_workspace(M, nr), SA_ERR_VALUE,
@@ -365,11 +494,22 @@ extern "C" int sa_ln_route(const float* x, const float* gain, const float* bias,
     const int smem = kRouteTok * (32 + 4) * 4;
     ln_route_kernel<32><<<nb, kRouteTok, smem, s>>>(x, gain, bias, y, M, eps, nr, wg0, wg1,
                                                     wg2, tie_thresh, expert_of, gate, block_cnt1);
-  } else {
+  } else if (d == 64) {
     const int smem = kRouteTok * (64 + 4) * 4;
     cudaFuncSetAttribute(ln_route_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     ln_route_kernel<64><<<nb, kRouteTok, smem, s>>>(x, gain, bias, y, M, eps, nr, wg0, wg1,
                                                     wg2, tie_thresh, expert_of, gate, block_cnt1);
+  } else {
+#define SA_LNRW(P)                                                                             \
+  case P:                                                                                      \
+    ln_route_warp_kernel<P><<<nb, 1024, 0, s>>>(x, gain, bias, y, M, eps, nr, wg0, wg1,      \
+                                                     wg2, tie_thresh, expert_of, gate,       \
+                                                     block_cnt1);                            \
+    break;
+    switch (d / 32) {
+      SA_LNRW(1) SA_LNRW(2) SA_LNRW(3) SA_LNRW(4) SA_LNRW(5) SA_LNRW(6) SA_LNRW(7) SA_LNRW(8)
+    }
+#undef SA_LNRW
   }
   route_scan_kernel<<<nr, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
   partition_kernel<<<dim3(nb, nr), kRouteTok, 0, s>>>(expert_of, block_off1, counts, M, perm);

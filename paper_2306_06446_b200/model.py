@@ -548,7 +548,7 @@ class Block:
         x = to_device(x)
         batch, n, d = x.shape
         x2 = x.reshape(batch * n, d)
-        fuse = FUSE_LN_ROUTE and d in (32, 64)
+        fuse = FUSE_LN_ROUTE and d % 32 == 0 and d <= 256
         qkv = [self.attn.proj[k] for k in ("q", "k", "v")]
         if self._fused_qkv_ok(d, n, qkv):
             h = self._fused_attention(x2, batch, n, d, qkv).reshape(batch, n, d)

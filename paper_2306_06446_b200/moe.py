@@ -170,7 +170,7 @@ def route_plan(x: torch.Tensor, w_g: torch.Tensor, want_logits=False):
 
 
 def ln_route_plans(x: torch.Tensor, gain, bias, w_gs, eps: float = 1e-5):
-    """LayerNorm of x fused with 1..3 routers on its output (d = 32 / 64).
+    """LayerNorm of x fused with 1..3 routers on its output (d = 32k <= 256).
     Returns (y, [DispatchPlan per router]); the plans are views of stacked
     device buffers, no host synchronisation."""
     M, d = x.shape

@@ -1,6 +1,8 @@
 #!/usr/bin/env python3
 """Per-call device time of one PVTv2-B0 forward (CUDA events around every
-C-ABI call), with the call's algorithmic bytes and achieved GB/s."""
+C-ABI call), with the call's algorithmic bytes and achieved GB/s. The forward
+is enqueued behind a device sleep, so the host is far ahead of the GPU and the
+events time the kernels, not host launch gaps."""
 import os
 import sys
 
@@ -18,6 +20,7 @@ m.forward(x)
 m.forward(x)
 torch.cuda.synchronize()
 t = OpTimer()
+torch.cuda._sleep(int(3e8))   # ~150 ms of device time: the whole forward is queued before it runs
 with t.record():
     m.forward(x)
 torch.cuda.synchronize()

@@ -386,7 +386,9 @@ def test_mlp_gelu_vs_oracle(golden):
         assert rel_err(y, ref) < 1e-5
 
 
-@pytest.mark.parametrize("M,d,nr", [(50_000, 32, 3), (777, 64, 1), (4096, 64, 3)])
+@pytest.mark.parametrize("M,d,nr", [(50_000, 32, 3), (777, 64, 1), (4096, 64, 3),
+                                    (50_176, 160, 3), (1001, 160, 1), (333, 256, 2),
+                                    (4097, 96, 3)])
 def test_ln_route_fused_vs_oracle(M, d, nr):
     """LayerNorm fused with 1..3 routers: y within fp32 tolerance of the
     oracle LN, winners / permutations bit-exact against the oracle router
@@ -406,6 +408,29 @@ def test_ln_route_fused_vs_oracle(M, d, nr):
         assert np.array_equal(plan.expert_of, e)
         assert np.array_equal(np.concatenate(plan.index_of), np.concatenate(idx))
         assert rel_err(plan.gate_of, gate) < 1e-6
+
+
+@pytest.mark.parametrize("M,d,nr", [(50_176, 160, 3), (999, 160, 1), (2000, 256, 2)])
+def test_ln_route_wide_matches_unfused(M, d, nr):
+    """The warp-per-row LN+router kernel (d = 32k > 64) writes exactly
+    sa_layernorm's y, and its winners / gates / partitions equal the unfused
+    router's on that y."""
+    from paper_2306_06446_b200 import moe as MOE
+    from paper_2306_06446_b200 import tensor as T
+    g = ops.rng(M * 7 + d)
+    x = (g.standard_normal((M, d)) * 1.7 - 0.2).astype(F32)
+    gain = (1 + 0.1 * g.standard_normal(d)).astype(F32)
+    bias = (0.05 * g.standard_normal(d)).astype(F32)
+    wgs = [(g.standard_normal((d, 2)) * 0.3).astype(F32) for _ in range(nr)]
+    y, plans = MOE.ln_route_plans(dev(x), dev(gain), dev(bias), [dev(w) for w in wgs])
+    y_ref, _ = T.layernorm(dev(x), dev(gain), dev(bias))
+    assert np.array_equal(host(y), host(y_ref))
+    for w, plan in zip(wgs, plans):
+        ref, _ = MOE.route_plan(y_ref, dev(w))
+        assert np.array_equal(plan.expert_of, ref.expert_of)
+        assert np.array_equal(plan.gate_of, ref.gate_of)
+        for a, b in zip(plan.index_of, ref.index_of):
+            assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("B,n,d,h,with_dw", [(3, 3136, 32, 1, True), (2, 784, 64, 2, True),
