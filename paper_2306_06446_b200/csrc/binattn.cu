@@ -461,7 +461,14 @@ static int check_attn_shapes(const char* who, int64_t B, int64_t n, int64_t d, i
 int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq, const float* gk,
                          const float* v, const float* dw, float* out, int64_t B, int64_t n,
                          int64_t d, int64_t heads, float eps, cudaStream_t s);
-static int g_attn_mode = 0;   // 0: fused single-pass kernel when the shape allows; 1: multi-kernel
+size_t binattn_split_ws_bytes(int64_t B, int64_t heads);
+int binattn_split_launch(const uint32_t* cq, const uint32_t* ck, const float* gq, const float* gk,
+                         const float* v, const float* dw, float* out, int64_t B, int64_t n,
+                         int64_t d, int64_t heads, float eps, void* ws, size_t ws_bytes,
+                         cudaStream_t s);
+// 0: fused single-pass kernel when the shape allows; 1: multi-kernel; 2: split
+// two-kernel form of the fused kernel (bit-identical)
+static int g_attn_mode = 0;
 
 }  // namespace sa
 
@@ -479,6 +486,7 @@ extern "C" size_t sa_linear_binary_attn_workspace(int64_t B, int64_t n, int64_t 
   bytes += size_t(BH * nsplit * dk) * 4;       // partial counts
   bytes += size_t(BH * dk * dk) * 4;           // kv
   bytes += size_t(BH * dk) * 4;                // cnt
+  if (dk == 32 && binattn_split_ws_bytes(B, heads) > bytes) bytes = binattn_split_ws_bytes(B, heads);
   return bytes + 256;
 }
 
@@ -492,6 +500,11 @@ extern "C" int sa_linear_binary_attn(const uint32_t* codes_q, const uint32_t* co
   SA_REQUIRE(ws_bytes >= sa_linear_binary_attn_workspace(B, n, d, heads), SA_ERR_VALUE,
              "sa_linear_binary_attn: workspace too small");
   const int64_t dk = d / heads;
+  if (dk == 32 && g_attn_mode == 2) {
+    st = binattn_split_launch(codes_q, codes_k, gamma_q, gamma_k, v, dw, out, B, n, d, heads, eps,
+                              ws, ws_bytes, as_stream(stream));
+    if (st != SA_ERR_VALUE) return st;
+  }
   if (dk == 32 && g_attn_mode == 0) {
     st = binattn_fused_launch(codes_q, codes_k, gamma_q, gamma_k, v, dw, out, B, n, d, heads, eps,
                               as_stream(stream));

@@ -43,6 +43,7 @@ constexpr int kThreads = 256;
 constexpr int kStreams = 16;        // pass-1 token streams (16 threads each)
 constexpr int kMaxCluster = 8;
 constexpr int kSeg = 6;             // pass-2 tokens per row segment (multiple of 3)
+constexpr int kMaxBandRows = 32;    // split out kernel: static mbarrier array bound
 
 struct Params {
   const uint32_t* cq;
@@ -372,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
         row[3] += x[r][3];
       }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) row[i] *= g;
+    for (int i = 0; i < 4; ++i) row[i] = __fmul_rn(row[i], g);   // not contracted into the table sums
     float val[16];
     val[0] = 0.f;
     val[1] = row[0];
@@ -477,7 +478,8 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
                        (Tb[512 + ((q >> 16) & 255)] + Tb[768 + (q >> 24)]);
       const float sc = gq * rcp_approx(fmaf(gg, D_, p.eps));
       const float2 x01 = unpack2(a01), x23 = unpack2(a23);
-      float4 o = make_float4(x01.x * sc, x01.y * sc, x23.x * sc, x23.y * sc);
+      float4 o = make_float4(__fmul_rn(x01.x, sc), __fmul_rn(x01.y, sc), __fmul_rn(x23.x, sc),
+                             __fmul_rn(x23.y, sc));
       if (has_dw) {
         unsigned long long s01 = 0ull, s23 = 0ull;
 #pragma unroll
@@ -490,10 +492,489 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
           fma2(s23, wn.r[R].y, tapu[R * 3 + 2].y);
         }
         const float2 y01 = unpack2(s01), y23 = unpack2(s23);
-        o.x += y01.x;
-        o.y += y01.y;
-        o.z += y23.x;
-        o.w += y23.y;
+        o.x = __fadd_rn(o.x, y01.x);
+        o.y = __fadd_rn(o.y, y01.y);
+        o.z = __fadd_rn(o.z, y23.x);
+        o.w = __fadd_rn(o.w, y23.y);
+      }
+      *reinterpret_cast<float4*>(ob + size_t(t) * ld) = o;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Split form (two kernels, no cluster): the same band geometry and the same
+// arithmetic in the same order as binattn_fused_kernel, so the output is
+// bit-identical; the band partials travel through global memory (L2) instead
+// of distributed shared memory. Without the cluster barriers each kernel runs
+// at its own occupancy: pass 1 is FP32-pipe work over a shared-memory V band,
+// pass 2 streams outputs with the DWConv window read through L1.
+
+// shared-memory layout of the pass-1 kernel (byte offsets): two band buffers
+// (V rows, K codes) so the next band's copies overlap this band's FMA work
+struct KvSmem {
+  uint32_t v[2], ck[2], scr, mt, bar, total;
+};
+__host__ __device__ inline KvSmem kv_smem_layout(int side, int band_rows, int nbuf) {
+  KvSmem s;
+  uint32_t o = 0;
+  for (int i = 0; i < 2; ++i) {
+    s.v[i] = o;                                          // band rows, no halo
+    if (i < nbuf) o += uint32_t(band_rows) * side * DK * 4;
+  }
+  for (int i = 0; i < 2; ++i) {
+    s.ck[i] = o;
+    if (i < nbuf) o += (uint32_t(band_rows) * side * 4 + 15) & ~15u;
+  }
+  s.scr = o;                                             // [4][DK][DK] + [kStreams][DK]
+  o += 4 * DK * DK * 4 + kStreams * DK * 4;
+  s.mt = o;                                              // [256][8] 0/1 masks
+  o += 256 * 8 * 4;
+  s.bar = o;                                             // [2][band_rows] mbarriers
+  o += 2 * band_rows * 8;
+  s.total = o;
+  return s;
+}
+
+// pass 1, persistent: CTA c takes work items c, c + G, ... (item = (image,
+// head, band)); per item the band partial of K^T V (un-scaled) and of the
+// code-bit counts → part[item][DK*DK], cntp[item][DK]
+template <int SIDE>
+__global__ void __launch_bounds__(kThreads, 2) binattn_kv_kernel(Params p, float* __restrict__ part_g,
+                                                                 int* __restrict__ cnt_g, int CL,
+                                                                 int items) {
+  constexpr uint32_t ROWB = uint32_t(SIDE) * DK * 4;
+  constexpr uint32_t TOKB = uint32_t(DK) * 4;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int H = p.heads, ld = p.ld, n = p.n, BR = p.band_rows;
+  // one item per CTA (grid = items): a single band buffer; persistent: two
+  const KvSmem L = kv_smem_layout(SIDE, BR, int(gridDim.x) >= items ? 1 : 2);
+  float* tab = reinterpret_cast<float*>(smem + L.scr);
+  float* mt = reinterpret_cast<float*>(smem + L.mt);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool bulk = ld == DK;   // contiguous rows: bulk copies; head slices: cp.async
+  struct Item {
+    int b, hz, rank, r0, r1, t_lo, nt;
+  };
+  auto geom = [&](int it) {
+    Item I;
+    I.rank = it % CL;
+    const int bh = it / CL;
+    I.b = bh / H;
+    I.hz = bh - I.b * H;
+    I.r0 = I.rank * BR;
+    I.r1 = min(p.rows_total, I.r0 + BR);
+    I.t_lo = min(n, I.r0 * SIDE);
+    I.nt = min(n, I.r1 * SIDE) - I.t_lo;
+    return I;
+  };
+  // V of item I into buffer `buf` (rows arrive on bar[buf][R] in bulk mode)
+  auto issue = [&](const Item& I, int buf) {
+    const float* vb = p.v + size_t(I.b) * n * ld + I.hz * DK;
+    uint8_t* Vb = smem + L.v[buf];
+    if (bulk) {
+      if (tid == 0) {
+        for (int R = 0; R < BR; ++R) {
+          const int rr = I.r0 + R;
+          const int ntok = rr < p.rows_total ? max(0, min(SIDE, n - rr * SIDE)) : 0;
+          const uint32_t bytes = uint32_t(ntok) * TOKB;
+          uint64_t* br = bar + buf * BR + R;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(br)),
+                       "r"(bytes)
+                       : "memory");
+          if (bytes == 0) continue;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  su32(Vb + R * ROWB)),
+              "l"(vb + size_t(rr) * SIDE * DK), "r"(bytes), "r"(su32(br))
+              : "memory");
+        }
+      }
+    } else {
+      for (int i = tid; i < I.nt * (DK / 4); i += kThreads) {
+        const int t = i / (DK / 4), c4 = i % (DK / 4);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(Vb) + uint32_t(t) * TOKB + c4 * 16),
+                     "l"(vb + size_t(I.t_lo + t) * ld + c4 * 4)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  };
+  constexpr int kCodesPerThread = (kMaxCluster * 64 + kThreads - 1) / kThreads;   // unused bound
+  (void)kCodesPerThread;
+  if (tid == 0) {
+    for (int i = 0; i < 2 * BR; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + i)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  for (int i = tid; i < 256 * 8; i += kThreads) mt[i] = ((i >> 3) >> (i & 7)) & 1 ? 1.0f : 0.0f;
+  int it = blockIdx.x;
+  if (it < items) {
+    const Item I0 = geom(it);
+    issue(I0, 0);
+    uint32_t* ck0 = reinterpret_cast<uint32_t*>(smem + L.ck[0]);
+    for (int i = tid; i < I0.nt; i += kThreads)
+      ck0[i] = __ldg(p.ck + (size_t(I0.b) * H + I0.hz) * n + I0.t_lo + i);
+  }
+  __syncthreads();
+  uint32_t use_par[2] = {0u, 0u};
+  const int s_id = tid >> 4, rg = (tid >> 2) & 3, cgp = tid & 3;
+  const uint8_t* mtb = reinterpret_cast<const uint8_t*>(mt);
+  for (int k = 0; it < items; it += gridDim.x, ++k) {
+    const int buf = k & 1;
+    const Item I = geom(it);
+    const int it_n = it + gridDim.x;
+    Item In;
+    uint32_t ckn[2] = {0u, 0u};   // next item's codes, held in registers until this band is done
+    if (it_n < items) {
+      In = geom(it_n);
+      issue(In, buf ^ 1);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = tid + u * kThreads;
+        if (i < In.nt) ckn[u] = __ldg(p.ck + (size_t(In.b) * H + In.hz) * n + In.t_lo + i);
+      }
+    }
+    if (!bulk) {   // this band's cp.async group (the next band's may stay in flight)
+      if (it_n < items) asm volatile("cp.async.wait_group 1;" ::: "memory");
+      else asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncthreads();
+    }
+    const uint8_t* Vb = smem + L.v[buf];
+    const uint32_t* cks = reinterpret_cast<const uint32_t*>(smem + L.ck[buf]);
+    auto wait_row = [&](int R) {
+      asm volatile(
+          "{\n\t.reg .pred q;\n\tW_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n\t"
+          "@!q bra W_%=;\n\t}" ::"r"(su32(bar + buf * BR + R)),
+          "r"(use_par[buf])
+          : "memory");
+    };
+    unsigned long long acc[8][4], cacc[4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0ull;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cacc[j] = 0ull;
+    const uint8_t* vp = Vb + (cgp * 8) * 4 + s_id * TOKB;
+    const uint32_t* kp = cks + s_id;
+    int next_row = 0, R_w = 0;
+#pragma unroll 2
+    for (int t = s_id; t < I.nt; t += kStreams) {
+      if (bulk) {
+        while (t >= next_row) {
+          wait_row(R_w);
+          ++R_w;
+          next_row += SIDE;
+        }
+      }
+      const ulonglong2 va = lds128(vp);
+      const ulonglong2 vc = lds128(vp + 16);
+      const uint8_t* mrow = mtb + (((*kp) >> (rg * 8)) & 0xffu) * 32;
+      const ulonglong2 mp0 = lds128(mrow);
+      const ulonglong2 mp1 = lds128(mrow + 16);
+      const float2 m01 = unpack2(mp0.x), m23 = unpack2(mp0.y);
+      const float2 m45 = unpack2(mp1.x), m67 = unpack2(mp1.y);
+      const float m[8] = {m01.x, m01.y, m23.x, m23.y, m45.x, m45.y, m67.x, m67.y};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        add2_mask(acc[i][0], va.x, m[i]);
+        add2_mask(acc[i][1], va.y, m[i]);
+        add2_mask(acc[i][2], vc.x, m[i]);
+        add2_mask(acc[i][3], vc.y, m[i]);
+      }
+      add2(cacc[0], mp0.x);
+      add2(cacc[1], mp0.y);
+      add2(cacc[2], mp1.x);
+      add2(cacc[3], mp1.y);
+      vp += kStreams * TOKB;
+      kp += kStreams;
+    }
+    if (bulk) {   // consume every row's phase (streams with few tokens skip rows)
+      while (R_w < BR) {
+        wait_row(R_w);
+        ++R_w;
+      }
+    }
+    use_par[buf] ^= 1u;
+    // same fixed-order combine as binattn_fused_kernel
+    float2 cmb[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 a = unpack2(acc[i][j]);
+        cmb[i][j] = make_float2(a.x + __shfl_down_sync(0xffffffffu, a.x, 16),
+                                a.y + __shfl_down_sync(0xffffffffu, a.y, 16));
+      }
+    float* scr = tab + (warp & 3) * DK * DK + rg * 8 * DK + cgp * 8;
+    if (warp >= 4 && lane < 16) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) *reinterpret_cast<float2*>(scr + i * DK + 2 * j) = cmb[i][j];
+    }
+    if (cgp == 0) {
+      float* cs = tab + 4 * DK * DK + s_id * DK + rg * 8;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) *reinterpret_cast<float2*>(cs + 2 * j) = unpack2(cacc[j]);
+    }
+    __syncthreads();
+    if (warp < 4 && lane < 16) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float2* q = reinterpret_cast<float2*>(scr + i * DK + 2 * j);
+          const float2 o = *q;
+          *q = make_float2(cmb[i][j].x + o.x, cmb[i][j].y + o.y);
+        }
+    }
+    __syncthreads();
+    {
+      const int e = tid * 4;
+      float4 s4 = *reinterpret_cast<const float4*>(tab + e);
+#pragma unroll
+      for (int w4 = 1; w4 < 4; ++w4) {
+        const float4 q4 = *reinterpret_cast<const float4*>(tab + w4 * DK * DK + e);
+        s4.x += q4.x;
+        s4.y += q4.y;
+        s4.z += q4.z;
+        s4.w += q4.w;
+      }
+      *reinterpret_cast<float4*>(part_g + size_t(it) * DK * DK + e) = s4;
+    }
+    if (tid < DK) {
+      const float* cs = tab + 4 * DK * DK + tid;
+      float c = 0.f;
+#pragma unroll
+      for (int st = 0; st < kStreams; ++st) c += cs[st * DK];
+      cnt_g[size_t(it) * DK + tid] = int(c);
+    }
+    if (it_n < items) {   // next band's codes into the other buffer
+      uint32_t* ckb = reinterpret_cast<uint32_t*>(smem + L.ck[buf ^ 1]);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = tid + u * kThreads;
+        if (i < In.nt) ckb[i] = ckn[u];
+      }
+      for (int i = tid + 2 * kThreads; i < In.nt; i += kThreads)
+        ckb[i] = __ldg(p.ck + (size_t(In.b) * H + In.hz) * n + In.t_lo + i);
+    }
+    __syncthreads();   // scratch, this buffer and the codes may be reused
+  }
+}
+
+// pass 2: rank-order sum of the CL band partials, nibble / byte tables, and the
+// output loop of binattn_fused_kernel with the DWConv window read from global
+template <int SIDE>
+__global__ void __launch_bounds__(kThreads, 2) binattn_out_kernel(Params p, const float* __restrict__ part_g,
+                                                                  const int* __restrict__ cnt_g, int CL) {
+  constexpr int NCG = DK / 4;
+  constexpr int SLOTS = kThreads / NCG;
+  constexpr int SEGS = (SIDE + kSeg - 1) / kSeg;
+  constexpr uint32_t ROWB = uint32_t(SIDE) * DK * 4;
+  constexpr uint32_t TOKB = uint32_t(DK) * 4;
+  __shared__ __align__(16) float tab[(DK / 4) * 16 * DK];   // 16 KB nibble tables
+  __shared__ __align__(16) float tcb[4 * 256];
+  __shared__ int cntw[DK];
+  __shared__ __align__(8) uint64_t bar[kMaxBandRows + 2];
+  extern __shared__ __align__(16) uint8_t dsm[];            // V band + halo rows, then q codes
+  const int rank = blockIdx.x, b = blockIdx.y, hz = blockIdx.z, H = p.heads;
+  const int ld = p.ld, n = p.n, BR = p.band_rows;
+  const int tid = threadIdx.x;
+  const int r0 = rank * BR;
+  const int r1 = min(p.rows_total, r0 + BR);
+  const int t_lo = min(n, r0 * SIDE), t_hi = min(n, r1 * SIDE);
+  const int nt = t_hi - t_lo;
+  const size_t slot0 = (size_t(b) * H + hz) * CL;
+  uint8_t* Vb = dsm;
+  uint32_t* cqs = reinterpret_cast<uint32_t*>(dsm + size_t(BR + 2) * ROWB);
+  {
+    // V rows r0-1 .. r0+BR (smem row R = grid row r0-1+R), as binattn_fused_kernel
+    const float* vb = p.v + size_t(b) * n * ld + hz * DK;
+    if (tid == 0) {
+      for (int R = 0; R < BR + 2; ++R)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + R)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int i = 0; i < BR + 2; ++i) {
+        const int R = i < BR ? i + 1 : (i == BR ? 0 : BR + 1);
+        const int rr = r0 - 1 + R;
+        const int ntok = (rr >= 0 && rr < p.rows_total) ? max(0, min(SIDE, n - rr * SIDE)) : 0;
+        const uint32_t bytes = ld == DK ? uint32_t(ntok) * TOKB : 0u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar + R)),
+                     "r"(bytes)
+                     : "memory");
+        if (bytes == 0) continue;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                su32(Vb + R * ROWB)),
+            "l"(vb + size_t(rr) * SIDE * DK), "r"(bytes), "r"(su32(bar + R))
+            : "memory");
+      }
+    }
+    if (ld != DK) {
+      const int tok_lo = max(0, (r0 - 1) * SIDE);
+      const int tok_hi = min(n, (r0 + BR + 1) * SIDE);
+      const int smem_tok0 = (r0 - 1) * SIDE;
+      for (int i = tid; i < (tok_hi - tok_lo) * (DK / 4); i += kThreads) {
+        const int t = tok_lo + i / (DK / 4), c4 = i % (DK / 4);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(Vb) + uint32_t(t - smem_tok0) * TOKB + c4 * 16),
+                     "l"(vb + size_t(t) * ld + c4 * 4)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int R = 0; R < BR + 2; ++R) {   // zero the cells no copy fills
+      const int rr = r0 - 1 + R;
+      const int ntok = (rr >= 0 && rr < p.rows_total) ? max(0, min(SIDE, n - rr * SIDE)) : 0;
+      float4* z = reinterpret_cast<float4*>(Vb + R * ROWB + ntok * TOKB);
+      const int nz = (SIDE - ntok) * DK / 4;
+      for (int i = tid; i < nz; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  for (int i = tid; i < nt; i += kThreads) cqs[i] = __ldg(p.cq + (size_t(b) * H + hz) * n + t_lo + i);
+  {
+    const float g = __ldg(p.gk + b * H + hz);
+    const int grp = tid / DK, c = tid % DK;
+    float x[kMaxCluster][4];
+#pragma unroll
+    for (int r = 0; r < kMaxCluster; ++r) {
+      if (r < CL) {
+        const float* pr = part_g + (slot0 + r) * DK * DK + 4 * grp * DK + c;
+        x[r][0] = __ldg(pr);
+        x[r][1] = __ldg(pr + DK);
+        x[r][2] = __ldg(pr + 2 * DK);
+        x[r][3] = __ldg(pr + 3 * DK);
+      }
+    }
+    float row[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int r = 0; r < kMaxCluster; ++r)
+      if (r < CL) {
+        row[0] += x[r][0];
+        row[1] += x[r][1];
+        row[2] += x[r][2];
+        row[3] += x[r][3];
+      }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) row[i] = __fmul_rn(row[i], g);   // not contracted into the table sums
+    float val[16];
+    val[0] = 0.f;
+    val[1] = row[0];
+    val[2] = row[1];
+    val[4] = row[2];
+    val[8] = row[3];
+#pragma unroll
+    for (int m = 3; m < 16; ++m)
+      if (m & (m - 1)) val[m] = val[m & (m - 1)] + val[m & -m];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) tab[(grp * 16 + m) * DK + c] = val[m];
+    if (tid < DK) {
+      int s = 0;
+      for (int r = 0; r < CL; ++r) s += __ldg(cnt_g + (slot0 + r) * DK + tid);
+      cntw[tid] = s;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < 4 * 256; e += kThreads) {
+    const int g8 = e >> 8, m = e & 255;
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if ((m >> i) & 1) s += cntw[8 * g8 + i];
+    tcb[e] = float(s);
+  }
+  __syncthreads();
+  const int cgi = tid % NCG, slot = tid / NCG;
+  const int ch = cgi * 4;
+  const float gq = __ldg(p.gq + b * H + hz), gk = __ldg(p.gk + b * H + hz);
+  const float gg = gq * gk;
+  ulonglong2 tapu[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q)
+    tapu[q] = p.dw ? __ldg(reinterpret_cast<const ulonglong2*>(p.dw + q * ld + hz * DK + ch))
+                   : make_ulonglong2(0ull, 0ull);
+  const bool has_dw = p.dw != nullptr;
+  const uint8_t* T = reinterpret_cast<const uint8_t*>(tab + ch);
+  float* ob = p.out + size_t(b) * n * ld + hz * DK + ch;
+  const ulonglong2 z2 = make_ulonglong2(0ull, 0ull);
+  const int units = (r1 - r0) * SEGS;
+  if (ld != DK) asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();   // zero fill and strided copies visible
+  for (int R = 0; R < BR + 2; ++R) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 q, [%0], 0;\n\t"
+        "@!q bra W_%=;\n\t}" ::"r"(su32(bar + R))
+        : "memory");
+  }
+  for (int u = slot; u < units; u += SLOTS) {
+    const int rl = u / SEGS, sg = u - rl * SEGS;
+    const int r = r0 + rl;
+    const int c0 = sg * kSeg;
+    const int c1 = min(SIDE, c0 + kSeg);
+    const uint8_t* colb = Vb + rl * ROWB + ch * 4;
+    auto load_col = [&](Win& w, int c) {
+      if (c >= 0 && c < SIDE) {
+        const uint8_t* q = colb + c * TOKB;
+        w.r[0] = lds128(q);
+        w.r[1] = lds128(q + ROWB);
+        w.r[2] = lds128(q + 2 * ROWB);
+      } else {
+        w.r[0] = z2;
+        w.r[1] = z2;
+        w.r[2] = z2;
+      }
+    };
+    Win wr[3];
+    load_col(wr[0], c0 - 1);
+    load_col(wr[1], c0);
+    const int tb = r * SIDE + c0;
+    const int kmax = min(c1 - c0, n - tb);
+#pragma unroll
+    for (int k = 0; k < kSeg; ++k) {
+      if (k >= kmax) break;
+      const int c = c0 + k;
+      Win& wl = wr[k % 3];
+      Win& wc = wr[(k + 1) % 3];
+      Win& wn = wr[(k + 2) % 3];
+      load_col(wn, c + 1);
+      const int t = tb + k;
+      const uint32_t q = cqs[t - t_lo];
+      unsigned long long a01 = 0ull, a23 = 0ull;
+#pragma unroll
+      for (int g = 0; g < DK / 4; ++g) {
+        const uint32_t off = (g >= 2 ? (q >> (4 * g - 7)) : (q << (7 - 4 * g))) & 0x780u;
+        const ulonglong2 tv = lds128(T + g * 16 * DK * 4 + off);
+        add2(a01, tv.x);
+        add2(a23, tv.y);
+      }
+      const float D_ = (tcb[q & 255] + tcb[256 + ((q >> 8) & 255)]) +
+                       (tcb[512 + ((q >> 16) & 255)] + tcb[768 + (q >> 24)]);
+      const float sc = gq * rcp_approx(fmaf(gg, D_, p.eps));
+      const float2 x01 = unpack2(a01), x23 = unpack2(a23);
+      float4 o = make_float4(__fmul_rn(x01.x, sc), __fmul_rn(x01.y, sc), __fmul_rn(x23.x, sc),
+                             __fmul_rn(x23.y, sc));
+      if (has_dw) {
+        unsigned long long s01 = 0ull, s23 = 0ull;
+#pragma unroll
+        for (int R = 0; R < 3; ++R) {
+          fma2(s01, wl.r[R].x, tapu[R * 3 + 0].x);
+          fma2(s23, wl.r[R].y, tapu[R * 3 + 0].y);
+          fma2(s01, wc.r[R].x, tapu[R * 3 + 1].x);
+          fma2(s23, wc.r[R].y, tapu[R * 3 + 1].y);
+          fma2(s01, wn.r[R].x, tapu[R * 3 + 2].x);
+          fma2(s23, wn.r[R].y, tapu[R * 3 + 2].y);
+        }
+        const float2 y01 = unpack2(s01), y23 = unpack2(s23);
+        o.x = __fadd_rn(o.x, y01.x);
+        o.y = __fadd_rn(o.y, y01.y);
+        o.z = __fadd_rn(o.z, y23.x);
+        o.w = __fadd_rn(o.w, y23.y);
       }
       *reinterpret_cast<float4*>(ob + size_t(t) * ld) = o;
     }
@@ -556,6 +1037,70 @@ int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
     return SA_ERR_CUDA;
   }
   count_launch(1);
+  return SA_OK;
+}
+
+// Split launch (see binattn_kv_kernel / binattn_out_kernel): same geometry as
+// binattn_fused_launch; the band partials go to `ws` ([B*H][CL][DK*DK] floats,
+// then [B*H][CL][DK] ints). Returns SA_ERR_VALUE outside the envelope.
+static int g_kv_persistent = 0;
+extern "C" void sa_debug_attn_kv_persistent(int on) { g_kv_persistent = on; }
+
+size_t binattn_split_ws_bytes(int64_t B, int64_t heads) {
+  using namespace baf;
+  return size_t(B * heads * kMaxCluster) * (DK * DK + DK) * 4;
+}
+
+int binattn_split_launch(const uint32_t* cq, const uint32_t* ck, const float* gq, const float* gk,
+                         const float* v, const float* dw, float* out, int64_t B, int64_t n,
+                         int64_t d, int64_t heads, float eps, void* ws, size_t ws_bytes,
+                         cudaStream_t s) {
+  using namespace baf;
+  if (d != heads * DK || d % 4 != 0) return SA_ERR_VALUE;
+  if (ws_bytes < binattn_split_ws_bytes(B, heads)) return SA_ERR_VALUE;
+  int side = 0;
+  while (int64_t(side) * side < n) ++side;
+  const int rows_total = int((n + side - 1) / side);
+  int cl = int((n + 399) / 400);
+  cl = cl < 1 ? 1 : (cl > kMaxCluster ? kMaxCluster : cl);
+  cl = cl > rows_total ? rows_total : cl;
+  const int br = (rows_total + cl - 1) / cl;
+  cl = (rows_total + br - 1) / br;
+  const int items = int(B * heads * cl);
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // one band per CTA (two CTAs per SM) measured faster than a persistent,
+  // double-buffered grid of one CTA per SM (8 warps cannot hide the per-token
+  // shared-memory chain); g_kv_persistent selects the latter for A/B runs
+  const int g1 = g_kv_persistent ? (items < sms ? items : sms) : items;
+  const KvSmem L = kv_smem_layout(side, br, g1 >= items ? 1 : 2);
+  if (L.total > 220 * 1024) return SA_ERR_VALUE;
+  Params p{cq, ck, gq, gk, v, dw, out, int(n), DK, int(heads), side, rows_total, br, eps, int(d)};
+  float* part = static_cast<float*>(ws);
+  int* cntp = reinterpret_cast<int*>(part + size_t(B * heads * cl) * DK * DK);
+  if (br > kMaxBandRows) return SA_ERR_VALUE;
+  const size_t out_smem = size_t(br + 2) * side * DK * 4 + size_t(br) * side * 4;
+  void (*k1)(Params, float*, int*, int, int) = nullptr;
+  void (*k2)(Params, const float*, const int*, int) = nullptr;
+  switch (side) {
+#define SA_SPLIT_CASE(S)                   \
+  case S:                                  \
+    k1 = binattn_kv_kernel<S>;             \
+    k2 = binattn_out_kernel<S>;            \
+    break;
+    SA_SPLIT_CASE(56) SA_SPLIT_CASE(28) SA_SPLIT_CASE(14) SA_SPLIT_CASE(7)
+    SA_SPLIT_CASE(15) SA_SPLIT_CASE(18) SA_SPLIT_CASE(3)
+#undef SA_SPLIT_CASE
+    default: return SA_ERR_VALUE;
+  }
+  cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total));
+  cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(out_smem));
+  const dim3 grid{unsigned(cl), unsigned(B), unsigned(heads)};
+  k1<<<g1, kThreads, L.total, s>>>(p, part, cntp, cl, items);
+  k2<<<grid, kThreads, out_smem, s>>>(p, part, cntp, cl);
+  count_launch(2);
+  SA_LAUNCH_CHECK("sa_linear_binary_attn (split)");
   return SA_OK;
 }
 

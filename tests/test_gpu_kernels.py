@@ -456,6 +456,12 @@ def test_fused_binary_attention_matches_multikernel(B, n, d, h, with_dw):
         lib.sa_debug_attn_mode(0)
     fused = host(A.binary_core(*args))
     assert rel_err(fused, legacy) < 2e-6
+    try:   # the split two-kernel form computes the fused kernel's arithmetic
+        lib.sa_debug_attn_mode(2)
+        split = host(A.binary_core(*args))
+    finally:
+        lib.sa_debug_attn_mode(0)
+    assert np.array_equal(split, fused)
     fold = lambda t: ops.heads_split(t.reshape(B, n, d), h).reshape(B * h, n, d // h)  # noqa
     qf, _ = ops.binary_features(fold(q))
     kf, _ = ops.binary_features(fold(kk))
