@@ -393,6 +393,16 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
       const int ob = int(j & 1);
       const uint32_t oph = par(j >> 1);
       ++j;
+      // the draining group's row metadata (dependent perm → gate loads) is
+      // issued before the tile's GELU chunks so its latency overlaps them
+      const int64_t r = r0 + rl;
+      const bool r_ok = r < r1;
+      int64_t orow = -1;
+      float gt = 1.f;
+      if (ob == g && r_ok) {
+        orow = p.perm ? int64_t(__ldg(p.perm + r)) : r;
+        if (p.gate) gt = __ldg(p.gate + orow);
+      }
       for (int c = 0; c < nchunk; ++c) {
         const int64_t q = q0 + c;
         if (int(q & 1) != g) continue;
@@ -437,22 +447,32 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
       q0 += nchunk;
       if (ob != g) continue;   // the other group drains this tile's acc2
       // ---- final epilogue: acc2 (128 x D) → × gate → + residual → scatter ----
-      const int64_t r = r0 + rl;
-      const bool r_ok = r < r1;
-      int64_t orow = -1;
-      float gt = 1.f;
-      if (r_ok) {
-        orow = p.perm ? int64_t(__ldg(p.perm + r)) : r;
-        if (p.gate) gt = __ldg(p.gate + orow);
-      }
       int64_t* rt = rowtab + g * 128;
       asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");   // previous table consumed
       rt[rl] = orow;
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");   // table published
+      // the lane's 4 output rows (it * 8 + lane / 4) and 4 channels per 16-wide
+      // column block; residual rows are prefetched one block ahead, the first
+      // block before waiting for the accumulator
+      const int c4 = (lane & 3) * 4;
+      int64_t orow_l[4];
+#pragma unroll
+      for (int it = 0; it < 4; ++it) orow_l[it] = rt[quad * 32 + it * 8 + (lane >> 2)];
+      float4 res[2][4];
+      auto load_res = [&](int cb, float4 (&dst)[4]) {
+#pragma unroll
+        for (int it = 0; it < 4; ++it)
+          dst[it] = (p.residual && orow_l[it] >= 0)
+                        ? __ldg(reinterpret_cast<const float4*>(p.residual + orow_l[it] * D + cb + c4))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      };
+      load_res(0, res[0]);
       PWAIT(P_OF, &o_full[ob], oph);
       tc_fence_after();
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
-#pragma unroll 1
+#pragma unroll
       for (int cb = 0; cb < D; cb += 16) {
+        const int rb = (cb >> 4) & 1;
+        if (cb + 16 < D) load_res(cb + 16, res[rb ^ 1]);
         float v[16];
         tmem_ld16(tmem + (uint32_t(quad * 32) << 16) + L::T_ACC2 + uint32_t(ob * D + cb), v);
 #pragma unroll
@@ -460,16 +480,15 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
           *reinterpret_cast<float4*>(xb + lane * kXPitch + t) =
               make_float4(v[t] * gt, v[t + 1] * gt, v[t + 2] * gt, v[t + 3] * gt);
         __syncwarp();
-        const int c4 = (lane & 3) * 4;
         const int n = cb + c4;
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
           const int ri = it * 8 + (lane >> 2);
-          const int64_t orow_i = rt[quad * 32 + ri];
+          const int64_t orow_i = orow_l[it];
           if (orow_i < 0) continue;
           float4 o = *reinterpret_cast<const float4*>(xb + ri * kXPitch + c4);
           if (p.residual) {
-            const float4 rr = __ldg(reinterpret_cast<const float4*>(p.residual + orow_i * D + n));
+            const float4 rr = res[rb][it];
             o = make_float4(rr.x + o.x, rr.y + o.y, rr.z + o.z, rr.w + o.w);
           }
           *reinterpret_cast<float4*>(p.y + orow_i * D + n) = o;
