@@ -75,7 +75,7 @@ struct TcParams {
   int rb;      // 1: every weight tile resident in shared memory for the whole kernel
   uint32_t rb_bytes[2];   // resident bytes per expert (packed planes, [n_tile][kc][plane])
   int dbg;     // debug role isolation (0 in production): 1 no A loads, 2 no C stores, 4 no MMAs
-  int tma_c;   // 1: C rows are the tile rows (no scatter / residual / position): TMA-store epilogue
+  int tma_c;   // 1: C rows are the tile rows (no scatter / position): TMA-store epilogue
   int kq_min;  // K stages alternate between producer groups when kchunks > kq_min (else whole tiles)
 };
 
@@ -157,7 +157,9 @@ __host__ __device__ inline size_t tc_fixed_smem() {
          + (2 * 8 + 4 + 2 * 8) * 8 + 16;            // barriers (+ staging) + TMEM slot
 }
 
-template <int BN, int AM>
+// RES: the TMA-store epilogue adds a residual (plain rows only); a separate
+// instantiation so kernels without one carry no residual code (register cap 96)
+template <int BN, int AM, bool RES = false>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
                                                               const __grid_constant__ CUtensorMap tmC) {
   // direct epilogue (thread = row, no shared-memory transpose) for wide tiles
@@ -543,6 +545,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
       // every warp of the group once they all reach this barrier
       asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
       orow_t[rl] = r_ok ? (p.pos ? (orow | (pos_idx << 40)) : orow) : int64_t(-1);
+      // the residual row (one contiguous N-float run) is pulled into L2 by the
+      // TMA engine while the accumulator is still being computed: the
+      // epilogue's per-block residual loads then hit L2 instead of HBM
+      if (p.residual && r_ok && (p.N & 3) == 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.residual + orow * p.N),
+                     "r"(uint32_t(p.N) * 4u)
+                     : "memory");
       mbar_wait(&tfull[acc], acc_phase[ah]);
       acc_phase[ah] ^= 1u;
       tc_fence_after();
@@ -568,8 +577,24 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
         // M clipped by the tensor map).
         uint8_t* box = tma_box + warp * kWarpSlot;
         const int row0 = int(ti.r0) + quad * 32;
+        // plain rows: the residual row of this thread is row r itself (L2-prefetched)
+        const float* rres = (RES && r_ok) ? p.residual + r * p.N + n_base : nullptr;
 #pragma unroll 1
         for (int cb = 0; cb < BN; cb += 32) {
+          if (lane == 0) bulk_wait_read0();   // the box's previous store has read it
+          __syncwarp();
+          // residual: the row's 32-column segment is copied straight into this
+          // thread's swizzled box row (cp.async, no registers), then added in place
+          const bool has_res = rres != nullptr;   // (tma_c with a residual implies N % 32 == 0)
+          if (has_res) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(
+                               smem_u32(box + lane * 128 + ((c ^ (lane & 7)) * 16))),
+                           "l"(rres + cb + 4 * c)
+                           : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+          }
           uint32_t raw[32];
           tmem_ld32_nowait(t_base + uint32_t(cb), raw);
           tmem_ld_wait();
@@ -577,8 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
           }
-          if (lane == 0) bulk_wait_read0();   // the box's previous store has read it
-          __syncwarp();
+          if (has_res) asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             float4 o = make_float4(__uint_as_float(raw[4 * c]), __uint_as_float(raw[4 * c + 1]),
@@ -587,7 +611,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
               o.x = gelu_fast(o.x); o.y = gelu_fast(o.y); o.z = gelu_fast(o.z); o.w = gelu_fast(o.w);
             }
             if (p.gate) { o.x *= gt; o.y *= gt; o.z *= gt; o.w *= gt; }
-            *reinterpret_cast<float4*>(box + lane * 128 + ((c ^ (lane & 7)) * 16)) = o;
+            float4* slot = reinterpret_cast<float4*>(box + lane * 128 + ((c ^ (lane & 7)) * 16));
+            if (has_res) {
+              const float4 q = *slot;
+              o = make_float4(q.x + o.x, q.y + o.y, q.z + o.z, q.w + o.w);
+            }
+            *slot = o;
           }
           fence_proxy_async_smem();
           __syncwarp();

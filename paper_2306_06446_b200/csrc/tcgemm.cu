@@ -140,7 +140,9 @@ static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cu
   CUtensorMap tmC;
   memset(&tmC, 0, sizeof(tmC));
   p.tma_c = 0;
-  if (g_tc_tma && bn % 32 == 0 && p.c_rows == nullptr && p.residual == nullptr &&
+  if (g_tc_tma && bn % 32 == 0 && p.c_rows == nullptr &&
+      (p.residual == nullptr ||
+       ((reinterpret_cast<uintptr_t>(p.residual) & 15) == 0 && p.N % 32 == 0)) &&
       p.pos == nullptr && (p.img_tokens == 0 || p.extra == 0) && (p.N % 4) == 0 &&
       (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && p.M < (int64_t(1) << 31)) {
     const cuuint64_t dims[2] = {cuuint64_t(p.N), cuuint64_t(p.M)};
@@ -153,9 +155,13 @@ static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cu
         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r == CUDA_SUCCESS) p.tma_c = 1;
   }
+  // a residual on the TMA path needs the RES instantiation (plain A rows only)
+  const bool res_tma = p.tma_c && p.residual != nullptr;
+  if (res_tma && amode != A_PLAIN) p.tma_c = 0;
 #define SA_TC_CASE(BNV)                                                                          \
   case BNV: {                                                                                    \
-    auto kfn = amode == A_PLAIN    ? tc_gemm_kernel<BNV, A_PLAIN>                               \
+    auto kfn = amode == A_PLAIN                                                                  \
+                   ? (res_tma ? tc_gemm_kernel<BNV, A_PLAIN, true> : tc_gemm_kernel<BNV, A_PLAIN>) \
                : amode == A_GATHER ? tc_gemm_kernel<BNV, A_GATHER>                              \
                                    : tc_gemm_kernel<BNV, A_PATCH>;                              \
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));          \
