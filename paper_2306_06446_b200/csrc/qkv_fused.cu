@@ -9,12 +9,13 @@
 // per (image, head) (quantize.py:123-140 via model.py:355-358).
 //
 // One persistent CTA per SM walks 128-token tiles of the flat (B·n, d) input:
-//   warps 4-7  producers (thread = token row): the x row, LayerNorm in fp32
+//   warps 4-7  producers (thread = token row; d = 32 q/k/v: a second group,
+//              warps 8-11, takes alternate tiles): the x row, LayerNorm in fp32
 //              (the exact arithmetic of sa_ln_route), three fp64 router dots →
 //              winner / gate (numpy-exp tie rule), written to the dispatch
 //              arrays and to a shared route table; the normalised row split
 //              into hi/mid/lo bf16 planes and stored to TMEM (A operand);
-//   warp 8     MMA issuer: per projection the dense expert (6 plane products)
+//   last warp  MMA issuer: per projection the dense expert (6 plane products)
 //              and the shift expert (3, exact bf16 weights) into TMEM
 //              accumulators — both experts for every token, so no
 //              permutation / gather / scatter exists (the selection is a per-row
@@ -37,8 +38,9 @@ namespace qkv {
 
 using namespace tc;
 
-constexpr int kEpi = 0, kProd = 4, kMma = 8;
-constexpr int kThreads = 288;   // 9 warps
+// warps 0-3 epilogue, then Cfg::PG producer groups of 4 warps (alternate
+// tiles, one A buffer each), then the MMA issuer (Cfg::MMA_WARP, Cfg::THREADS)
+constexpr int kEpi = 0, kProd = 4;
 constexpr uint32_t kPlaneCols = 16;
 constexpr int kRT = 4;           // route-table ring slots
 
@@ -48,6 +50,11 @@ struct Cfg {
   static constexpr int H = D / 32;                  // heads (dk = 32)
   static constexpr int NA = (NP == 3 && D == 64) ? 1 : 2;          // A buffers in TMEM
   static constexpr int NACC = NP == 3 ? (D == 32 ? 2 : 1) : (D == 32 ? 4 : 2);
+  // two producer groups for the d = 32 q/k/v form (its LN + three interleaved
+  // fp64 router chains per row pace the tile); one elsewhere (register budget)
+  static constexpr int PG = (NP == 3 && D == 32) ? 2 : 1;
+  static constexpr int MMA_WARP = kProd + 4 * PG;
+  static constexpr int THREADS = (MMA_WARP + 1) * 32;
   static constexpr uint32_t A_COLS = KC1 * 3 * kPlaneCols;
   static constexpr uint32_t T_A = 0;
   static constexpr uint32_t T_ACC = (NA * A_COLS + 31) / 32 * 32;  // 2·NP parts of D columns
@@ -103,9 +110,10 @@ __device__ __forceinline__ int decide2(float l0, float l1, float tie_thresh, flo
 }
 
 template <int D, int NP>
-__global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid_constant__ CUtensorMap tmV) {
+__global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, const __grid_constant__ CUtensorMap tmV) {
   using C = Cfg<D, NP>;
   using S = Smem<D, NP>;
+  constexpr int kMma = C::MMA_WARP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   double* swg = reinterpret_cast<double*>(smem + S::WG);
@@ -145,19 +153,23 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid
       bulk_g2s(smem + S::W + r * (C::WD + C::WS) + C::WD, p.wsh[r], C::WS, wbar);
     }
   }
-  for (int i = tid; i < NP * 2 * D; i += kThreads) swg[i] = double(p.wg[i / (2 * D)][i % (2 * D)]);
+  for (int i = tid; i < NP * 2 * D; i += C::THREADS) swg[i] = double(p.wg[i / (2 * D)][i % (2 * D)]);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int ntile = int((p.M + 127) / 128);
 
-  if (warp >= kProd && warp < kProd + 4) {
+  if (warp >= kProd && warp < kMma) {
     // ---------------- producers: LN + routers + A planes ----------------
-    const int rl = (warp - kProd) * 32 + lane;
-    const uint32_t lane_base = uint32_t((warp - kProd) * 32) << 16;
-    int j = 0;
-    // the next tile's row is loaded while this tile is normalised / routed
+    // PG groups of 4 warps take alternate tiles (group g: the CTA's tiles
+    // j = g, g + PG, ...; with PG = 2 each group owns one of the two A buffers)
+    constexpr int NPG = C::PG;
+    const int pg = (warp - kProd) >> 2, pw = (warp - kProd) & 3;
+    const int rl = pw * 32 + lane;
+    const uint32_t lane_base = uint32_t(pw * 32) << 16;
+    int j = pg;
+    // the group's next tile row is loaded while this tile is normalised / routed
     float4 xn[D / 4];
     auto load_row = [&](int mm) {
       const int64_t rr = int64_t(mm) * 128 + rl;
@@ -166,8 +178,8 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid
       for (int i = 0; i < D / 4; ++i)
         xn[i] = (mm < ntile && rr < p.M) ? __ldg(xr + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     };
-    load_row(blockIdx.x);
-    for (int m = blockIdx.x; m < ntile; m += gridDim.x, ++j) {
+    load_row(blockIdx.x + pg * gridDim.x);
+    for (int m = blockIdx.x + pg * gridDim.x; m < ntile; m += NPG * gridDim.x, j += NPG) {
       const int64_t row = int64_t(m) * 128 + rl;
       const bool ok = row < p.M;
       float v[D];
@@ -175,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid
       for (int i = 0; i < D / 4; ++i) {
         v[4 * i] = xn[i].x; v[4 * i + 1] = xn[i].y; v[4 * i + 2] = xn[i].z; v[4 * i + 3] = xn[i].w;
       }
-      load_row(m + gridDim.x);
+      load_row(m + NPG * gridDim.x);
       if (NP == 3 && ok) {
         // LayerNorm: the exact operation sequence of ln_route_kernel (moe.cu)
         float s = 0.f;
@@ -202,24 +214,41 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_kernel(Params p, const __grid
       // routers (fp64 dots in channel order, as ln_route_kernel / route_kernel)
       const int rs = j % kRT;
       mbar_wait(&rt_empty[rs], (uint32_t(j / kRT) & 1u) ^ 1u);
+      // d = 32: the NP routers' chains are interleaved (2·NP independent fp64
+      // chains in flight, each in channel order, so the logits are unchanged);
+      // d = 64 keeps one router at a time (register budget)
+      constexpr int RI = D == 32 ? NP : 1;
 #pragma unroll 1
-      for (int r = 0; r < NP; ++r) {
-        double s0 = 0.0, s1 = 0.0;
-        const double* w = swg + r * 2 * D;
+      for (int r0 = 0; r0 < NP; r0 += RI) {
+        double s0[RI], s1[RI];
+#pragma unroll
+        for (int i = 0; i < RI; ++i) {
+          s0[i] = 0.0;
+          s1[i] = 0.0;
+        }
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          s0 = fma(double(v[c]), w[2 * c], s0);
-          s1 = fma(double(v[c]), w[2 * c + 1], s1);
+          const double vc = double(v[c]);
+#pragma unroll
+          for (int i = 0; i < RI; ++i) {
+            const double2 w = *reinterpret_cast<const double2*>(swg + (r0 + i) * 2 * D + 2 * c);
+            s0[i] = fma(vc, w.x, s0[i]);
+            s1[i] = fma(vc, w.y, s1[i]);
+          }
         }
-        float g = 1.f;
-        int e = 0;
-        if (ok) {
-          e = decide2(float(s0), float(s1), p.tie, g);
-          p.expert_of[r * p.M + row] = e;
-          p.gate[r * p.M + row] = g;
+#pragma unroll
+        for (int i = 0; i < RI; ++i) {
+          const int r = r0 + i;
+          float g = 1.f;
+          int e = 0;
+          if (ok) {
+            e = decide2(float(s0[i]), float(s1[i]), p.tie, g);
+            p.expert_of[r * p.M + row] = e;
+            p.gate[r * p.M + row] = g;
+          }
+          rt_e[(rs * NP + r) * 128 + rl] = e;
+          rt_g[(rs * NP + r) * 128 + rl] = g;
         }
-        rt_e[(rs * NP + r) * 128 + rl] = e;
-        rt_g[(rs * NP + r) * 128 + rl] = g;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&rt_full[rs]);
@@ -486,11 +515,11 @@ extern "C" int sa_ln_qkv_hash(const float* x, const float* gain, const float* bi
   if (d == 32) {
     const int smem = int(Smem<32, 3>::TOTAL);
     cudaFuncSetAttribute(qkv_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    qkv_kernel<32, 3><<<grid, qkv::kThreads, smem, s>>>(p, tmV);
+    qkv_kernel<32, 3><<<grid, qkv::Cfg<32, 3>::THREADS, smem, s>>>(p, tmV);
   } else {
     const int smem = int(Smem<64, 3>::TOTAL);
     cudaFuncSetAttribute(qkv_kernel<64, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    qkv_kernel<64, 3><<<grid, qkv::kThreads, smem, s>>>(p, tmV);
+    qkv_kernel<64, 3><<<grid, qkv::Cfg<64, 3>::THREADS, smem, s>>>(p, tmV);
   }
   const int64_t H = d / 32;
   gamma_finalize_qkv<<<unsigned(cdiv(2 * B * H, 256)), 256, 0, s>>>(p.gpart, p.nseg, int(H), B,
@@ -549,11 +578,11 @@ extern "C" int sa_fused_moe_linear(const float* x, const float* wg, const void* 
   if (d == 32) {
     const int smem = int(Smem<32, 1>::TOTAL);
     cudaFuncSetAttribute(qkv_kernel<32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    qkv_kernel<32, 1><<<grid, qkv::kThreads, smem, s>>>(p, tmY);
+    qkv_kernel<32, 1><<<grid, qkv::Cfg<32, 1>::THREADS, smem, s>>>(p, tmY);
   } else {
     const int smem = int(Smem<64, 1>::TOTAL);
     cudaFuncSetAttribute(qkv_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    qkv_kernel<64, 1><<<grid, qkv::kThreads, smem, s>>>(p, tmY);
+    qkv_kernel<64, 1><<<grid, qkv::Cfg<64, 1>::THREADS, smem, s>>>(p, tmY);
   }
   count_launch(1);
   SA_LAUNCH_CHECK("sa_fused_moe_linear");
