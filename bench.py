@@ -164,7 +164,7 @@ def op_bytes(name, args):
     if name == "sa_layernorm":
         M, d = args[4], args[5]
         return 2 * M * d * A
-    if name in ("sa_patch_embed", "sa_tc_patch_embed"):
+    if name in ("sa_patch_embed", "sa_tc_patch_embed", "sa_tc_patch_embed_ln"):
         B, H, W, C, p = args[1:6]
         d = args[8] if name == "sa_patch_embed" else args[9]
         n = (H // p) * (W // p)

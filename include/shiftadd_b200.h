@@ -244,6 +244,13 @@ int sa_fused_moe_linear(const float* x, const float* wg, const void* w_dense, co
 int sa_tc_patch_embed(const float* grid, int64_t B, int64_t H, int64_t W, int64_t C,
                       int64_t patch, float sub, const void* wpack, int bn, int64_t d,
                       const float* cls, const float* pos, float* y, void* stream);
+/* the same followed by the stage's embedding LayerNorm (model.py:565-570 →
+ * LayerNorm.forward, model.py:174-178) in the GEMM epilogue: y = LN(embed) with
+ * sa_layernorm's arithmetic; d = 32 or 64, no cls / pos rows */
+int sa_tc_patch_embed_ln_ok(int64_t d, int has_cls, int has_pos);
+int sa_tc_patch_embed_ln(const float* grid, int64_t B, int64_t H, int64_t W, int64_t C,
+                         int64_t patch, float sub, const void* wpack, int bn, int64_t d,
+                         const float* gain, const float* bias, float eps, float* y, void* stream);
 
 /* ---- glue ------------------------------------------------------------------ */
 /* LayerNorm.forward (model.py:174-178 → tensor.layernorm, tensor.py:114-128) */

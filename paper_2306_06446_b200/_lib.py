@@ -76,6 +76,9 @@ _SIGS = {
                              _P, _SZ, _P]),
     "sa_tc_patch_embed": (_I32, [_P, _I64, _I64, _I64, _I64, _I64, _F32, _P, _I32, _I64, _P, _P,
                                  _P, _P]),
+    "sa_tc_patch_embed_ln_ok": (_I32, [_I64, _I32, _I32]),
+    "sa_tc_patch_embed_ln": (_I32, [_P, _I64, _I64, _I64, _I64, _I64, _F32, _P, _I32, _I64, _P,
+                                    _P, _F32, _P, _P]),
     "sa_tc_fused_mlp_ok": (_I32, [_I64, _I64]),
     "sa_tc_moe_mlp_fused": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64,
                                    _P]),

@@ -77,6 +77,9 @@ struct TcParams {
   int dbg;     // debug role isolation (0 in production): 1 no A loads, 2 no C stores, 4 no MMAs
   int tma_c;   // 1: C rows are the tile rows (no scatter / position): TMA-store epilogue
   int kq_min;  // K stages alternate between producer groups when kchunks > kq_min (else whole tiles)
+  const float* ln_g;   // LNE instantiation: LayerNorm of each output row (N = BN ∈ {32, 64})
+  const float* ln_b;
+  float ln_eps;
 };
 
 // TMEM accumulators: four buffers when they fit (BN <= 128), so the MMA can run
@@ -159,7 +162,7 @@ __host__ __device__ inline size_t tc_fixed_smem() {
 
 // RES: the TMA-store epilogue adds a residual (plain rows only); a separate
 // instantiation so kernels without one carry no residual code (register cap 96)
-template <int BN, int AM, bool RES = false>
+template <int BN, int AM, bool RES = false, bool LNE = false>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
                                                               const __grid_constant__ CUtensorMap tmC) {
   // direct epilogue (thread = row, no shared-memory transpose) for wide tiles
@@ -579,6 +582,40 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
         const int row0 = int(ti.r0) + quad * 32;
         // plain rows: the residual row of this thread is row r itself (L2-prefetched)
         const float* rres = (RES && r_ok) ? p.residual + r * p.N + n_base : nullptr;
+        // LNE: LayerNorm of the thread's output row (the whole row is this tile,
+        // N = BN) with layernorm_row_kernel's arithmetic: sums over float4
+        // groups in column order, two passes over TMEM for mean and variance
+        float ln_mean = 0.f, ln_inv = 0.f;
+        if (LNE) {
+          float sum = 0.f;
+#pragma unroll 1
+          for (int cb = 0; cb < BN; cb += 32) {
+            uint32_t raw[32];
+            tmem_ld32_nowait(t_base + uint32_t(cb), raw);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              sum += (__uint_as_float(raw[4 * i]) + __uint_as_float(raw[4 * i + 1])) +
+                     (__uint_as_float(raw[4 * i + 2]) + __uint_as_float(raw[4 * i + 3]));
+          }
+          ln_mean = sum / float(BN);
+          float q = 0.f;
+#pragma unroll 1
+          for (int cb = 0; cb < BN; cb += 32) {
+            uint32_t raw[32];
+            tmem_ld32_nowait(t_base + uint32_t(cb), raw);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float x0 = __uint_as_float(raw[4 * i]) - ln_mean;
+              const float x1 = __uint_as_float(raw[4 * i + 1]) - ln_mean;
+              const float x2 = __uint_as_float(raw[4 * i + 2]) - ln_mean;
+              const float x3 = __uint_as_float(raw[4 * i + 3]) - ln_mean;
+              q += (x0 * x0 + x1 * x1) + (x2 * x2 + x3 * x3);
+            }
+          }
+          ln_inv = 1.0f / sqrtf(q / float(BN) + p.ln_eps);
+        }
 #pragma unroll 1
         for (int cb = 0; cb < BN; cb += 32) {
           if (lane == 0) bulk_wait_read0();   // the box's previous store has read it
@@ -611,6 +648,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
               o.x = gelu_fast(o.x); o.y = gelu_fast(o.y); o.z = gelu_fast(o.z); o.w = gelu_fast(o.w);
             }
             if (p.gate) { o.x *= gt; o.y *= gt; o.z *= gt; o.w *= gt; }
+            if (LNE) {
+              const float4 g4 = __ldg(reinterpret_cast<const float4*>(p.ln_g + cb + 4 * c));
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.ln_b + cb + 4 * c));
+              o.x -= ln_mean; o.y -= ln_mean; o.z -= ln_mean; o.w -= ln_mean;
+              o = make_float4(o.x * ln_inv * g4.x + b4.x, o.y * ln_inv * g4.y + b4.y,
+                              o.z * ln_inv * g4.z + b4.z, o.w * ln_inv * g4.w + b4.w);
+            }
             float4* slot = reinterpret_cast<float4*>(box + lane * 128 + ((c ^ (lane & 7)) * 16));
             if (has_res) {
               const float4 q = *slot;

@@ -158,12 +158,18 @@ static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cu
   // a residual on the TMA path needs the RES instantiation (plain A rows only)
   const bool res_tma = p.tma_c && p.residual != nullptr;
   if (res_tma && amode != A_PLAIN) p.tma_c = 0;
+  // the fused LayerNorm lives in the TMA epilogue of a single-column-tile patch GEMM
+  if (p.ln_g && !(p.tma_c && amode == A_PATCH && p.ntiles == 1 && p.N == bn && (bn == 32 || bn == 64))) {
+    set_error("fused LayerNorm epilogue needs one 32/64-wide column tile on the TMA path");
+    return SA_ERR_VALUE;
+  }
 #define SA_TC_CASE(BNV)                                                                          \
   case BNV: {                                                                                    \
     auto kfn = amode == A_PLAIN                                                                  \
                    ? (res_tma ? tc_gemm_kernel<BNV, A_PLAIN, true> : tc_gemm_kernel<BNV, A_PLAIN>) \
                : amode == A_GATHER ? tc_gemm_kernel<BNV, A_GATHER>                              \
-                                   : tc_gemm_kernel<BNV, A_PATCH>;                              \
+               : (p.ln_g ? tc_gemm_kernel<BNV, A_PATCH, false, (BNV == 32 || BNV == 64)>         \
+                         : tc_gemm_kernel<BNV, A_PATCH>);                                       \
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));          \
     kfn<<<grid, kThreads, smem, s>>>(p, tmC);                                                    \
   } break;
@@ -326,9 +332,36 @@ extern "C" int sa_tc_moe_mlp(const float* x, const int32_t* perm, const int32_t*
   return launch_tc(p2, tc::A_PLAIN, bn2, cdiv(M, tc::kBM) + 1, s);
 }
 
+static int tc_patch_embed_impl(const float* grid, int64_t B, int64_t H, int64_t W, int64_t C,
+                               int64_t patch, float sub, const void* wpack, int bn, int64_t d,
+                               const float* cls, const float* pos, float* y, const float* ln_g,
+                               const float* ln_b, float ln_eps, void* stream);
+
 extern "C" int sa_tc_patch_embed(const float* grid, int64_t B, int64_t H, int64_t W, int64_t C,
                                  int64_t patch, float sub, const void* wpack, int bn, int64_t d,
                                  const float* cls, const float* pos, float* y, void* stream) {
+  return tc_patch_embed_impl(grid, B, H, W, C, patch, sub, wpack, bn, d, cls, pos, y, nullptr,
+                             nullptr, 0.f, stream);
+}
+
+extern "C" int sa_tc_patch_embed_ln_ok(int64_t d, int has_cls, int has_pos) {
+  return (d == 32 || d == 64) && !has_cls && !has_pos;
+}
+
+extern "C" int sa_tc_patch_embed_ln(const float* grid, int64_t B, int64_t H, int64_t W, int64_t C,
+                                    int64_t patch, float sub, const void* wpack, int bn, int64_t d,
+                                    const float* gain, const float* bias, float eps, float* y,
+                                    void* stream) {
+  SA_REQUIRE(gain != nullptr && bias != nullptr && sa_tc_patch_embed_ln_ok(d, 0, 0), SA_ERR_VALUE,
+             "sa_tc_patch_embed_ln: d=%lld unsupported (32 or 64)", (long long)d);
+  return tc_patch_embed_impl(grid, B, H, W, C, patch, sub, wpack, bn, d, nullptr, nullptr, y, gain,
+                             bias, eps, stream);
+}
+
+static int tc_patch_embed_impl(const float* grid, int64_t B, int64_t H, int64_t W, int64_t C,
+                               int64_t patch, float sub, const void* wpack, int bn, int64_t d,
+                               const float* cls, const float* pos, float* y, const float* ln_g,
+                               const float* ln_b, float ln_eps, void* stream) {
   SA_REQUIRE(B > 0 && H > 0 && W > 0 && C > 0 && patch > 0 && d > 0, SA_ERR_SHAPE,
              "sa_tc_patch_embed: bad extents");
   SA_REQUIRE(H % patch == 0 && W % patch == 0 && H == W, SA_ERR_SHAPE,
@@ -356,6 +389,9 @@ extern "C" int sa_tc_patch_embed(const float* grid, int64_t B, int64_t H, int64_
   p.pos = pos;
   p.img_tokens = n;
   p.extra = cls ? 1 : 0;
+  p.ln_g = ln_g;
+  p.ln_b = ln_b;
+  p.ln_eps = ln_eps;
   cudaStream_t s = as_stream(stream);
   int st = launch_tc(p, tc::A_PATCH, bn, cdiv(B * n, tc::kBM), s);
   if (st) return st;

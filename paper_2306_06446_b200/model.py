@@ -114,6 +114,7 @@ def tc_enabled() -> bool:
 
 # LayerNorm fused with the routers that read its output (d = 32 / 64)
 FUSE_LN_ROUTE = os.environ.get("SA_FUSE_LN_ROUTE", "1") == "1"
+FUSE_EMBED_LN = os.environ.get("SA_FUSE_EMBED_LN", "1") == "1"
 # fc1 → GELU → fc2 in one tensor-core kernel (d = 32 / 64)
 FUSE_MLP = os.environ.get("SA_FUSE_MLP", "1") == "1"
 # LN1 + q/k/v routers + both experts of q/k/v + sign-hash in one kernel (d = 32 / 64)
@@ -780,19 +781,29 @@ class Network:
         tok = None
         for S in self.stages:
             tok = torch.empty((B * S.rows, S.d), dtype=torch.float32, device=x.device)
+            fused_ln = False
             if tc_enabled():
                 pk, bn, _ = S.patch_embed.tc_pack()
-                _lib.call("sa_tc_patch_embed", _lib.ptr(grid), B, H, W, C, S.patch, sub, _lib.ptr(pk),
-                          bn, S.d, _lib.ptr(S.cls.value if S.cls is not None else None),
-                          _lib.ptr(S.pos.value if S.pos is not None else None), _lib.ptr(tok),
-                          _stream())
+                fused_ln = (FUSE_EMBED_LN and S.embed_ln is not None and bool(
+                    _lib.load().sa_tc_patch_embed_ln_ok(S.d, S.cls is not None, S.pos is not None)))
+                if fused_ln:   # embed + LayerNorm in one kernel (LN in the GEMM epilogue)
+                    _lib.call("sa_tc_patch_embed_ln", _lib.ptr(grid), B, H, W, C, S.patch, sub,
+                              _lib.ptr(pk), bn, S.d, _lib.ptr(S.embed_ln.gain.value),
+                              _lib.ptr(S.embed_ln.bias.value), 1e-5, _lib.ptr(tok),
+                              _stream())
+                else:
+                    _lib.call("sa_tc_patch_embed", _lib.ptr(grid), B, H, W, C, S.patch, sub,
+                              _lib.ptr(pk), bn, S.d,
+                              _lib.ptr(S.cls.value if S.cls is not None else None),
+                              _lib.ptr(S.pos.value if S.pos is not None else None), _lib.ptr(tok),
+                              _stream())
             else:
                 _lib.call("sa_patch_embed", _lib.ptr(grid), B, H, W, C, S.patch, sub,
                           _lib.ptr(S.patch_embed.w.value), S.d,
                           _lib.ptr(S.cls.value if S.cls is not None else None),
                           _lib.ptr(S.pos.value if S.pos is not None else None), _lib.ptr(tok),
                           _stream())
-            if S.embed_ln is not None:
+            if S.embed_ln is not None and not fused_ln:
                 tok = S.embed_ln.forward(tok)
             t3 = tok.reshape(B, S.rows, S.d)
             for blk in S.blocks:

@@ -221,3 +221,26 @@ def test_fused_qkv_matches_unfused(golden, name):
             assert np.array_equal(host(c0), host(c1))
     assert rel_err(got, ref) < 1e-6
     assert rel_err(got, fx["logits"]) < LOGIT_TOL
+
+
+@pytest.mark.parametrize("name", ["pvt_small", "pvt_b0_full"])
+def test_fused_embed_layernorm_bit_identical(golden, name):
+    """sa_tc_patch_embed_ln (embedding LayerNorm in the patch GEMM's epilogue)
+    reproduces sa_tc_patch_embed + sa_layernorm exactly: identical logits."""
+    from paper_2306_06446_b200 import model as MD
+    fx = golden(name)
+    spec = FIXTURES[name]()
+    m = MD.Network(spec)
+    b = min(int(fx["batch"]), 4)
+    images = fx["images"][:b] if "images" in fx else ops.rng(int(fx["images_seed"])).uniform(
+        0, 1, (b, spec["img"], spec["img"], 3)).astype(F32)
+    x = dev(images)
+    old = MD.FUSE_EMBED_LN
+    try:
+        MD.FUSE_EMBED_LN = False
+        ref = host(m.forward(x))
+        MD.FUSE_EMBED_LN = True
+        got = host(m.forward(x))
+    finally:
+        MD.FUSE_EMBED_LN = old
+    assert np.array_equal(got, ref)
