@@ -10,7 +10,14 @@ tail -2 gpurun_out/pytest_gpu.log
 timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
   --profile-from-start off --csv --log-file gpurun_out/traffic.csv \
   python scripts/profile_forward.py --record gpurun_out/op_calls.json > gpurun_out/traffic.log 2>&1
-for k in mlp_kernel binattn_fused tc_gemm_kernel sign_hash_stream_kernel ln_route_kernel route_kernel; do
+# north-star kernels standalone at the bench shape (K1, K2a, K3, K5)
+for k in sign_hash_stream_kernel binattn_fused tc_gemm_kernel mlp_kernel; do
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 \
+    --profile-from-start off -o gpurun_out/full_$k -f python scripts/kernels_standalone.py \
+    > gpurun_out/ncu_full_$k.log 2>&1
+done
+# the forward's fused kernels (first launch inside the profiled forward)
+for k in qkv_kernel ln_route_kernel; do
   timeout 300 ncu --set full --clock-control none --import-source on -k regex:$k -s 0 -c 1 \
     --profile-from-start off -o gpurun_out/full_$k -f python scripts/profile_forward.py --warm 1 \
     > gpurun_out/ncu_full_$k.log 2>&1
