@@ -106,16 +106,20 @@ __global__ void __launch_bounds__(kHashThreads) sign_hash_kernel(
 // every d, each thread keeps d/4 independent 128-bit loads in flight.
 constexpr int kStreamTok = 256;
 
-template <int D>
-__global__ void __launch_bounds__(kHashThreads) sign_hash_stream_kernel(
+// T threads per CTA with 4·T a multiple of D (T = 256 when D divides 1024;
+// T = lcm(D/4, 32) scaled to >= 128 otherwise, e.g. 160 for D = 160), so each
+// thread's channel 4t mod D is the same in every iteration.
+template <int D, int T = kHashThreads, int R = kStreamTok>   // R tokens per CTA
+__global__ void __launch_bounds__(T) sign_hash_stream_kernel(
     const float* __restrict__ x, int n, int heads, int dk, int W, int chunks,
     uint32_t* __restrict__ codes, double* __restrict__ partial) {
+  static_assert((4 * T) % D == 0 && T % 32 == 0, "fixed channel per thread");
   constexpr int DW = D / 32;
-  __shared__ uint32_t sm_codes[kStreamTok * DW];
-  __shared__ double red[kHashThreads];
+  __shared__ uint32_t sm_codes[R * DW];
+  __shared__ double red[T];
   const int b = blockIdx.y, chunk = blockIdx.x;
-  const int t0 = chunk * kStreamTok;
-  const int rows = min(kStreamTok, n - t0);
+  const int t0 = chunk * R;
+  const int rows = min(R, n - t0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float4* src = reinterpret_cast<const float4*>(x + (size_t(b) * n + t0) * D);
   const int nf4 = rows * (D / 4);
@@ -124,7 +128,8 @@ __global__ void __launch_bounds__(kHashThreads) sign_hash_stream_kernel(
   // the loop bound is CTA-uniform, so every lane reaches the shuffles; nf4 is a
   // multiple of 8 (D/4 >= 8), so an 8-lane word group is either fully active
   // or fully past the end (and then never stored).
-  for (int base = 0; base < nf4; base += kHashThreads) {
+#pragma unroll 4
+  for (int base = 0; base < nf4; base += T) {
     const int f = base + tid;
     const bool act = f < nf4;
     const float4 v = act ? __ldg(src + f) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -147,7 +152,7 @@ __global__ void __launch_bounds__(kHashThreads) sign_hash_stream_kernel(
   __syncthreads();
 
   const int total = heads * rows * W;
-  for (int idx = tid; idx < total; idx += kHashThreads) {
+  for (int idx = tid; idx < total; idx += T) {
     const int wi = idx % W;
     const int r = (idx / W) % rows;
     const int h = idx / (W * rows);
@@ -162,9 +167,9 @@ __global__ void __launch_bounds__(kHashThreads) sign_hash_stream_kernel(
   }
   // per head: fixed-order sum over the threads whose 4 channels lie in the head
   // (dk >= 4 so a thread's channels never straddle two heads)
-  for (int h = warp; h < heads; h += kHashThreads / 32) {
+  for (int h = warp; h < heads; h += T / 32) {
     double s = 0.0;
-    for (int j = lane; j < kHashThreads; j += 32)
+    for (int j = lane; j < T; j += 32)
       if (((4 * j) % D) / dk == h) s += red[j];
     s = warp_sum(s);
     if (lane == 0) partial[(size_t(b) * chunks + chunk) * heads + h] = s;
@@ -187,7 +192,7 @@ using namespace sa;
 
 extern "C" size_t sa_sign_hash_workspace(int64_t B, int64_t n, int64_t d, int64_t heads) {
   (void)d;
-  return size_t(B) * size_t(cdiv(n, kTokPerCta)) * size_t(heads) * sizeof(double);
+  return size_t(B) * size_t(cdiv(n, kTokPerCta)) * size_t(heads) * sizeof(double);   // >= stream chunks
 }
 
 extern "C" int sa_sign_hash(const float* x, int64_t B, int64_t n, int64_t d, int64_t heads,
@@ -224,6 +229,23 @@ extern "C" int sa_sign_hash(const float* x, int64_t B, int64_t n, int64_t d, int
       SA_HASH_STREAM(512)
     }
 #undef SA_HASH_STREAM
+  } else if (d == 96 || d == 160 || d == 192 || d == 320 || d == 384) {
+    constexpr int R = 64;   // wide rows: 64 tokens per CTA (enough CTAs at small n)
+    chunks = int(cdiv(n, R));
+    dim3 grid(chunks, unsigned(B));
+#define SA_HASH_STREAM_T(DV, TV)                                                            \
+  case DV:                                                                                  \
+    sign_hash_stream_kernel<DV, TV, R><<<grid, TV, 0, s>>>(x, int(n), int(heads), int(dk), \
+                                                           W, chunks, codes, partial);     \
+    break;
+    switch (d) {
+      SA_HASH_STREAM_T(96, 192)
+      SA_HASH_STREAM_T(160, 160)
+      SA_HASH_STREAM_T(192, 192)
+      SA_HASH_STREAM_T(320, 160)
+      SA_HASH_STREAM_T(384, 192)
+    }
+#undef SA_HASH_STREAM_T
   } else {
     chunks = int(cdiv(n, kTokPerCta));
     const size_t smem = size_t(kTokPerCta) * (d / 32) * 4 + size_t(kHashThreads / 32) * d * 4;

@@ -40,7 +40,8 @@ def rel_err(a, b):
 
 @pytest.mark.parametrize("B,n,d,h", [(2, 196, 64, 4), (3, 3136, 32, 1), (2, 784, 64, 2),
                                      (2, 196, 160, 5), (2, 197, 192, 3), (1, 5, 32, 2),
-                                     (2, 49, 256, 8)])
+                                     (2, 49, 256, 8), (3, 300, 96, 3), (2, 513, 320, 10),
+                                     (1, 77, 384, 12), (2, 1000, 160, 5)])
 def test_sign_hash_codes_bit_exact(B, n, d, h):
     from paper_2306_06446_b200 import quantize as Q
     g = ops.rng(B * 1000 + n)
