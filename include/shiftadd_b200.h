@@ -189,6 +189,13 @@ int sa_tc_moe_linear(const float* x, const int32_t* perm, const int32_t* counts,
                      const float* gate, const void* wpack_dense, const void* wpack_shift, int bn,
                      float* y, const float* residual, int64_t M, int64_t K, int64_t N,
                      void* stream);
+/* the q/k/v MoE projections of one AttentionLayer (model.py:342-345) in ONE
+ * launch, from stacked plans (perm / gate [nprob][M], counts [nprob][2]);
+ * wpack_dense / wpack_shift: nprob packed weight pointers; y [nprob][M][N] */
+int sa_tc_moe_linear_grouped(const float* x, const int32_t* perm, const int32_t* counts,
+                             const float* gate, const void* const* wpack_dense,
+                             const void* const* wpack_shift, int nprob, int bn, float* y,
+                             int64_t M, int64_t K, int64_t N, void* stream);
 size_t sa_tc_mlp_workspace(int64_t M, int64_t hidden);
 /* Mlp.forward (model.py:204-208) */
 int sa_tc_mlp(const float* x, const void* w1pack, int w1_kind, int bn1, const void* w2pack,

@@ -68,6 +68,8 @@ _SIGS = {
     "sa_weight_pack_bytes": (_SZ, [_I64, _I64, _I32, _I32]),
     "sa_weight_pack": (_I32, [_P, _I32, _I64, _I64, _I32, _I32, _P, _P]),
     "sa_tc_linear": (_I32, [_P, _P, _I32, _I32, _P, _I64, _I64, _I64, _P, _I32, _P]),
+    "sa_tc_moe_linear_grouped": (_I32, [_P, _P, _P, _P, _P, _P, _I32, _I32, _P, _I64, _I64, _I64,
+                                        _P]),
     "sa_tc_moe_linear": (_I32, [_P, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _I64, _I64, _P]),
     "sa_tc_mlp_workspace": (_SZ, [_I64, _I64]),
     "sa_tc_mlp": (_I32, [_P, _P, _I32, _I32, _P, _I32, _I32, _P, _I64, _I64, _I64, _P, _P, _SZ,

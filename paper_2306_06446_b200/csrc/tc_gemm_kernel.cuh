@@ -56,8 +56,8 @@ struct TcParams {
   const int32_t* a_rows;
   int64_t pH, pW, pC, patch, pside;
   float sub;
-  const uint16_t* Bp[2];
-  int nplanes[2];
+  const uint16_t* Bp[6];     // packed weights per row group (expert; or problem x expert)
+  int nplanes[6];
   int64_t M, K, N;
   int kchunks;
   int ntiles;
@@ -77,6 +77,10 @@ struct TcParams {
   int dbg;     // debug role isolation (0 in production): 1 no A loads, 2 no C stores, 4 no MMAs
   int tma_c;   // 1: C rows are the tile rows (no scatter / position): TMA-store epilogue
   int kq_min;  // K stages alternate between producer groups when kchunks > kq_min (else whole tiles)
+  int ngroups;         // > 2: grouped problems — counts[2i], counts[2i+1] are problem i's
+                       // expert sizes, its rows are [i·prob_rows, (i+1)·prob_rows) of the
+                       // gathered / scattered row space (a_rows, c_rows stacked per problem)
+  int64_t prob_rows;
   const float* ln_g;   // LNE instantiation: LayerNorm of each output row (N = BN ∈ {32, 64})
   const float* ln_b;
   float ln_eps;
@@ -98,14 +102,49 @@ struct TileInfo {
   int n_tile;
 };
 
-__device__ __forceinline__ int64_t num_m_tiles(const TcParams& p, int64_t c0) {
-  if (!p.counts) return (p.M + kBM - 1) / kBM;
-  return (c0 + kBM - 1) / kBM + (p.M - c0 + kBM - 1) / kBM;
+// Row groups of the GEMM (one per expert, or per problem x expert) with their
+// first m-tile, first row and size; built once per CTA in shared memory.
+struct GroupTab {
+  int n;
+  int tile0[7];
+  int64_t row0[6], cnt[6];
+};
+
+__device__ __forceinline__ void build_groups(const TcParams& p, GroupTab& g) {
+  if (!p.counts) {
+    g.n = 1;
+    g.row0[0] = 0;
+    g.cnt[0] = p.M;
+  } else if (p.ngroups > 2) {
+    g.n = p.ngroups;
+    for (int i = 0; i < g.n; ++i) {
+      const int64_t c = p.counts[i & ~1];   // the problem's expert-0 size
+      g.row0[i] = int64_t(i >> 1) * p.prob_rows + ((i & 1) ? c : 0);
+      g.cnt[i] = (i & 1) ? p.prob_rows - c : c;
+    }
+  } else {
+    const int64_t c0 = p.counts[0];
+    g.n = 2;
+    g.row0[0] = 0;
+    g.cnt[0] = c0;
+    g.row0[1] = c0;
+    g.cnt[1] = p.M - c0;
+  }
+  int t = 0;
+  for (int i = 0; i < g.n; ++i) {
+    g.tile0[i] = t;
+    t += int((g.cnt[i] + kBM - 1) / kBM);
+  }
+  g.tile0[g.n] = t;
 }
 
-// m-tiles: with grouping, expert 0 owns ceil(c0/128) tiles, expert 1 the rest.
+__device__ __forceinline__ int64_t num_m_tiles(const GroupTab& g) { return g.tile0[g.n]; }
+
+// m-tiles: group i owns tiles [tile0[i], tile0[i+1]) over its rows.
 // t < 2^31 (checked on the host); ntiles == 1 (N <= BN) avoids the division.
-__device__ __forceinline__ TileInfo tile_info(const TcParams& p, int64_t c0, int t) {
+// GRP: grouped problems (table walk); otherwise at most two expert groups.
+template <bool GRP>
+__device__ __forceinline__ TileInfo tile_info(const TcParams& p, const GroupTab& G, int t) {
   TileInfo ti;
   int m = t;
   ti.n_tile = 0;
@@ -113,32 +152,42 @@ __device__ __forceinline__ TileInfo tile_info(const TcParams& p, int64_t c0, int
     m = t / p.ntiles;
     ti.n_tile = t - m * p.ntiles;
   }
-  if (!p.counts) {
+  if (!p.counts) {   // one group: no table lookups
     ti.group = 0;
     ti.r0 = int64_t(m) * kBM;
     ti.r1 = min(p.M, ti.r0 + kBM);
     return ti;
   }
-  const int64_t t0 = (c0 + kBM - 1) / kBM;
-  if (m < t0) {
-    ti.group = 0;
-    ti.r0 = int64_t(m) * kBM;
-    ti.r1 = min(c0, ti.r0 + kBM);
-  } else {
-    ti.group = 1;
-    ti.r0 = c0 + (int64_t(m) - t0) * kBM;
-    ti.r1 = min(p.M, ti.r0 + kBM);
+  if (!GRP) {        // expert 0 owns ceil(c0/128) tiles, expert 1 the rest
+    const int t0 = G.tile0[1];
+    const int64_t c0 = G.cnt[0];
+    if (m < t0) {
+      ti.group = 0;
+      ti.r0 = int64_t(m) * kBM;
+      ti.r1 = min(c0, ti.r0 + kBM);
+    } else {
+      ti.group = 1;
+      ti.r0 = c0 + (int64_t(m) - t0) * kBM;
+      ti.r1 = min(p.M, ti.r0 + kBM);
+    }
+    return ti;
   }
+  int g = 0;
+  while (g + 1 < G.n && m >= G.tile0[g + 1]) ++g;
+  ti.group = g;
+  ti.r0 = G.row0[g] + int64_t(m - G.tile0[g]) * kBM;
+  ti.r1 = min(G.row0[g] + G.cnt[g], ti.r0 + kBM);
   return ti;
 }
 
 // The next non-empty tile at or after t whose ordinal among the CTA's non-empty
 // tiles has parity g (the tiles a producer / epilogue group owns; g < 0: any);
 // j counts the ordinals. Returns total when there is none.
-__device__ __forceinline__ int next_group_tile(const TcParams& p, int64_t c0, int total, int g,
-                                               int t, int& j, int& jj, TileInfo& ti) {
+template <bool GRP>
+__device__ __forceinline__ int next_group_tile(const TcParams& p, const GroupTab& G, int total,
+                                               int g, int t, int& j, int& jj, TileInfo& ti) {
   for (; t < total; t += gridDim.x) {
-    ti = tile_info(p, c0, t);
+    ti = tile_info<GRP>(p, G, t);
     if (ti.r0 >= ti.r1) continue;
     jj = j++;
     if (g < 0 || (jj & 1) == g) return t;   // g < 0: every non-empty tile
@@ -162,7 +211,7 @@ __host__ __device__ inline size_t tc_fixed_smem() {
 
 // RES: the TMA-store epilogue adds a residual (plain rows only); a separate
 // instantiation so kernels without one carry no residual code (register cap 96)
-template <int BN, int AM, bool RES = false, bool LNE = false>
+template <int BN, int AM, bool RES = false, bool LNE = false, bool GRP = false>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
                                                               const __grid_constant__ CUtensorMap tmC) {
   // direct epilogue (thread = row, no shared-memory transpose) for wide tiles
@@ -206,7 +255,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + NST + 1);   // (+ resident-B barrier)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ GroupTab gtab;
   if (warp == kMmaWarp) tmem_alloc<TCOLS>(tmem_slot);
+  if (tid == 0) build_groups(p, gtab);
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 4);     // the four warps of the owning producer group
@@ -235,8 +286,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
   tc_fence_after();
   if (p.rb) mbar_wait(sempty + NST, 0);
   const uint32_t tmem = *tmem_slot;
-  const int64_t c0 = p.counts ? int64_t(p.counts[0]) : 0;
-  const int total = int(num_m_tiles(p, c0) * p.ntiles);
+  const GroupTab& gt = gtab;
+  const int total = int(num_m_tiles(gtab) * p.ntiles);
 
   if (warp >= 8 && warp < 16) {
     // ================= producers =================
@@ -260,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
     const bool kq = p.kchunks > p.kq_min;
     const int gsel = kq ? -1 : g;
     int q = 0;
-    int t_n = next_group_tile(p, c0, total, gsel, blockIdx.x, j, jj_unused, ti_n);
+    int t_n = next_group_tile<GRP>(p, gt, total, gsel, blockIdx.x, j, jj_unused, ti_n);
     int idx_n[8];
     auto load_idx = [&](const TileInfo& tq, int (&ix)[8]) {
 #pragma unroll
@@ -275,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
       int idx[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) idx[i] = idx_n[i];
-      t_n = next_group_tile(p, c0, total, gsel, t_n + gridDim.x, j, jj_unused, ti_n);
+      t_n = next_group_tile<GRP>(p, gt, total, gsel, t_n + gridDim.x, j, jj_unused, ti_n);
       if (t_n < total) load_idx(ti_n, idx_n);
       const int npb = p.nplanes[ti.group];
       const uint16_t* Bg = p.Bp[ti.group] + size_t(ti.n_tile) * p.kchunks * npb * (BN * kBK);
@@ -391,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
       const int c = lane & 7, rs = lane >> 3;
       auto next_tile = [&](int t) {
         for (; t < total; t += gridDim.x) {
-          const TileInfo ti = tile_info(p, c0, t);
+          const TileInfo ti = tile_info<GRP>(p, gt, t);
           if (ti.r0 < ti.r1) break;
         }
         return t;
@@ -399,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
       auto rows_of = [&](int t, int (&src)[32], int& nrows) {
         nrows = 0;
         if (t >= total) return;
-        const TileInfo ti = tile_info(p, c0, t);
+        const TileInfo ti = tile_info<GRP>(p, gt, t);
         nrows = int(ti.r1 - ti.r0);
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
@@ -456,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
     int qm = 0;
     int j = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const TileInfo ti = tile_info(p, c0, t);
+      const TileInfo ti = tile_info<GRP>(p, gt, t);
       if (ti.r0 >= ti.r1) continue;
       const int jj = j++;
       const int acc = jj & (NACC - 1);      // TMEM accumulator
@@ -512,17 +563,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
     auto scatter_row = [&](const TileInfo& tq) -> int64_t {
       const int64_t r = tq.r0 + rl;
       if (r >= tq.r1) return -1;
-      return p.c_rows ? int64_t(__ldg(p.c_rows + r)) : r;
+      // grouped problems: c_rows holds problem-local rows; the problem's block of C
+      const int64_t off = GRP ? int64_t(tq.group >> 1) * p.prob_rows : 0;
+      return p.c_rows ? int64_t(__ldg(p.c_rows + r)) + off : r;
     };
     TileInfo tiA, tiB, tiC;
     int jjA = 0, jjB = 0, jjC = 0;
-    int tA = next_group_tile(p, c0, total, g, blockIdx.x, j, jjA, tiA);
-    int tB = tA < total ? next_group_tile(p, c0, total, g, tA + gridDim.x, j, jjB, tiB) : total;
+    int tA = next_group_tile<GRP>(p, gt, total, g, blockIdx.x, j, jjA, tiA);
+    int tB = tA < total ? next_group_tile<GRP>(p, gt, total, g, tA + gridDim.x, j, jjB, tiB) : total;
     int64_t crA = tA < total ? scatter_row(tiA) : -1;
     int64_t crB = tB < total ? scatter_row(tiB) : -1;
     float gA = (p.gate && crA >= 0 && p.img_tokens == 0) ? __ldg(p.gate + crA) : 1.f;
     while (tA < total) {
-      const int tC = tB < total ? next_group_tile(p, c0, total, g, tB + gridDim.x, j, jjC, tiC)
+      const int tC = tB < total ? next_group_tile<GRP>(p, gt, total, g, tB + gridDim.x, j, jjC, tiC)
                                 : total;
       const int64_t crC = tC < total ? scatter_row(tiC) : -1;
       const float gB = (p.gate && crB >= 0 && p.img_tokens == 0) ? __ldg(p.gate + crB) : 1.f;

@@ -92,12 +92,14 @@ static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cu
   using namespace tc;
   if (p.M == 0) return SA_OK;
   p.ntiles = int(cdiv(p.N, bn));
-  const int npb_max = max(p.nplanes[0], p.counts ? p.nplanes[1] : 0);
+  const int ng = p.ngroups > 2 ? p.ngroups : (p.counts ? 2 : 1);
+  int npb_max = 0;
+  for (int i = 0; i < ng; ++i) npb_max = max(npb_max, p.nplanes[i]);
   // resident weights when both experts' packed tiles fit in 48 KB
   p.ntiles = int(cdiv(p.N, bn));
   const size_t wb0 = size_t(p.ntiles) * p.kchunks * p.nplanes[0] * bn * kBK * 2;
   const size_t wb1 = p.counts ? size_t(p.ntiles) * p.kchunks * p.nplanes[1] * bn * kBK * 2 : 0;
-  p.rb = (g_tc_resident && wb0 + wb1 <= 48 * 1024) ? 1 : 0;
+  p.rb = (g_tc_resident && p.ngroups <= 2 && wb0 + wb1 <= 48 * 1024) ? 1 : 0;
   p.dbg = g_tc_dbg;
   p.kq_min = g_tc_kq;
   p.rb_bytes[0] = p.rb ? uint32_t(wb0) : 0u;
@@ -167,7 +169,9 @@ static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cu
   case BNV: {                                                                                    \
     auto kfn = amode == A_PLAIN                                                                  \
                    ? (res_tma ? tc_gemm_kernel<BNV, A_PLAIN, true> : tc_gemm_kernel<BNV, A_PLAIN>) \
-               : amode == A_GATHER ? tc_gemm_kernel<BNV, A_GATHER>                              \
+               : amode == A_GATHER                                                             \
+                   ? (p.ngroups > 2 ? tc_gemm_kernel<BNV, A_GATHER, false, false, true>            \
+                                    : tc_gemm_kernel<BNV, A_GATHER>)                               \
                : (p.ln_g ? tc_gemm_kernel<BNV, A_PATCH, false, (BNV == 32 || BNV == 64)>         \
                          : tc_gemm_kernel<BNV, A_PATCH>);                                       \
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));          \
@@ -257,6 +261,35 @@ extern "C" int sa_tc_linear(const float* x, const void* wpack, int w_kind, int b
   p.residual = residual;
   p.act = act;
   return launch_tc(p, tc::A_PLAIN, bn, cdiv(M, tc::kBM), as_stream(stream));
+}
+
+// The q/k/v projections of one attention layer routed by one fused LN+router
+// pass (stacked plans: perm [nprob][M], counts [nprob][2], gate [nprob][M]) in
+// ONE launch: 2·nprob row groups (problem x expert) over the same input x, y
+// stacked [nprob][M][N]. Per problem identical to sa_tc_moe_linear.
+extern "C" int sa_tc_moe_linear_grouped(const float* x, const int32_t* perm, const int32_t* counts,
+                                        const float* gate, const void* const* wpack_dense,
+                                        const void* const* wpack_shift, int nprob, int bn,
+                                        float* y, int64_t M, int64_t K, int64_t N, void* stream) {
+  SA_REQUIRE(nprob >= 1 && nprob <= 3, SA_ERR_VALUE, "sa_tc_moe_linear_grouped: 1..3 problems");
+  SA_REQUIRE(M * nprob < (int64_t(1) << 31), SA_ERR_SHAPE, "sa_tc_moe_linear_grouped: too many rows");
+  if (int st = tc_check("sa_tc_moe_linear_grouped", M * nprob, K, N, bn)) return st;
+  tc::TcParams p = tc_base(M * nprob, K, N);
+  p.A = x;
+  p.a_rows = perm;
+  for (int i = 0; i < nprob; ++i) {
+    p.Bp[2 * i] = static_cast<const uint16_t*>(wpack_dense[i]);
+    p.nplanes[2 * i] = 3;
+    p.Bp[2 * i + 1] = static_cast<const uint16_t*>(wpack_shift[i]);
+    p.nplanes[2 * i + 1] = 1;
+  }
+  p.ngroups = 2 * nprob;
+  p.prob_rows = M;
+  p.counts = counts;
+  p.C = y;
+  p.c_rows = perm;
+  p.gate = gate;
+  return launch_tc(p, tc::A_GATHER, bn, nprob * (cdiv(M, tc::kBM) + 1), as_stream(stream));
 }
 
 extern "C" int sa_tc_moe_linear(const float* x, const int32_t* perm, const int32_t* counts,

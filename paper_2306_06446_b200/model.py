@@ -115,6 +115,7 @@ def tc_enabled() -> bool:
 # LayerNorm fused with the routers that read its output (d = 32 / 64)
 FUSE_LN_ROUTE = os.environ.get("SA_FUSE_LN_ROUTE", "1") == "1"
 FUSE_EMBED_LN = os.environ.get("SA_FUSE_EMBED_LN", "1") == "1"
+FUSE_GROUPED_QKV = os.environ.get("SA_FUSE_GROUPED_QKV", "1") == "1"
 # fc1 → GELU → fc2 in one tensor-core kernel (d = 32 / 64)
 FUSE_MLP = os.environ.get("SA_FUSE_MLP", "1") == "1"
 # LN1 + q/k/v routers + both experts of q/k/v + sign-hash in one kernel (d = 32 / 64)
@@ -497,7 +498,9 @@ class AttentionLayer:
         x = to_device(x)
         batch, n, d = x.shape
         flat = x.reshape(batch * n, d)
-        if plans is not None:   # q/k/v routed by the fused LN1+router pass
+        if plans is not None and self._grouped_qkv_ok(flat, plans):
+            q, k, v = self._grouped_qkv(flat, plans)
+        elif plans is not None:   # q/k/v routed by the fused LN1+router pass
             q = self.proj["q"].forward(flat, plan=plans[0])
             k = self.proj["k"].forward(flat, plan=plans[1])
             v = self.proj["v"].forward(flat, plan=plans[2])
@@ -517,6 +520,43 @@ class AttentionLayer:
         res = residual.reshape(batch * n, d) if residual is not None else None
         y = self.proj["o"].forward(merged, residual=res)
         return y.reshape(batch, n, d)
+
+    def _grouped_qkv_ok(self, flat, plans) -> bool:
+        """One grouped launch for q/k/v: tensor-core path, (Linear, Shift) experts
+        of one shape, and plans stacked in one device buffer (sa_ln_route)."""
+        if not (FUSE_GROUPED_QKV and tc_enabled() and len(plans) == 3):
+            return False
+        projs = [self.proj[k] for k in ("q", "k", "v")]
+        if not all(isinstance(p, MoeModule) and _dual_expert_linear(p) for p in projs):
+            return False
+        M = flat.shape[0]
+        for attr, stride in (("perm_dev", M * 4), ("gate_dev", M * 4), ("counts_dev", 8)):
+            base = getattr(plans[0], attr)
+            if base is None or not base.is_contiguous():
+                return False
+            for r in (1, 2):
+                t = getattr(plans[r], attr)
+                if t is None or t.data_ptr() != base.data_ptr() + r * stride:
+                    return False
+        return True
+
+    def _grouped_qkv(self, flat, plans):
+        """sa_tc_moe_linear_grouped: the three MoE projections in one launch."""
+        import ctypes
+        M, d = flat.shape
+        projs = [self.proj[k] for k in ("q", "k", "v")]
+        N = projs[0].experts[0].out_dim
+        y = torch.empty((3, M, N), dtype=torch.float32, device=flat.device)
+        dense = (ctypes.c_void_p * 3)(*[_lib.ptr(p.experts[0].tc_pack()[0]) for p in projs])
+        shift = (ctypes.c_void_p * 3)(*[_lib.ptr(p.experts[1].tc_pack()[0]) for p in projs])
+        bn = projs[0].experts[0].tc_pack()[1]
+        _lib.call("sa_tc_moe_linear_grouped", _lib.ptr(flat), _lib.ptr(plans[0].perm_dev),
+                  _lib.ptr(plans[0].counts_dev), _lib.ptr(plans[0].gate_dev),
+                  ctypes.addressof(dense), ctypes.addressof(shift), 3, bn, _lib.ptr(y), M, d, N,
+                  _stream())
+        for p, plan in zip(projs, plans):
+            p.last_plan = plan
+        return y[0], y[1], y[2]
 
     def named_params(self, prefix):
         for key in ("q", "k", "v", "o"):

@@ -244,3 +244,27 @@ def test_fused_embed_layernorm_bit_identical(golden, name):
     finally:
         MD.FUSE_EMBED_LN = old
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("name", ["pvt_small", "pvt_b0_full"])
+def test_grouped_qkv_projections_bit_identical(golden, name):
+    """sa_tc_moe_linear_grouped (the q/k/v MoE projections of a d = 160 stage in
+    one launch) computes each problem exactly as sa_tc_moe_linear."""
+    from paper_2306_06446_b200 import model as MD
+    fx = golden(name)
+    spec = FIXTURES[name]()
+    m = MD.Network(spec)
+    b = min(int(fx["batch"]), 4)
+    images = fx["images"][:b] if "images" in fx else ops.rng(int(fx["images_seed"])).uniform(
+        0, 1, (b, spec["img"], spec["img"], 3)).astype(F32)
+    x = dev(images)
+    old = MD.FUSE_GROUPED_QKV
+    try:
+        MD.FUSE_GROUPED_QKV = False
+        ref = host(m.forward(x))
+        MD.FUSE_GROUPED_QKV = True
+        got = host(m.forward(x))
+    finally:
+        MD.FUSE_GROUPED_QKV = old
+    assert np.array_equal(got, ref)
+    assert rel_err(got, fx["logits"][:b]) < LOGIT_TOL
