@@ -420,25 +420,28 @@ __global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, c
   if (warp == kMma) tmem_dealloc<512>(tmem);
 }
 
-// γ[r][b·H + h] = Σ |y| over image b's rows of head h / (n · 32), summing the
-// 32-row segment partials in segment order (deterministic).
+// γ[r][b·H + h] = Σ |y| over image b's rows of head h / (n · 32): one warp per
+// (r, b, h); lane l sums the segments l, l + 32, ... of the image in order and
+// the lanes meet in a fixed xor tree (deterministic, no atomics).
 __global__ void gamma_finalize_qkv(const double* __restrict__ gpart, int nseg, int H, int64_t B,
                                    int n, float* __restrict__ gq, float* __restrict__ gk) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= 2 * B * H) return;
+  const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= 2 * B * H) return;   // warp-uniform
   const int r = int(i / (B * H));
   const int64_t bh = i % (B * H);
   const int64_t b = bh / H;
   const int h = int(bh % H);
   const int64_t lo = b * n, hi = (b + 1) * n;   // rows of image b
   double s = 0.0;
-  for (int64_t sg = lo >> 5; sg <= (hi - 1) >> 5; ++sg) {
+  for (int64_t sg = (lo >> 5) + lane; sg <= (hi - 1) >> 5; sg += 32) {
     const int64_t b0 = (sg * 32) / n;             // image of the segment's first row
     const double* gp = gpart + ((int64_t(r) * nseg + sg) * H + h) * 2;
     s += (b0 == b) ? gp[0] : gp[1];
   }
-  const float gv = float(s / (double(n) * 32.0));
-  (r == 0 ? gq : gk)[bh] = gv;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) (r == 0 ? gq : gk)[bh] = float(s / (double(n) * 32.0));
 }
 
 }  // namespace qkv
@@ -522,8 +525,8 @@ extern "C" int sa_ln_qkv_hash(const float* x, const float* gain, const float* bi
     qkv_kernel<64, 3><<<grid, qkv::Cfg<64, 3>::THREADS, smem, s>>>(p, tmV);
   }
   const int64_t H = d / 32;
-  gamma_finalize_qkv<<<unsigned(cdiv(2 * B * H, 256)), 256, 0, s>>>(p.gpart, p.nseg, int(H), B,
-                                                                   int(n), gamma_q, gamma_k);
+  gamma_finalize_qkv<<<unsigned(cdiv(2 * B * H, 8)), 256, 0, s>>>(p.gpart, p.nseg, int(H), B,
+                                                                 int(n), gamma_q, gamma_k);
   count_launch(2);
   SA_LAUNCH_CHECK("sa_ln_qkv_hash");
   return SA_OK;
