@@ -273,6 +273,11 @@ int sa_patch_embed(const float* grid, int64_t B, int64_t H, int64_t W, int64_t C
  * attention.py:92-97, folded as at model.py:346-351): out (B*n, d) merged. */
 int sa_softmax_attn(const float* q, const float* k, const float* v, float* out, int64_t B,
                     int64_t n, int64_t d, int64_t heads, void* stream);
+/* the same on q / k / v with input row stride ld >= d (e.g. column blocks of
+ * one concatenated q|k|v projection); out is (B*n, d) */
+int sa_softmax_attn_strided(const float* q, const float* k, const float* v, int64_t ld,
+                            float* out, int64_t B, int64_t n, int64_t d, int64_t heads,
+                            void* stream);
 /* tokens.mean(axis=1) (model.py:574) or the cls token (mode 1): y (B, d) */
 int sa_pool(const float* x, float* y, int64_t B, int64_t n, int64_t d, int mode, void* stream);
 

@@ -62,6 +62,7 @@ _SIGS = {
     "sa_gemm": (_I32, [_P, _P, _P, _I64, _I64, _I64, _P]),
     "sa_layernorm": (_I32, [_P, _P, _P, _P, _I64, _I64, _F32, _P]),
     "sa_patch_embed": (_I32, [_P, _I64, _I64, _I64, _I64, _I64, _F32, _P, _I64, _P, _P, _P, _P]),
+    "sa_softmax_attn_strided": (_I32, [_P, _P, _P, _I64, _P, _I64, _I64, _I64, _I64, _P]),
     "sa_softmax_attn": (_I32, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
     "sa_pool": (_I32, [_P, _P, _I64, _I64, _I64, _I32, _P]),
     "sa_tc_tile_n": (_I32, [_I64]),

@@ -86,7 +86,8 @@ __global__ void __launch_bounds__(256) softmax_attn_kernel(const float* __restri
                                                           const float* __restrict__ k,
                                                           const float* __restrict__ v,
                                                           float* __restrict__ out, int n, int d,
-                                                          int heads, int dk, float scale_div) {
+                                                          int heads, int dk, float scale_div,
+                                                          int ld) {
   extern __shared__ __align__(16) float sm[];
   const int kp = dk + 1;
   float* sk = sm;                         // [n][dk+1]
@@ -98,14 +99,14 @@ __global__ void __launch_bounds__(256) softmax_attn_kernel(const float* __restri
   const size_t rowbase = size_t(b) * n;
   for (int idx = threadIdx.x; idx < n * dk; idx += blockDim.x) {
     const int j = idx / dk, c = idx % dk;
-    sk[j * kp + c] = k[(rowbase + j) * d + h * dk + c];
-    sv[j * dk + c] = v[(rowbase + j) * d + h * dk + c];
+    sk[j * kp + c] = k[(rowbase + j) * ld + h * dk + c];
+    sv[j * dk + c] = v[(rowbase + j) * ld + h * dk + c];
   }
   __syncthreads();
   float* myq = sq + warp * dk;
   float* myp = sp + warp * n;
   for (int i = warp; i < n; i += 8) {
-    for (int c = lane; c < dk; c += 32) myq[c] = q[(rowbase + i) * d + h * dk + c];
+    for (int c = lane; c < dk; c += 32) myq[c] = q[(rowbase + i) * ld + h * dk + c];
     __syncwarp();
     float mx = -INFINITY;
     for (int j = lane; j < n; j += 32) {
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(128) softmax_attn32_kernel(const float* __rest
                                                             const float* __restrict__ k,
                                                             const float* __restrict__ v,
                                                             float* __restrict__ out, int n, int d,
-                                                            int heads, float scale_div) {
+                                                            int heads, float scale_div, int ld) {
   constexpr int NK = 32 * NJ;
   __shared__ __align__(16) float sk[NK][36];   // pitch 36: conflict-free 128-bit row reads
   __shared__ __align__(16) float sv[NK][32];
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(128) softmax_attn32_kernel(const float* __rest
     const int j = idx >> 3, c4 = (idx & 7) * 4;
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f), bk = a, cv = a;
     if (j < n) {
-      const size_t off = (rowbase + j) * d + h * 32 + c4;
+      const size_t off = (rowbase + j) * ld + h * 32 + c4;   // inputs: row stride ld
       a = __ldg(reinterpret_cast<const float4*>(q + off));
       bk = __ldg(reinterpret_cast<const float4*>(k + off));
       cv = __ldg(reinterpret_cast<const float4*>(v + off));
@@ -330,18 +331,30 @@ static int g_softmax_qb = 4;   // queries per warp iteration (debug sweep)
 extern "C" void sa_debug_softmax_qb(int qb) { g_softmax_qb = qb; }
 extern "C" void sa_debug_softmax_generic(int on) { g_softmax_generic = on; }
 
+extern "C" int sa_softmax_attn_strided(const float* q, const float* k, const float* v,
+                                       int64_t ld, float* out, int64_t B, int64_t n, int64_t d,
+                                       int64_t heads, void* stream);
+
 extern "C" int sa_softmax_attn(const float* q, const float* k, const float* v, float* out,
                                int64_t B, int64_t n, int64_t d, int64_t heads, void* stream) {
-  SA_REQUIRE(B > 0 && n > 0 && d > 0 && heads > 0 && d % heads == 0, SA_ERR_SHAPE,
+  return sa_softmax_attn_strided(q, k, v, d, out, B, n, d, heads, stream);
+}
+
+extern "C" int sa_softmax_attn_strided(const float* q, const float* k, const float* v,
+                                       int64_t ld, float* out, int64_t B, int64_t n, int64_t d,
+                                       int64_t heads, void* stream) {
+  SA_REQUIRE(B > 0 && n > 0 && d > 0 && heads > 0 && d % heads == 0 && ld >= d, SA_ERR_SHAPE,
              "sa_softmax_attn: bad extents");
   const int64_t dk = d / heads;
   const float scale_div0 = sqrtf(float(dk));  // python float math.sqrt(dk) → f32
-  if (!g_softmax_generic && dk == 32 && n <= 64 && (d % 4) == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
+  if (!g_softmax_generic && dk == 32 && n <= 64 && (d % 4) == 0 && (ld % 4) == 0 &&
+      (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(k) & 15) == 0 && (reinterpret_cast<uintptr_t>(v) & 15) == 0) {
     const unsigned grid = unsigned(B * heads);
     cudaStream_t st = as_stream(stream);
 #define SA_SM32(NJ, QB) \
-  softmax_attn32_kernel<NJ, QB><<<grid, 128, 0, st>>>(q, k, v, out, int(n), int(d), int(heads), scale_div0)
+  softmax_attn32_kernel<NJ, QB><<<grid, 128, 0, st>>>(q, k, v, out, int(n), int(d), int(heads), \
+                                                      scale_div0, int(ld))
     if (n <= 32) {
       if (g_softmax_qb == 2) SA_SM32(1, 2);
       else if (g_softmax_qb == 8) SA_SM32(1, 8);
@@ -362,7 +375,7 @@ extern "C" int sa_softmax_attn(const float* q, const float* k, const float* v, f
   cudaFuncSetAttribute(softmax_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   const float scale_div = sqrtf(float(dk));  // python float math.sqrt(dk) → f32
   softmax_attn_kernel<<<unsigned(B * heads), 256, smem, as_stream(stream)>>>(
-      q, k, v, out, int(n), int(d), int(heads), int(dk), scale_div);
+      q, k, v, out, int(n), int(d), int(heads), int(dk), scale_div, int(ld));
   count_launch(1);
   SA_LAUNCH_CHECK("sa_softmax_attn");
   return SA_OK;

@@ -116,6 +116,7 @@ def tc_enabled() -> bool:
 FUSE_LN_ROUTE = os.environ.get("SA_FUSE_LN_ROUTE", "1") == "1"
 FUSE_EMBED_LN = os.environ.get("SA_FUSE_EMBED_LN", "1") == "1"
 FUSE_GROUPED_QKV = os.environ.get("SA_FUSE_GROUPED_QKV", "1") == "1"
+FUSE_DENSE_QKV = os.environ.get("SA_FUSE_DENSE_QKV", "1") == "1"
 # fc1 → GELU → fc2 in one tensor-core kernel (d = 32 / 64)
 FUSE_MLP = os.environ.get("SA_FUSE_MLP", "1") == "1"
 # LN1 + q/k/v routers + both experts of q/k/v + sign-hash in one kernel (d = 32 / 64)
@@ -258,7 +259,10 @@ def _linear_call(layer, x, residual, act):
     y = torch.empty((x2.shape[0], layer.out_dim), dtype=torch.float32, device=x.device)
     res = residual.reshape(y.shape) if residual is not None else None
     if tc_enabled():
-        pk, bn, kind = layer.tc_pack()
+        # few row tiles (e.g. the classifier head, M = batch): narrow column
+        # tiles so the grid covers more SMs
+        small = x2.shape[0] <= 4096 and layer.out_dim > 256
+        pk, bn, kind = layer.tc_pack(64) if small else layer.tc_pack()
         _lib.call("sa_tc_linear", _lib.ptr(x2), _lib.ptr(pk), kind, bn, _lib.ptr(y), x2.shape[0],
                   layer.in_dim, layer.out_dim, _lib.ptr(res), int(act), _stream())
         return y.reshape(*lead, layer.out_dim)
@@ -498,6 +502,15 @@ class AttentionLayer:
         x = to_device(x)
         batch, n, d = x.shape
         flat = x.reshape(batch * n, d)
+        if plans is None and self.cfg.attn_mode == "softmax" and self._dense_qkv_ok():
+            # exempt MSA stage: one GEMM against [W_q | W_k | W_v], strided core
+            y = self._qkv_cat_linear().forward(flat)
+            merged = torch.empty_like(flat)
+            _lib.call("sa_softmax_attn_strided", _lib.ptr(y), y.data_ptr() + 4 * d,
+                      y.data_ptr() + 8 * d, 3 * d, _lib.ptr(merged), batch, n, d, self.heads,
+                      _stream())
+            res = residual.reshape(batch * n, d) if residual is not None else None
+            return self.proj["o"].forward(merged, residual=res).reshape(batch, n, d)
         if plans is not None and self._grouped_qkv_ok(flat, plans):
             q, k, v = self._grouped_qkv(flat, plans)
         elif plans is not None:   # q/k/v routed by the fused LN1+router pass
@@ -520,6 +533,19 @@ class AttentionLayer:
         res = residual.reshape(batch * n, d) if residual is not None else None
         y = self.proj["o"].forward(merged, residual=res)
         return y.reshape(batch, n, d)
+
+    def _dense_qkv_ok(self) -> bool:
+        projs = [self.proj[k] for k in ("q", "k", "v")]
+        return (FUSE_DENSE_QKV and tc_enabled() and all(type(p) is Linear for p in projs)
+                and len({(p.in_dim, p.out_dim) for p in projs}) == 1)
+
+    def _qkv_cat_linear(self):
+        """[W_q | W_k | W_v] as one Linear (built once; column tiles of the
+        concatenation are the separate projections' tiles, bit for bit)."""
+        if getattr(self, "_qkv_cat", None) is None:
+            w = torch.cat([self.proj[k].w.value for k in ("q", "k", "v")], dim=1).contiguous()
+            self._qkv_cat = Linear(w)
+        return self._qkv_cat
 
     def _grouped_qkv_ok(self, flat, plans) -> bool:
         """One grouped launch for q/k/v: tensor-core path, (Linear, Shift) experts
@@ -571,6 +597,7 @@ class AttentionLayer:
     def post_step(self):
         for key in ("q", "k", "v", "o"):
             self.proj[key].post_step()
+        self._qkv_cat = None   # weights may have changed
 
 
 class Block:

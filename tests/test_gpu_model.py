@@ -268,3 +268,26 @@ def test_grouped_qkv_projections_bit_identical(golden, name):
         MD.FUSE_GROUPED_QKV = old
     assert np.array_equal(got, ref)
     assert rel_err(got, fx["logits"][:b]) < LOGIT_TOL
+
+
+@pytest.mark.parametrize("name", ["pvt_small", "pvt_b0_full"])
+def test_dense_qkv_concat_bit_identical(golden, name):
+    """The exempt MSA stage's q/k/v as one GEMM against [W_q | W_k | W_v] and
+    the strided softmax core reproduce the three-GEMM path exactly."""
+    from paper_2306_06446_b200 import model as MD
+    fx = golden(name)
+    spec = FIXTURES[name]()
+    m = MD.Network(spec)
+    b = min(int(fx["batch"]), 4)
+    images = fx["images"][:b] if "images" in fx else ops.rng(int(fx["images_seed"])).uniform(
+        0, 1, (b, spec["img"], spec["img"], 3)).astype(F32)
+    x = dev(images)
+    old = MD.FUSE_DENSE_QKV
+    try:
+        MD.FUSE_DENSE_QKV = False
+        ref = host(m.forward(x))
+        MD.FUSE_DENSE_QKV = True
+        got = host(m.forward(x))
+    finally:
+        MD.FUSE_DENSE_QKV = old
+    assert np.array_equal(got, ref)
