@@ -467,6 +467,152 @@ __global__ void __launch_bounds__(1024, 1) ln_route_warp_kernel(
   }
 }
 
+// Wide rows, 8 lanes per row (4 rows per warp step): lane t of a row's group
+// holds channels 32i + 4t .. 32i + 4t + 3 (i < PER), i.e. the partials of the
+// 32 "virtual lanes" l = 4t + j of layernorm_kernel. Its xor butterfly over
+// 16, 8, 4 becomes shuffles by 4, 2, 1 inside the group, and over 2, 1 adds
+// inside the thread: y is bit-identical to sa_layernorm, with ~3x fewer
+// instructions per row than one warp per row. Routers: fp64 lane chains over
+// the lane's channels + a fixed xor tree. LN = false: routers on x itself.
+constexpr int kOctThreads = 128, kOctRows = 64;   // 4 warps x 4 steps x 4 rows
+
+template <int PER, bool LN>
+__global__ void __launch_bounds__(kOctThreads) ln_route_oct_kernel(
+    const float* __restrict__ x, const float* __restrict__ gain, const float* __restrict__ bias,
+    float* __restrict__ y, int64_t M, float eps, int nr, const float* __restrict__ wg0,
+    const float* __restrict__ wg1, const float* __restrict__ wg2, float tie_thresh,
+    int32_t* __restrict__ expert_of, float* __restrict__ gate, int32_t* __restrict__ block_cnt1) {
+  constexpr int D = 32 * PER;
+  constexpr int kSteps = kOctRows / (kOctThreads / 32 * 4);
+  __shared__ __align__(16) double sw[kMaxRouters][2][D];   // [router][expert][channel]
+  __shared__ int wcnt[kMaxRouters][kOctThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane >> 3, t = lane & 7;
+  const float* wgs[kMaxRouters] = {wg0, wg1, wg2};
+  for (int r = 0; r < nr; ++r)
+    for (int i = threadIdx.x; i < 2 * D; i += kOctThreads) sw[r][i & 1][i >> 1] = double(wgs[r][i]);
+  __syncthreads();
+  const int64_t base = int64_t(blockIdx.x) * kOctRows + warp * (kSteps * 4);
+  int cnt[kMaxRouters] = {0, 0, 0};
+  float4 vn[PER];
+  auto load_row = [&](int step, float4 (&dst)[PER]) {
+    const int64_t row = base + step * 4 + sub;
+#pragma unroll
+    for (int i = 0; i < PER; ++i)
+      dst[i] = row < M ? __ldg(reinterpret_cast<const float4*>(x + row * D + 32 * i + 4 * t))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  load_row(0, vn);
+#pragma unroll 1
+  for (int step = 0; step < kSteps; ++step) {
+    const int64_t row = base + step * 4 + sub;
+    float4 v[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) v[i] = vn[i];
+    if (step + 1 < kSteps) load_row(step + 1, vn);   // next rows in flight
+    if (LN) {
+      // virtual-lane partials (channel order within each virtual lane)
+      float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        p0 += v[i].x;
+        p1 += v[i].y;
+        p2 += v[i].z;
+        p3 += v[i].w;
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+        p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+        p2 += __shfl_xor_sync(0xffffffffu, p2, o);
+        p3 += __shfl_xor_sync(0xffffffffu, p3, o);
+      }
+      const float mean = ((p0 + p2) + (p1 + p3)) / float(D);
+      float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        v[i].x = v[i].x - mean;
+        v[i].y = v[i].y - mean;
+        v[i].z = v[i].z - mean;
+        v[i].w = v[i].w - mean;
+        q0 += v[i].x * v[i].x;
+        q1 += v[i].y * v[i].y;
+        q2 += v[i].z * v[i].z;
+        q3 += v[i].w * v[i].w;
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        q0 += __shfl_xor_sync(0xffffffffu, q0, o);
+        q1 += __shfl_xor_sync(0xffffffffu, q1, o);
+        q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+        q3 += __shfl_xor_sync(0xffffffffu, q3, o);
+      }
+      const float var = ((q0 + q2) + (q1 + q3)) / float(D);
+      const float inv = 1.0f / sqrtf(var + eps);
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const float4 g4 = __ldg(reinterpret_cast<const float4*>(gain + 32 * i + 4 * t));
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + 32 * i + 4 * t));
+        v[i].x = v[i].x * inv * g4.x + b4.x;
+        v[i].y = v[i].y * inv * g4.y + b4.y;
+        v[i].z = v[i].z * inv * g4.z + b4.z;
+        v[i].w = v[i].w * inv * g4.w + b4.w;
+        if (row < M) *reinterpret_cast<float4*>(y + row * D + 32 * i + 4 * t) = v[i];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kMaxRouters; ++r) {
+      if (r >= nr) break;   // uniform
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int c = 32 * i + 4 * t;
+        const double2 a0 = *reinterpret_cast<const double2*>(&sw[r][0][c]);
+        const double2 a1 = *reinterpret_cast<const double2*>(&sw[r][0][c + 2]);
+        const double2 b0 = *reinterpret_cast<const double2*>(&sw[r][1][c]);
+        const double2 b1 = *reinterpret_cast<const double2*>(&sw[r][1][c + 2]);
+        s0 = fma(double(v[i].x), a0.x, s0);
+        s1 = fma(double(v[i].x), b0.x, s1);
+        s0 = fma(double(v[i].y), a0.y, s0);
+        s1 = fma(double(v[i].y), b0.y, s1);
+        s0 = fma(double(v[i].z), a1.x, s0);
+        s1 = fma(double(v[i].z), b1.x, s1);
+        s0 = fma(double(v[i].w), a1.y, s0);
+        s1 = fma(double(v[i].w), b1.y, s1);
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      }
+      float gt;
+      const int e = decide(float(s0), float(s1), tie_thresh, gt);
+      if (t == 0 && row < M) {
+        expert_of[size_t(r) * M + row] = e;
+        gate[size_t(r) * M + row] = gt;
+        cnt[r] += e;
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kMaxRouters; ++r) {
+    const int c = __reduce_add_sync(0xffffffffu, cnt[r]);
+    if (lane == 0 && r < nr) wcnt[r][warp] = c;
+  }
+  __syncthreads();
+  // the 256-token block count (zeroed by the host) gets this CTA's share:
+  // integer adds, so the result is order-independent
+  if (threadIdx.x < nr) {
+    int c = 0;
+    for (int w = 0; w < kOctThreads / 32; ++w) c += wcnt[threadIdx.x][w];
+    const int nb = int((M + kRouteTok - 1) / kRouteTok);
+    atomicAdd(&block_cnt1[size_t(threadIdx.x) * nb + blockIdx.x / (kRouteTok / kOctRows)], c);
+  }
+}
+
+static int g_route_oct = 1;
+extern "C" void sa_debug_route_oct(int on) { g_route_oct = on; }
+
 }  // namespace sa
 
 using namespace sa;
@@ -499,6 +645,19 @@ extern "C" int sa_ln_route(const float* x, const float* gain, const float* bias,
     cudaFuncSetAttribute(ln_route_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     ln_route_kernel<64><<<nb, kRouteTok, smem, s>>>(x, gain, bias, y, M, eps, nr, wg0, wg1,
                                                     wg2, tie_thresh, expert_of, gate, block_cnt1);
+  } else if (g_route_oct) {
+    cudaMemsetAsync(block_cnt1, 0, size_t(nb) * nr * sizeof(int32_t), s);
+#define SA_LNRO(P)                                                                              \
+  case P:                                                                                       \
+    ln_route_oct_kernel<P, true><<<unsigned(cdiv(M, kOctRows)), kOctThreads, 0, s>>>(         \
+        x, gain, bias, y, M, eps, nr, wg0,                                                      \
+                                                          wg1, wg2, tie_thresh, expert_of,     \
+                                                          gate, block_cnt1);                   \
+    break;
+    switch (d / 32) {
+      SA_LNRO(1) SA_LNRO(2) SA_LNRO(3) SA_LNRO(4) SA_LNRO(5) SA_LNRO(6) SA_LNRO(7) SA_LNRO(8)
+    }
+#undef SA_LNRO
   } else {
 #define SA_LNRW(P)                                                                             \
   case P:                                                                                      \
@@ -540,11 +699,25 @@ extern "C" int sa_moe_route(const float* x, const float* wg, int64_t M, int64_t 
   const int nb = int(cdiv(M, kRouteTok));
   int32_t* block_cnt1 = static_cast<int32_t*>(ws);
   int32_t* block_off1 = block_cnt1 + nb;
-  // one thread per token for every width: the row streams in 64-channel
-  // chunks with all loads of a chunk in flight (8 lanes per token with a
-  // per-pass loop serialised 8 passes of latency per block)
-  route_kernel<1><<<nb, 256, 0, s>>>(x, wg, M, int(d), tie_thresh, logits, expert_of, gate,
-                                     block_cnt1);
+  if (g_route_oct && logits == nullptr && d % 32 == 0 && d >= 96 && d <= 256) {
+    // wide rows: 8 lanes per row (the LN+router kernel without its LayerNorm)
+    cudaMemsetAsync(block_cnt1, 0, size_t(nb) * sizeof(int32_t), s);
+#define SA_RO(P)                                                                               \
+  case P:                                                                                      \
+    ln_route_oct_kernel<P, false><<<unsigned(cdiv(M, kOctRows)), kOctThreads, 0, s>>>(        \
+        x, nullptr, nullptr, nullptr, M,                                                        \
+                                                           0.f, 1, wg, nullptr, nullptr,      \
+                                                           tie_thresh, expert_of, gate,       \
+                                                           block_cnt1);                       \
+    break;
+    switch (d / 32) { SA_RO(3) SA_RO(4) SA_RO(5) SA_RO(6) SA_RO(7) SA_RO(8) }
+#undef SA_RO
+  } else {
+    // one thread per token: the row streams in 64-channel chunks with all
+    // loads of a chunk in flight
+    route_kernel<1><<<nb, 256, 0, s>>>(x, wg, M, int(d), tie_thresh, logits, expert_of, gate,
+                                       block_cnt1);
+  }
   route_scan_kernel<<<1, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
   partition_kernel<<<nb, kRouteTok, 0, s>>>(expert_of, block_off1, counts, M, perm);
   count_launch(3);
