@@ -44,20 +44,44 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict_
 
 // narrow rows (d = 32 / 64): one thread per row, the whole row in registers
 // via 128-bit loads — d/4 independent loads in flight per thread.
+// Each warp's 32 rows are staged through shared memory (coalesced 128-bit
+// loads and stores of the contiguous 32·D block, row pitch D + 4: conflict-free
+// 128-bit row reads), the arithmetic stays per thread = row.
 template <int D>
-__global__ void __launch_bounds__(256) layernorm_row_kernel(const float* __restrict__ x,
+__global__ void __launch_bounds__(128) layernorm_row_kernel(const float* __restrict__ x,
                                                            const float* __restrict__ gain,
                                                            const float* __restrict__ bias,
                                                            float* __restrict__ y, int64_t M,
                                                            float eps) {
-  const int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (row >= M) return;
-  const float4* xr = reinterpret_cast<const float4*>(x + row * D);
+  constexpr int P = D + 4;
+  __shared__ __align__(16) float tile[4][32 * P];   // 4 warps per block
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = int64_t(blockIdx.x) * blockDim.x + warp * 32;
+  const int nrows = int(min(int64_t(32), M - row0));
+  if (nrows <= 0) return;
+  float* tw = tile[warp];
+  {
+    const float4* src = reinterpret_cast<const float4*>(x + row0 * D);
+    float4 buf[D / 4];
+#pragma unroll
+    for (int u = 0; u < D / 4; ++u) {
+      const int i = lane + 32 * u;   // float4 index in the warp's block
+      buf[u] = i < nrows * (D / 4) ? __ldg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < D / 4; ++u) {
+      const int i = lane + 32 * u;
+      *reinterpret_cast<float4*>(tw + (i / (D / 4)) * P + 4 * (i % (D / 4))) = buf[u];
+    }
+  }
+  __syncwarp();
+  const int64_t row = row0 + lane;
+  const float4* xr = reinterpret_cast<const float4*>(tw + lane * P);
   float4 v[D / 4];
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < D / 4; ++i) {
-    v[i] = __ldg(xr + i);
+    v[i] = xr[i];
     s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
   }
   const float mean = s / float(D);
@@ -68,7 +92,7 @@ __global__ void __launch_bounds__(256) layernorm_row_kernel(const float* __restr
     q += (v[i].x * v[i].x + v[i].y * v[i].y) + (v[i].z * v[i].z + v[i].w * v[i].w);
   }
   const float inv = 1.0f / sqrtf(q / float(D) + eps);
-  float4* yr = reinterpret_cast<float4*>(y + row * D);
+  float4* yr = reinterpret_cast<float4*>(tw + lane * P);
   const float4* g4 = reinterpret_cast<const float4*>(gain);
   const float4* b4 = reinterpret_cast<const float4*>(bias);
 #pragma unroll
@@ -76,6 +100,15 @@ __global__ void __launch_bounds__(256) layernorm_row_kernel(const float* __restr
     const float4 g = __ldg(g4 + i), bb = __ldg(b4 + i);
     yr[i] = make_float4(v[i].x * inv * g.x + bb.x, v[i].y * inv * g.y + bb.y,
                         v[i].z * inv * g.z + bb.z, v[i].w * inv * g.w + bb.w);
+  }
+  (void)row;
+  __syncwarp();
+  float4* dst = reinterpret_cast<float4*>(y + row0 * D);
+#pragma unroll
+  for (int u = 0; u < D / 4; ++u) {
+    const int i = lane + 32 * u;
+    if (i < nrows * (D / 4))
+      dst[i] = *reinterpret_cast<const float4*>(tw + (i / (D / 4)) * P + 4 * (i % (D / 4)));
   }
 }
 
@@ -306,9 +339,9 @@ extern "C" int sa_layernorm(const float* x, const float* gain, const float* bias
   if (M == 0) return SA_OK;
   cudaStream_t s = as_stream(stream);
   if (d == 32 || d == 64) {
-    const unsigned g = unsigned(cdiv(M, 256));
-    if (d == 32) layernorm_row_kernel<32><<<g, 256, 0, s>>>(x, gain, bias, y, M, eps);
-    else layernorm_row_kernel<64><<<g, 256, 0, s>>>(x, gain, bias, y, M, eps);
+    const unsigned g = unsigned(cdiv(M, 128));
+    if (d == 32) layernorm_row_kernel<32><<<g, 128, 0, s>>>(x, gain, bias, y, M, eps);
+    else layernorm_row_kernel<64><<<g, 128, 0, s>>>(x, gain, bias, y, M, eps);
     count_launch(1);
     SA_LAUNCH_CHECK("sa_layernorm");
     return SA_OK;
