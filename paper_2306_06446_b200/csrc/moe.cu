@@ -224,49 +224,48 @@ __global__ void __launch_bounds__(kRouteTok) partition_kernel(const int32_t* __r
 // writes y and, per router, the fp64 logits → winner / gate → block counts.
 constexpr int kMaxRouters = 3;
 
+constexpr int kLrThreads = 128;   // ln_route_kernel: 4 warps, each staging its own 32 rows
+
 template <int D>
-__global__ void __launch_bounds__(kRouteTok, 3) ln_route_kernel(
+__global__ void __launch_bounds__(kLrThreads) ln_route_kernel(
     const float* __restrict__ x, const float* __restrict__ gain, const float* __restrict__ bias,
     float* __restrict__ y, int64_t M, float eps, int nr, const float* __restrict__ wg0,
     const float* __restrict__ wg1, const float* __restrict__ wg2, float tie_thresh,
     int32_t* __restrict__ expert_of, float* __restrict__ gate, int32_t* __restrict__ block_cnt1) {
-  constexpr int PITCH = D + 4;  // floats; keeps the per-thread row reads 4-wavefront
+  constexpr int PITCH = D + 4;  // floats; conflict-free 128-bit row reads
   __shared__ double sw[kMaxRouters][2 * D];
-  __shared__ int wcnt[kMaxRouters][kRouteTok / 32];
-  extern __shared__ __align__(16) float tile[];  // [kRouteTok][PITCH]
+  __shared__ int wcnt[kMaxRouters][kLrThreads / 32];
+  extern __shared__ __align__(16) float tile[];  // [kLrThreads][PITCH]
   const float* wgs[kMaxRouters] = {wg0, wg1, wg2};
   for (int r = 0; r < nr; ++r)
-    for (int i = threadIdx.x; i < 2 * D; i += kRouteTok) sw[r][i] = double(wgs[r][i]);
-  // coalesced stage-in of the block's rows (one contiguous run of float4s)
-  const int64_t row0 = int64_t(blockIdx.x) * kRouteTok;
-  const int nrows = int(min(int64_t(kRouteTok), M - row0));
+    for (int i = threadIdx.x; i < 2 * D; i += kLrThreads) sw[r][i] = double(wgs[r][i]);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // each warp stages its 32 rows (one contiguous run of float4s) with
+  // coalesced loads, all issued before the first store
+  const int64_t row0 = int64_t(blockIdx.x) * kLrThreads + warp * 32;
+  const int nrows = int(max(int64_t(0), min(int64_t(32), M - row0)));
+  float* tw = tile + warp * 32 * PITCH;
   {
-    // all of a thread's 128-bit loads are issued before the first store, so
-    // the row block costs one memory latency, not D/4 of them
     const float4* src = reinterpret_cast<const float4*>(x + row0 * D);
-    constexpr int PER = D / 4;   // float4 per thread (kRouteTok rows x D/4 / kRouteTok)
-    constexpr int CH = PER < 8 ? PER : 8;   // loads in flight per batch (register budget)
+    constexpr int PER = D / 4;
+    float4 buf[PER];
 #pragma unroll
-    for (int u0 = 0; u0 < PER; u0 += CH) {
-      float4 buf[CH];
+    for (int u = 0; u < PER; ++u) {
+      const int i = lane + 32 * u;
+      buf[u] = i < nrows * (D / 4) ? __ldg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
 #pragma unroll
-      for (int u = 0; u < CH; ++u) {
-        const int i = threadIdx.x + (u0 + u) * kRouteTok;
-        buf[u] = i < nrows * (D / 4) ? __ldg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int u = 0; u < CH; ++u) {
-        const int i = threadIdx.x + (u0 + u) * kRouteTok;
-        const int rr = i / (D / 4), c4 = i % (D / 4);
-        if (i < nrows * (D / 4)) *reinterpret_cast<float4*>(tile + rr * PITCH + 4 * c4) = buf[u];
-      }
+    for (int u = 0; u < PER; ++u) {
+      const int i = lane + 32 * u;
+      *reinterpret_cast<float4*>(tw + (i / (D / 4)) * PITCH + 4 * (i % (D / 4))) = buf[u];
     }
   }
-  __syncthreads();
-  const int64_t row = row0 + threadIdx.x;
+  __syncwarp();
+  const int64_t row = row0 + lane;
   const bool ok = row < M;
   float v[D];
-  float* trow = tile + threadIdx.x * PITCH;
+  float* trow = tw + lane * PITCH;
   if (ok) {
     float s = 0.f;
 #pragma unroll
@@ -295,19 +294,20 @@ __global__ void __launch_bounds__(kRouteTok, 3) ln_route_kernel(
           make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
     }
   }
-  __syncthreads();
-  {  // coalesced write-back of the normalized rows
+  __syncwarp();
+  {  // coalesced write-back of the warp's normalized rows
     float4* dst = reinterpret_cast<float4*>(y + row0 * D);
-    for (int i = threadIdx.x; i < nrows * (D / 4); i += kRouteTok) {
-      const int rr = i / (D / 4), c4 = i % (D / 4);
-      dst[i] = *reinterpret_cast<const float4*>(tile + rr * PITCH + 4 * c4);
+#pragma unroll
+    for (int u = 0; u < D / 4; ++u) {
+      const int i = lane + 32 * u;
+      if (i < nrows * (D / 4))
+        dst[i] = *reinterpret_cast<const float4*>(tw + (i / (D / 4)) * PITCH + 4 * (i % (D / 4)));
     }
   }
   for (int r = 0; r < nr; ++r) {
     int e = 0;
     if (ok) {
-      // router dot on the normalized row, re-read from the tile (keeps the
-      // register footprint small: no spills at 3 CTAs / SM)
+      // router dot on the normalized row, re-read from the tile
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll 4
       for (int c4 = 0; c4 < D / 4; ++c4) {
@@ -328,13 +328,16 @@ __global__ void __launch_bounds__(kRouteTok, 3) ln_route_kernel(
       gate[size_t(r) * M + row] = g;
     }
     const unsigned bal = __ballot_sync(0xffffffffu, e == 1);
-    if ((threadIdx.x & 31) == 0) wcnt[r][threadIdx.x >> 5] = __popc(bal);
+    if (lane == 0) wcnt[r][warp] = __popc(bal);
   }
   __syncthreads();
+  // this CTA's share of its 256-token block count (zeroed by the host;
+  // integer adds, order-independent)
   if (threadIdx.x < nr) {
     int c = 0;
-    for (int w = 0; w < kRouteTok / 32; ++w) c += wcnt[threadIdx.x][w];
-    block_cnt1[size_t(threadIdx.x) * gridDim.x + blockIdx.x] = c;
+    for (int w = 0; w < kLrThreads / 32; ++w) c += wcnt[threadIdx.x][w];
+    const int nb = int((M + kRouteTok - 1) / kRouteTok);
+    atomicAdd(&block_cnt1[size_t(threadIdx.x) * nb + blockIdx.x / (kRouteTok / kLrThreads)], c);
   }
 }
 
@@ -636,15 +639,18 @@ extern "C" int sa_ln_route(const float* x, const float* gain, const float* bias,
   const int nb = int(cdiv(M, kRouteTok));
   int32_t* block_cnt1 = static_cast<int32_t*>(ws);
   int32_t* block_off1 = block_cnt1 + size_t(nb) * nr;
-  if (d == 32) {
-    const int smem = kRouteTok * (32 + 4) * 4;
-    ln_route_kernel<32><<<nb, kRouteTok, smem, s>>>(x, gain, bias, y, M, eps, nr, wg0, wg1,
-                                                    wg2, tie_thresh, expert_of, gate, block_cnt1);
-  } else if (d == 64) {
-    const int smem = kRouteTok * (64 + 4) * 4;
-    cudaFuncSetAttribute(ln_route_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    ln_route_kernel<64><<<nb, kRouteTok, smem, s>>>(x, gain, bias, y, M, eps, nr, wg0, wg1,
-                                                    wg2, tie_thresh, expert_of, gate, block_cnt1);
+  if (d == 32 || d == 64) {
+    cudaMemsetAsync(block_cnt1, 0, size_t(nb) * nr * sizeof(int32_t), s);
+    const unsigned g = unsigned(cdiv(M, kLrThreads));
+    if (d == 32) {
+      const int smem = kLrThreads * (32 + 4) * 4;
+      ln_route_kernel<32><<<g, kLrThreads, smem, s>>>(x, gain, bias, y, M, eps, nr, wg0, wg1,
+                                                      wg2, tie_thresh, expert_of, gate, block_cnt1);
+    } else {
+      const int smem = kLrThreads * (64 + 4) * 4;
+      ln_route_kernel<64><<<g, kLrThreads, smem, s>>>(x, gain, bias, y, M, eps, nr, wg0, wg1,
+                                                      wg2, tie_thresh, expert_of, gate, block_cnt1);
+    }
   } else if (g_route_oct) {
     cudaMemsetAsync(block_cnt1, 0, size_t(nb) * nr * sizeof(int32_t), s);
 #define SA_LNRO(P)                                                                              \
