@@ -193,6 +193,12 @@ def op_bytes(name, args):
     if name == "sa_softmax_attn":
         B, n, d = args[4], args[5], args[6]
         return 4 * B * n * d * A
+    if name == "sa_softmax_attn_strided":
+        B, n, d = args[5], args[6], args[7]
+        return 4 * B * n * d * A
+    if name == "sa_tc_moe_linear_grouped":
+        nprob, M, K, N = args[6], args[9], args[10], args[11]
+        return nprob * (M * K * A + M * N * A + K * N * 8 + M * 12)
     if name == "sa_ln_qkv_hash":
         # x in, v out, q/k codes, three (expert, gate) dispatch arrays
         B, n, d = args[14], args[15], args[16]
