@@ -46,7 +46,9 @@ constexpr uint32_t kStgBytes = kBM * kBK * 4;   // one fp32 staging slot (128 ro
 constexpr uint32_t kPlaneA = kBM * kBK * 2;  // bytes per A plane
 constexpr int kXPitch = 20;                   // transpose buffer pitch (floats, 16B rows)
 constexpr int kXPitchW = 36;                  // 32-column transpose pitch (wide tiles)
-constexpr uint32_t kWarpSlot = 5120;          // per-epilogue-warp smem slot (>= 32*36*4, 1 KB multiple)
+// per-epilogue-warp smem slot (1 KB multiple): a TMA box (32x32 fp32) or the
+// transpose buffer (32 x kXPitch) + residual staging [2][32][16]
+constexpr uint32_t kWarpSlot = 7168;
 
 enum AMode { A_PLAIN = 0, A_GATHER = 1, A_PATCH = 2 };
 
@@ -827,9 +829,43 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
           }
           __syncwarp();
         }
-      } else
+      } else {
+      // residual rows (scattered MoE rows) staged one 16-column block ahead in
+      // the warp's slot with cp.async: each lane copies exactly the (row, 4
+      // columns) pieces it adds below, so no cross-lane synchronisation
+      float* rs = xb + 32 * kXPitch;   // [2][32][16]
+      const int c4r = (lane & 3) * 4;
+      const bool stage_res = p.residual != nullptr && vec4;
+      int64_t orow_r[4];
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int64_t meta = orow_t[quad * 32 + it * 8 + (lane >> 2)];
+        orow_r[it] = meta < 0 ? int64_t(-1) : (p.pos ? (meta & ((int64_t(1) << 40) - 1)) : meta);
+      }
+      auto issue_res = [&](int cb, int buf) {
+        const int64_t n = n_base + cb + c4r;
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          if (orow_r[it] >= 0 && n + 3 < p.N)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(
+                             smem_u32(rs + (buf * 32 + it * 8 + (lane >> 2)) * 16 + c4r)),
+                         "l"(p.residual + orow_r[it] * p.N + n)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      if (stage_res) issue_res(0, 0);
 #pragma unroll 1
       for (int cb = 0; cb < BN; cb += 16) {
+        const int rbuf = (cb >> 4) & 1;
+        if (stage_res) {
+          if (cb + 16 < BN) {
+            issue_res(cb + 16, rbuf ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+          } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+          }
+        }
         float v[16];
         tmem_ld16(t_base + uint32_t(cb), v);
 #pragma unroll
@@ -861,8 +897,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
               o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
             }
             if (p.residual) {
-              const float4 q =
-                  __ldg(reinterpret_cast<const float4*>(p.residual + orow_i * p.N + n));
+              const float4 q = *reinterpret_cast<const float4*>(rs + (rbuf * 32 + ri) * 16 + c4);
               o = make_float4(q.x + o.x, q.y + o.y, q.z + o.z, q.w + o.w);
             }
             if (!(p.dbg & 2)) *reinterpret_cast<float4*>(p.C + orow_i * p.N + n) = o;
@@ -879,6 +914,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
           }
         }
         __syncwarp();
+      }
       }
       if (!tma_tile) {
         tc_fence_before();
