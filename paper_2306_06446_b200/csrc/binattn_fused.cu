@@ -42,7 +42,12 @@ constexpr int DK = 32;
 constexpr int kThreads = 256;
 constexpr int kStreams = 16;        // pass-1 token streams (16 threads each)
 constexpr int kMaxCluster = 8;
-constexpr int kSeg = 6;             // pass-2 tokens per row segment (multiple of 3)
+// pass-2 tokens per row segment (a multiple of 3: the window ring), chosen per
+// grid side so a band's (row, segment) units fill the 32 thread slots in one
+// round where possible (side 56: 4 segments x 7 rows = 28 units)
+__host__ __device__ constexpr int seg_len(int side) {
+  return side >= 28 ? 15 : (side >= 14 ? 9 : 6);
+}
 constexpr int kMaxBandRows = 32;    // split out kernel: static mbarrier array bound
 
 struct Params {
@@ -410,6 +415,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
   wait_row(BR + 1);
   constexpr int NCG = D / 4;                 // channel groups of 4
   constexpr int SLOTS = kThreads / NCG;      // (row, segment) units per round
+  constexpr int kSeg = seg_len(SIDE);
   constexpr int SEGS = (SIDE + kSeg - 1) / kSeg;
   const int cgi = tid % NCG, slot = tid / NCG;
   if (slot >= SLOTS) return;
@@ -775,6 +781,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_out_kernel(Params p, cons
                                                                   const int* __restrict__ cnt_g, int CL) {
   constexpr int NCG = DK / 4;
   constexpr int SLOTS = kThreads / NCG;
+  constexpr int kSeg = seg_len(SIDE);
   constexpr int SEGS = (SIDE + kSeg - 1) / kSeg;
   constexpr uint32_t ROWB = uint32_t(SIDE) * DK * 4;
   constexpr uint32_t TOKB = uint32_t(DK) * 4;
