@@ -506,3 +506,45 @@ def test_fused_moe_linear_matches_unfused(M, d):
     ref = nets.moe_fwd(L, x, "m", tr)
     assert np.array_equal(e1, tr.moe[0]["expert_of"])
     assert rel_err(y1, res + ref) < 1e-5
+
+
+@pytest.mark.parametrize("M,d", [(1000, 160), (50_176, 160), (333, 96)])
+def test_grouped_moe_linear_matches_per_problem(M, d):
+    """sa_tc_moe_linear_grouped (three problems, six row groups in one launch)
+    equals three sa_tc_moe_linear calls bit for bit, including empty groups
+    (a problem routed entirely to one expert) and ragged M."""
+    import ctypes
+    from paper_2306_06446_b200 import _lib
+    from paper_2306_06446_b200 import model as MD
+    g = ops.rng(M + 7 * d)
+    x = dev(g.standard_normal((M, d)).astype(F32))
+    mods = []
+    for r in range(3):
+        w = (g.standard_normal((d, d)) / np.sqrt(d)).astype(F32)
+        mods.append((MD.Linear(w), MD.ShiftLinearLayer(w.copy())))
+    perm = np.zeros((3, M), np.int32)
+    counts = np.zeros((3, 2), np.int32)
+    gate = (0.5 + 0.5 * g.random((3, M))).astype(F32)
+    e = g.integers(0, 2, M)                       # problem 0: a random split
+    perm[0] = np.concatenate([np.flatnonzero(e == 0), np.flatnonzero(e == 1)])
+    counts[0] = [(e == 0).sum(), (e == 1).sum()]
+    perm[1] = np.arange(M)                        # problem 1: all expert 0
+    counts[1] = [M, 0]
+    perm[2] = g.permutation(M)                    # problem 2: all expert 1
+    counts[2] = [0, M]
+    perm_d, counts_d, gate_d = dev(perm), dev(counts), dev(gate)
+    packs = [(a.tc_pack(), b.tc_pack()) for a, b in mods]
+    bn = packs[0][0][1]
+    y = torch.empty((3, M, d), dtype=torch.float32, device="cuda")
+    dense = (ctypes.c_void_p * 3)(*[_lib.ptr(p[0][0]) for p in packs])
+    shift = (ctypes.c_void_p * 3)(*[_lib.ptr(p[1][0]) for p in packs])
+    _lib.call("sa_tc_moe_linear_grouped", _lib.ptr(x), _lib.ptr(perm_d), _lib.ptr(counts_d),
+              _lib.ptr(gate_d), ctypes.addressof(dense), ctypes.addressof(shift), 3, bn,
+              _lib.ptr(y), M, d, d, _lib.stream())
+    got = host(y)
+    for r in range(3):
+        yr = torch.empty((M, d), dtype=torch.float32, device="cuda")
+        _lib.call("sa_tc_moe_linear", _lib.ptr(x), _lib.ptr(perm_d[r]), _lib.ptr(counts_d[r]),
+                  _lib.ptr(gate_d[r]), _lib.ptr(packs[r][0][0]), _lib.ptr(packs[r][1][0]), bn,
+                  _lib.ptr(yr), None, M, d, d, _lib.stream())
+        assert np.array_equal(got[r], host(yr)), r
