@@ -226,7 +226,7 @@ constexpr int kMaxRouters = 3;
 
 constexpr int kLrThreads = 128;   // ln_route_kernel: 4 warps, each staging its own 32 rows
 
-template <int D>
+template <int D, bool LN = true>   // LN = false: routers on x itself (sa_moe_route), no y
 __global__ void __launch_bounds__(kLrThreads) ln_route_kernel(
     const float* __restrict__ x, const float* __restrict__ gain, const float* __restrict__ bias,
     float* __restrict__ y, int64_t M, float eps, int nr, const float* __restrict__ wg0,
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(kLrThreads) ln_route_kernel(
   const bool ok = row < M;
   float v[D];
   float* trow = tw + lane * PITCH;
-  if (ok) {
+  if (LN && ok) {
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < D / 4; ++i) {
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kLrThreads) ln_route_kernel(
     }
   }
   __syncwarp();
-  {  // coalesced write-back of the warp's normalized rows
+  if (LN) {  // coalesced write-back of the warp's normalized rows
     float4* dst = reinterpret_cast<float4*>(y + row0 * D);
 #pragma unroll
     for (int u = 0; u < D / 4; ++u) {
@@ -705,7 +705,21 @@ extern "C" int sa_moe_route(const float* x, const float* wg, int64_t M, int64_t 
   const int nb = int(cdiv(M, kRouteTok));
   int32_t* block_cnt1 = static_cast<int32_t*>(ws);
   int32_t* block_off1 = block_cnt1 + nb;
-  if (g_route_oct && logits == nullptr && d % 32 == 0 && d >= 96 && d <= 256) {
+  if (logits == nullptr && (d == 32 || d == 64)) {
+    // narrow rows: the warp-staged LN+router kernel without its LayerNorm
+    // (coalesced row staging; the same sequential fp64 channel order as
+    // route_kernel, so identical logits)
+    cudaMemsetAsync(block_cnt1, 0, size_t(nb) * sizeof(int32_t), s);
+    const unsigned g = unsigned(cdiv(M, kLrThreads));
+    if (d == 32)
+      ln_route_kernel<32, false><<<g, kLrThreads, kLrThreads * (32 + 4) * 4, s>>>(
+          x, nullptr, nullptr, nullptr, M, 0.f, 1, wg, nullptr, nullptr, tie_thresh, expert_of,
+          gate, block_cnt1);
+    else
+      ln_route_kernel<64, false><<<g, kLrThreads, kLrThreads * (64 + 4) * 4, s>>>(
+          x, nullptr, nullptr, nullptr, M, 0.f, 1, wg, nullptr, nullptr, tie_thresh, expert_of,
+          gate, block_cnt1);
+  } else if (g_route_oct && logits == nullptr && d % 32 == 0 && d >= 96 && d <= 256) {
     // wide rows: 8 lanes per row (the LN+router kernel without its LayerNorm)
     cudaMemsetAsync(block_cnt1, 0, size_t(nb) * sizeof(int32_t), s);
 #define SA_RO(P)                                                                               \
