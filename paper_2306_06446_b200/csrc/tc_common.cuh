@@ -391,14 +391,23 @@ __device__ __forceinline__ void mma_chain6_ss_w(uint32_t d, uint64_t a0, uint64_
 struct Split3 {
   __nv_bfloat162 h, m, l;
 };
+// packed fp32 pair helpers (one f32x2 instruction, each lane rounded as the
+// scalar operation would be)
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("{\n\t.reg .b64 ta, tb;\n\tmov.b64 ta, {%1, %2};\n\tmov.b64 tb, {%3, %4};\n\t"
+      "sub.rn.f32x2 %0, ta, tb;\n\t}"
+      : "=l"(r)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return make_float2(__uint_as_float(uint32_t(r)), __uint_as_float(uint32_t(r >> 32)));
+}
 __device__ __forceinline__ Split3 split3x2(float a, float b) {
   Split3 s;
   s.h = __floats2bfloat162_rn(a, b);
-  float2 hf = __bfloat1622float2(s.h);
-  float ra = a - hf.x, rb = b - hf.y;
-  s.m = __floats2bfloat162_rn(ra, rb);
-  float2 mf = __bfloat1622float2(s.m);
-  s.l = __floats2bfloat162_rn(ra - mf.x, rb - mf.y);
+  const float2 r = sub2(make_float2(a, b), __bfloat1622float2(s.h));
+  s.m = __floats2bfloat162_rn(r.x, r.y);
+  const float2 l = sub2(r, __bfloat1622float2(s.m));
+  s.l = __floats2bfloat162_rn(l.x, l.y);
   return s;
 }
 __device__ __forceinline__ uint32_t bf2_bits(__nv_bfloat162 v) {

@@ -205,6 +205,39 @@ __device__ __forceinline__ float gelu_fast(float x) {
   return __fdividef(x, 1.0f + __expf(-2.0f * u));
 }
 
+// gelu_fast on a pair with packed f32x2 multiplies / fma / add: per lane the
+// same operations as gelu_fast (x·x, x·x², fma(x³, a, x), ·c, ·(-2), ·log2e,
+// ex2.approx, +1, div.approx), so the results are bitwise identical
+__device__ __forceinline__ void gelu_fast2(float& x0, float& x1) {
+  float t0, t1;
+  asm("{\n\t.reg .b64 x, q, u, k;\n\t"
+      "mov.b64 x, {%2, %3};\n\t"
+      "mul.rn.f32x2 q, x, x;\n\t"
+      "mul.rn.f32x2 q, x, q;\n\t"
+      "mov.b64 k, {%4, %4};\n\t"
+      "fma.rn.f32x2 u, q, k, x;\n\t"
+      "mov.b64 k, {%5, %5};\n\t"
+      "mul.rn.f32x2 u, u, k;\n\t"
+      "mov.b64 k, {%6, %6};\n\t"
+      "mul.rn.f32x2 u, u, k;\n\t"
+      "mov.b64 k, {%7, %7};\n\t"
+      "mul.rn.f32x2 u, u, k;\n\t"
+      "mov.b64 {%0, %1}, u;\n\t}"
+      : "=f"(t0), "=f"(t1)
+      : "f"(x0), "f"(x1), "f"(0.044715f), "f"(0.7978845608028654f), "f"(-2.0f),
+        "f"(1.4426950408889634f));
+  float e0, e1;
+  asm("ex2.approx.f32 %0, %1;" : "=f"(e0) : "f"(t0));
+  asm("ex2.approx.f32 %0, %1;" : "=f"(e1) : "f"(t1));
+  float d0, d1;
+  asm("{\n\t.reg .b64 e, o;\n\tmov.b64 e, {%2, %3};\n\tmov.b64 o, {%4, %4};\n\t"
+      "add.rn.f32x2 e, e, o;\n\tmov.b64 {%0, %1}, e;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(e0), "f"(e1), "f"(1.0f));
+  asm("div.approx.f32 %0, %1, %2;" : "=f"(x0) : "f"(x0), "f"(d0));
+  asm("div.approx.f32 %0, %1, %2;" : "=f"(x1) : "f"(x1), "f"(d1));
+}
+
 __host__ __device__ inline size_t tc_fixed_smem() {
   return size_t(8) * kWarpSlot + 1024             // epilogue slots (+ 1 KB alignment)
          + 2 * 128 * sizeof(int64_t)                // per-group row tables
@@ -700,7 +733,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
             float4 o = make_float4(__uint_as_float(raw[4 * c]), __uint_as_float(raw[4 * c + 1]),
                                    __uint_as_float(raw[4 * c + 2]), __uint_as_float(raw[4 * c + 3]));
             if (p.act == 1) {
-              o.x = gelu_fast(o.x); o.y = gelu_fast(o.y); o.z = gelu_fast(o.z); o.w = gelu_fast(o.w);
+              gelu_fast2(o.x, o.y);
+              gelu_fast2(o.z, o.w);
             }
             if (p.gate) { o.x *= gt; o.y *= gt; o.z *= gt; o.w *= gt; }
             if (LNE) {
@@ -789,7 +823,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
             float4 o = make_float4(__uint_as_float(raw[q]), __uint_as_float(raw[q + 1]),
                                    __uint_as_float(raw[q + 2]), __uint_as_float(raw[q + 3]));
             if (p.act == 1) {
-              o.x = gelu_fast(o.x); o.y = gelu_fast(o.y); o.z = gelu_fast(o.z); o.w = gelu_fast(o.w);
+              gelu_fast2(o.x, o.y);
+              gelu_fast2(o.z, o.w);
             }
             if (p.gate) { o.x *= gt; o.y *= gt; o.z *= gt; o.w *= gt; }
             *reinterpret_cast<float4*>(xb + lane * kXPitchW + q) = o;

@@ -429,7 +429,9 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
           uint32_t hp[16], mp[16], lp[16];
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
-            const Split3 sp = split3x2(gelu_fast(v[2 * t]), gelu_fast(v[2 * t + 1]));
+            float g0 = v[2 * t], g1 = v[2 * t + 1];
+            gelu_fast2(g0, g1);
+            const Split3 sp = split3x2(g0, g1);
             hp[t] = bf2_bits(sp.h);
             mp[t] = bf2_bits(sp.m);
             lp[t] = bf2_bits(sp.l);

@@ -61,6 +61,38 @@ __global__ void weight_pack_kernel(const void* __restrict__ w, int kind, int64_t
 
 }  // namespace tc
 
+// debug: gelu_fast2 / split3x2 against their scalar forms on n patterned
+// inputs spanning [-16, 16] and the float edge values; counts mismatching bits
+__global__ void gelu_pair_check_kernel(int64_t n, unsigned long long* bad) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t h = uint32_t(i) * 2654435761u;
+  float a = (float(h >> 8) / 16777216.0f - 0.5f) * 32.0f;
+  float b = __uint_as_float(h);   // arbitrary bit patterns (incl. huge / tiny / inf / nan)
+  if (!isfinite(b)) b = -a;
+  float p0 = a, p1 = b;
+  tc::gelu_fast2(p0, p1);
+  const float s0 = tc::gelu_fast(a), s1 = tc::gelu_fast(b);
+  const tc::Split3 sp = tc::split3x2(a, b);
+  const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+  const float2 hf = __bfloat1622float2(h2);
+  const float ra = a - hf.x, rb = b - hf.y;
+  const __nv_bfloat162 m2 = __floats2bfloat162_rn(ra, rb);
+  const float2 mf = __bfloat1622float2(m2);
+  const __nv_bfloat162 l2 = __floats2bfloat162_rn(ra - mf.x, rb - mf.y);
+  const bool ok = __float_as_uint(p0) == __float_as_uint(s0) &&
+                  __float_as_uint(p1) == __float_as_uint(s1) &&
+                  tc::bf2_bits(sp.h) == tc::bf2_bits(h2) && tc::bf2_bits(sp.m) == tc::bf2_bits(m2) &&
+                  tc::bf2_bits(sp.l) == tc::bf2_bits(l2);
+  if (!ok) atomicAdd(bad, 1ull);
+}
+
+extern "C" int sa_debug_gelu_pair_check(int64_t n, unsigned long long* bad_dev, void* stream) {
+  gelu_pair_check_kernel<<<unsigned(cdiv(n, 256)), 256, 0, as_stream(stream)>>>(n, bad_dev);
+  SA_LAUNCH_CHECK("sa_debug_gelu_pair_check");
+  return SA_OK;
+}
+
 static int tc_tile_n_ok(int bn) {
   return bn == 32 || bn == 64 || bn == 128 || bn == 160 || bn == 256;
 }

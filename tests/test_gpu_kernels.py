@@ -548,3 +548,25 @@ def test_grouped_moe_linear_matches_per_problem(M, d):
                   _lib.ptr(gate_d[r]), _lib.ptr(packs[r][0][0]), _lib.ptr(packs[r][1][0]), bn,
                   _lib.ptr(yr), None, M, d, d, _lib.stream())
         assert np.array_equal(got[r], host(yr)), r
+
+
+def test_packed_gelu_and_split_bitwise_equal_scalar():
+    """gelu_fast2 / split3x2 (packed f32x2 arithmetic) reproduce the scalar
+    gelu_fast and bf16 plane split bit for bit over 2^24 patterned inputs
+    (range [-16, 16] and arbitrary finite bit patterns)."""
+    from paper_2306_06446_b200 import _lib
+    lib = _lib.load()
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    assert lib.sa_debug_gelu_pair_check(ctypes_i64(1 << 24), ctypes_p(bad.data_ptr()), None) == 0
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 0
+
+
+def ctypes_i64(v):
+    import ctypes
+    return ctypes.c_int64(v)
+
+
+def ctypes_p(v):
+    import ctypes
+    return ctypes.c_void_p(v)
