@@ -218,6 +218,74 @@ __global__ void __launch_bounds__(kRouteTok) partition_kernel(const int32_t* __r
   perm[pos] = int32_t(t);
 }
 
+// Stable partition with the block-count scan folded in: each CTA sums the
+// expert-1 counts of the blocks before it (and of all blocks, for counts[]),
+// integer adds in a fixed tree, so the result equals route_scan_kernel +
+// partition_kernel while saving the single-CTA scan launch.
+__global__ void __launch_bounds__(kRouteTok) partition_scan_kernel(
+    const int32_t* __restrict__ expert_of, const int32_t* __restrict__ block_cnt1, int64_t M,
+    int32_t* __restrict__ counts, int32_t* __restrict__ perm) {
+  const int nb = gridDim.x;
+  expert_of += size_t(blockIdx.y) * M;
+  perm += size_t(blockIdx.y) * M;
+  block_cnt1 += size_t(blockIdx.y) * nb;
+  counts += 2 * blockIdx.y;
+  __shared__ int wpre[kRouteTok / 32], wtot[kRouteTok / 32];
+  __shared__ int wc[kRouteTok / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int pre = 0, tot = 0;
+  for (int i = threadIdx.x; i < nb; i += kRouteTok) {
+    const int c = __ldg(block_cnt1 + i);
+    tot += c;
+    if (i < int(blockIdx.x)) pre += c;
+  }
+  pre = __reduce_add_sync(0xffffffffu, pre);
+  tot = __reduce_add_sync(0xffffffffu, tot);
+  if (lane == 0) {
+    wpre[warp] = pre;
+    wtot[warp] = tot;
+  }
+  const int64_t t = int64_t(blockIdx.x) * kRouteTok + threadIdx.x;
+  const bool valid = t < M;
+  const int e = valid ? expert_of[t] : 0;
+  const unsigned b1 = __ballot_sync(0xffffffffu, valid && e == 1);
+  if (lane == 0) wc[warp] = __popc(b1);
+  __syncthreads();
+  int off1 = 0, c1 = 0;
+#pragma unroll
+  for (int w = 0; w < kRouteTok / 32; ++w) {
+    off1 += wpre[w];
+    c1 += wtot[w];
+  }
+  const int64_t c0 = M - c1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    counts[0] = int32_t(c0);
+    counts[1] = c1;
+  }
+  int before1 = 0;
+  for (int w = 0; w < warp; ++w) before1 += wc[w];
+  before1 += __popc(b1 & ((1u << lane) - 1u));
+  if (!valid) return;
+  const int64_t blk0 = int64_t(blockIdx.x) * kRouteTok;
+  const int64_t pos = (e == 1) ? c0 + off1 + before1 : (blk0 - off1) + (threadIdx.x - before1);
+  perm[pos] = int32_t(t);
+}
+
+static int g_fused_partition = 1;
+extern "C" void sa_debug_fused_partition(int on) { g_fused_partition = on; }
+
+// scan + partition of nr stacked plans
+static void launch_partition(const int32_t* expert_of, int32_t* block_cnt1, int32_t* block_off1,
+                             int32_t* counts, int32_t* perm, int64_t M, int nb, int nr,
+                             cudaStream_t s) {
+  if (g_fused_partition) {
+    partition_scan_kernel<<<dim3(nb, nr), kRouteTok, 0, s>>>(expert_of, block_cnt1, M, counts, perm);
+  } else {
+    route_scan_kernel<<<nr, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
+    partition_kernel<<<dim3(nb, nr), kRouteTok, 0, s>>>(expert_of, block_off1, counts, M, perm);
+  }
+}
+
 // LayerNorm (ref tensor.py:114-128) fused with up to three routers reading the
 // normalized rows (the q/k/v projections of an AttentionLayer share one input,
 // ref model.py:342-345): one thread per row holds the D floats in registers,
@@ -676,9 +744,8 @@ extern "C" int sa_ln_route(const float* x, const float* gain, const float* bias,
     }
 #undef SA_LNRW
   }
-  route_scan_kernel<<<nr, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
-  partition_kernel<<<dim3(nb, nr), kRouteTok, 0, s>>>(expert_of, block_off1, counts, M, perm);
-  count_launch(3);
+  launch_partition(expert_of, block_cnt1, block_off1, counts, perm, M, nb, nr, s);
+  count_launch(g_fused_partition ? 2 : 3);
   SA_LAUNCH_CHECK("sa_ln_route");
   return SA_OK;
 }
@@ -738,9 +805,8 @@ extern "C" int sa_moe_route(const float* x, const float* wg, int64_t M, int64_t 
     route_kernel<1><<<nb, 256, 0, s>>>(x, wg, M, int(d), tie_thresh, logits, expert_of, gate,
                                        block_cnt1);
   }
-  route_scan_kernel<<<1, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
-  partition_kernel<<<nb, kRouteTok, 0, s>>>(expert_of, block_off1, counts, M, perm);
-  count_launch(3);
+  launch_partition(expert_of, block_cnt1, block_off1, counts, perm, M, nb, 1, s);
+  count_launch(g_fused_partition ? 2 : 3);
   SA_LAUNCH_CHECK("sa_moe_route");
   return SA_OK;
 }
@@ -760,9 +826,8 @@ extern "C" int sa_moe_dispatch(const float* logits, int64_t M, float tie_thresh,
   int32_t* block_cnt1 = static_cast<int32_t*>(ws);
   int32_t* block_off1 = block_cnt1 + nb;
   dispatch_kernel<<<nb, kRouteTok, 0, s>>>(logits, M, tie_thresh, expert_of, gate, block_cnt1);
-  route_scan_kernel<<<1, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
-  partition_kernel<<<nb, kRouteTok, 0, s>>>(expert_of, block_off1, counts, M, perm);
-  count_launch(3);
+  launch_partition(expert_of, block_cnt1, block_off1, counts, perm, M, nb, 1, s);
+  count_launch(g_fused_partition ? 2 : 3);
   SA_LAUNCH_CHECK("sa_moe_dispatch");
   return SA_OK;
 }
@@ -799,9 +864,8 @@ extern "C" int sa_moe_partition(const int32_t* expert_of, int64_t M, int32_t* co
   int32_t* block_cnt1 = static_cast<int32_t*>(ws);
   int32_t* block_off1 = block_cnt1 + nb;
   count_kernel<<<nb, kRouteTok, 0, s>>>(expert_of, M, block_cnt1);
-  route_scan_kernel<<<1, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
-  partition_kernel<<<nb, kRouteTok, 0, s>>>(expert_of, block_off1, counts, M, perm);
-  count_launch(3);
+  launch_partition(expert_of, block_cnt1, block_off1, counts, perm, M, nb, 1, s);
+  count_launch(g_fused_partition ? 2 : 3);
   SA_LAUNCH_CHECK("sa_moe_partition");
   return SA_OK;
 }
