@@ -31,7 +31,7 @@
 //     over the shared-memory band (3 new float4 per token).
 #include <cooperative_groups.h>
 
-#include "common.cuh"
+#include "tc_common.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -138,7 +138,8 @@ struct Win {   // one window column: 4 channels of 3 grid rows (packed pairs)
 // D = model dim (heads = D / 32), SIDE = token-grid side: every shared-memory
 // stride is a compile-time constant.
 template <int D, int SIDE>
-__global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
+__global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
+                                                                    const __grid_constant__ CUtensorMap tmV) {
   constexpr int HEADS = D / DK;
   constexpr uint32_t ROWB = uint32_t(SIDE) * D * 4;   // bytes per smem grid row
   constexpr uint32_t TOKB = uint32_t(D) * 4;          // bytes per token
@@ -167,8 +168,6 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
   const int r1 = min(p.rows_total, r0 + BR);
   const int t_lo = min(n, r0 * SIDE), t_hi = min(n, r1 * SIDE);
   const int nt = t_hi - t_lo;
-  const float* vb = p.v + size_t(b) * n * ld + hz * DK;
-
   // ---- 1. band of V (+ halo rows) → shared memory ----------------------------
   // smem row R holds grid row r0 - 1 + R; cells past n and rows outside the
   // grid are zero (the reference's zero-padded token grid, attention.py:170-179)
@@ -178,44 +177,23 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
     for (int R = 0; R < BR + 2; ++R)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + R)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // band rows first (pass 1 needs them), the two halo rows last
+    // one TMA copy per grid row from the (channel, token, image) tensor map:
+    // box = the head's 32 channels x SIDE tokens; rows outside the grid and
+    // cells past n are out of bounds and arrive as zeros (the reference's
+    // zero-padded token grid, attention.py:170-179). Band rows first, halos last.
     for (int i = 0; i < BR + 2; ++i) {
       const int R = i < BR ? i + 1 : (i == BR ? 0 : BR + 1);
       const int rr = r0 - 1 + R;
-      const int ntok = (rr >= 0 && rr < p.rows_total) ? max(0, min(SIDE, n - rr * SIDE)) : 0;
-      // single-head images: a grid row is one contiguous run (bulk copy);
-      // head slices of a wider model are strided and come in by cp.async below
-      const uint32_t bytes = ld == D ? uint32_t(ntok) * TOKB : 0u;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar + R)),
-                   "r"(bytes)
+                   "r"(ROWB)
                    : "memory");
-      if (bytes == 0) continue;
       asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              su32(Vb + R * ROWB)),
-          "l"(vb + size_t(rr) * SIDE * D), "r"(bytes), "r"(su32(bar + R))
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(su32(Vb + R * ROWB)),
+          "l"(reinterpret_cast<uint64_t>(&tmV)), "r"(hz * DK), "r"(rr * SIDE), "r"(b),
+          "r"(su32(bar + R))
           : "memory");
     }
-  }
-  if (ld != D) {   // strided head slice: 16-byte cp.async per (token, chunk)
-    const int tok_lo = max(0, (r0 - 1) * SIDE);
-    const int tok_hi = min(n, (r0 + BR + 1) * SIDE);
-    const int smem_tok0 = (r0 - 1) * SIDE;          // token of smem row 0, column 0
-    for (int i = tid; i < (tok_hi - tok_lo) * (D / 4); i += kThreads) {
-      const int t = tok_lo + i / (D / 4), c4 = i % (D / 4);
-      const uint32_t dst = su32(Vb) + uint32_t(t - smem_tok0) * TOKB + c4 * 16;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
-                   "l"(vb + size_t(t) * ld + c4 * 4)
-                   : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  for (int R = 0; R < BR + 2; ++R) {   // zero the cells no copy fills
-    const int rr = r0 - 1 + R;
-    const int ntok = (rr >= 0 && rr < p.rows_total) ? max(0, min(SIDE, n - rr * SIDE)) : 0;
-    float4* z = reinterpret_cast<float4*>(Vb + R * ROWB + ntok * TOKB);
-    const int nz = (SIDE - ntok) * D / 4;
-    for (int i = tid; i < nz; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   for (int i = tid; i < HEADS * nt; i += kThreads) {   // codes of the band, [head][token]
     const int h = i / nt, t = i - h * nt;
@@ -225,8 +203,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p) {
   }
   for (int i = tid; i < 256 * 8; i += kThreads)          // byte → 8 masks
     mt[i] = ((i >> 3) >> (i & 7)) & 1 ? 1.0f : 0.0f;
-  if (ld != D) asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();  // barrier init, codes, masks (and strided V) visible
+  __syncthreads();  // barrier init, codes, masks visible
   auto wait_row = [&](int R) {
     asm volatile(
         "{\n\t.reg .pred q;\n\tW_%=:\n\t"
@@ -1013,7 +990,7 @@ int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
   if (L.total > 220 * 1024) return SA_ERR_VALUE;
   if (br * side > 32 * 63) return SA_ERR_VALUE;   // bit-sliced counters hold 63 tokens/lane
   Params p{cq, ck, gq, gk, v, dw, out, int(n), DK, int(heads), side, rows_total, br, eps, int(d)};
-  void (*kern)(Params) = nullptr;
+  void (*kern)(Params, CUtensorMap) = nullptr;
   switch (side) {
     case 56: kern = binattn_fused_kernel<DK, 56>; break;
     case 28: kern = binattn_fused_kernel<DK, 28>; break;
@@ -1038,7 +1015,23 @@ int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
+  // V as a (channel, token, image) tensor: per-image token bounds make the
+  // cells past n out of bounds (zero fill), the halo rows negative / past n
+  CUtensorMap tmV;
+  memset(&tmV, 0, sizeof(tmV));
+  {
+    const cuuint64_t dims[3] = {cuuint64_t(d), cuuint64_t(n), cuuint64_t(B)};
+    const cuuint64_t strides[2] = {cuuint64_t(d) * 4, cuuint64_t(n) * cuuint64_t(d) * 4};
+    const cuuint32_t box[3] = {cuuint32_t(DK), cuuint32_t(side), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    if ((reinterpret_cast<uintptr_t>(v) & 15) != 0 ||
+        encode_tmap_tiled(&tmV, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(v), dims,
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return SA_ERR_VALUE;   // (the caller falls back to the multi-kernel path)
+  }
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p, tmV);
   if (e != cudaSuccess) {
     set_error("sa_linear_binary_attn: fused launch failed: %s", cudaGetErrorString(e));
     return SA_ERR_CUDA;
