@@ -93,8 +93,8 @@ __host__ __device__ inline Smem smem_layout(int d, int heads, int side, int band
   o += heads * 4 * 256 * 4;
   s.mt = o;                                    // [256][8] float: 0/1 masks of a code byte
   o += 256 * 8 * 4;
-  s.bar = o;                                   // one mbarrier per smem row
-  o += (band_rows + 2) * 8;
+  s.bar = o;                                   // one mbarrier per smem row (+ codes)
+  o += (band_rows + 3) * 8;
   s.total = o;
   return s;
 }
@@ -173,10 +173,24 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
   // grid are zero (the reference's zero-padded token grid, attention.py:170-179)
   // one mbarrier per smem row, so pass 1 starts on the first rows while the
   // rest of the band is still in flight
+  // the band's q / k codes (one head per CTA: contiguous runs) by bulk copy
+  // when 16-byte aligned, completing on bar[BR + 2]
+  const size_t code0 = (size_t(b) * H + hz) * n + t_lo;
+  const bool code_bulk = HEADS == 1 && nt > 0 && (nt * 4) % 16 == 0 && (code0 * 4) % 16 == 0 &&
+                         (reinterpret_cast<uintptr_t>(p.cq) & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(p.ck) & 15) == 0 &&
+                         (su32(cqs) & 15u) == 0 && (su32(cks) & 15u) == 0;
   if (tid == 0) {
-    for (int R = 0; R < BR + 2; ++R)
+    for (int R = 0; R < BR + 3; ++R)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + R)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (code_bulk) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar + BR + 2)),
+                   "r"(uint32_t(2 * nt * 4))
+                   : "memory");
+      tc::bulk_g2s(cqs, p.cq + code0, uint32_t(nt * 4), bar + BR + 2);
+      tc::bulk_g2s(cks, p.ck + code0, uint32_t(nt * 4), bar + BR + 2);
+    }
     // one TMA copy per grid row from the (channel, token, image) tensor map:
     // box = the head's 32 channels x SIDE tokens; rows outside the grid and
     // cells past n are out of bounds and arrive as zeros (the reference's
@@ -195,11 +209,13 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
           : "memory");
     }
   }
-  for (int i = tid; i < HEADS * nt; i += kThreads) {   // codes of the band, [head][token]
-    const int h = i / nt, t = i - h * nt;
-    const size_t g = (size_t(b) * H + hz + h) * n + t_lo + t;
-    cqs[h * nt + t] = __ldg(p.cq + g);
-    cks[h * nt + t] = __ldg(p.ck + g);
+  if (!code_bulk) {
+    for (int i = tid; i < HEADS * nt; i += kThreads) {   // codes of the band, [head][token]
+      const int h = i / nt, t = i - h * nt;
+      const size_t g = (size_t(b) * H + hz + h) * n + t_lo + t;
+      cqs[h * nt + t] = __ldg(p.cq + g);
+      cks[h * nt + t] = __ldg(p.ck + g);
+    }
   }
   for (int i = tid; i < 256 * 8; i += kThreads)          // byte → 8 masks
     mt[i] = ((i >> 3) >> (i & 7)) & 1 ? 1.0f : 0.0f;
@@ -212,6 +228,13 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
         : "memory");
   };
 
+  if (code_bulk) {   // the band's codes have landed
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tWC_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 q, [%0], 0;\n\t"
+        "@!q bra WC_%=;\n\t}" ::"r"(su32(bar + BR + 2))
+        : "memory");
+  }
   // ---- 2. pass 1: band partial of K^T V and of the code-bit counts -----------
   const int s_id = tid >> 4;               // stream 0..15 (two per warp)
   const int rg = (tid >> 2) & 3;           // code bits 8rg .. 8rg+7
