@@ -408,7 +408,10 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
     }
     __syncthreads();
   }
-  cluster.sync();   // every peer has read this CTA's partials; tables complete
+  // this CTA has read every peer's partials: arrive now, wait only before
+  // exiting (peers may still be reading this CTA's part / cntp, which pass 2
+  // does not touch), so an early CTA goes straight on to its outputs
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 
   // ---- 4. pass 2: outputs ------------------------------------------------------
   wait_row(0);
@@ -417,8 +420,8 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
   constexpr int SLOTS = kThreads / NCG;      // (row, segment) units per round
   constexpr int kSeg = seg_len(SIDE);
   constexpr int SEGS = (SIDE + kSeg - 1) / kSeg;
+  static_assert(kThreads % NCG == 0, "every thread has a pass-2 slot");
   const int cgi = tid % NCG, slot = tid / NCG;
-  if (slot >= SLOTS) return;
   const int h = cgi / (DK / 4), cgl = cgi % (DK / 4);
   const int ch = cgi * 4;
   const float gq = __ldg(p.gq + b * H + hz + h), gk = __ldg(p.gk + b * H + hz + h);
@@ -506,6 +509,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
       *reinterpret_cast<float4*>(ob + size_t(t) * ld) = o;
     }
   }
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
