@@ -180,8 +180,10 @@ __global__ void __launch_bounds__(256) softmax_attn_kernel(const float* __restri
 // Per key the score is the same fma chain over c = 0..31, the softmax the same
 // warp reductions, and P·V the same fma chain over j (zero-padded keys add
 // exact zeros), so the output is bit-identical to the generic kernel.
-template <int NJ, int QB>
-__global__ void __launch_bounds__(128) softmax_attn32_kernel(const float* __restrict__ q,
+// W warps × QB queries per round: W = QB = 7 covers n = 49 (the PVT stage-4
+// grid) in one round instead of four rounds of 4 × 4 with a 1-query tail.
+template <int NJ, int QB, int W>
+__global__ void __launch_bounds__(32 * W) softmax_attn32_kernel(const float* __restrict__ q,
                                                             const float* __restrict__ k,
                                                             const float* __restrict__ v,
                                                             float* __restrict__ out, int n, int d,
@@ -190,10 +192,10 @@ __global__ void __launch_bounds__(128) softmax_attn32_kernel(const float* __rest
   __shared__ __align__(16) float sk[NK][36];   // pitch 36: conflict-free 128-bit row reads
   __shared__ __align__(16) float sv[NK][32];
   __shared__ __align__(16) float sq[NK][32];
-  __shared__ __align__(16) float sp[4][QB][NK];
+  __shared__ __align__(16) float sp[W][QB][NK];
   const int bh = blockIdx.x, b = bh / heads, h = bh % heads;
   const size_t rowbase = size_t(b) * n;
-  for (int idx = threadIdx.x; idx < NK * 8; idx += 128) {
+  for (int idx = threadIdx.x; idx < NK * 8; idx += 32 * W) {
     const int j = idx >> 3, c4 = (idx & 7) * 4;
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f), bk = a, cv = a;
     if (j < n) {
@@ -208,8 +210,9 @@ __global__ void __launch_bounds__(128) softmax_attn32_kernel(const float* __rest
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // queries i0 + 4r (r < QB) per warp iteration; a missing query recomputes i0
-  for (int i0 = warp; i0 < n; i0 += 4 * QB) {
+  // queries i0 + W·r (r < QB) per warp iteration; a missing query recomputes i0
+  const int nk4 = (n + 3) & ~3;   // P·V stops at the last 4-key group holding a real key
+  for (int i0 = warp; i0 < n; i0 += W * QB) {
     float s[QB][NJ];
 #pragma unroll
     for (int r = 0; r < QB; ++r)
@@ -223,7 +226,7 @@ __global__ void __launch_bounds__(128) softmax_attn32_kernel(const float* __rest
         kk[u] = *reinterpret_cast<const float4*>(&sk[lane + 32 * u][4 * m]);
 #pragma unroll
       for (int r = 0; r < QB; ++r) {
-        const int i = i0 + 4 * r < n ? i0 + 4 * r : i0;
+        const int i = i0 + W * r < n ? i0 + W * r : i0;
         const float4 qq = *reinterpret_cast<const float4*>(&sq[i][4 * m]);
 #pragma unroll
         for (int u = 0; u < NJ; ++u) {
@@ -273,8 +276,8 @@ __global__ void __launch_bounds__(128) softmax_attn32_kernel(const float* __rest
     float acc[QB];
 #pragma unroll
     for (int r = 0; r < QB; ++r) acc[r] = 0.f;
-#pragma unroll
-    for (int j4 = 0; j4 < NK; j4 += 4) {
+#pragma unroll 4
+    for (int j4 = 0; j4 < nk4; j4 += 4) {
       const float v0 = sv[j4][lane], v1 = sv[j4 + 1][lane], v2 = sv[j4 + 2][lane],
                   v3 = sv[j4 + 3][lane];
 #pragma unroll
@@ -288,7 +291,7 @@ __global__ void __launch_bounds__(128) softmax_attn32_kernel(const float* __rest
     }
 #pragma unroll
     for (int r = 0; r < QB; ++r)
-      if (i0 + 4 * r < n) out[(rowbase + i0 + 4 * r) * d + h * 32 + lane] = acc[r];
+      if (i0 + W * r < n) out[(rowbase + i0 + W * r) * d + h * 32 + lane] = acc[r];
     __syncwarp();
   }
 }
@@ -386,9 +389,12 @@ extern "C" int sa_softmax_attn_strided(const float* q, const float* k, const flo
     const unsigned grid = unsigned(B * heads);
     cudaStream_t st = as_stream(stream);
 #define SA_SM32(NJ, QB) \
-  softmax_attn32_kernel<NJ, QB><<<grid, 128, 0, st>>>(q, k, v, out, int(n), int(d), int(heads), \
+  softmax_attn32_kernel<NJ, QB, 4><<<grid, 128, 0, st>>>(q, k, v, out, int(n), int(d), int(heads), \
                                                       scale_div0, int(ld))
-    if (n <= 32) {
+    if (n > 42 && n <= 49 && g_softmax_qb == 4) {
+      softmax_attn32_kernel<2, 7, 7><<<grid, 224, 0, st>>>(q, k, v, out, int(n), int(d),
+                                                          int(heads), scale_div0, int(ld));
+    } else if (n <= 32) {
       if (g_softmax_qb == 2) SA_SM32(1, 2);
       else if (g_softmax_qb == 8) SA_SM32(1, 8);
       else SA_SM32(1, 4);

@@ -340,7 +340,7 @@ def test_softmax_core_golden(golden):
     assert rel_err(host(out), k["sm_out"]) < 2e-6
 
 
-@pytest.mark.parametrize("n", [7, 32, 33, 49, 64])
+@pytest.mark.parametrize("n", [7, 32, 33, 43, 47, 49, 64])
 def test_softmax_attn32_bit_identical_to_generic(n):
     """The register-blocked dk=32 softmax kernel computes the generic kernel's
     arithmetic in the same order: bit-identical outputs, and the oracle's
