@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(1024, 1) ln_route_warp_kernel(
 constexpr int kOctThreads = 128, kOctRows = 64;   // 4 warps x 4 steps x 4 rows
 
 template <int PER, bool LN>
-__global__ void __launch_bounds__(kOctThreads) ln_route_oct_kernel(
+__global__ void __launch_bounds__(kOctThreads, 6) ln_route_oct_kernel(
     const float* __restrict__ x, const float* __restrict__ gain, const float* __restrict__ bias,
     float* __restrict__ y, int64_t M, float eps, int nr, const float* __restrict__ wg0,
     const float* __restrict__ wg1, const float* __restrict__ wg2, float tie_thresh,
