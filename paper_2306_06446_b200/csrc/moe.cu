@@ -557,13 +557,20 @@ __global__ void __launch_bounds__(kOctThreads, 6) ln_route_oct_kernel(
     int32_t* __restrict__ expert_of, float* __restrict__ gate, int32_t* __restrict__ block_cnt1) {
   constexpr int D = 32 * PER;
   constexpr int kSteps = kOctRows / (kOctThreads / 32 * 4);
-  __shared__ __align__(16) double sw[kMaxRouters][2][D];   // [router][expert][channel]
+  // [router][channel block i][k][lane t]: the k-th 16-byte weight pair of lane
+  // t (k = 0/1: expert 0 channels c, c+1 / c+2, c+3; k = 2/3: expert 1), so the
+  // 8 lanes of a row group read 128 contiguous bytes per load (no bank conflicts)
+  __shared__ __align__(16) double2 sw[kMaxRouters][PER][4][8];
   __shared__ int wcnt[kMaxRouters][kOctThreads / 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane >> 3, t = lane & 7;
   const float* wgs[kMaxRouters] = {wg0, wg1, wg2};
   for (int r = 0; r < nr; ++r)
-    for (int i = threadIdx.x; i < 2 * D; i += kOctThreads) sw[r][i & 1][i >> 1] = double(wgs[r][i]);
+    for (int idx = threadIdx.x; idx < PER * 32; idx += kOctThreads) {
+      const int i = idx >> 5, k = (idx >> 3) & 3, tt = idx & 7;
+      const int c = 32 * i + 4 * tt + 2 * (k & 1), e = k >> 1;   // wg layout [channel][expert]
+      sw[r][i][k][tt] = make_double2(double(wgs[r][2 * c + e]), double(wgs[r][2 * c + 2 + e]));
+    }
   __syncthreads();
   const int64_t base = int64_t(blockIdx.x) * kOctRows + warp * (kSteps * 4);
   int cnt[kMaxRouters] = {0, 0, 0};
@@ -639,11 +646,10 @@ __global__ void __launch_bounds__(kOctThreads, 6) ln_route_oct_kernel(
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
-        const int c = 32 * i + 4 * t;
-        const double2 a0 = *reinterpret_cast<const double2*>(&sw[r][0][c]);
-        const double2 a1 = *reinterpret_cast<const double2*>(&sw[r][0][c + 2]);
-        const double2 b0 = *reinterpret_cast<const double2*>(&sw[r][1][c]);
-        const double2 b1 = *reinterpret_cast<const double2*>(&sw[r][1][c + 2]);
+        const double2 a0 = sw[r][i][0][t];
+        const double2 a1 = sw[r][i][1][t];
+        const double2 b0 = sw[r][i][2][t];
+        const double2 b1 = sw[r][i][3][t];
         s0 = fma(double(v[i].x), a0.x, s0);
         s1 = fma(double(v[i].x), b0.x, s1);
         s0 = fma(double(v[i].y), a0.y, s0);
