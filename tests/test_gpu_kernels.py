@@ -242,7 +242,8 @@ def test_dispatch_ties_golden(golden):
     assert rel_err(plan.gate_of, k["tie_gate"]) < 1e-6
 
 
-@pytest.mark.parametrize("M,d", [(100_003, 32), (5000, 256), (1, 64), (70_000, 160)])
+@pytest.mark.parametrize("M,d", [(100_003, 32), (5000, 256), (1, 64), (70_000, 160),
+                                 (20_001, 192), (3000, 96)])
 def test_route_partition_vs_oracle(M, d):
     from paper_2306_06446_b200 import moe as MOE
     g = ops.rng(M + d)
@@ -255,6 +256,11 @@ def test_route_partition_vs_oracle(M, d):
     assert np.array_equal(plan.expert_of, e)
     assert np.array_equal(np.concatenate(plan.index_of), np.concatenate(idx))
     assert rel_err(plan.gate_of, gate) < 1e-6
+    # without logits d >= 96 takes the 8-lanes-per-row kernel: same plan
+    plan2, _ = MOE.route_plan(dev(x), dev(wg))
+    assert np.array_equal(plan2.expert_of, e)
+    assert np.array_equal(np.concatenate(plan2.index_of), np.concatenate(idx))
+    assert rel_err(plan2.gate_of, gate) < 1e-6
 
 
 def test_route_all_to_one_and_empty_expert():
