@@ -306,8 +306,9 @@ def kernel_microbench(torch, hbm_peak, iters=20):
     add("K3 shift_linear (literal exponent-add, variant 1)", f"({M // 16},{d})x({d},{hidden})",
         ms_b, (M // 16) * (d + hidden) * 4 + d * hidden, bound="alu",
         flops=(M // 16) * d * hidden)
+    wg_d = dev(wg)   # uploaded once: a per-call pageable copy would sync the host
     add("K4 moe_route (+stable partition)", f"({M},{d})",
-        timed(lambda: MOE.route_plan(x, dev(wg))), M * d * 4 + M * 12)
+        timed(lambda: MOE.route_plan(x, wg_d)), M * d * 4 + M * 12)
     mod = MD.MoeModule(wg, [MD.Mlp(MD.Linear(w1), MD.Linear(w2)),
                             MD.Mlp(MD.ShiftLinearLayer(w1.copy()),
                                    MD.ShiftLinearLayer(w2.copy()))], MD.MoeConfig())
