@@ -549,14 +549,19 @@ __global__ void __launch_bounds__(1024, 1) ln_route_warp_kernel(
 // the lane's channels + a fixed xor tree. LN = false: routers on x itself.
 constexpr int kOctThreads = 128, kOctRows = 64;   // 4 warps x 4 steps x 4 rows
 
-template <int PER, bool LN>
-__global__ void __launch_bounds__(kOctThreads, 6) ln_route_oct_kernel(
+// RT rows per thread and step (row (step·RT + rr)·4 + sub): the RT rows'
+// shuffle / fp64 chains interleave and share each weight load; every row's
+// arithmetic is the RT = 1 sequence. RT = 1 prefetches the next step's row.
+template <int PER, bool LN, int RT>
+__global__ void __launch_bounds__(kOctThreads, RT == 1 ? 6 : 4) ln_route_oct_kernel(
     const float* __restrict__ x, const float* __restrict__ gain, const float* __restrict__ bias,
     float* __restrict__ y, int64_t M, float eps, int nr, const float* __restrict__ wg0,
     const float* __restrict__ wg1, const float* __restrict__ wg2, float tie_thresh,
     int32_t* __restrict__ expert_of, float* __restrict__ gate, int32_t* __restrict__ block_cnt1) {
   constexpr int D = 32 * PER;
-  constexpr int kSteps = kOctRows / (kOctThreads / 32 * 4);
+  constexpr int kRows = kOctRows * RT;   // rows per CTA (RT = 2: 128, one wave at 4 CTAs/SM)
+  constexpr int kSteps = kRows / (kOctThreads / 32 * 4 * RT);
+  constexpr bool PF = RT == 1;
   // [router][channel block i][k][lane t]: the k-th 16-byte weight pair of lane
   // t (k = 0/1: expert 0 channels c, c+1 / c+2, c+3; k = 2/3: expert 1), so the
   // 8 lanes of a row group read 128 contiguous bytes per load (no bank conflicts)
@@ -572,104 +577,134 @@ __global__ void __launch_bounds__(kOctThreads, 6) ln_route_oct_kernel(
       sw[r][i][k][tt] = make_double2(double(wgs[r][2 * c + e]), double(wgs[r][2 * c + 2 + e]));
     }
   __syncthreads();
-  const int64_t base = int64_t(blockIdx.x) * kOctRows + warp * (kSteps * 4);
+  const int64_t base = int64_t(blockIdx.x) * kRows + warp * (kSteps * 4 * RT);
   int cnt[kMaxRouters] = {0, 0, 0};
-  float4 vn[PER];
-  auto load_row = [&](int step, float4 (&dst)[PER]) {
-    const int64_t row = base + step * 4 + sub;
+  auto row_of = [&](int step, int rr) { return base + (step * RT + rr) * 4 + sub; };
+  auto load_rows = [&](int step, float4 (&dst)[RT][PER]) {
 #pragma unroll
-    for (int i = 0; i < PER; ++i)
-      dst[i] = row < M ? __ldg(reinterpret_cast<const float4*>(x + row * D + 32 * i + 4 * t))
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int rr = 0; rr < RT; ++rr) {
+      const int64_t row = row_of(step, rr);
+#pragma unroll
+      for (int i = 0; i < PER; ++i)
+        dst[rr][i] = row < M ? __ldg(reinterpret_cast<const float4*>(x + row * D + 32 * i + 4 * t))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   };
-  load_row(0, vn);
+  float4 vn[PF ? RT : 1][PF ? PER : 1];
+  if constexpr (PF) load_rows(0, vn);
 #pragma unroll 1
   for (int step = 0; step < kSteps; ++step) {
-    const int64_t row = base + step * 4 + sub;
-    float4 v[PER];
+    float4 v[RT][PER];
+    if constexpr (PF) {
 #pragma unroll
-    for (int i = 0; i < PER; ++i) v[i] = vn[i];
-    if (step + 1 < kSteps) load_row(step + 1, vn);   // next rows in flight
+      for (int i = 0; i < PER; ++i) v[0][i] = vn[0][i];
+      if (step + 1 < kSteps) load_rows(step + 1, vn);   // next rows in flight
+    } else {
+      load_rows(step, v);
+    }
     if (LN) {
       // virtual-lane partials (channel order within each virtual lane)
-      float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+      float p[RT][4], q[RT][4], mean[RT], inv[RT];
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        p0 += v[i].x;
-        p1 += v[i].y;
-        p2 += v[i].z;
-        p3 += v[i].w;
+      for (int rr = 0; rr < RT; ++rr) {
+        p[rr][0] = p[rr][1] = p[rr][2] = p[rr][3] = 0.f;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          p[rr][0] += v[rr][i].x;
+          p[rr][1] += v[rr][i].y;
+          p[rr][2] += v[rr][i].z;
+          p[rr][3] += v[rr][i].w;
+        }
       }
 #pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
-        p0 += __shfl_xor_sync(0xffffffffu, p0, o);
-        p1 += __shfl_xor_sync(0xffffffffu, p1, o);
-        p2 += __shfl_xor_sync(0xffffffffu, p2, o);
-        p3 += __shfl_xor_sync(0xffffffffu, p3, o);
-      }
-      const float mean = ((p0 + p2) + (p1 + p3)) / float(D);
-      float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
+      for (int o = 4; o > 0; o >>= 1)
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        v[i].x = v[i].x - mean;
-        v[i].y = v[i].y - mean;
-        v[i].z = v[i].z - mean;
-        v[i].w = v[i].w - mean;
-        q0 += v[i].x * v[i].x;
-        q1 += v[i].y * v[i].y;
-        q2 += v[i].z * v[i].z;
-        q3 += v[i].w * v[i].w;
+        for (int rr = 0; rr < RT; ++rr)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) p[rr][j] += __shfl_xor_sync(0xffffffffu, p[rr][j], o);
+#pragma unroll
+      for (int rr = 0; rr < RT; ++rr) {
+        mean[rr] = ((p[rr][0] + p[rr][2]) + (p[rr][1] + p[rr][3])) / float(D);
+        q[rr][0] = q[rr][1] = q[rr][2] = q[rr][3] = 0.f;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          v[rr][i].x = v[rr][i].x - mean[rr];
+          v[rr][i].y = v[rr][i].y - mean[rr];
+          v[rr][i].z = v[rr][i].z - mean[rr];
+          v[rr][i].w = v[rr][i].w - mean[rr];
+          q[rr][0] += v[rr][i].x * v[rr][i].x;
+          q[rr][1] += v[rr][i].y * v[rr][i].y;
+          q[rr][2] += v[rr][i].z * v[rr][i].z;
+          q[rr][3] += v[rr][i].w * v[rr][i].w;
+        }
       }
 #pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
-        q0 += __shfl_xor_sync(0xffffffffu, q0, o);
-        q1 += __shfl_xor_sync(0xffffffffu, q1, o);
-        q2 += __shfl_xor_sync(0xffffffffu, q2, o);
-        q3 += __shfl_xor_sync(0xffffffffu, q3, o);
+      for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+        for (int rr = 0; rr < RT; ++rr)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) q[rr][j] += __shfl_xor_sync(0xffffffffu, q[rr][j], o);
+#pragma unroll
+      for (int rr = 0; rr < RT; ++rr) {
+        const float var = ((q[rr][0] + q[rr][2]) + (q[rr][1] + q[rr][3])) / float(D);
+        inv[rr] = 1.0f / sqrtf(var + eps);
       }
-      const float var = ((q0 + q2) + (q1 + q3)) / float(D);
-      const float inv = 1.0f / sqrtf(var + eps);
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         const float4 g4 = __ldg(reinterpret_cast<const float4*>(gain + 32 * i + 4 * t));
         const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + 32 * i + 4 * t));
-        v[i].x = v[i].x * inv * g4.x + b4.x;
-        v[i].y = v[i].y * inv * g4.y + b4.y;
-        v[i].z = v[i].z * inv * g4.z + b4.z;
-        v[i].w = v[i].w * inv * g4.w + b4.w;
-        if (row < M) *reinterpret_cast<float4*>(y + row * D + 32 * i + 4 * t) = v[i];
+#pragma unroll
+        for (int rr = 0; rr < RT; ++rr) {
+          const int64_t row = row_of(step, rr);
+          v[rr][i].x = v[rr][i].x * inv[rr] * g4.x + b4.x;
+          v[rr][i].y = v[rr][i].y * inv[rr] * g4.y + b4.y;
+          v[rr][i].z = v[rr][i].z * inv[rr] * g4.z + b4.z;
+          v[rr][i].w = v[rr][i].w * inv[rr] * g4.w + b4.w;
+          if (row < M) *reinterpret_cast<float4*>(y + row * D + 32 * i + 4 * t) = v[rr][i];
+        }
       }
     }
 #pragma unroll
     for (int r = 0; r < kMaxRouters; ++r) {
       if (r >= nr) break;   // uniform
-      double s0 = 0.0, s1 = 0.0;
+      double s0[RT], s1[RT];
+#pragma unroll
+      for (int rr = 0; rr < RT; ++rr) s0[rr] = s1[rr] = 0.0;
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         const double2 a0 = sw[r][i][0][t];
         const double2 a1 = sw[r][i][1][t];
         const double2 b0 = sw[r][i][2][t];
         const double2 b1 = sw[r][i][3][t];
-        s0 = fma(double(v[i].x), a0.x, s0);
-        s1 = fma(double(v[i].x), b0.x, s1);
-        s0 = fma(double(v[i].y), a0.y, s0);
-        s1 = fma(double(v[i].y), b0.y, s1);
-        s0 = fma(double(v[i].z), a1.x, s0);
-        s1 = fma(double(v[i].z), b1.x, s1);
-        s0 = fma(double(v[i].w), a1.y, s0);
-        s1 = fma(double(v[i].w), b1.y, s1);
+#pragma unroll
+        for (int rr = 0; rr < RT; ++rr) {
+          s0[rr] = fma(double(v[rr][i].x), a0.x, s0[rr]);
+          s1[rr] = fma(double(v[rr][i].x), b0.x, s1[rr]);
+          s0[rr] = fma(double(v[rr][i].y), a0.y, s0[rr]);
+          s1[rr] = fma(double(v[rr][i].y), b0.y, s1[rr]);
+          s0[rr] = fma(double(v[rr][i].z), a1.x, s0[rr]);
+          s1[rr] = fma(double(v[rr][i].z), b1.x, s1[rr]);
+          s0[rr] = fma(double(v[rr][i].w), a1.y, s0[rr]);
+          s1[rr] = fma(double(v[rr][i].w), b1.y, s1[rr]);
+        }
       }
 #pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
-        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      }
-      float gt;
-      const int e = decide(float(s0), float(s1), tie_thresh, gt);
-      if (t == 0 && row < M) {
-        expert_of[size_t(r) * M + row] = e;
-        gate[size_t(r) * M + row] = gt;
-        cnt[r] += e;
+      for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+        for (int rr = 0; rr < RT; ++rr) {
+          s0[rr] += __shfl_xor_sync(0xffffffffu, s0[rr], o);
+          s1[rr] += __shfl_xor_sync(0xffffffffu, s1[rr], o);
+        }
+#pragma unroll
+      for (int rr = 0; rr < RT; ++rr) {
+        const int64_t row = row_of(step, rr);
+        float gt;
+        const int e = decide(float(s0[rr]), float(s1[rr]), tie_thresh, gt);
+        if (t == 0 && row < M) {
+          expert_of[size_t(r) * M + row] = e;
+          gate[size_t(r) * M + row] = gt;
+          cnt[r] += e;
+        }
       }
     }
   }
@@ -685,12 +720,14 @@ __global__ void __launch_bounds__(kOctThreads, 6) ln_route_oct_kernel(
     int c = 0;
     for (int w = 0; w < kOctThreads / 32; ++w) c += wcnt[threadIdx.x][w];
     const int nb = int((M + kRouteTok - 1) / kRouteTok);
-    atomicAdd(&block_cnt1[size_t(threadIdx.x) * nb + blockIdx.x / (kRouteTok / kOctRows)], c);
+    atomicAdd(&block_cnt1[size_t(threadIdx.x) * nb + blockIdx.x / (kRouteTok / kRows)], c);
   }
 }
 
 static int g_route_oct = 1;
 extern "C" void sa_debug_route_oct(int on) { g_route_oct = on; }
+static int g_oct_rt = 2;   // rows per thread of the 8-lanes-per-row kernel (debug: 1)
+extern "C" void sa_debug_oct_rows(int r) { g_oct_rt = r; }
 
 }  // namespace sa
 
@@ -729,17 +766,19 @@ extern "C" int sa_ln_route(const float* x, const float* gain, const float* bias,
     }
   } else if (g_route_oct) {
     cudaMemsetAsync(block_cnt1, 0, size_t(nb) * nr * sizeof(int32_t), s);
-#define SA_LNRO(P)                                                                              \
-  case P:                                                                                       \
-    ln_route_oct_kernel<P, true><<<unsigned(cdiv(M, kOctRows)), kOctThreads, 0, s>>>(         \
-        x, gain, bias, y, M, eps, nr, wg0,                                                      \
-                                                          wg1, wg2, tie_thresh, expert_of,     \
-                                                          gate, block_cnt1);                   \
+#define SA_LNRO_RT(P, RT)                                                                      \
+  ln_route_oct_kernel<P, true, RT><<<unsigned(cdiv(M, kOctRows * RT)), kOctThreads, 0, s>>>(       \
+      x, gain, bias, y, M, eps, nr, wg0, wg1, wg2, tie_thresh, expert_of, gate, block_cnt1)
+#define SA_LNRO(P)                                                                             \
+  case P:                                                                                      \
+    if (g_oct_rt == 2) SA_LNRO_RT(P, 2);                                                       \
+    else SA_LNRO_RT(P, 1);                                                                     \
     break;
     switch (d / 32) {
       SA_LNRO(1) SA_LNRO(2) SA_LNRO(3) SA_LNRO(4) SA_LNRO(5) SA_LNRO(6) SA_LNRO(7) SA_LNRO(8)
     }
 #undef SA_LNRO
+#undef SA_LNRO_RT
   } else {
 #define SA_LNRW(P)                                                                             \
   case P:                                                                                      \
@@ -797,16 +836,18 @@ extern "C" int sa_moe_route(const float* x, const float* wg, int64_t M, int64_t 
   } else if (g_route_oct && logits == nullptr && d % 32 == 0 && d >= 96 && d <= 256) {
     // wide rows: 8 lanes per row (the LN+router kernel without its LayerNorm)
     cudaMemsetAsync(block_cnt1, 0, size_t(nb) * sizeof(int32_t), s);
+#define SA_RO_RT(P, RT)                                                                        \
+  ln_route_oct_kernel<P, false, RT><<<unsigned(cdiv(M, kOctRows * RT)), kOctThreads, 0, s>>>(      \
+      x, nullptr, nullptr, nullptr, M, 0.f, 1, wg, nullptr, nullptr, tie_thresh, expert_of,    \
+      gate, block_cnt1)
 #define SA_RO(P)                                                                               \
   case P:                                                                                      \
-    ln_route_oct_kernel<P, false><<<unsigned(cdiv(M, kOctRows)), kOctThreads, 0, s>>>(        \
-        x, nullptr, nullptr, nullptr, M,                                                        \
-                                                           0.f, 1, wg, nullptr, nullptr,      \
-                                                           tie_thresh, expert_of, gate,       \
-                                                           block_cnt1);                       \
+    if (g_oct_rt == 2) SA_RO_RT(P, 2);                                                         \
+    else SA_RO_RT(P, 1);                                                                       \
     break;
     switch (d / 32) { SA_RO(3) SA_RO(4) SA_RO(5) SA_RO(6) SA_RO(7) SA_RO(8) }
 #undef SA_RO
+#undef SA_RO_RT
   } else {
     // one thread per token: the row streams in 64-channel chunks with all
     // loads of a chunk in flight

@@ -29,8 +29,12 @@ def timeit(fn, reps=20):
     return s.elapsed_time(e) / reps * 1000
 
 
-for nr in (1, 3):
-    us = timeit(lambda: MOE.ln_route_plans(x, gain, bias, wgs[:nr]))
-    print(f"ln_route M={M} d={d} nr={nr}: {us:7.1f} us")
-us = timeit(lambda: MOE.route_plan(x, wgs[0]))
-print(f"moe_route M={M} d={d}: {us:7.1f} us")
+from paper_2306_06446_b200 import _lib  # noqa: E402
+for rt in (1, 2):   # rows per thread of the 8-lanes-per-row kernel (d >= 96)
+    _lib.load().sa_debug_oct_rows(rt)
+    for nr in (1, 3):
+        us = timeit(lambda: MOE.ln_route_plans(x, gain, bias, wgs[:nr]))
+        print(f"rt={rt} ln_route M={M} d={d} nr={nr}: {us:7.1f} us")
+    us = timeit(lambda: MOE.route_plan(x, wgs[0]))
+    print(f"rt={rt} moe_route M={M} d={d}: {us:7.1f} us")
+_lib.load().sa_debug_oct_rows(2)

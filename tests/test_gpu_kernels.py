@@ -417,6 +417,42 @@ def test_ln_route_fused_vs_oracle(M, d, nr):
         assert rel_err(plan.gate_of, gate) < 1e-6
 
 
+@pytest.mark.parametrize("M,d,nr,ln", [(50_176, 160, 3, True), (1001, 96, 1, True),
+                                       (333, 256, 2, True), (70_001, 160, 1, False),
+                                       (129, 192, 1, False)])
+def test_ln_route_two_rows_per_thread_bit_identical(M, d, nr, ln):
+    """The 8-lanes-per-row LN+router kernel with two rows per thread writes the
+    one-row-per-thread kernel's y, winners, gates and partitions bit for bit."""
+    from paper_2306_06446_b200 import _lib
+    from paper_2306_06446_b200 import moe as MOE
+    lib = _lib.load()
+    g = ops.rng(M + 3 * d + nr)
+    x = dev((g.standard_normal((M, d)) * 1.3 + 0.1).astype(F32))
+    gain = dev((1 + 0.1 * g.standard_normal(d)).astype(F32))
+    bias = dev((0.05 * g.standard_normal(d)).astype(F32))
+    wgs = [dev((g.standard_normal((d, 2)) * 0.3).astype(F32)) for _ in range(nr)]
+
+    def run():
+        if ln:
+            y, plans = MOE.ln_route_plans(x, gain, bias, wgs)
+            return host(y), plans
+        plan, _ = MOE.route_plan(x, wgs[0])
+        return None, [plan]
+    y2, p2 = run()
+    lib.sa_debug_oct_rows(1)
+    try:
+        y1, p1 = run()
+    finally:
+        lib.sa_debug_oct_rows(2)
+    if ln:
+        assert np.array_equal(y1, y2)
+    for a, b in zip(p1, p2):
+        assert np.array_equal(a.expert_of, b.expert_of)
+        assert np.array_equal(a.gate_of, b.gate_of)
+        for ia, ib in zip(a.index_of, b.index_of):
+            assert np.array_equal(ia, ib)
+
+
 @pytest.mark.parametrize("M,d,nr", [(50_176, 160, 3), (999, 160, 1), (2000, 256, 2)])
 def test_ln_route_wide_matches_unfused(M, d, nr):
     """The warp-per-row LN+router kernel (d = 32k > 64) writes exactly
