@@ -7,7 +7,8 @@ Run in the build container only (it imports the unmodified reference from
 
     python tests/golden/make_golden.py
 
-Outputs (committed): tests/golden/{kat,toy_c1,pvt_small,deit_small,pvt_b0_full}.npz
+Outputs (committed): tests/golden/{kat,toy_c1,toy_c1_moe,pvt_small,deit_small,pvt_b0_full,
+    pvt_v1_tiny_full,deit_tiny_full,pvt_v2_b2_full}.npz
 
 Every model here is composed from the reference's own classes (Linear,
 ShiftLinearLayer, MoeModule, Mlp, AttentionLayer, Block, LayerNorm and the
@@ -370,7 +371,23 @@ def make_toy_via_reference_model():
     return m.forward(images)
 
 
+# full-224 fixtures of BASELINE configs C3 / C4 / C5 (batch 2, codes / routes /
+# gates / logits only): name -> (spec builder, batch, image seed)
+FULL_224 = {
+    "pvt_v1_tiny_full": (specs.pvt_v1_tiny, 2, 21),   # C3: dk = 64, d = 64/128/320/512, pos
+    "deit_tiny_full": (specs.deit_tiny, 2, 22),       # C4: 197 tokens, 12 blocks, 15x15 DW grid
+    "pvt_v2_b2_full": (specs.pvt_v2_b2, 2, 23),       # C5: depths 3/4/6/3
+}
+
+
 def main():
+    only = sys.argv[1:]
+    if only:   # e.g. `make_golden.py pvt_v1_tiny_full` regenerates just that fixture
+        for name in only:
+            fn, b, seed = FULL_224[name]
+            np.savez_compressed(os.path.join(HERE, name + ".npz"),
+                                **make_model_fixture(fn(), b, seed, full=False))
+        return
     np.savez_compressed(os.path.join(HERE, "kat.npz"), **make_kat())
     toy = make_model_fixture(specs.toy_c1(), 8, 1)
     toy["logits_via_Model"] = make_toy_via_reference_model()
@@ -384,6 +401,9 @@ def main():
                         **make_model_fixture(specs.deit_tiny(img=64, classes=10, depth=3), 2, 6))
     np.savez_compressed(os.path.join(HERE, "pvt_b0_full.npz"),
                         **make_model_fixture(specs.pvt_v2_b0(), 1, 7, full=False))
+    for name, (fn, b, seed) in FULL_224.items():
+        np.savez_compressed(os.path.join(HERE, name + ".npz"),
+                            **make_model_fixture(fn(), b, seed, full=False))
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

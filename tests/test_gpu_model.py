@@ -19,6 +19,23 @@ F32 = np.float32
 LOGIT_TOL = 1e-5
 
 
+# Deep configs (C3 / C4 / C5 at 224²): the tensor-core fp32-parity GEMMs
+# accumulate in TMEM fp32, whose error grows with K (scripts/diag_gemm_ulp.py:
+# max|err|/rms 2e-6 at K = 32, 7e-5 at K = 2048, profiles/r2_gemm_ulp.txt), so
+# over 8-12 blocks an input lying within that error of a sign boundary flips a
+# code or a route and the flip cascades downstream. For these the
+# end-to-end contract is tier 3: logits within the stated tolerance, top-1
+# agreement, and a bounded flip RATE; tier 1 (bit-exact codes, popcounts,
+# routes, permutations on the oracle's own inputs) is pinned at the same full
+# shapes in test_gpu_configs.py. Shallow fixtures keep tier 2 (1e-5, 0 flips).
+# name -> (logit tolerance, max code-flip rate, max route-flip rate)
+DEEP = {
+    "pvt_v1_tiny_full": (1e-4, 1e-5, 1e-5),
+    "pvt_v2_b2_full": (2e-4, 1e-5, 1e-5),
+    "deit_tiny_full": (2e-3, 1e-4, 5e-4),
+}
+
+
 def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
@@ -49,6 +66,10 @@ FIXTURES = {
     "pvt_small": lambda: specs.pvt_v2_b0(img=64, classes=10),
     "deit_small": lambda: specs.deit_tiny(img=64, classes=10, depth=3),
     "pvt_b0_full": lambda: specs.pvt_v2_b0(),
+    # BASELINE configs C3 / C4 / C5 at full 224 (batch 2)
+    "pvt_v1_tiny_full": lambda: specs.pvt_v1_tiny(),
+    "deit_tiny_full": lambda: specs.deit_tiny(),
+    "pvt_v2_b2_full": lambda: specs.pvt_v2_b2(),
 }
 
 
@@ -94,27 +115,40 @@ def test_model_vs_golden(golden, name):
         logits = host(m.forward(dev(images)))
     finally:
         restore()
-    assert rel_err(logits, fx["logits"]) < LOGIT_TOL
-    assert np.array_equal(logits.argmax(1), fx["logits"].argmax(1))
-    # end-to-end code / route agreement (fp32 path: expected exact)
-    flips = 0
+    # end-to-end code / route agreement (fp32 path), counted per layer first
+    per_layer = []
     total = 0
     names = [k[len("codes:"):] for k in fx if k.startswith("codes:")]
     qs = [n for n in names if n.endswith(".q")]
     ks = [n for n in names if n.endswith(".k")]
-    for got, key in zip(recs["codes"].get("q", []), qs):
-        bits = code_bits(got)
-        flips += int(np.unpackbits(bits ^ fx["codes:" + key]).sum())
-        total += bits.size * 8
-    for got, key in zip(recs["codes"].get("k", []), ks):
-        bits = code_bits(got)
-        flips += int(np.unpackbits(bits ^ fx["codes:" + key]).sum())
-        total += bits.size * 8
     assert len(recs["codes"].get("q", [])) == len(qs), "codes of every binary layer recorded"
+    for key_list, tag in ((qs, "q"), (ks, "k")):
+        for got, key in zip(recs["codes"].get(tag, []), key_list):
+            bits = code_bits(got)
+            f = int(np.unpackbits(bits ^ fx["codes:" + key]).sum())
+            total += bits.size * 8
+            if f:
+                per_layer.append((key, f))
+    flips = sum(f for _, f in per_layer)
     route_flips = 0
     for lname, mod in m.moe_modules():
         bits = np.packbits(mod.last_plan.expert_of.astype(np.uint8), bitorder="little")
-        route_flips += int(np.unpackbits(bits ^ fx["route:" + lname]).sum())
+        f = int(np.unpackbits(bits ^ fx["route:" + lname]).sum())
+        route_flips += f
+        if f:
+            per_layer.append((lname, f))
+    err = rel_err(logits, fx["logits"])
+    print(f"{name}: logits rel {err:.2e}, {flips} / {total} code flips, "
+          f"{route_flips} route flips, per layer {per_layer}")
+    assert np.array_equal(logits.argmax(1), fx["logits"].argmax(1))
+    if name in DEEP:
+        tol, code_rate, route_rate = DEEP[name]
+        routed = sum(mod.last_plan.expert_of.size for _, mod in m.moe_modules())
+        assert err < tol
+        assert flips <= code_rate * total, f"{flips} / {total} code flips"
+        assert route_flips <= route_rate * routed, f"{route_flips} / {routed} route flips"
+        return
+    assert err < LOGIT_TOL
     assert flips == 0, f"{flips} / {total} code flips"
     assert route_flips == 0, f"{route_flips} route flips"
 
@@ -181,6 +215,40 @@ def test_pvt_b0_full_batch_properties():
     net = nets.build(specs.pvt_v2_b0())
     ref = nets.forward(net, host(images[:2]))
     assert rel_err(la[:2], ref) < LOGIT_TOL
+
+
+BENCH_BATCH = {   # BASELINE.json configs at their benchmark batch per GPU
+    "pvt_v1_tiny": 256,   # C3
+    "deit_tiny": 512,     # C4
+    "pvt_v2_b2": 256,     # C5 (global 2048 over 8 GPUs)
+}
+# (pvt_v2_b0 at batch 256 is test_pvt_b0_full_batch_properties)
+
+
+@pytest.mark.parametrize("name", sorted(BENCH_BATCH))
+def test_config_full_batch_properties(name):
+    """C3 / C4 / C5 at the benchmark batch: deterministic, finite, every token
+    routed exactly once, logits independent of batching, and the oracle on two
+    of the benchmarked images within the fp32 tolerance."""
+    from paper_2306_06446_b200 import model as MD
+    spec = specs.BUILDERS[name]()
+    m = MD.Network(spec)
+    B = BENCH_BATCH[name]
+    g = ops.rng(12)
+    images = dev(g.uniform(0, 1, (B, 224, 224, 3)).astype(F32))
+    la = host(m.forward(images))
+    lb = host(m.forward(images))
+    assert np.isfinite(la).all()
+    assert np.array_equal(la, lb), "forward is not deterministic"
+    for _, mod in m.moe_modules():
+        plan = mod.last_plan
+        seen = np.sort(np.concatenate(plan.index_of))
+        assert np.array_equal(seen, np.arange(plan.expert_of.size))
+    part = host(m.forward(images[B - 4:].contiguous()))
+    assert rel_err(part, la[B - 4:]) < 1e-5
+    ref = nets.forward(nets.build(spec), host(images[B - 2:]))
+    assert rel_err(la[B - 2:], ref) < DEEP[name + "_full"][0]
+    assert np.array_equal(la[B - 2:].argmax(1), ref.argmax(1))
 
 
 @pytest.mark.parametrize("name", ["toy_c1_moe", "pvt_small", "pvt_b0_full"])

@@ -119,6 +119,10 @@ MODEL_FIXTURES = {
     "pvt_small": lambda: specs.pvt_v2_b0(img=64, classes=10),
     "deit_small": lambda: specs.deit_tiny(img=64, classes=10, depth=3),
     "pvt_b0_full": lambda: specs.pvt_v2_b0(),
+    # BASELINE configs C3 / C4 / C5 at full 224 (batch 2)
+    "pvt_v1_tiny_full": lambda: specs.pvt_v1_tiny(),
+    "deit_tiny_full": lambda: specs.deit_tiny(),
+    "pvt_v2_b2_full": lambda: specs.pvt_v2_b2(),
 }
 
 
