@@ -8,6 +8,7 @@ ValueError, SA_ERR_STATE → StateError, SA_ERR_CUDA → RuntimeError.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 import threading
@@ -16,6 +17,8 @@ import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libshiftadd_b200.so")
+# same sources with -DSA_DEBUG: sa_debug_* kernel-variant setters + MMA probes
+DEBUG_LIB_PATH = os.path.join(HERE, "libshiftadd_b200_debug.so")
 
 SA_OK, SA_ERR_SHAPE, SA_ERR_VALUE, SA_ERR_CUDA, SA_ERR_STATE = 0, 1, 2, 3, 4
 SA_W_DENSE, SA_W_SHIFT = 0, 1
@@ -97,7 +100,21 @@ _SIGS = {
 }
 
 _lib = None
+_debug_lib = None
 _lock = threading.Lock()
+
+
+def _open(path):
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"{path} is missing: build it with `python -m paper_2306_06446_b200.build` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
 
 
 def load():
@@ -106,19 +123,26 @@ def load():
     if _lib is not None:
         return _lib
     with _lock:
-        if _lib is not None:
-            return _lib
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(
-                f"{LIB_PATH} is missing: build it with `python -m paper_2306_06446_b200.build` "
-                "(there is no CPU fallback)")
-        lib = C.CDLL(LIB_PATH)
-        for name, (res, args) in _SIGS.items():
-            fn = getattr(lib, name)
-            fn.restype = res
-            fn.argtypes = args
-        _lib = lib
+        if _lib is None:
+            _lib = _open(LIB_PATH)
     return _lib
+
+
+@contextlib.contextmanager
+def debug_library():
+    """Route every C-ABI call made inside the block to the debug build (same
+    kernels, plus the sa_debug_* variant switches); yields that library.
+    Test / diagnostics use only — the product never enters this."""
+    global _lib, _debug_lib
+    prev = load()
+    with _lock:
+        if _debug_lib is None:
+            _debug_lib = _open(DEBUG_LIB_PATH)
+        _lib = _debug_lib
+    try:
+        yield _debug_lib
+    finally:
+        _lib = prev
 
 
 def symbols():
@@ -172,6 +196,10 @@ class Workspace:
     """Grow-only scratch buffer per device (the library never allocates)."""
 
     _bufs: dict = {}
+    # Buffers replaced by a larger one are kept alive, never returned to the
+    # caching allocator: a CUDA graph captured while they were current keeps
+    # writing to them on every replay (runtime.GraphedForward).
+    _retired: list = []
 
     @classmethod
     def get(cls, nbytes: int, device=None, slot: int = 0) -> torch.Tensor:
@@ -179,6 +207,13 @@ class Workspace:
         key = (dev.index, slot)
         buf = cls._bufs.get(key)
         if buf is None or buf.numel() < nbytes:
+            if buf is not None:
+                cls._retired.append(buf)
             buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
             cls._bufs[key] = buf
         return buf
+
+    @classmethod
+    def live(cls) -> list:
+        """Every workspace buffer currently allocated (current and retired)."""
+        return list(cls._bufs.values()) + list(cls._retired)

@@ -5,6 +5,12 @@
 Object files go to paper_2306_06446_b200/_build/, the shared library next to
 this file. No fast-math / FTZ: the sign-hash and router must see negative
 subnormals and exact float32 rounding.
+
+Two libraries are built from the same sources:
+- libshiftadd_b200.so (the product): kernel-variant switches are compile-time
+  constants, no probe kernels;
+- libshiftadd_b200_debug.so (-DSA_DEBUG, + the MMA-rate probes of
+  tc_probe.cu): the sa_debug_* setters the A/B tests and scripts/ use.
 """
 
 from __future__ import annotations
@@ -20,6 +26,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libshiftadd_b200.so")
+DEBUG_LIB = os.path.join(HERE, "libshiftadd_b200_debug.so")
+DEBUG_ONLY = ("tc_probe.cu",)   # diagnostics kernels: never in the product library
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -34,8 +42,9 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def sources():
-    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
+def sources(debug=False):
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
+                  if f.endswith(".cu") and (debug or f not in DEBUG_ONLY))
 
 
 def _deps_mtime():
@@ -45,14 +54,27 @@ def _deps_mtime():
     return max(os.path.getmtime(p) for p in paths)
 
 
-def up_to_date() -> bool:
-    return os.path.exists(LIB) and os.path.getmtime(LIB) >= _deps_mtime()
+def up_to_date(lib=LIB) -> bool:
+    return os.path.exists(lib) and os.path.getmtime(lib) >= _deps_mtime()
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, debug: bool = True) -> str:
+    """Build the product library and (unless debug=False) the debug library."""
+    if debug:
+        with cf.ThreadPoolExecutor(max_workers=2) as ex:
+            futs = [ex.submit(_build_one, force, verbose, False),
+                    ex.submit(_build_one, force, verbose, True)]
+            return [f.result() for f in futs][0]
+    return _build_one(force, verbose, False)
+
+
+def _build_one(force: bool, verbose: bool, debug: bool) -> str:
+    lib_path = DEBUG_LIB if debug else LIB
+    if not force and up_to_date(lib_path):
+        return lib_path
+    obj_dir = os.path.join(OBJ, "debug") if debug else OBJ
+    os.makedirs(obj_dir, exist_ok=True)
+    flags = NVCC_FLAGS + (["-DSA_DEBUG"] if debug else [])
     cc = nvcc()
     hdr_mtime = max(os.path.getmtime(os.path.join(CSRC, f)) for f in os.listdir(CSRC)
                     if f.endswith((".cuh", ".h")))
@@ -60,29 +82,29 @@ def build(force: bool = False, verbose: bool = False) -> str:
                                    for f in os.listdir(INCLUDE)))
 
     def compile_one(src):
-        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
         if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(
                 os.path.getmtime(src), hdr_mtime):
             return obj, ""
-        cmd = [cc, *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+        cmd = [cc, *ARCH, *flags, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
         return obj, r.stderr
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        results = list(ex.map(compile_one, sources()))
+        results = list(ex.map(compile_one, sources(debug)))
     for _, log in results:
         if verbose and log.strip():
             print(log, file=sys.stderr)
     objs = [o for o, _ in results]
-    tmp = LIB + ".tmp"
+    tmp = lib_path + ".tmp"
     cmd = [cc, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 def main():

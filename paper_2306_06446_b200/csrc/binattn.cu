@@ -468,13 +468,12 @@ int binattn_split_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
                          cudaStream_t s);
 // 0: fused single-pass kernel when the shape allows; 1: multi-kernel; 2: split
 // two-kernel form of the fused kernel (bit-identical)
-static int g_attn_mode = 0;
 
 }  // namespace sa
 
 using namespace sa;
 
-extern "C" void sa_debug_attn_mode(int mode) { g_attn_mode = mode; }
+SA_DEBUG_SWITCH(int, g_attn_mode, 0, sa_debug_attn_mode)
 
 extern "C" size_t sa_linear_binary_attn_workspace(int64_t B, int64_t n, int64_t d, int64_t heads) {
   if (heads <= 0 || d % heads) return 0;

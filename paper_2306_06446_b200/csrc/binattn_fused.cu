@@ -1070,8 +1070,7 @@ int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
 // Split launch (see binattn_kv_kernel / binattn_out_kernel): same geometry as
 // binattn_fused_launch; the band partials go to `ws` ([B*H][CL][DK*DK] floats,
 // then [B*H][CL][DK] ints). Returns SA_ERR_VALUE outside the envelope.
-static int g_kv_persistent = 0;
-extern "C" void sa_debug_attn_kv_persistent(int on) { g_kv_persistent = on; }
+SA_DEBUG_SWITCH(int, g_kv_persistent, 0, sa_debug_attn_kv_persistent)
 
 size_t binattn_split_ws_bytes(int64_t B, int64_t heads) {
   using namespace baf;

@@ -34,6 +34,18 @@ int write_cls_rows(const float* cls, const float* pos, float* y, int64_t B, int6
     }                                                                              \
   } while (0)
 
+// Kernel-variant switches for A/B experiments. Only the debug library
+// (libshiftadd_b200_debug.so, built with -DSA_DEBUG) has them as mutable state
+// with an sa_debug_* setter; in the product library they are compile-time
+// constants, so kernel selection depends on the call arguments alone.
+#ifdef SA_DEBUG
+#define SA_DEBUG_SWITCH(type, name, init, setter) \
+  static type name = init;                        \
+  extern "C" void setter(type v) { name = v; }
+#else
+#define SA_DEBUG_SWITCH(type, name, init, setter) static constexpr type name = init;
+#endif
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -362,10 +362,9 @@ extern "C" int sa_layernorm(const float* x, const float* gain, const float* bias
   return SA_OK;
 }
 
-static int g_softmax_generic = 0;
-static int g_softmax_qb = 4;   // queries per warp iteration (debug sweep)
-extern "C" void sa_debug_softmax_qb(int qb) { g_softmax_qb = qb; }
-extern "C" void sa_debug_softmax_generic(int on) { g_softmax_generic = on; }
+SA_DEBUG_SWITCH(int, g_softmax_generic, 0, sa_debug_softmax_generic)
+// queries per warp iteration (debug sweep)
+SA_DEBUG_SWITCH(int, g_softmax_qb, 4, sa_debug_softmax_qb)
 
 extern "C" int sa_softmax_attn_strided(const float* q, const float* k, const float* v,
                                        int64_t ld, float* out, int64_t B, int64_t n, int64_t d,

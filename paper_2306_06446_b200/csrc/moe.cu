@@ -271,8 +271,7 @@ __global__ void __launch_bounds__(kRouteTok) partition_scan_kernel(
   perm[pos] = int32_t(t);
 }
 
-static int g_fused_partition = 1;
-extern "C" void sa_debug_fused_partition(int on) { g_fused_partition = on; }
+SA_DEBUG_SWITCH(int, g_fused_partition, 1, sa_debug_fused_partition)
 
 // scan + partition of nr stacked plans
 static void launch_partition(const int32_t* expert_of, int32_t* block_cnt1, int32_t* block_off1,
@@ -724,10 +723,9 @@ __global__ void __launch_bounds__(kOctThreads, RT == 1 ? 6 : 4) ln_route_oct_ker
   }
 }
 
-static int g_route_oct = 1;
-extern "C" void sa_debug_route_oct(int on) { g_route_oct = on; }
-static int g_oct_rt = 2;   // rows per thread of the 8-lanes-per-row kernel (debug: 1)
-extern "C" void sa_debug_oct_rows(int r) { g_oct_rt = r; }
+SA_DEBUG_SWITCH(int, g_route_oct, 1, sa_debug_route_oct)
+// rows per thread of the 8-lanes-per-row kernel (debug: 1)
+SA_DEBUG_SWITCH(int, g_oct_rt, 2, sa_debug_oct_rows)
 
 }  // namespace sa
 

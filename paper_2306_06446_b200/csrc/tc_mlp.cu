@@ -514,12 +514,15 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
 
 }  // namespace tcm
 
+#ifdef SA_DEBUG
 static unsigned long long* g_mlp_prof = nullptr;
-static int g_mlp_dbg = 0;
 extern "C" void sa_debug_mlp_profile(void* dev_buf) {
   g_mlp_prof = static_cast<unsigned long long*>(dev_buf);
 }
-extern "C" void sa_debug_mlp_mode(int mode) { g_mlp_dbg = mode; }
+#else
+static constexpr unsigned long long* g_mlp_prof = nullptr;
+#endif
+SA_DEBUG_SWITCH(int, g_mlp_dbg, 0, sa_debug_mlp_mode)
 
 static int g_sms_mlp = 0;
 
@@ -571,6 +574,8 @@ extern "C" int sa_tc_moe_mlp_fused(const float* x, const int32_t* perm, const in
   SA_REQUIRE(sa_tc_fused_mlp_ok(d, hidden), SA_ERR_SHAPE,
              "sa_tc_moe_mlp_fused: d=%lld hidden=%lld unsupported", (long long)d,
              (long long)hidden);
+  SA_REQUIRE(M >= 0 && M < (int64_t(1) << 31), SA_ERR_SHAPE, "sa_tc_moe_mlp_fused: M=%lld out of range",
+             (long long)M);
   tcm::MlpParams p;
   memset(&p, 0, sizeof(p));
   p.x = x;
@@ -595,6 +600,8 @@ extern "C" int sa_tc_mlp_fused(const float* x, const void* w1pack, int w1_kind,
                                int64_t hidden, const float* residual, void* stream) {
   SA_REQUIRE(sa_tc_fused_mlp_ok(d, hidden), SA_ERR_SHAPE,
              "sa_tc_mlp_fused: d=%lld hidden=%lld unsupported", (long long)d, (long long)hidden);
+  SA_REQUIRE(M >= 0 && M < (int64_t(1) << 31), SA_ERR_SHAPE, "sa_tc_mlp_fused: M=%lld out of range",
+             (long long)M);
   SA_REQUIRE(w1_kind == w2_kind, SA_ERR_VALUE, "sa_tc_mlp_fused: fc1/fc2 kinds differ");
   tcm::MlpParams p;
   memset(&p, 0, sizeof(p));

@@ -61,6 +61,7 @@ __global__ void weight_pack_kernel(const void* __restrict__ w, int kind, int64_t
 
 }  // namespace tc
 
+#ifdef SA_DEBUG
 // debug: gelu_fast2 / split3x2 against their scalar forms on n patterned
 // inputs spanning [-16, 16] and the float edge values; counts mismatching bits
 __global__ void gelu_pair_check_kernel(int64_t n, unsigned long long* bad) {
@@ -92,6 +93,7 @@ extern "C" int sa_debug_gelu_pair_check(int64_t n, unsigned long long* bad_dev, 
   SA_LAUNCH_CHECK("sa_debug_gelu_pair_check");
   return SA_OK;
 }
+#endif
 
 static int tc_tile_n_ok(int bn) {
   return bn == 32 || bn == 64 || bn == 128 || bn == 160 || bn == 256;
@@ -109,16 +111,15 @@ static int num_sms() {
   return g_num_sms;
 }
 
-static int g_tc_dbg = 0;
-static int g_tc_tma = 1;   // TMA-store epilogue for plain outputs
-extern "C" void sa_debug_tc_tma(int on) { g_tc_tma = on; }
-extern "C" void sa_debug_tc_mode(int m) { g_tc_dbg = m; }
-static int g_tc_resident = 1;   // weights resident in shared memory when they fit
-extern "C" void sa_debug_tc_resident(int on) { g_tc_resident = on; }
-static int g_tc_kq = 4;   // stage alternation when kchunks > 4 (measured: whole tiles per group win below)
-extern "C" void sa_debug_tc_kq(int v) { g_tc_kq = v; }
-static int g_tc_stage = 0;   // A staging: 0 = direct A path (default), 1 = auto, 2/4/8 = force slots
-extern "C" void sa_debug_tc_stage(int on) { g_tc_stage = on; }
+SA_DEBUG_SWITCH(int, g_tc_dbg, 0, sa_debug_tc_mode)
+// TMA-store epilogue for plain outputs
+SA_DEBUG_SWITCH(int, g_tc_tma, 1, sa_debug_tc_tma)
+// weights resident in shared memory when they fit
+SA_DEBUG_SWITCH(int, g_tc_resident, 1, sa_debug_tc_resident)
+// stage alternation when kchunks > 4 (measured: whole tiles per group win below)
+SA_DEBUG_SWITCH(int, g_tc_kq, 4, sa_debug_tc_kq)
+// A staging: 0 = direct A path (default), 1 = auto, 2/4/8 = force slots
+SA_DEBUG_SWITCH(int, g_tc_stage, 0, sa_debug_tc_stage)
 
 static int launch_tc(tc::TcParams& p, int amode, int bn, int64_t m_tiles_max, cudaStream_t s) {
   using namespace tc;
@@ -275,7 +276,8 @@ extern "C" int sa_weight_pack(const void* w, int w_kind, int64_t K, int64_t N, i
 }
 
 static int tc_check(const char* who, int64_t M, int64_t K, int64_t N, int bn) {
-  SA_REQUIRE(M >= 0 && K > 0 && N > 0, SA_ERR_SHAPE, "%s: bad extents", who);
+  SA_REQUIRE(M >= 0 && M < (int64_t(1) << 31) && K > 0 && N > 0, SA_ERR_SHAPE, "%s: bad extents",
+             who);
   SA_REQUIRE(K % 4 == 0, SA_ERR_SHAPE, "%s: K=%lld must be a multiple of 4", who, (long long)K);
   SA_REQUIRE(tc_tile_n_ok(bn), SA_ERR_VALUE, "%s: tile N=%d unsupported", who, bn);
   return SA_OK;

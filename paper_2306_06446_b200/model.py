@@ -308,8 +308,9 @@ class Mlp:
         _no_train(train)
         x = to_device(x)
         if not (hasattr(self.fc1, "weight_arg") and hasattr(self.fc2, "weight_arg")):
-            h = self.fc1.forward(x)
-            raise NotImplementedError(f"unsupported MLP layers {type(self.fc1)}, {type(h)}")
+            # the fused device MLP needs this package's Linear / ShiftLinearLayer
+            raise NotImplementedError(f"unsupported MLP layers {type(self.fc1).__name__}, "
+                                      f"{type(self.fc2).__name__}")
         lead = x.shape[:-1]
         x2 = x.reshape(-1, x.shape[-1])
         M, d = x2.shape

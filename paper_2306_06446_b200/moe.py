@@ -68,6 +68,16 @@ class Router:
         return self.w_g.shape[1]
 
 
+# Bumped by runtime.GraphedForward on every replay: a replay rewrites the
+# device buffers of the plans created at capture time, so host copies pulled
+# before it (and partitions built outside the graph) are stale.
+_generation = [0]
+
+
+def bump_generation():
+    _generation[0] += 1
+
+
 class DispatchPlan:
     """Winning expert, gate and per-expert token lists (ref moe.py:64-71).
 
@@ -81,9 +91,11 @@ class DispatchPlan:
         self.counts_dev = counts_dev
         self.perm_dev = perm_dev
         self._host = None
+        self._host_gen = -1
 
     def _pull(self):
-        if self._host is None:
+        if self._host is None or self._host_gen != _generation[0]:
+            self._host_gen = _generation[0]
             e = self.expert_of_dev.cpu().numpy().astype(np.int64)
             g = self.gate_dev.cpu().numpy()
             c = self.counts_dev.cpu().numpy()
@@ -114,10 +126,17 @@ class LazyDispatchPlan(DispatchPlan):
     by sa_moe_partition on first use, on the then-current stream."""
 
     def __init__(self, expert_of_dev, gate_dev):
+        self._in_graph = False
+        self._part_gen = -1
         super().__init__(expert_of_dev, gate_dev, None, None)
 
     def _partition(self):
-        if self._counts is None:
+        # a partition enqueued while a graph was being captured is re-run by
+        # every replay; one built outside a graph is rebuilt after a replay
+        stale = not self._in_graph and self._part_gen != _generation[0]
+        if self._counts is None or stale:
+            self._in_graph = torch.cuda.is_current_stream_capturing()
+            self._part_gen = _generation[0]
             M = self.expert_of_dev.shape[0]
             dev = self.expert_of_dev.device
             counts = torch.empty(2, dtype=torch.int32, device=dev)
@@ -195,7 +214,18 @@ def route(x, router: Router):
     x = to_device(x)
     _check_two(router)
     _, logits = route_plan(x, router.w_g.contiguous(), want_logits=True)
-    return torch.softmax(logits, dim=-1), logits
+    return softmax2(logits), logits
+
+
+def softmax2(logits: torch.Tensor) -> torch.Tensor:
+    """Row softmax of (M, 2) f32 logits in the reference's operation order
+    (max-shift, exp, sum, divide; ref tensor.py:97-103) and with the router
+    kernel's arithmetic (moe.cu `decide`): a deficit inside numpy's exp tie
+    band gives exactly 1, as numpy's f32 exp does, so argmax(p) and p[winner]
+    equal the device plan's winner and gate bit for bit."""
+    sh = logits - logits.max(dim=1, keepdim=True).values
+    e = torch.where(sh >= -tie_threshold(), torch.ones_like(sh), torch.exp(sh))
+    return e / (e[:, :1] + e[:, 1:])
 
 
 def dispatch(p, logits) -> DispatchPlan:

@@ -20,6 +20,15 @@ P_MIN_DEFAULT = -15   # ref quantize.py:27
 P_MAX_DEFAULT = 15    # ref quantize.py:28
 
 
+def check_packable(p_min: int, p_max: int):
+    """The device shift code is one byte: bit 7 = sign, bits 0-4 = P - p_min,
+    decoded to the f32 exponent field (include/shiftadd_b200.h). Same rule as
+    sa_quantize_shift (gemm.cu): ValueError outside it."""
+    if p_max - p_min > 31 or p_min < -126 or p_max > 127:
+        raise ValueError(f"exponent range [{p_min}, {p_max}] does not fit the 5-bit device "
+                         "shift code (need p_max - p_min <= 31, -126 <= p_min, p_max <= 127)")
+
+
 @dataclass
 class QuantConfig:
     """ref quantize.py:31-41"""
@@ -31,6 +40,7 @@ class QuantConfig:
     def __post_init__(self):
         if self.p_min >= self.p_max:
             raise ValueError(f"p_min {self.p_min} must be below p_max {self.p_max}")
+        check_packable(self.p_min, self.p_max)
         if self.scale_mode not in ("per-matrix", "per-head"):
             raise ValueError(f"unknown scale_mode {self.scale_mode!r}")
 
@@ -51,6 +61,7 @@ class ShiftLinear:
         self.p = to_device(self.p, torch.int32)
         if self.s.shape != self.p.shape or self.s.ndim != 2:
             raise ShapeError(f"s/p shapes differ: {tuple(self.s.shape)} vs {tuple(self.p.shape)}")
+        check_packable(self.p_min, self.p_max)
         if self.packed is None:
             if int(self.p.min()) < self.p_min or int(self.p.max()) > self.p_max:
                 raise ValueError("exponents outside [p_min, p_max]")

@@ -15,6 +15,7 @@ from collections import defaultdict
 import torch
 
 from . import _lib
+from . import moe as MOE
 
 
 class OpTimer:
@@ -72,11 +73,18 @@ class GraphedForward:
         with torch.cuda.graph(self.graph):
             self.static_out = self.model.forward(self.static_in)
         torch.cuda.synchronize()
+        # the graph holds raw pointers into the library workspaces: pin them
+        # for the graph's lifetime (Workspace also never frees retired ones)
+        self._workspaces = _lib.Workspace.live()
+
+    def replay(self):
+        MOE.bump_generation()   # host copies of the plans are stale after this
+        self.graph.replay()
 
     def __call__(self, images: torch.Tensor = None) -> torch.Tensor:
         if images is not None and images.data_ptr() != self.static_in.data_ptr():
             self.static_in.copy_(images, non_blocking=True)
-        self.graph.replay()
+        self.replay()
         return self.static_out
 
 
@@ -112,7 +120,7 @@ class PipelinedForward:
             with torch.cuda.stream(self.comp):
                 self.comp.wait_event(self.in_ready[k])
                 self.comp.wait_event(self.read[k])         # logits k already read back
-                f.graph.replay()
+                f.replay()
                 self.done[k].record(self.comp)
             with torch.cuda.stream(self.d2h):
                 self.d2h.wait_event(self.done[k])

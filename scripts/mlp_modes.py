@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2306_06446_b200 import _lib, model as MD, moe as MOE  # noqa: E402
 from oracle import ops  # noqa: E402
 
-lib = _lib.load()
+lib = _lib.debug_library().__enter__()   # the whole script runs on the debug build
 lib.sa_debug_mlp_profile.argtypes = [ctypes.c_void_p]
 lib.sa_debug_mlp_mode.argtypes = [ctypes.c_int]
 MODES = [int(a) for a in sys.argv[1:]] or [0, 2, 4, 6, 8]

@@ -15,7 +15,7 @@ from oracle import ops  # noqa: E402
 SITES = ["prod a1_empty", "w1stream empty", "w2stream empty", "mma a1_full", "mma w1_full",
          "mma h_empty(fc1)", "mma o_empty", "mma w2_full", "mma h_empty(fc2)", "gelu h_full",
          "gelu a2_empty", "epi o_full", "T prod", "T mma", "T gelu", "mma issue fc1", "mma issue fc2"]
-lib = _lib.load()
+lib = _lib.debug_library().__enter__()   # the whole script runs on the debug build
 lib.sa_debug_mlp_profile.argtypes = [ctypes.c_void_p]
 lib.sa_debug_mlp_mode.argtypes = [ctypes.c_int]
 MODE = int(sys.argv[1]) if len(sys.argv) > 1 else 0

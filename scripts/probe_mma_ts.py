@@ -10,7 +10,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2306_06446_b200 import _lib  # noqa: E402
 
-lib = _lib.load()
+lib = _lib.debug_library().__enter__()   # the whole script runs on the debug build
 lib.sa_probe_mma_ts.argtypes = [ctypes.c_int, ctypes.c_int] + [ctypes.c_void_p] * 5
 torch.manual_seed(0)
 out = torch.zeros(2, dtype=torch.int64, device="cuda")

@@ -41,3 +41,12 @@ def golden():
                 cache[name] = {k: z[k] for k in z.files}
         return cache[name]
     return load
+
+
+@pytest.fixture
+def debug_lib():
+    """The debug build of the library (sa_debug_* variant switches); every
+    C-ABI call inside the test goes to it."""
+    from paper_2306_06446_b200 import _lib
+    with _lib.debug_library() as lib:
+        yield lib

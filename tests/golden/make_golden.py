@@ -8,7 +8,7 @@ Run in the build container only (it imports the unmodified reference from
     python tests/golden/make_golden.py
 
 Outputs (committed): tests/golden/{kat,toy_c1,toy_c1_moe,pvt_small,deit_small,pvt_b0_full,
-    pvt_v1_tiny_full,deit_tiny_full,pvt_v2_b2_full}.npz
+    pvt_v1_tiny_full,deit_tiny_full,pvt_v2_b2_full,apply_stage}.npz
 
 Every model here is composed from the reference's own classes (Linear,
 ShiftLinearLayer, MoeModule, Mlp, AttentionLayer, Block, LayerNorm and the
@@ -380,10 +380,61 @@ FULL_224 = {
 }
 
 
+def _ref_model_weights(m):
+    """Reference `Model` parameters in paper_2306_06446_b200 Network.named_weights order."""
+    yield "s0.pe", m.patch_embed.w.value
+    yield "s0.pos", m.pos.value
+    for bi, blk in enumerate(m.blocks):
+        pre = f"s0.b{bi}"
+        for k in ("q", "k", "v", "o"):
+            yield from _ref_layer_weights(f"{pre}.attn.{k}", blk.attn.proj[k])
+        if blk.attn.dw is not None:
+            yield f"{pre}.attn.dw", blk.attn.dw.value
+        yield from _ref_layer_weights(f"{pre}.mlp", blk.mlp)
+    yield "head", m.head.w.value
+
+
+def _digest_pairs(pairs):
+    h = hashlib.sha256()
+    for name, arr in pairs:
+        h.update(name.encode())
+        h.update(np.ascontiguousarray(arr).tobytes())
+    return h.hexdigest()
+
+
+def make_apply_stage():
+    """ref model.py:897-930 on a softmax/dense toy Model (last block exempt):
+    logits and weight digests after stage 1 (linear-binary attention) and after
+    stage 2 (MoE projections and MLPs, routers from PCG64(77))."""
+    bcs = [MD.BlockConfig(d=64, h=4, mlp_ratio=4.0, attn_mode="softmax", mlp_mode="dense",
+                          attn_linear_mode="dense", exempt=(i == 2)) for i in range(3)]
+    m = MD.Model(MD.ModelConfig(blocks=bcs, patch=4, img=32, classes=10, seed=5))
+    images = T.make_rng(9).uniform(0, 1, (3, 32, 32, 3)).astype(F32)
+    out = {"images": images, "logits0": m.forward(images),
+           "sha0": np.array(_digest_pairs(_ref_model_weights(m)))}
+    MD.apply_stage(m, 1)
+    out["logits1"] = m.forward(images)
+    out["sha1"] = np.array(_digest_pairs(_ref_model_weights(m)))
+    MD.apply_stage(m, 2, mlp_target="moe", attn_target="moe")
+    out["logits2"] = m.forward(images)
+    out["sha2"] = np.array(_digest_pairs(_ref_model_weights(m)))
+    for bi, blk in enumerate(m.blocks):
+        for k in ("q", "k", "v", "o"):
+            if isinstance(blk.attn.proj[k], MD.MoeModule):
+                plan = blk.attn.proj[k].last_plan
+                out[f"route:s0.b{bi}.attn.{k}"] = plan.expert_of.astype(np.int32)
+        if isinstance(blk.mlp, MD.MoeModule):
+            out[f"route:s0.b{bi}.mlp"] = blk.mlp.last_plan.expert_of.astype(np.int32)
+    return out
+
+
 def main():
     only = sys.argv[1:]
     if only:   # e.g. `make_golden.py pvt_v1_tiny_full` regenerates just that fixture
         for name in only:
+            if name == "apply_stage":
+                np.savez_compressed(os.path.join(HERE, "apply_stage.npz"), **make_apply_stage())
+                continue
             fn, b, seed = FULL_224[name]
             np.savez_compressed(os.path.join(HERE, name + ".npz"),
                                 **make_model_fixture(fn(), b, seed, full=False))
@@ -404,6 +455,7 @@ def main():
     for name, (fn, b, seed) in FULL_224.items():
         np.savez_compressed(os.path.join(HERE, name + ".npz"),
                             **make_model_fixture(fn(), b, seed, full=False))
+    np.savez_compressed(os.path.join(HERE, "apply_stage.npz"), **make_apply_stage())
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

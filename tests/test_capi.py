@@ -69,3 +69,24 @@ def test_sm100a_cubin_present(lib):
     out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in out
+
+
+def test_product_library_has_no_debug_state():
+    """The product .so carries no sa_debug_* variant switches and no probe
+    kernels; those live in the -DSA_DEBUG build only."""
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    assert "sa_debug_" not in out and "sa_probe" not in out and "probe_kernel" not in out
+    if os.path.exists(_lib.DEBUG_LIB_PATH):
+        dbg = subprocess.run(["nm", "-D", "--defined-only", _lib.DEBUG_LIB_PATH],
+                             capture_output=True, text=True, check=True).stdout
+        assert "sa_debug_attn_mode" in dbg and "sa_probe_mma" in dbg
+
+
+def test_quant_range_checks_match_device_packing():
+    from paper_2306_06446_b200 import quantize as Q
+    with pytest.raises(ValueError):
+        Q.QuantConfig(p_min=-20, p_max=20)
+    with pytest.raises(ValueError):
+        Q.QuantConfig(p_min=-130, p_max=-110)
+    Q.QuantConfig(p_min=-16, p_max=15)   # 31-wide: fits the 5-bit code

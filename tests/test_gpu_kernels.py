@@ -347,13 +347,13 @@ def test_softmax_core_golden(golden):
 
 
 @pytest.mark.parametrize("n", [7, 32, 33, 43, 47, 49, 64])
-def test_softmax_attn32_bit_identical_to_generic(n):
+def test_softmax_attn32_bit_identical_to_generic(n, debug_lib):
     """The register-blocked dk=32 softmax kernel computes the generic kernel's
     arithmetic in the same order: bit-identical outputs, and the oracle's
     softmax core within fp32 tolerance."""
     from paper_2306_06446_b200 import _lib
     from paper_2306_06446_b200 import attention as A
-    lib = _lib.load()
+    lib = debug_lib
     g = ops.rng(n)
     B, heads, dk = 5, 3, 32
     q, k, v = (g.standard_normal((B * n, heads * dk)).astype(F32) for _ in range(3))
@@ -420,12 +420,12 @@ def test_ln_route_fused_vs_oracle(M, d, nr):
 @pytest.mark.parametrize("M,d,nr,ln", [(50_176, 160, 3, True), (1001, 96, 1, True),
                                        (333, 256, 2, True), (70_001, 160, 1, False),
                                        (129, 192, 1, False)])
-def test_ln_route_two_rows_per_thread_bit_identical(M, d, nr, ln):
+def test_ln_route_two_rows_per_thread_bit_identical(M, d, nr, ln, debug_lib):
     """The 8-lanes-per-row LN+router kernel with two rows per thread writes the
     one-row-per-thread kernel's y, winners, gates and partitions bit for bit."""
     from paper_2306_06446_b200 import _lib
     from paper_2306_06446_b200 import moe as MOE
-    lib = _lib.load()
+    lib = debug_lib
     g = ops.rng(M + 3 * d + nr)
     x = dev((g.standard_normal((M, d)) * 1.3 + 0.1).astype(F32))
     gain = dev((1 + 0.1 * g.standard_normal(d)).astype(F32))
@@ -480,13 +480,13 @@ def test_ln_route_wide_matches_unfused(M, d, nr):
                                              (2, 196, 160, 5, True), (2, 300, 96, 3, True),
                                              (3, 197, 64, 2, False), (1, 5, 32, 1, True),
                                              (2, 49, 256, 8, True)])
-def test_fused_binary_attention_matches_multikernel(B, n, d, h, with_dw):
+def test_fused_binary_attention_matches_multikernel(B, n, d, h, with_dw, debug_lib):
     """The single-pass cluster kernel (dk = 32) against the three-kernel path
     and the oracle, including non-square token grids and partial last rows."""
     import ctypes
     from paper_2306_06446_b200 import _lib
     from paper_2306_06446_b200 import attention as A
-    lib = _lib.load()
+    lib = debug_lib
     lib.sa_debug_attn_mode.argtypes = [ctypes.c_int]
     g = ops.rng(11 + n + d)
     q, kk, v = (g.standard_normal((B * n, d)).astype(F32) for _ in range(3))
@@ -592,12 +592,12 @@ def test_grouped_moe_linear_matches_per_problem(M, d):
         assert np.array_equal(got[r], host(yr)), r
 
 
-def test_packed_gelu_and_split_bitwise_equal_scalar():
+def test_packed_gelu_and_split_bitwise_equal_scalar(debug_lib):
     """gelu_fast2 / split3x2 (packed f32x2 arithmetic) reproduce the scalar
     gelu_fast and bf16 plane split bit for bit over 2^24 patterned inputs
     (range [-16, 16] and arbitrary finite bit patterns)."""
     from paper_2306_06446_b200 import _lib
-    lib = _lib.load()
+    lib = debug_lib
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
     assert lib.sa_debug_gelu_pair_check(ctypes_i64(1 << 24), ctypes_p(bad.data_ptr()), None) == 0
     torch.cuda.synchronize()

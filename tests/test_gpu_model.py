@@ -359,3 +359,30 @@ def test_dense_qkv_concat_bit_identical(golden, name):
     finally:
         MD.FUSE_DENSE_QKV = old
     assert np.array_equal(got, ref)
+
+
+def test_apply_stage_matches_reference(golden):
+    """`apply_stage` (ref model.py:897-930) on a softmax/dense toy Model: the
+    same weights (digest), logits and MoE winners as the reference after
+    stage 1 (linear-binary attention, zero DW kernels) and stage 2 (MoE
+    projections and MLPs with routers drawn from PCG64(77)); exempt block
+    untouched."""
+    from paper_2306_06446_b200 import model as MD
+    fx = golden("apply_stage")
+    bcs = [MD.BlockConfig(d=64, h=4, mlp_ratio=4.0, attn_mode="softmax", mlp_mode="dense",
+                          attn_linear_mode="dense", exempt=(i == 2)) for i in range(3)]
+    m = MD.Model(MD.ModelConfig(blocks=bcs, patch=4, img=32, classes=10, seed=5))
+    x = dev(fx["images"])
+    assert digest(m.named_weights()) == str(fx["sha0"])
+    assert rel_err(host(m.forward(x)), fx["logits0"]) < LOGIT_TOL
+    MD.apply_stage(m, 1)
+    assert digest(m.named_weights()) == str(fx["sha1"])
+    assert all(b.cfg.attn_mode == ("softmax" if b.cfg.exempt else "linear-binary") for b in m.blocks)
+    assert rel_err(host(m.forward(x)), fx["logits1"]) < LOGIT_TOL
+    MD.apply_stage(m, 2, mlp_target="moe", attn_target="moe")
+    assert digest(m.named_weights()) == str(fx["sha2"])
+    assert rel_err(host(m.forward(x)), fx["logits2"]) < LOGIT_TOL
+    for lname, mod in m.moe_modules():
+        assert np.array_equal(mod.last_plan.expert_of, fx["route:" + lname]), lname
+    with pytest.raises(ValueError):
+        MD.apply_stage(m, 3)
