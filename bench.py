@@ -36,8 +36,26 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-METRIC = "ShiftAddViT-PVTv2-B0 images/sec"
 UNIT = "images/s"
+
+# BASELINE.json configs benched here: name -> (builder, images per GPU (None =
+# global batch split over the ranks), global batch, metric, model description)
+CONFIGS = {
+    "c2": ("pvt_v2_b0", 256, None, "ShiftAddViT-PVTv2-B0 images/sec",
+           "ShiftAddViT-PVTv2-B0 (LA+Quant+MoE both, last stage MSA)"),
+    "c3": ("pvt_v1_tiny", 256, None, "ShiftAddViT-PVTv1-Tiny-MoE images/sec",
+           "ShiftAddViT-PVTv1-Tiny (LA+Quant+MoE both, MoE MLP, last stage MSA)"),
+    "c4": ("deit_tiny", 512, None, "ShiftAddViT-DeiT-T images/sec",
+           "ShiftAddViT-DeiT-T (quadratic binary Hamming attention, 197 tokens, 12 blocks)"),
+    "c5": ("pvt_v2_b2", None, 2048, "ShiftAddViT-PVTv2-B2 images/sec",
+           "ShiftAddViT-PVTv2-B2 (LA+Quant+MoE both, last stage MSA), global batch 2048"),
+}
+# parity gate tolerance: tier 3 of tests/test_gpu_model.py for every config
+# (full-size forwards on arbitrary images: an fp32-accumulation difference can
+# flip a hash code or a route near its boundary and the flip cascades; the
+# measured values are reported in the line): (logit tol relative to max|logit|,
+# max code-flip rate, max route-flip rate)
+GATE = {c: (2e-3, 1e-4, 5e-4) for c in ("c2", "c3", "c4", "c5")}
 
 
 def parse():
@@ -46,7 +64,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=256, help="images per GPU")
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS),
+                    help="BASELINE.json config (c2 = the headline PVTv2-B0 metric)")
+    ap.add_argument("--batch", type=int, default=None, help="images per GPU (default: config's)")
+    ap.add_argument("--router", default="random", choices=["random", "balanced"],
+                    help="MoE router weights: random init (reference draw order) or the "
+                         "latency-aware routers trained by the reference procedure")
+    ap.add_argument("--backend", default=os.environ.get("SA_DIST_BACKEND", "nccl"),
+                    help="torch.distributed backend (gloo: several ranks sharing one GPU)")
+    ap.add_argument("--skip-parity", action="store_true", help="no parity gate (debug only)")
     ap.add_argument("--variant", default="moe")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -55,20 +81,40 @@ def parse():
     return ap.parse_args()
 
 
-def config_dict(args, world):
-    return {"workload": f"pvt_v2_b0-{args.variant} forward, 224x224, batch {args.batch}/GPU",
-            "model": "ShiftAddViT-PVTv2-B0 (LA+Quant+MoE both, last stage MSA)",
-            "global_batch": args.batch * world, "img": 224, "parallelism": f"dp{world}",
-            "l2": "inputs larger than L2 (154 MB/step)", "precision": "fp32 parity mode"}
+def batch_per_gpu(args, world):
+    per, glob = CONFIGS[args.config][1], CONFIGS[args.config][2]
+    if args.batch is not None:
+        return args.batch
+    return per if per is not None else glob // world
+
+
+def config_dict(args, world, cpu_sample=None):
+    name, _, glob, _, model = CONFIGS[args.config]
+    b = batch_per_gpu(args, world)
+    d = {"workload": f"{name}-{args.variant} forward, 224x224, batch {b}/GPU",
+         "model": model, "config": args.config, "global_batch": b * world, "img": 224,
+         "parallelism": f"dp{world}", "router": args.router,
+         "l2": f"inputs larger than L2 ({b * 224 * 224 * 3 * 4 / 1e6:.0f} MB/step)",
+         "precision": "fp32 parity mode"}
+    if cpu_sample is not None:   # the reference arm runs a bounded sample per step
+        d["workload"] = f"{name}-{args.variant} forward, 224x224, {cpu_sample} images per step (CPU)"
+        d["cpu_images_per_step"] = cpu_sample
+    return d
+
+
+def scaling(args):
+    return "strong" if CONFIGS[args.config][1] is None and args.batch is None else "weak"
 
 
 # ---------------------------------------------------------------- CPU baseline
 
 
-def cpu_reference(spec, images_per_step, seconds, max_steps=None):
+def cpu_reference(spec, images_per_step, seconds, max_steps=None, router=None):
     """Oracle forward on a bounded sample; returns (img/s, images, seconds, cores)."""
     from oracle import nets, ops
     net = nets.build(spec)
+    if router is not None:
+        apply_router_oracle(router, net)
     g = ops.rng(1234)
     imgs = g.uniform(0, 1, (images_per_step, 224, 224, 3)).astype(np.float32)
     nets.forward(net, imgs[:1])   # warm-up (BLAS init)
@@ -83,6 +129,114 @@ def cpu_reference(spec, images_per_step, seconds, max_steps=None):
             break
     cores = len(os.sched_getaffinity(0))
     return done / el, done, el, cores
+
+
+def apply_router_oracle(router, net):
+    """Install a RouterSet (paper_2306_06446_b200.routers) into an oracle net
+    dict (oracle/nets.py layout) so the checker runs the same routers."""
+    for si, S in enumerate(net["stages"]):
+        for bi, B in enumerate(S["blocks"]):
+            for key in "qkvo":
+                L = B["proj"][key]
+                if L["kind"] == "moe":
+                    L["wg"] = router.weights[f"s{si}.b{bi}.attn.{key}"]
+            if B["mlp"]["kind"] == "moe":
+                B["mlp"]["wg"] = router.weights[f"s{si}.b{bi}.mlp"]
+
+
+def cpu_host_info(spec, router=None):
+    """CPU model, BLAS library / thread count, and the reference CLI's pinned
+    single-thread figure (ref cli.py:347-355: BLAS limited to one thread) on
+    one image."""
+    from oracle import nets, ops
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    info = {"cpu_model": model, "cores": len(os.sched_getaffinity(0))}
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        blas = [p for p in threadpool_info() if p.get("user_api") == "blas"]
+        if blas:
+            info["blas"] = f"{blas[0].get('internal_api')} {blas[0].get('version')}"
+            info["blas_threads"] = blas[0].get("num_threads")
+        net = nets.build(spec)
+        if router is not None:
+            apply_router_oracle(router, net)
+        img = ops.rng(99).uniform(0, 1, (1, 224, 224, 3)).astype(np.float32)
+        with threadpool_limits(limits=1, user_api="blas"):
+            nets.forward(net, img)
+            t0 = time.perf_counter()
+            nets.forward(net, img)
+            el = time.perf_counter() - t0
+        info["one_thread"] = {"value": 1.0 / el, "unit": UNIT, "sample": "1 image, BLAS pinned to 1 thread"}
+    except Exception as e:   # pragma: no cover - informational only
+        info["one_thread"] = {"error": str(e)[:200]}
+    return info
+
+
+def parity_gate(m, spec, images, logits_full, tol):
+    """Bench correctness gate (pattern of ref cli.py:141-172: check, then time):
+    the oracle (test infrastructure, oracle/) on two of the benchmarked images
+    against the device forward of the same two images — logits, top-1, every
+    layer's hash codes and MoE winners — plus batch invariance against the
+    full-batch logits the timed forward produced. Returns the report dict."""
+    import torch
+    from oracle import nets
+    from paper_2306_06446_b200 import attention as A
+    logit_tol, code_rate, route_rate = tol
+    imgs2 = images[:2].contiguous()
+    host2 = imgs2.cpu().numpy()
+    tr = nets.Trace()
+    net = nets.build(spec)
+    if getattr(m, "_balanced_router", None) is not None:
+        apply_router_oracle(m._balanced_router, net)
+    t0 = time.perf_counter()
+    ref = nets.forward(net, host2, tr)
+    oracle_s = time.perf_counter() - t0
+    got_codes = []
+    orig = A.binary_core_codes
+
+    def capture(cq, ck, *a, **k):
+        got_codes.append((cq.clone(), ck.clone()))
+        return orig(cq, ck, *a, **k)
+    A.binary_core_codes = capture
+    try:
+        dev2 = m.forward(imgs2)
+        torch.cuda.synchronize()
+    finally:
+        A.binary_core_codes = orig
+    got = dev2.cpu().numpy()
+    recs = [r for r in tr.attn if "codes_q" in r]
+    code_flips = code_total = 0
+    for (cq, ck), r in zip(got_codes, recs):
+        for dev_c, ref_c in ((cq, r["codes_q"]), (ck, r["codes_k"])):
+            a = dev_c.cpu().numpy().view(np.uint32).reshape(ref_c.shape)
+            code_flips += int(np.unpackbits((a ^ ref_c).view(np.uint8)).sum())
+            heads = ref_c.shape[0] // 2              # codes are (2 images * h, n, words)
+            code_total += ref_c.shape[0] * ref_c.shape[1] * (r["q"].shape[1] // heads)
+    route_flips = routed = 0
+    ref_routes = {r["name"]: r["expert_of"] for r in tr.moe}
+    for name, mod in m.moe_modules():
+        e = mod.last_plan.expert_of
+        route_flips += int((e != ref_routes[name]).sum())
+        routed += e.size
+    err = float(np.max(np.abs(got.astype(np.float64) - ref)) / np.max(np.abs(ref)))
+    full2 = logits_full[:2].cpu().numpy()
+    batch_err = float(np.max(np.abs(full2.astype(np.float64) - got)) / np.max(np.abs(got)))
+    ok = (err < logit_tol and np.array_equal(got.argmax(1), ref.argmax(1))
+          and len(got_codes) == len(recs) and code_flips <= code_rate * max(code_total, 1)
+          and route_flips <= route_rate * max(routed, 1) and batch_err == 0.0)
+    return {"ok": bool(ok), "images": 2, "logits_rel_err": err, "logit_tol": logit_tol,
+            "top1_agree": bool(np.array_equal(got.argmax(1), ref.argmax(1))),
+            "code_flips": code_flips, "codes": code_total, "route_flips": route_flips,
+            "routes": routed, "batch_invariance_rel_err": batch_err,
+            "oracle_seconds": oracle_s,
+            "checker": "oracle/ (numpy restatement pinned to the reference's golden vectors)"}
 
 
 # ---------------------------------------------------------------- clocks
@@ -318,28 +472,41 @@ def kernel_microbench(torch, hbm_peak, iters=20):
     return rows
 
 
+def load_router(args, spec_name):
+    """The latency-aware routers (--router balanced) or None."""
+    if args.router != "balanced":
+        return None
+    from paper_2306_06446_b200 import routers
+    return routers.load_balanced(spec_name)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     from paper_2306_06446_b200 import specs
-    spec = specs.pvt_v2_b0(variant=args.variant)
+    spec_name, _, _, METRIC, _ = CONFIGS[args.config]
+    spec = specs.BUILDERS[spec_name](variant=args.variant)
+    router = load_router(args, spec_name)
 
     if args.impl == "reference":
         if rank != 0:
             return
         per_step = 4
         t0 = time.perf_counter()
-        ips, done, el, cores = cpu_reference(spec, per_step, 0, max_steps=max(args.steps, 1))
+        ips, done, el, cores = cpu_reference(spec, per_step, 0, max_steps=max(args.steps, 1),
+                                             router=router)
+        host = cpu_host_info(spec, router)
         line = {"metric": METRIC, "value": ips, "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * el / max(args.steps, 1),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "higher_is_better": True, "scaling": scaling(args), "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic uniform(0,1) 224x224x3 images, PCG64 random-init weights",
-                "config": config_dict(args, world), "impl": "reference",
+                "config": config_dict(args, world, cpu_sample=per_step), "impl": "reference",
                 "cpu_baseline": {"value": ips, "unit": UNIT, "cores": cores, "kind": "port",
                                  "sample": f"{args.steps} steps x {per_step} images, numpy oracle "
-                                           f"(oracle/nets.py) with all host BLAS threads"},
+                                           f"(oracle/nets.py) with all host BLAS threads",
+                                 **{k: v for k, v in host.items() if k != "cores"}},
                 "e2e": {"value": ips, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
                 "wall_s": time.perf_counter() - t0}
         print(json.dumps(line), flush=True)
@@ -347,19 +514,25 @@ def main():
 
     import torch
     import torch.distributed as dist
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % torch.cuda.device_count())   # gloo: ranks may share a GPU
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.backend)
     from paper_2306_06446_b200 import _lib
+    from paper_2306_06446_b200 import dist as D
     from paper_2306_06446_b200 import model as MD
     from paper_2306_06446_b200.runtime import GraphedForward, OpTimer
 
-    B = args.batch
+    B = batch_per_gpu(args, world)
     m = MD.Network(spec)
+    if router is not None:
+        router.apply_model(m)
+        m._balanced_router = router
     g = np.random.Generator(np.random.PCG64(4242 + rank))
     host_imgs = torch.from_numpy(g.uniform(0, 1, (B, 224, 224, 3)).astype(np.float32)).pin_memory()
     images = host_imgs.cuda()
-    gathered = torch.empty((world * B, spec["classes"]), dtype=torch.float32, device="cuda")
 
     def barrier():
         if world > 1:
@@ -369,13 +542,24 @@ def main():
 
     def step(inp):
         logits = fwd(inp)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, logits)
+        if world > 1:   # the path's single collective (dist.gather_logits)
+            D.gather_logits(logits, world * B)
         return logits
 
     for _ in range(args.warmup):
-        step(images)
+        out = step(images)
     torch.cuda.synchronize()
+
+    # ---- parity gate before timing (ref cli.py:141-172): rank 0 checks two
+    # of its benchmarked images against the oracle ----
+    parity = None
+    if rank == 0 and not args.skip_parity:
+        parity = parity_gate(m, spec, images, out, GATE[args.config])
+        if not parity["ok"]:
+            print(json.dumps({"metric": METRIC, "error": "parity gate failed", "parity": parity}),
+                  flush=True)
+            sys.exit(1)
+    barrier()
 
     # ---- device-timed region (inputs resident) ----
     launches0 = _lib.launch_count()
@@ -391,10 +575,7 @@ def main():
     barrier()
     ms = s_ev.elapsed_time(e_ev) / args.steps
     launches = _lib.launch_count() - launches0
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = D.max_over_ranks(ms)
     value = world * B / (ms / 1000.0)
 
     # launches per forward (eager count: graphs replay the same kernels)
@@ -437,10 +618,7 @@ def main():
         barrier()
         ms2 = s2.elapsed_time(e2) / args.steps
         e2e_mode = "serial (copy, forward, read-back per step)"
-    if world > 1:
-        t = torch.tensor([ms2], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms2 = float(t.item())
+    ms2 = D.max_over_ranks(ms2)
     e2e = {"value": world * B / (ms2 / 1000.0), "unit": UNIT,
            "h2d_bytes_per_step": host_imgs.numel() * 4, "d2h_bytes_per_step": outs[0].numel() * 4,
            "ms_per_step": ms2, "mode": e2e_mode}
@@ -473,7 +651,7 @@ def main():
     dom = next(r for r in ops_rows if r["achieved_gbs"] is not None)
     traffic = None
     tr_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
-    if os.path.exists(tr_path):   # DRAM bytes per call of the op from the committed ncu capture
+    if os.path.exists(tr_path) and args.config == "c2" and B == 256:   # capture's own shape   # DRAM bytes per call of the op from the committed ncu capture
         tr = json.load(open(tr_path)).get(dom["op"])
         traffic = tr["dram_bytes_per_call"] if isinstance(tr, dict) else tr
     roofline = {"bound": "hbm", "kernel": dom["op"], "achieved": dom["achieved_gbs"],
@@ -482,22 +660,27 @@ def main():
                 "per_launch_bytes": dom["bytes_per_fwd"] / max(dom["calls_per_fwd"], 1),
                 "ms_per_fwd": dom["ms_per_fwd"],
                 "timing": "CUDA events around each library call inside 3 eager forwards, each enqueued behind a device sleep"}
-    kernels = None if args.skip_kernels else kernel_microbench(torch, hbm_peak)
+    kernels = None if (args.skip_kernels or args.config != "c2") else kernel_microbench(torch, hbm_peak)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": scaling(args),
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic uniform(0,1) 224x224x3 images, PCG64 random-init weights",
             "config": config_dict(args, world), "e2e": e2e, "gpu_launches": int(gpu_launches),
             "launches_per_forward": int(per_fwd), "cuda_graph": not args.no_graph,
             "roofline": roofline, "clocks": clk.summary(), "ops": ops_rows[:14],
-            "kernels": kernels}
+            "kernels": kernels, "parity": parity}
+    if router is not None:
+        line["expert_shares"] = router.shares(m)
 
     if rank == 0 and world == 1 and not args.skip_cpu:
-        ips, done, el, cores = cpu_reference(spec, 4, args.cpu_seconds)
+        ips, done, el, cores = cpu_reference(spec, 4, args.cpu_seconds, router=router)
+        host = cpu_host_info(spec, router)
         line["cpu_baseline"] = {"value": ips, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": f"{done} images (batches of 4) in {el:.1f}s, numpy oracle "
-                                          "with all host BLAS threads"}
+                                          "with all host BLAS threads",
+                                **{k: v for k, v in host.items() if k != "cores"}}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -39,8 +39,26 @@ def gather_logits(logits: torch.Tensor, global_batch: int, group=None) -> torch.
     sizes = [shard_bounds(global_batch, r, ws) for r in range(ws)]
     width = max(hi - lo for lo, hi in sizes)
     classes = logits.shape[1]
-    padded = torch.zeros((width, classes), dtype=logits.dtype, device=logits.device)
-    padded[: logits.shape[0]] = logits
+    # NCCL gathers device tensors over NVLink; gloo (CPU tests, or several
+    # ranks sharing one GPU) gathers host copies
+    dev = logits.device if _backend(group) == "nccl" else torch.device("cpu")
+    padded = torch.zeros((width, classes), dtype=logits.dtype, device=dev)
+    padded[: logits.shape[0]] = logits.to(dev)
     out = [torch.empty_like(padded) for _ in range(ws)]
     dist.all_gather(out, padded, group=group)
     return torch.cat([o[: hi - lo] for o, (lo, hi) in zip(out, sizes)], dim=0)
+
+
+def _backend(group=None) -> str:
+    return str(dist.get_backend(group)).lower()
+
+
+def max_over_ranks(value: float, group=None) -> float:
+    """Max of a host float over all ranks (device-timed step times)."""
+    if not dist.is_available() or not dist.is_initialized():
+        return float(value)
+    dev = torch.device("cuda", torch.cuda.current_device()) if _backend(group) == "nccl" \
+        else torch.device("cpu")
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())

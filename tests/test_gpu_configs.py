@@ -115,3 +115,31 @@ def test_routing_teacher_forced(name):
         assert np.array_equal(plan.expert_of, rec["expert_of"]), rec["name"]
         assert np.array_equal(np.concatenate(plan.index_of), rec["perm"]), rec["name"]
         assert rel_err(plan.gate_of, rec["gate"]) < 1e-6, rec["name"]
+
+
+def test_balanced_routers_pvt_b0():
+    """PVTv2-B0 with the latency-aware routers (trained by the reference's
+    router-only procedure, paper_2306_06446_b200/data): routes bit-exact when
+    each MoE layer is fed the oracle's input, logits within tier 3 end to end,
+    and the shift expert takes the majority of the tokens."""
+    from paper_2306_06446_b200 import model as MD
+    from paper_2306_06446_b200 import moe as MOE
+    from paper_2306_06446_b200 import routers
+    import bench
+    rs = routers.load_balanced("pvt_v2_b0")
+    spec = specs.pvt_v2_b0()
+    m = rs.apply_model(MD.Network(spec))
+    net = nets.build(spec)
+    bench.apply_router_oracle(rs, net)
+    images = ops.rng(41).uniform(0, 1, (2, 224, 224, 3)).astype(F32)
+    tr = nets.Trace()
+    ref = nets.forward(net, images, tr)
+    got = host(m.forward(dev(images)))
+    assert rel_err(got, ref) < 2e-3
+    assert np.array_equal(got.argmax(1), ref.argmax(1))
+    wg = dict(rs.weights)
+    for rec in tr.moe:
+        plan, _ = MOE.route_plan(dev(rec["x"]), dev(wg[rec["name"]]))
+        assert np.array_equal(plan.expert_of, rec["expert_of"]), rec["name"]
+    shares = routers.RouterSet.shares(m)
+    assert shares["overall"] > 0.6, shares

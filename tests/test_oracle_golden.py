@@ -149,3 +149,25 @@ def test_model_forward_bit_exact(golden, name):
             bits = np.packbits((~(rec[key] < 0)).astype(np.uint8).ravel(), bitorder="little")
             assert np.array_equal(bits, fx[f"codes:{rec['name']}.{key}"])
         assert np.array_equal(rec["gq"], fx[f"gamma:{rec['name']}.q"])
+
+
+def test_balanced_router_set_matches_model_layout():
+    """The committed latency-aware routers cover exactly the MoE layers of
+    PVTv2-B0 with (d, 2) f32 matrices, and reached the latency-balanced split
+    on their training tokens wherever a bias-free router can split them."""
+    from paper_2306_06446_b200 import routers
+    rs = routers.load_balanced("pvt_v2_b0")
+    net = nets.build(specs.pvt_v2_b0())
+    names = {}
+    for si, S in enumerate(net["stages"]):
+        for bi, B in enumerate(S["blocks"]):
+            for key in "qkvo":
+                if B["proj"][key]["kind"] == "moe":
+                    names[f"s{si}.b{bi}.attn.{key}"] = B["proj"][key]["wg"].shape
+            if B["mlp"]["kind"] == "moe":
+                names[f"s{si}.b{bi}.mlp"] = B["mlp"]["wg"].shape
+    assert set(rs.weights) == set(names)
+    for k, shape in names.items():
+        assert rs.weights[k].shape == shape and rs.weights[k].dtype == np.float32
+    near = [k for k, s in rs.train_shares.items() if abs(s - 0.75) <= 0.10]
+    assert len(near) >= len(names) // 2
