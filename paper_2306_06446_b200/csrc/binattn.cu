@@ -458,6 +458,9 @@ static int check_attn_shapes(const char* who, int64_t B, int64_t n, int64_t d, i
   return SA_OK;
 }
 
+int binattn_tc_launch(const uint32_t* cq, const uint32_t* ck, const float* gq, const float* gk,
+                      const float* v, const float* dw, float* out, int64_t B, int64_t n,
+                      int64_t d, int64_t heads, float eps, cudaStream_t s);
 int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq, const float* gk,
                          const float* v, const float* dw, float* out, int64_t B, int64_t n,
                          int64_t d, int64_t heads, float eps, cudaStream_t s);
@@ -466,8 +469,11 @@ int binattn_split_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
                          const float* v, const float* dw, float* out, int64_t B, int64_t n,
                          int64_t d, int64_t heads, float eps, void* ws, size_t ws_bytes,
                          cudaStream_t s);
-// 0: fused single-pass kernel when the shape allows; 1: multi-kernel; 2: split
-// two-kernel form of the fused kernel (bit-identical)
+// 0: product choice — dk = 64: tensor-core cluster kernel (binattn_tc.cu);
+// dk = 32: CUDA-core single-pass cluster kernel (binattn_fused.cu), measured
+// faster at dk = 32 (profiles/r2_attn_bench.txt); 1: multi-kernel; 2: split
+// two-kernel form of the CUDA-core fused kernel (bit-identical to it); 3: the
+// tensor-core kernel at any dk it supports
 
 }  // namespace sa
 
@@ -502,6 +508,11 @@ extern "C" int sa_linear_binary_attn(const uint32_t* codes_q, const uint32_t* co
   if (dk == 32 && g_attn_mode == 2) {
     st = binattn_split_launch(codes_q, codes_k, gamma_q, gamma_k, v, dw, out, B, n, d, heads, eps,
                               ws, ws_bytes, as_stream(stream));
+    if (st != SA_ERR_VALUE) return st;
+  }
+  if ((dk == 64 && g_attn_mode == 0) || g_attn_mode == 3) {
+    st = binattn_tc_launch(codes_q, codes_k, gamma_q, gamma_k, v, dw, out, B, n, d, heads, eps,
+                           as_stream(stream));
     if (st != SA_ERR_VALUE) return st;
   }
   if (dk == 32 && g_attn_mode == 0) {

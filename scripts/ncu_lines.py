@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Per-CUDA-source-line instruction counts and stall samples of an ncu report
-(needs -lineinfo): python ncu_lines.py REPORT [top]"""
+(needs -lineinfo): python ncu_lines.py REPORT [top] [kernel-regex]"""
 import csv
 import io
 import subprocess
@@ -8,35 +8,32 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda"],
-                     capture_output=True, text=True).stdout
-rows = []
-fname = None
-lines = out.splitlines()
-i = 0
-while i < len(lines):
-    if lines[i].startswith('"File Name"'):
-        fname = lines[i].split(",", 1)[1].strip('"').split("/")[-1]
-        hdr = next(csv.reader([lines[i + 1]]))
-        i += 2
-        while i < len(lines) and not lines[i].startswith('"File Name"'):
-            r = next(csv.reader([lines[i]]))
-            if len(r) == len(hdr):
-                d = dict(zip(hdr, r))
-                rows.append((fname, d))
-            i += 1
-    else:
-        i += 1
-ie = "Instructions Executed"
-iw = "Warp Stall Sampling (All Samples)"
-def f(x):
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
+       "--launch-count", "1"]
+if len(sys.argv) > 3:
+    cmd += ["-k", f"regex:{sys.argv[3]}"]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
+rows, fname, hdr = [], None, None
+for r in csv.reader(io.StringIO(out)):
+    if not r:
+        continue
+    if r[0] == "File Path":
+        fname = r[1].split("/")[-1]
+        continue
+    if r[0] == "Line No":
+        hdr = r
+        continue
+    if hdr is None or not r[0]:
+        continue
+    d = dict(zip(["line", "src", "addr", "sass"] + hdr[4:], r))
     try:
-        return float(x)
-    except Exception:
-        return 0.0
-tot_e = sum(f(d.get(ie, 0)) for _, d in rows)
-tot_w = sum(f(d.get(iw, 0)) for _, d in rows)
-rows.sort(key=lambda x: -f(x[1].get(iw, 0)))
-print(f"total instructions {tot_e:.0f}, stall samples {tot_w:.0f}")
-for fn, d in rows[:top]:
-    print(f"{fn[:16]:16s}:{d['Line No']:>4} inst {100*f(d.get(ie,0))/max(tot_e,1):5.1f}%  stall {100*f(d.get(iw,0))/max(tot_w,1):5.1f}%  {d['Source'].strip()[:70]}")
+        inst = float(d["Instructions Executed"] or 0)
+        st = float(d["Warp Stall Sampling (All Samples)"] or 0)
+    except (KeyError, ValueError):
+        continue
+    rows.append((fname, int(r[0]), r[1].strip(), inst, st))
+ti = sum(x[3] for x in rows) or 1
+ts = sum(x[4] for x in rows) or 1
+print(f"total instructions {ti:.0f}, stall samples {ts:.0f}")
+for f, ln, src, inst, st in sorted(rows, key=lambda x: -(x[3] / ti + x[4] / ts))[:top]:
+    print(f"{f[:16]:16s}:{ln:4d} inst {100 * inst / ti:5.1f}%  stall {100 * st / ts:5.1f}%  {src[:70]}")

@@ -479,12 +479,16 @@ def test_ln_route_wide_matches_unfused(M, d, nr):
 @pytest.mark.parametrize("B,n,d,h,with_dw", [(3, 3136, 32, 1, True), (2, 784, 64, 2, True),
                                              (2, 196, 160, 5, True), (2, 300, 96, 3, True),
                                              (3, 197, 64, 2, False), (1, 5, 32, 1, True),
-                                             (2, 49, 256, 8, True)])
-def test_fused_binary_attention_matches_multikernel(B, n, d, h, with_dw, debug_lib):
-    """The single-pass cluster kernel (dk = 32) against the three-kernel path
-    and the oracle, including non-square token grids and partial last rows."""
+                                             (2, 49, 256, 8, True), (2, 3136, 64, 1, True),
+                                             (2, 784, 128, 2, True), (2, 196, 320, 5, True),
+                                             (2, 197, 192, 3, True), (1, 5, 64, 1, True),
+                                             (2, 1000, 128, 2, False)])
+def test_tc_binary_attention_vs_oracle_and_cuda_core(B, n, d, h, with_dw, debug_lib):
+    """The tensor-core cluster kernel (product path, dk = 32 and 64) against the
+    oracle and the CUDA-core kernels (single-pass fused dk = 32 and the
+    three-kernel path), on square and non-square token grids with partial last
+    rows; the split two-kernel form is bit-identical to the fused CUDA-core one."""
     import ctypes
-    from paper_2306_06446_b200 import _lib
     from paper_2306_06446_b200 import attention as A
     lib = debug_lib
     lib.sa_debug_attn_mode.argtypes = [ctypes.c_int]
@@ -492,19 +496,17 @@ def test_fused_binary_attention_matches_multikernel(B, n, d, h, with_dw, debug_l
     q, kk, v = (g.standard_normal((B * n, d)).astype(F32) for _ in range(3))
     dw = (g.standard_normal((3, 3, d)) * 0.1).astype(F32) if with_dw else None
     args = (dev(q), dev(kk), dev(v), B, h, dev(dw) if with_dw else None)
-    try:
-        lib.sa_debug_attn_mode(1)
-        legacy = host(A.binary_core(*args))
-    finally:
-        lib.sa_debug_attn_mode(0)
-    fused = host(A.binary_core(*args))
-    assert rel_err(fused, legacy) < 2e-6
-    try:   # the split two-kernel form computes the fused kernel's arithmetic
-        lib.sa_debug_attn_mode(2)
-        split = host(A.binary_core(*args))
-    finally:
-        lib.sa_debug_attn_mode(0)
-    assert np.array_equal(split, fused)
+
+    def run(mode):
+        try:
+            lib.sa_debug_attn_mode(mode)
+            return host(A.binary_core(*args))
+        finally:
+            lib.sa_debug_attn_mode(0)
+    prod = host(A.binary_core(*args))        # default path (dk 32: CUDA-core fused, 64: tc)
+    assert np.array_equal(run(0), prod)
+    tc = run(3)                              # the tensor-core kernel at every dk
+    legacy = run(1)
     fold = lambda t: ops.heads_split(t.reshape(B, n, d), h).reshape(B * h, n, d // h)  # noqa
     qf, _ = ops.binary_features(fold(q))
     kf, _ = ops.binary_features(fold(kk))
@@ -513,7 +515,15 @@ def test_fused_binary_attention_matches_multikernel(B, n, d, h, with_dw, debug_l
     if with_dw:
         merged = merged + np.concatenate([ops.dwconv_tokens(v[i * n:(i + 1) * n], dw)
                                           for i in range(B)])
-    assert rel_err(fused, merged) < 2e-5
+    assert rel_err(tc, merged) < 2e-5
+    assert rel_err(legacy, merged) < 2e-5
+    assert rel_err(tc, legacy) < 2e-5
+    assert rel_err(prod, merged) < 2e-5
+    if d // h == 32:
+        assert rel_err(prod, legacy) < 2e-6   # CUDA-core fused vs three-kernel path
+        assert np.array_equal(run(2), prod)   # split form: same arithmetic
+    else:
+        assert np.array_equal(prod, tc)
     # all-negative query rows give exactly the DWConv term (zero attention part)
     q2 = q.copy()
     q2[0, :] = -np.abs(q2[0, :]) - 1.0
