@@ -461,6 +461,9 @@ static int check_attn_shapes(const char* who, int64_t B, int64_t n, int64_t d, i
 int binattn_tc_launch(const uint32_t* cq, const uint32_t* ck, const float* gq, const float* gk,
                       const float* v, const float* dw, float* out, int64_t B, int64_t n,
                       int64_t d, int64_t heads, float eps, cudaStream_t s);
+int hamming_tc_launch(const uint32_t* cq, const uint32_t* ck, const float* gq, const float* gk,
+                      const float* v, const float* dw, float* out, int64_t B, int64_t n,
+                      int64_t d, int64_t heads, float eps, cudaStream_t s);
 int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq, const float* gk,
                          const float* v, const float* dw, float* out, int64_t B, int64_t n,
                          int64_t d, int64_t heads, float eps, cudaStream_t s);
@@ -480,6 +483,9 @@ int binattn_split_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
 using namespace sa;
 
 SA_DEBUG_SWITCH(int, g_attn_mode, 0, sa_debug_attn_mode)
+// quadratic form: 0 = tensor-core kernel (hamming_tc.cu) when the shape allows,
+// 1 = the CUDA-core kernel below
+SA_DEBUG_SWITCH(int, g_ham_mode, 0, sa_debug_ham_mode)
 
 extern "C" size_t sa_linear_binary_attn_workspace(int64_t B, int64_t n, int64_t d, int64_t heads) {
   if (heads <= 0 || d % heads) return 0;
@@ -575,6 +581,11 @@ extern "C" int sa_hamming_attn(const uint32_t* codes_q, const uint32_t* codes_k,
                                int64_t heads, float eps, void* stream) {
   int st = check_attn_shapes("sa_hamming_attn", B, n, d, heads);
   if (st) return st;
+  if (g_ham_mode == 0) {
+    st = hamming_tc_launch(codes_q, codes_k, gamma_q, gamma_k, v, dw, out, B, n, d, heads, eps,
+                           as_stream(stream));
+    if (st != SA_ERR_VALUE) return st;
+  }
   const int64_t dk = d / heads;
   const int64_t W = cdiv(dk, 32);
   const size_t smem = size_t(n) * dk * 4 + size_t(n) * W * 4 + size_t(kAttnThreads / 32) * n * 4;

@@ -18,6 +18,7 @@ from paper_2306_06446_b200 import _lib, attention as A, quantize as Q  # noqa: E
 SHAPES = [  # (label, B, n, d, heads)
     ("b0-s1", 256, 3136, 32, 1), ("b0-s2", 256, 784, 64, 2), ("b0-s3", 256, 196, 160, 5),
     ("t-s1", 256, 3136, 64, 1), ("t-s2", 256, 784, 128, 2), ("t-s3", 256, 196, 320, 5),
+    ("deit-q", 512, 197, 192, 3),   # quadratic (Hamming) order, DeiT-T block
 ]
 
 
@@ -60,19 +61,22 @@ def main():
         ck, gk = Q.sign_hash(k, h, B)
         dk = d // h
         byt = 8 * M * d + 2 * M * h * ((dk + 31) // 32) * 4
-        f = lambda: A.binary_core_codes(cq, ck, gq, gk, v, B, h, dw, A.EPS_NORM, "linear")  # noqa
+        order = "quadratic" if label.endswith("-q") else "linear"
+        f = lambda: A.binary_core_codes(cq, ck, gq, gk, v, B, h, dw, A.EPS_NORM, order)  # noqa
         res = {"shape": label, "B": B, "n": n, "d": d, "heads": h}
         us = time_it(f)
         res["prod_us"] = round(us, 1)
         res["prod_frac"] = round(byt / us / 1e3 / peak, 3)
         if a.debug:
             with _lib.debug_library() as lib:
-                lib.sa_debug_attn_mode.argtypes = [ctypes.c_int]
-                for mode, name in ((3, "tc"), (1, "multi")):
-                    lib.sa_debug_attn_mode(mode)
+                setm = lib.sa_debug_ham_mode if order == "quadratic" else lib.sa_debug_attn_mode
+                setm.argtypes = [ctypes.c_int]
+                modes = ((1, "cuda_core"),) if order == "quadratic" else ((3, "tc"), (1, "multi"))
+                for mode, name in modes:
+                    setm(mode)
                     us = time_it(f)
                     res[name + "_us"] = round(us, 1)
-                lib.sa_debug_attn_mode(0)
+                setm(0)
         print(json.dumps(res), flush=True)
         rows.append(res)
         del x, k, v

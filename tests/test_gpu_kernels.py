@@ -120,6 +120,43 @@ def test_hamming_matches_linear_order():
     assert rel_err(a, b) < 2e-5
 
 
+@pytest.mark.parametrize("B,n,d,h,with_dw", [(2, 197, 192, 3, True), (3, 197, 192, 3, False),
+                                             (2, 49, 64, 2, True), (1, 5, 64, 1, True),
+                                             (2, 256, 128, 2, True), (2, 200, 32, 1, True),
+                                             (1, 129, 64, 1, True), (2, 17, 192, 3, True)])
+def test_tc_hamming_vs_oracle_and_cuda_core(B, n, d, h, with_dw, debug_lib):
+    """K2b on the tensor cores (S = Cq Ck^T and S V on tcgen05) against the
+    oracle (the same function in K^T V order, associativity) and the CUDA-core
+    quadratic kernel; all-negative query rows give exactly the DWConv term."""
+    import ctypes
+    from paper_2306_06446_b200 import attention as A
+    lib = debug_lib
+    lib.sa_debug_ham_mode.argtypes = [ctypes.c_int]
+    g = ops.rng(23 + n + d)
+    q, kk, v = (g.standard_normal((B * n, d)).astype(F32) for _ in range(3))
+    q[0, :] = -np.abs(q[0, :]) - 1.0          # one all-negative query row per image 0
+    dw = (g.standard_normal((3, 3, d)) * 0.1).astype(F32) if with_dw else None
+    args = (dev(q), dev(kk), dev(v), B, h, dev(dw) if with_dw else None, A.EPS_NORM, "quadratic")
+    tc = host(A.binary_core(*args))
+    try:
+        lib.sa_debug_ham_mode(1)
+        cc = host(A.binary_core(*args))
+    finally:
+        lib.sa_debug_ham_mode(0)
+    fold = lambda t: ops.heads_split(t.reshape(B, n, d), h).reshape(B * h, n, d // h)  # noqa
+    qf, _ = ops.binary_features(fold(q))
+    kf, _ = ops.binary_features(fold(kk))
+    o = ops.qkv_linear_core(qf, kf, fold(v))
+    merged = ops.heads_merge(o.reshape(B, h, n, d // h)).reshape(B * n, d)
+    if with_dw:
+        merged = merged + np.concatenate([ops.dwconv_tokens(v[i * n:(i + 1) * n], dw)
+                                          for i in range(B)])
+    assert rel_err(tc, merged) < 2e-5
+    assert rel_err(tc, cc) < 2e-5
+    if not with_dw:
+        assert np.all(tc[0] == 0)
+
+
 @pytest.mark.parametrize("dk,n", [(32, 300), (64, 197), (16, 196)])
 def test_popcounts_bit_exact(dk, n):
     from paper_2306_06446_b200 import attention as A
