@@ -363,6 +363,13 @@ extern "C" int sa_layernorm(const float* x, const float* gain, const float* bias
 }
 
 SA_DEBUG_SWITCH(int, g_softmax_generic, 0, sa_debug_softmax_generic)
+// 0: tensor-core kernel (softmax_tc.cu) for dk = 64, or dk = 32 with n > 64
+SA_DEBUG_SWITCH(int, g_softmax_tc, 0, sa_debug_softmax_tc)
+namespace sa {
+int softmax_tc_launch(const float* q, const float* k, const float* v, int64_t ld, float* out,
+                      int64_t B, int64_t n, int64_t d, int64_t heads, float scale_div,
+                      cudaStream_t s);
+}
 // queries per warp iteration (debug sweep)
 SA_DEBUG_SWITCH(int, g_softmax_qb, 4, sa_debug_softmax_qb)
 
@@ -406,6 +413,11 @@ extern "C" int sa_softmax_attn_strided(const float* q, const float* k, const flo
     count_launch(1);
     SA_LAUNCH_CHECK("sa_softmax_attn");
     return SA_OK;
+  }
+  if (!g_softmax_generic && g_softmax_tc == 0 && (dk == 64 || (dk == 32 && n > 64))) {
+    const int st = softmax_tc_launch(q, k, v, ld, out, B, n, d, heads, scale_div0,
+                                     as_stream(stream));
+    if (st != SA_ERR_VALUE) return st;
   }
   const size_t smem = size_t(n * (dk + 1) + n * dk + 8 * dk + 8 * n) * sizeof(float);
   SA_REQUIRE(smem <= 220 * 1024, SA_ERR_SHAPE, "sa_softmax_attn: n=%lld dk=%lld too large",

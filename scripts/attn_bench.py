@@ -19,6 +19,8 @@ SHAPES = [  # (label, B, n, d, heads)
     ("b0-s1", 256, 3136, 32, 1), ("b0-s2", 256, 784, 64, 2), ("b0-s3", 256, 196, 160, 5),
     ("t-s1", 256, 3136, 64, 1), ("t-s2", 256, 784, 128, 2), ("t-s3", 256, 196, 320, 5),
     ("deit-q", 512, 197, 192, 3),   # quadratic (Hamming) order, DeiT-T block
+    ("deit-sm", 512, 197, 192, 3),  # softmax core of the exempt DeiT-T block
+    ("t-s4-sm", 256, 49, 512, 8),   # PVTv1-Tiny / PVTv2-B2 stage-4 softmax core
 ]
 
 
@@ -63,15 +65,21 @@ def main():
         byt = 8 * M * d + 2 * M * h * ((dk + 31) // 32) * 4
         order = "quadratic" if label.endswith("-q") else "linear"
         f = lambda: A.binary_core_codes(cq, ck, gq, gk, v, B, h, dw, A.EPS_NORM, order)  # noqa
+        if label.endswith("-sm"):
+            order = "softmax"
+            byt = 4 * M * d * 4
+            f = lambda: A.softmax_core_flat(x, k, v, B, h)  # noqa
         res = {"shape": label, "B": B, "n": n, "d": d, "heads": h}
         us = time_it(f)
         res["prod_us"] = round(us, 1)
         res["prod_frac"] = round(byt / us / 1e3 / peak, 3)
         if a.debug:
             with _lib.debug_library() as lib:
-                setm = lib.sa_debug_ham_mode if order == "quadratic" else lib.sa_debug_attn_mode
+                setm = {"quadratic": lib.sa_debug_ham_mode, "softmax": lib.sa_debug_softmax_tc}.get(
+                    order, lib.sa_debug_attn_mode)
                 setm.argtypes = [ctypes.c_int]
-                modes = ((1, "cuda_core"),) if order == "quadratic" else ((3, "tc"), (1, "multi"))
+                modes = {"quadratic": ((1, "cuda_core"),), "softmax": ((1, "cuda_core"),)}.get(
+                    order, ((3, "tc"), (1, "multi")))
                 for mode, name in modes:
                     setm(mode)
                     us = time_it(f)

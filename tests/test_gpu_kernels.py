@@ -414,6 +414,42 @@ def test_softmax_attn32_bit_identical_to_generic(n, debug_lib):
             assert rel_err(fast[sl], ref) < 2e-6
 
 
+@pytest.mark.parametrize("B,n,heads,dk", [(3, 197, 3, 64), (2, 49, 8, 64), (2, 5, 2, 64),
+                                          (2, 256, 2, 64), (2, 100, 3, 32), (1, 129, 1, 64),
+                                          (2, 200, 5, 32)])
+def test_softmax_tc_vs_oracle_and_generic(B, n, heads, dk, debug_lib):
+    """Tensor-core softmax core (six-product fp32 split of q k^T and p v) against
+    the oracle's softmax core and the CUDA-core generic kernel, on the strided
+    q|k|v layout the exempt stage uses."""
+    from paper_2306_06446_b200 import attention as A
+    from paper_2306_06446_b200 import _lib
+    lib = debug_lib
+    g = ops.rng(31 + n + dk)
+    d = heads * dk
+    qkv = (g.standard_normal((B * n, 3 * d)) * 1.5).astype(F32)
+    t = dev(qkv)
+    out = torch.empty((B * n, d), dtype=torch.float32, device="cuda")
+
+    def run():
+        base = _lib.ptr(t)
+        _lib.call("sa_softmax_attn_strided", base, base + 4 * d, base + 8 * d, 3 * d,
+                  _lib.ptr(out), B, n, d, heads, _lib.stream())
+        return host(out).copy()
+    tc = run()
+    lib.sa_debug_softmax_tc(1)
+    try:
+        cc = run()
+    finally:
+        lib.sa_debug_softmax_tc(0)
+    q, k, v = qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:]
+    fold = lambda x: ops.heads_split(x.reshape(B, n, d), heads).reshape(B * heads, n, dk)  # noqa
+    ref = ops.heads_merge(ops.softmax_core(fold(q), fold(k), fold(v)).reshape(B, heads, n, dk))
+    ref = ref.reshape(B * n, d)
+    assert rel_err(tc, ref) < 2e-5
+    assert rel_err(cc, ref) < 2e-6
+    assert rel_err(tc, cc) < 2e-5
+
+
 def test_mlp_gelu_vs_oracle(golden):
     from paper_2306_06446_b200 import model as MD
     g = ops.rng(1)
