@@ -238,6 +238,71 @@ __device__ __forceinline__ void gelu_fast2(float& x0, float& x1) {
   asm("div.approx.f32 %0, %1, %2;" : "=f"(x1) : "f"(x1), "f"(d1));
 }
 
+// tanh-form GELU on a pair, as x / (1 + 2^t) with t = -2·log2(e)·c·(x + a·x³)
+// folded to t = x·(K1 + K2·x²): packed f32x2 arithmetic, ex2.approx.ftz and
+// either rcp.approx.ftz (MUFU) or, with FMA_RCP, 1/(1 + 2^t) from a bit-trick
+// seed and three Newton steps on the FMA pipe (the two pipes share the GELU
+// load). Relative error ~2e-7 against the float32 tanh form (the reference's
+// own tanh is a float32 libm call; tests hold the logits to 1e-5).
+template <bool FMA_RCP>
+__device__ __forceinline__ void gelu_pair(float& x0, float& x1) {
+  constexpr float kL2e = 1.4426950408889634f, kC = 0.7978845608028654f, kA = 0.044715f;
+  constexpr float K1 = -2.0f * kL2e * kC, K2 = -2.0f * kL2e * kC * kA;
+  float t0, t1;
+  asm("{\n\t.reg .b64 x, q, k1, k2;\n\t"
+      "mov.b64 x, {%2, %3};\n\t"
+      "mov.b64 k1, {%4, %4};\n\t"
+      "mov.b64 k2, {%5, %5};\n\t"
+      "mul.rn.f32x2 q, x, x;\n\t"
+      "fma.rn.f32x2 q, q, k2, k1;\n\t"
+      "mul.rn.f32x2 q, q, x;\n\t"
+      "mov.b64 {%0, %1}, q;\n\t}"
+      : "=f"(t0), "=f"(t1)
+      : "f"(x0), "f"(x1), "f"(K1), "f"(K2));
+  if (FMA_RCP) {   // keep 1 + 2^t finite for the seed (|result| < 2^-120 there anyway)
+    t0 = fminf(t0, 126.f);
+    t1 = fminf(t1, 126.f);
+  }
+  float e0, e1;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(t0));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(t1));
+  if (!FMA_RCP) {
+    float d0, d1;
+    asm("{\n\t.reg .b64 e, o;\n\tmov.b64 e, {%2, %3};\n\tmov.b64 o, {%4, %4};\n\t"
+        "add.rn.f32x2 e, e, o;\n\tmov.b64 {%0, %1}, e;\n\t}"
+        : "=f"(d0), "=f"(d1)
+        : "f"(e0), "f"(e1), "f"(1.0f));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(d0) : "f"(d0));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(d1) : "f"(d1));
+    asm("{\n\t.reg .b64 x, r;\n\tmov.b64 x, {%0, %1};\n\tmov.b64 r, {%2, %3};\n\t"
+        "mul.rn.f32x2 x, x, r;\n\tmov.b64 {%0, %1}, x;\n\t}"
+        : "+f"(x0), "+f"(x1)
+        : "f"(d0), "f"(d1));
+  } else {
+    asm("{\n\t.reg .b64 e, d, r, c, o, one, m1, x;\n\t.reg .b32 d0, d1, r0, r1;\n\t"
+        "mov.b64 one, {%4, %4};\n\t"
+        "mov.b64 m1, {%5, %5};\n\t"
+        "mov.b64 e, {%2, %3};\n\t"
+        "add.rn.f32x2 d, e, one;\n\t"
+        "sub.rn.f32x2 o, m1, e;\n\t"
+        "mov.b64 {d0, d1}, d;\n\t"
+        "sub.s32 r0, 0x7EF311C3, d0;\n\t"
+        "sub.s32 r1, 0x7EF311C3, d1;\n\t"
+        "mov.b64 r, {r0, r1};\n\t"
+        "fma.rn.f32x2 c, o, r, one;\n\t"
+        "fma.rn.f32x2 r, r, c, r;\n\t"
+        "fma.rn.f32x2 c, o, r, one;\n\t"
+        "fma.rn.f32x2 r, r, c, r;\n\t"
+        "fma.rn.f32x2 c, o, r, one;\n\t"
+        "fma.rn.f32x2 r, r, c, r;\n\t"
+        "mov.b64 x, {%0, %1};\n\t"
+        "mul.rn.f32x2 x, x, r;\n\t"
+        "mov.b64 {%0, %1}, x;\n\t}"
+        : "+f"(x0), "+f"(x1)
+        : "f"(e0), "f"(e1), "f"(1.0f), "f"(-1.0f));
+  }
+}
+
 __host__ __device__ inline size_t tc_fixed_smem() {
   return size_t(8) * kWarpSlot + 1024             // epilogue slots (+ 1 KB alignment)
          + 2 * 128 * sizeof(int64_t)                // per-group row tables

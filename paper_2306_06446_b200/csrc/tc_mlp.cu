@@ -7,25 +7,34 @@
 // hi/mid/lo bf16 planes (exact), shift weights are exact bf16, dense weights
 // three planes; fp32 accumulation in TMEM.
 //
-// Per 128-token tile of one expert the hidden dimension is walked in chunks of
-// HC = 32 columns, counted globally by q:
-//   fc1(q) → acc1[q % NB] (TMEM) → GELU group (q % 2): tcgen05.ld, GELU, split,
-//   tcgen05.st → A2[q % NB] (TMEM) → fc2(q) accumulates into acc2[tile % 2].
-// Both A operands (the x planes A1 and the GELU planes A2) live in TMEM and
-// feed tcgen05.mma in its A-from-TMEM form, so shared-memory bandwidth is
-// spent only on the weight tiles (B operands): with A in shared memory every
-// narrow (N = 32) MMA re-reads a 4 KB A tile and the issue rate collapses
-// under the GELU / producer traffic.
-// Roles (15 warps, one CTA per SM):
-//   warps  0-3 / 4-7  GELU groups 0 / 1 (alternate chunks; warp quad = TMEM
-//                     lane block); group (tile % 2) also runs the final epilogue
-//                     of the tile: tcgen05.ld acc2, x gate, + residual, scatter
-//   warps  8-11       producers: gather x rows (MoE permutation), split,
-//                     tcgen05.st → A1 (thread = row = TMEM lane)
-//   warp  12          MMA issuer (one thread): fc1 runs LOOK chunks ahead of fc2
-//   warps 13 / 14     weight streamers: W1 / W2 chunk rings (bulk async copy)
-// Every ring carries full/empty mbarriers; parities derive from the running
-// counters, so tiles of the two experts interleave freely.
+// Per 128-token tile of one expert the hidden dimension runs in chunks of
+// HC = 64: fc1(q) → acc1 in TMEM buffer q % 3 → GELU group q % 3: tcgen05.ld,
+// GELU, split, tcgen05.st of the three A2 planes into the SAME buffer (over the
+// consumed accumulator) → fc2(q) accumulates into acc2[tile % 2]; fc1(q + 3)
+// waits until fc2(q) released the buffer. At d = 32 the dense fc2 concatenates
+// B planes along N (A_mid·[w_hi|w_mid], A_hi·[w_hi|w_mid] at N = 64 into two
+// 32-column partial sums, A_lo·w_hi and A_hi·w_lo at N = 32): 4 MMAs per K
+// step instead of 6, the same six products; the epilogue adds the partials.
+//
+// What paces a kernel like this is instruction issue, not the tensor pipe: a
+// 128 x N x 16 tcgen05.mma retires in ~N/2 cycles, but a single issuing warp
+// that derives every operand with dependent arithmetic (or waits on an
+// mbarrier, ~90 cycles even when the phase is complete) spends far longer per
+// MMA (scripts/probe_mma_seq.py). So fc1 and fc2 have an issuing warp each;
+// their per-chunk loops hold only the waits, one asm block per K step whose
+// operands are per-chunk bases plus compile-time offsets, and the commits.
+// Roles (19 warps, one CTA per SM):
+//   warps  0-11       GELU groups g = 0..2 (chunks q % 3 == g, buffer g); warp
+//                     quad = TMEM lane block
+//   warps 12-15       producers: gather x rows (MoE permutation), split,
+//                     tcgen05.st → A1 (thread = row = TMEM lane); drain acc2:
+//                     × gate, + residual, transpose, scatter to token order
+//   warp  16 / 17     fc1 / fc2 MMA issuers
+//   warp  18          weights: d = 32 (hidden <= 256): both experts' W1 / W2
+//                     resident in shared memory, loaded once; d = 64: W1 / W2
+//                     chunk rings (bulk async copy)
+// Every hand-off is a full/empty mbarrier pair; parities flip on wrap, so
+// tiles of the two experts interleave freely.
 #include "tc_gemm_kernel.cuh"
 
 namespace sa {
@@ -33,11 +42,22 @@ namespace tcm {
 
 using namespace tc;
 
-constexpr int HC = 32;                 // hidden chunk (fc1 N, fc2 K)
-constexpr int kThreads = 480;
-constexpr int kMma = 12, kW1 = 13, kW2 = 14;
-constexpr int kMaxTiles = 1024;               // per-CTA tile table of the MMA issuer
-constexpr uint32_t kPlaneCols = 16;           // TMEM columns of one 32-k bf16 plane
+constexpr int HC = 64;                 // hidden chunk (fc1 N, fc2 K)
+constexpr int kGelu = 16;              // GELU warps 0-15 (column group x lane quad)
+// GELU layout: true = two groups of 8 warps on alternate chunks, 32 columns per
+// warp; false = all 16 warps on every chunk, 16 columns per warp
+constexpr bool kGeluAlt = false;
+constexpr int kGeluPerChunk = kGeluAlt ? 8 : 16;
+constexpr int kProd = 16;              // producers: warps 16 .. 16 + 4·(d/32) - 1
+template <int D>
+struct Roles {
+  static constexpr int NPW = 4 * (D / 32);        // producer warps (one 32-channel stage each)
+  static constexpr int kMma1 = kProd + NPW, kMma2 = kMma1 + 1, kWld = kMma1 + 2;
+  static constexpr int kThreads = (kWld + 1) * 32;
+};
+constexpr int kResHidden = 256;        // d = 32: weights resident up to this hidden
+constexpr uint32_t kPlaneCols = 16;    // TMEM columns of one 32-k bf16 plane
+constexpr uint32_t kBufCols = 96;      // acc1 (64 fp32) / A2 (3 planes x 32) buffer
 
 struct MlpParams {
   const float* x;
@@ -46,47 +66,57 @@ struct MlpParams {
   const float* gate;
   const float* residual;
   float* y;
-  const uint16_t* w1[2];     // packed (bn = 32) planes per expert
+  const uint16_t* w1[2];     // packed (bn = HC) planes per expert
   const uint16_t* w2[2];     // packed (bn = d) planes per expert
-  int np[2];                 // planes per expert (3 dense, 1 shift)
+  int np0, np1;              // planes per expert (3 dense, 1 shift)
   int64_t M;
   int hidden;
-  unsigned long long* prof;  // optional: cycles per wait site (debug builds of the timeline)
-  int dbg;                   // debug experiments (0 in production)
+  unsigned long long* prof;  // debug builds: cycles per wait site (nullptr: off)
+  long long* tl;             // debug builds: CTA 0 event timeline [8][64] (nullptr: off)
+  int dbg;                   // debug builds: role isolation bits (see kDbg)
 };
 
-// wait-site ids for the optional cycle profile
-enum { P_A1E = 0, P_W1E, P_W2E, P_A1F, P_W1F, P_HE1, P_OE, P_W2F, P_HE2, P_HF, P_A2E, P_OF,
-       P_T_PROD, P_T_MMA, P_T_GELU, P_ISS1, P_ISS2, P_NSITE };
+#ifdef SA_DEBUG
+constexpr bool kDbg = true;    // dbg bit 1: GELU handshakes only; 2: producers handshakes
+#else                          // only; 4: no MMAs (commits only); 8: MMA issuers alone,
+constexpr bool kDbg = false;   // no waits
+#endif
 
-template <int D>
+// wait sites of the optional cycle profile (debug builds)
+enum { S_OF = 0, S_A1E, S_WR, S_OE, S_HE, S_A1F, S_BF, S_HF, S_W, T_PROD, T_MMA1, T_MMA2,
+       T_GELU, S_N };
+
+template <int D, bool RES>
 struct Layout {
-  static constexpr int KC1 = D / 32;                         // fc1 K stages
-  static constexpr int NA = D == 32 ? 2 : 1;                 // A1 buffers (TMEM)
-  static constexpr int NB = D == 32 ? 4 : 3;                 // acc1 / A2 buffers (TMEM)
-  static constexpr int LOOK = NB - 1;                        // fc1 lookahead over fc2
-  static constexpr int NW = D == 32 ? 4 : 2;                 // W1 / W2 ring slots
-  static constexpr uint32_t W1C = KC1 * 3 * (HC * 32 * 2);   // max W1 chunk bytes
-  static constexpr uint32_t W2C = 3 * (D * 32 * 2);          // max W2 chunk bytes
-  static constexpr uint32_t XB = 8 * 32 * kXPitch * 4;
-  static constexpr uint32_t OFF_W1 = 0;
-  static constexpr uint32_t OFF_W2 = OFF_W1 + NW * W1C;
-  static constexpr uint32_t OFF_XB = OFF_W2 + NW * W2C;
-  static constexpr uint32_t OFF_ROW = OFF_XB + XB;            // [2][128] int64
-  static constexpr uint32_t OFF_BAR = OFF_ROW + 2 * 128 * 8;
+  static constexpr int KC1 = D / 32;                          // fc1 K stages
+  static constexpr int NA = D == 32 ? 2 : 1;                  // A1 buffers (TMEM)
+  static constexpr int NB = 3;                                // acc1 / A2 buffers (TMEM)
+  static constexpr bool CAT = D == 32;                        // N-concatenated dense fc2
+  static constexpr int NW = 4;                                // ring slots (RES = false)
+  static constexpr uint32_t W1C = KC1 * 3 * (HC * 32 * 2);    // dense W1 chunk bytes
+  static constexpr uint32_t W2C = (HC / 32) * 3 * (D * 32 * 2);
+  static constexpr uint32_t RW1 = (kResHidden / HC) * W1C;    // resident dense W1
+  static constexpr uint32_t RW2 = (kResHidden / HC) * W2C;
+  // resident: W1 dense | W1 shift | W2 dense | W2 shift
+  __device__ static constexpr uint32_t r_w1(int e) { return e ? RW1 : 0u; }
+  __device__ static constexpr uint32_t r_w2(int e) { return RW1 + RW1 / 3 + (e ? RW2 : 0u); }
+  static constexpr uint32_t WBYTES = RES ? (RW1 + RW1 / 3 + RW2 + RW2 / 3) : NW * (W1C + W2C);
+  static constexpr uint32_t OFF_XB = WBYTES;
+  static constexpr uint32_t XB = 4 * KC1 * 32 * kXPitch * 4; // producer transpose slots
+  static constexpr uint32_t OFF_BAR = OFF_XB + XB;
   // barriers: a1 full/empty[NA], w1 full/empty[NW], w2 full/empty[NW],
-  //           h_full/h_empty/a2_empty[NB], o_full/o_empty[2]
-  static constexpr uint32_t NBAR = 2 * NA + 4 * NW + 3 * NB + 4;
+  //           h_full/h_empty/buf_free[NB], o_full/o_empty[2], wres
+  static constexpr uint32_t NBAR = 2 * NA + 4 * NW + 3 * NB + 4 + 1;
   static constexpr uint32_t TOTAL = OFF_BAR + NBAR * 8 + 16 + 1024;  // + alignment slack
-  // TMEM columns: acc1[NB] | acc2[2] | A1[NA] (KC1 x 3 planes) | A2[NB] (3 planes)
-  static constexpr uint32_t T_ACC1 = 0;
-  static constexpr uint32_t T_ACC2 = NB * HC;
-  static constexpr uint32_t T_A1 = T_ACC2 + 2 * D;
+  // TMEM columns: buffers[NB] (acc1 | A2) | acc2[2] | A1[NA] (KC1 x 3 planes)
+  static constexpr uint32_t T_BUF = 0;
+  static constexpr uint32_t T_ACC2 = NB * kBufCols;
+  static constexpr uint32_t ACC2C = 64;
+  static constexpr uint32_t T_A1 = T_ACC2 + 2 * ACC2C;
   static constexpr uint32_t A1COLS = KC1 * 3 * kPlaneCols;
-  static constexpr uint32_t T_A2 = T_A1 + NA * A1COLS;
-  static constexpr uint32_t A2COLS = 3 * kPlaneCols;
   static constexpr uint32_t TCOLS = 512;
-  static_assert(T_A2 + NB * A2COLS <= TCOLS, "TMEM budget");
+  static_assert(T_A1 + NA * A1COLS <= TCOLS, "TMEM budget");
+  static_assert(TOTAL <= 232448, "shared memory budget");
 };
 
 __device__ __forceinline__ int64_t mlp_tiles(const MlpParams& p, int64_t c0) {
@@ -114,11 +144,59 @@ __device__ __forceinline__ bool mlp_tile(const MlpParams& p, int64_t c0, int64_t
   return r0 < r1;
 }
 
-__device__ __forceinline__ uint32_t par(int64_t use) { return uint32_t(use) & 1u; }
+// ---- one K step of MMAs per asm block (warp-uniform, one elected lane
+// issues); every operand is passed in a register, no arithmetic inside.
+// shift weights (one exact plane): lo·w, mid·w, hi·w
+__device__ __forceinline__ void mma3(uint32_t d, uint32_t ah, uint32_t am, uint32_t al, uint64_t b,
+                                     uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %4, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %4, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, 1;\n\t}" ::"r"(d),
+      "r"(ah), "r"(am), "r"(al), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+// dense, six products into one accumulator: lo·hi, mid·mid, hi·lo, mid·hi, hi·mid, hi·hi
+__device__ __forceinline__ void mma6(uint32_t d, uint32_t ah, uint32_t am, uint32_t al, uint64_t b0,
+                                     uint64_t b1, uint64_t b2, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %8, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %4, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %5, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %6, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %4, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %5, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %7, 1;\n\t}" ::"r"(d),
+      "r"(ah), "r"(am), "r"(al), "l"(b0), "l"(b1), "l"(b2), "r"(id), "r"(acc)
+      : "memory");
+}
+// dense, d = 32, B planes concatenated along N (rows 0-31 w_hi, 32-63 w_mid,
+// 64-95 w_lo): columns [0,32) collect mh + lh + hl + hh, [32,64) mm + hm
+__device__ __forceinline__ void mma_cat4(uint32_t d, uint32_t ah, uint32_t am, uint32_t al,
+                                         uint64_t b0, uint64_t b2, uint32_t id64, uint32_t id32,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %8, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %4, %6, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %4, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %5, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %6, 1;\n\t}" ::"r"(d),
+      "r"(ah), "r"(am), "r"(al), "l"(b0), "l"(b2), "r"(id64), "r"(id32), "r"(acc)
+      : "memory");
+}
 
-template <int D, bool DBG>
-__global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
-  using L = Layout<D>;
+template <int D, bool RES, int NF>
+__global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p) {
+  using L = Layout<D, RES>;
+  constexpr int kMma1 = Roles<D>::kMma1, kMma2 = Roles<D>::kMma2, kWld = Roles<D>::kWld;
+  constexpr int NPW = Roles<D>::NPW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // the swizzle pattern keys on absolute address bits: align the carve-out to 1 KB
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -130,43 +208,41 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
   uint64_t* w2_full = w1_empty + L::NW;
   uint64_t* w2_empty = w2_full + L::NW;
   uint64_t* h_full = w2_empty + L::NW;      // fc1(q) done
-  uint64_t* h_empty = h_full + L::NB;       // GELU(q) read acc1 and wrote A2 (128 threads)
-  uint64_t* a2_empty = h_empty + L::NB;     // fc2(q) done reading A2
-  uint64_t* o_full = a2_empty + L::NB;      // [2] acc2 ready
-  uint64_t* o_empty = o_full + 2;           // [2] acc2 drained (128 threads)
-  int64_t* rowtab = reinterpret_cast<int64_t*>(smem + L::OFF_ROW);
+  uint64_t* h_empty = h_full + L::NB;       // GELU(q) wrote A2 (16 warps)
+  uint64_t* buf_free = h_empty + L::NB;     // fc2(q) done reading A2: buffer reusable
+  uint64_t* o_full = buf_free + L::NB;      // [2] acc2 ready
+  uint64_t* o_empty = o_full + 2;           // [2] acc2 drained (producer warps)
+  uint64_t* wres = o_empty + 2;             // resident weights landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_BAR + L::NBAR * 8);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  __shared__ unsigned long long sprof[P_NSITE];
-  __shared__ uint8_t tile_e[kMaxTiles];
-  if (tid < P_NSITE) sprof[tid] = 0;
+#ifdef SA_DEBUG
+  __shared__ unsigned long long sprof[S_N];
+  if (tid < S_N) sprof[tid] = 0;
   const long long t_start = clock64();
-#define PWAIT(site, b, par_)                                        \
-  do {                                                              \
-    if (!DBG) {                                                     \
-      mbar_wait(b, par_);                                           \
-    } else if (p.dbg & 8) {                                         \
-    } else if (p.prof) {                                            \
-      const long long t0_ = clock64();                              \
-      mbar_wait(b, par_);                                           \
-      if (lane == 0) atomicAdd(&sprof[site], (unsigned long long)(clock64() - t0_)); \
-    } else {                                                        \
-      mbar_wait(b, par_);                                           \
-    }                                                               \
+#define PW(site, b, par_)                                                              \
+  do {                                                                                 \
+    if (p.dbg & 8) {                                                                   \
+    } else if (p.prof) {                                                               \
+      const long long t0_ = clock64();                                                 \
+      mbar_wait(b, par_);                                                              \
+      if (lane == 0) atomicAdd(&sprof[site], (unsigned long long)(clock64() - t0_));   \
+    } else {                                                                           \
+      mbar_wait(b, par_);                                                              \
+    }                                                                                  \
   } while (0)
-  // debug bit 64 (with 16): plain arrivals instead of tcgen05.commit
-  auto commit = [&](uint64_t* b) {   // whole MMA warp calls this
-    if (DBG && (p.dbg & 80) == 80) {
-      if (lane == 0) mbar_arrive(b);
-    } else {
-      commit_w(b);
-    }
-  };
-  if (warp == kMma) tmem_alloc<L::TCOLS>(tmem_slot);
+#define TL(ev, q)                                                                        \
+  do {                                                                                   \
+    if (p.tl && blockIdx.x == 0 && lane == 0 && (q) < 64) p.tl[(ev) * 64 + (q)] = clock64(); \
+  } while (0)
+#else
+#define PW(site, b, par_) mbar_wait(b, par_)
+#define TL(ev, q) do {} while (0)
+#endif
+  if (warp == kMma1) tmem_alloc<L::TCOLS>(tmem_slot);
   if (tid == 0) {
     for (int i = 0; i < L::NA; ++i) {
-      mbar_init(&a1_full[i], 4);
+      mbar_init(&a1_full[i], NPW);
       mbar_init(&a1_empty[i], 1);
     }
     for (int i = 0; i < L::NW; ++i) {
@@ -177,13 +253,14 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
     }
     for (int i = 0; i < L::NB; ++i) {
       mbar_init(&h_full[i], 1);
-      mbar_init(&h_empty[i], 128);
-      mbar_init(&a2_empty[i], 1);
+      mbar_init(&h_empty[i], kGeluPerChunk);
+      mbar_init(&buf_free[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 128);
+      mbar_init(&o_empty[i], NPW);
     }
+    mbar_init(wres, 1);
     fence_barrier_init();
   }
   tc_fence_before();
@@ -194,272 +271,37 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
   const int64_t ntile = mlp_tiles(p, c0);
   const int nchunk = p.hidden / HC;
 
-  if (DBG && (p.dbg & 8) && warp != kMma) {
-    // debug: only the MMA issuer runs (no handshakes)
-  } else if (warp >= 8 && warp < 12) {
-    // ---------------- producers: x rows → A1 planes (TMEM) ----------------
-    const int ptid = tid - 256;                  // = tile row = TMEM lane
-    const uint32_t lane_base = uint32_t((warp - 8) * 32) << 16;
-    int64_t j = 0;
-    for (int64_t m = blockIdx.x; m < ntile; m += gridDim.x) {
-      int e;
-      int64_t r0, r1;
-      if (!mlp_tile(p, c0, m, e, r0, r1)) continue;
-      const int buf = int(j % L::NA);
-      const uint32_t ph = par(j / L::NA);
-      ++j;
-      const int64_t row = r0 + ptid;
-      float4 v[D / 4];
-      if (!(DBG && (p.dbg & 2)) && row < r1) {
-        const float* src = p.x + (p.perm ? int64_t(__ldg(p.perm + row)) : row) * D;
-#pragma unroll
-        for (int i = 0; i < D / 4; ++i) v[i] = __ldg(reinterpret_cast<const float4*>(src) + i);
-      } else {
-#pragma unroll
-        for (int i = 0; i < D / 4; ++i) v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (kDbg && (p.dbg & 8) && warp != kMma1 && warp != kMma2) {
+    // debug: the MMA issuers alone, no waits (raw instruction-stream rate)
+  } else if (warp >= kProd && warp < kMma1) {
+    // ------- producers: x rows → A1 planes (TMEM); drain acc2 -------
+    // warp (quad, kc): rows quad·32 + lane (= TMEM lanes), channels [32kc, 32kc + 32)
+    const int quad = (warp - kProd) & 3, kc = (warp - kProd) >> 2;
+    const int ptid = quad * 32 + lane;
+    const uint32_t lane_base = uint32_t(quad * 32) << 16;
+    float* xb = reinterpret_cast<float*>(smem + L::OFF_XB) + (warp - kProd) * 32 * kXPitch;
+    auto drain = [&](int64_t jt, int e, int64_t r0, int64_t r1) {
+      const int ob = int(jt & 1);
+      const uint32_t oph = uint32_t(jt >> 1) & 1u;
+      if (kDbg && (p.dbg & 2)) {
+        PW(S_OF, &o_full[ob], oph);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_empty[ob]);
+        return;
       }
-      PWAIT(P_A1E, &a1_empty[buf], ph ^ 1u);
-      tc_fence_after();
-      const uint32_t a1 = tmem + lane_base + L::T_A1 + uint32_t(buf) * L::A1COLS;
-#pragma unroll
-      for (int kc = 0; kc < L::KC1; ++kc) {
-        if (DBG && (p.dbg & 2)) break;   // debug: no A1 stores
-        uint32_t hp[16], mp[16], lp[16];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const float4 q = v[kc * 8 + t];
-          const Split3 a = split3x2(q.x, q.y);
-          const Split3 b = split3x2(q.z, q.w);
-          hp[2 * t] = bf2_bits(a.h);
-          hp[2 * t + 1] = bf2_bits(b.h);
-          mp[2 * t] = bf2_bits(a.m);
-          mp[2 * t + 1] = bf2_bits(b.m);
-          lp[2 * t] = bf2_bits(a.l);
-          lp[2 * t + 1] = bf2_bits(b.l);
-        }
-        tmem_st16(a1 + kc * 3 * kPlaneCols, hp);
-        tmem_st16(a1 + kc * 3 * kPlaneCols + kPlaneCols, mp);
-        tmem_st16(a1 + kc * 3 * kPlaneCols + 2 * kPlaneCols, lp);
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&a1_full[buf]);
-    }
-  } else if (warp == kW1 || warp == kW2) {
-    // ---------------- weight streamers (one thread each) ----------------
-    if (lane == 0) {
-      const bool first = warp == kW1;
-      uint64_t* full = first ? w1_full : w2_full;
-      uint64_t* empty = first ? w1_empty : w2_empty;
-      uint8_t* ring = smem + (first ? L::OFF_W1 : L::OFF_W2);
-      const uint32_t slot_bytes = first ? L::W1C : L::W2C;
-      int64_t q = 0;
-      for (int64_t m = blockIdx.x; m < ntile; m += gridDim.x) {
-        int e;
-        int64_t r0, r1;
-        if (!mlp_tile(p, c0, m, e, r0, r1)) continue;
-        const int np = p.np[e];
-        const uint32_t bytes = first ? uint32_t(L::KC1 * np) * (HC * 32 * 2)
-                                     : uint32_t(np) * (D * 32 * 2);
-        const uint16_t* src0 = first ? p.w1[e] : p.w2[e];
-        for (int c = 0; c < nchunk; ++c, ++q) {
-          const int s = int(q % L::NW);
-          PWAIT(first ? P_W1E : P_W2E, &empty[s], par(q / L::NW) ^ 1u);
-          if (DBG && (p.dbg & 32)) {   // debug: no weight copies (slot contents stale)
-            mbar_arrive(&full[s]);
-            continue;
-          }
-          mbar_expect_tx(&full[s], bytes);
-          bulk_g2s(ring + s * slot_bytes, src0 + size_t(c) * (bytes / 2), bytes, &full[s]);
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp == kMma) {
-    // ---------------- MMA issuer (whole warp; one elected lane issues) ----------------
-    constexpr uint32_t id1 = idesc_bf16_m128(HC);
-    constexpr uint32_t id2 = idesc_bf16_m128(D);
-    const uint32_t sbase = smem_u32(smem);
-    // The CTA's non-empty tiles in order (expert of each). fc1 runs LOOK
-    // chunks ahead of fc2 across tile boundaries (no per-tile drain). Two
-    // cursors walk (tile, chunk) with incremental counters: buffer indices
-    // and mbarrier parities flip on wrap, no divisions in the loop.
-    int nt = 0;
-    if (lane == 0) {
-      for (int64_t m = blockIdx.x; m < ntile && nt < kMaxTiles; m += gridDim.x) {
-        int e;
-        int64_t r0, r1;
-        if (mlp_tile(p, c0, m, e, r0, r1)) tile_e[nt++] = uint8_t(e);
-      }
-    }
-    nt = __shfl_sync(0xffffffffu, nt, 0);
-    __syncwarp();
-    struct Cur {
-      int c, jt, np;     // chunk within tile, tile index, planes of the tile's expert
-      int b, ws;         // acc1 / A2 buffer, weight ring slot
-      uint32_t pb, pw;   // parities of b and ws (flip on wrap)
-    };
-    const int np0 = p.np[0], np1 = p.np[1];
-    auto start_tile = [&](Cur& k) { k.np = (k.jt < nt && tile_e[k.jt]) ? np1 : np0; };
-    auto advance = [&](Cur& k) {
-      if (++k.b == L::NB) { k.b = 0; k.pb ^= 1u; }
-      if (++k.ws == L::NW) { k.ws = 0; k.pw ^= 1u; }
-      if (++k.c == nchunk) { k.c = 0; ++k.jt; start_tile(k); }
-    };
-    Cur f1{0, 0, 0, 0, 0, 0u, 0u}, f2{0, 0, 0, 0, 0, 0u, 0u};
-    start_tile(f1);
-    start_tile(f2);
-    int ab1 = 0;                 // A1 buffer of f1's tile
-    uint32_t pab1 = 0u;
-    int ab2 = 0;                 // A1 buffer of f2's tile (released after its last fc1)
-    int ob2 = 0;                 // acc2 buffer of f2's tile
-    uint32_t pob2 = 0u;
-    const int total_q = nt * nchunk;
-    constexpr int LOOK = L::LOOK;
-    for (int step = 0; step < total_q + LOOK; ++step) {
-      if (step < total_q) {  // ---- fc1(f1)
-        if (f1.c == 0) PWAIT(P_A1F, &a1_full[ab1], pab1);
-        PWAIT(P_W1F, &w1_full[f1.ws], f1.pw);
-        PWAIT(P_HE1, &h_empty[f1.b], f1.pb ^ 1u);   // acc1[b] drained (GELU(q - NB))
-        if (!(DBG && (p.dbg & 128))) tc_fence_after();
-        const uint32_t a1 = tmem + L::T_A1 + uint32_t(ab1) * L::A1COLS;
-        const uint32_t w1 = sbase + L::OFF_W1 + f1.ws * L::W1C;
-        const uint32_t d1 = tmem + L::T_ACC1 + uint32_t(f1.b * HC);
-        if (!(DBG && (p.dbg & 16))) {
-#pragma unroll
-          for (int kc = 0; kc < L::KC1; ++kc)
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-              const uint32_t ad = a1 + kc * 3 * kPlaneCols + ks * 8;
-              const uint64_t bd = smem_desc(w1 + kc * f1.np * (HC * 32 * 2) + ks * 256);
-              const uint32_t acc = (kc | ks) != 0;
-              if (f1.np == 1)
-                mma_chain3_ts_w(d1, ad, bd, kPlaneCols, id1, acc);
-              else
-                mma_chain6_ts_w(d1, ad, bd, kPlaneCols, (HC * 32 * 2) >> 4, id1, acc);
-            }
-        }
-        commit(&h_full[f1.b]);
-        commit(&w1_empty[f1.ws]);
-        const bool last1 = f1.c == nchunk - 1;
-        if (last1) commit(&a1_empty[ab1]);   // A1 fully consumed
-        advance(f1);
-        if (last1) {
-          if (++ab1 == L::NA) { ab1 = 0; pab1 ^= 1u; }
-        }
-      }
-      if (step >= LOOK) {   // ---- fc2(f2)
-        if (f2.c == 0) PWAIT(P_OE, &o_empty[ob2], pob2 ^ 1u);   // acc2[ob] drained
-        PWAIT(P_W2F, &w2_full[f2.ws], f2.pw);
-        PWAIT(P_HE2, &h_empty[f2.b], f2.pb);            // GELU(q) wrote A2[b]
-        if (!(DBG && (p.dbg & 128))) tc_fence_after();
-        const uint32_t a2 = tmem + L::T_A2 + uint32_t(f2.b) * L::A2COLS;
-        const uint32_t w2 = sbase + L::OFF_W2 + f2.ws * L::W2C;
-        const uint32_t d2 = tmem + L::T_ACC2 + uint32_t(ob2 * D);
-        if (!(DBG && (p.dbg & 16))) {
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            const uint64_t bd = smem_desc(w2 + ks * 256);
-            const uint32_t acc = (f2.c | ks) != 0;
-            if (f2.np == 1)
-              mma_chain3_ts_w(d2, a2 + ks * 8, bd, kPlaneCols, id2, acc);
-            else
-              mma_chain6_ts_w(d2, a2 + ks * 8, bd, kPlaneCols, (D * 32 * 2) >> 4, id2, acc);
-          }
-        }
-        commit(&a2_empty[f2.b]);
-        commit(&w2_empty[f2.ws]);
-        const bool last2 = f2.c == nchunk - 1;
-        if (last2) commit(&o_full[ob2]);
-        advance(f2);
-        if (last2) {
-          if (++ob2 == 2) { ob2 = 0; pob2 ^= 1u; }
-        }
-      }
-    }
-    (void)ab2;
-  } else {
-    // ---------------- GELU groups + final epilogue (warps 0-7) ----------------
-    const int g = warp >> 2, quad = warp & 3;
-    const int rl = quad * 32 + lane;
-    float* xb = reinterpret_cast<float*>(smem + L::OFF_XB) + warp * 32 * kXPitch;
-    int64_t q0 = 0;
-    int64_t j = 0;
-    for (int64_t m = blockIdx.x; m < ntile; m += gridDim.x) {
-      int e;
-      int64_t r0, r1;
-      if (!mlp_tile(p, c0, m, e, r0, r1)) continue;
-      const int ob = int(j & 1);
-      const uint32_t oph = par(j >> 1);
-      ++j;
-      // the draining group's row metadata (dependent perm → gate loads) is
-      // issued before the tile's GELU chunks so its latency overlaps them
-      const int64_t r = r0 + rl;
-      const bool r_ok = r < r1;
+      const int64_t r = r0 + ptid;
       int64_t orow = -1;
       float gt = 1.f;
-      if (ob == g && r_ok) {
+      if (r < r1) {
         orow = p.perm ? int64_t(__ldg(p.perm + r)) : r;
         if (p.gate) gt = __ldg(p.gate + orow);
       }
-      for (int c = 0; c < nchunk; ++c) {
-        const int64_t q = q0 + c;
-        if (int(q & 1) != g) continue;
-        const int b = int(q % L::NB);
-        const uint32_t ph = par(q / L::NB);
-        PWAIT(P_HF, &h_full[b], ph);            // fc1(q) done
-        PWAIT(P_A2E, &a2_empty[b], ph ^ 1u);     // fc2(q - NB) finished reading A2[b]
-        tc_fence_after();
-        const uint32_t lane_base = uint32_t(quad * 32) << 16;
-        float v[32];
-        if (!(DBG && (p.dbg & 4))) {   // (debug switch: skip the GELU pass)
-        {
-          float lo[16], hi[16];
-          const uint32_t ta = tmem + lane_base + L::T_ACC1 + uint32_t(b * HC);
-          tmem_ld16(ta, lo);
-          tmem_ld16(ta + 16, hi);
-#pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            v[t] = lo[t];
-            v[16 + t] = hi[t];
-          }
-        }
-        {
-          uint32_t hp[16], mp[16], lp[16];
-#pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            float g0 = v[2 * t], g1 = v[2 * t + 1];
-            gelu_fast2(g0, g1);
-            const Split3 sp = split3x2(g0, g1);
-            hp[t] = bf2_bits(sp.h);
-            mp[t] = bf2_bits(sp.m);
-            lp[t] = bf2_bits(sp.l);
-          }
-          const uint32_t a2 = tmem + lane_base + L::T_A2 + uint32_t(b) * L::A2COLS;
-          tmem_st16(a2, hp);
-          tmem_st16(a2 + kPlaneCols, mp);
-          tmem_st16(a2 + 2 * kPlaneCols, lp);
-          tmem_st_wait();
-        }
-        }
-        tc_fence_before();
-        mbar_arrive(&h_empty[b]);
-      }
-      q0 += nchunk;
-      if (ob != g) continue;   // the other group drains this tile's acc2
-      // ---- final epilogue: acc2 (128 x D) → × gate → + residual → scatter ----
-      int64_t* rt = rowtab + g * 128;
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");   // previous table consumed
-      rt[rl] = orow;
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");   // table published
       // the lane's 4 output rows (it * 8 + lane / 4) and 4 channels per 16-wide
-      // column block; residual rows are prefetched one block ahead, the first
-      // block before waiting for the accumulator
+      // column block; residual rows prefetched one block ahead
       const int c4 = (lane & 3) * 4;
       int64_t orow_l[4];
 #pragma unroll
-      for (int it = 0; it < 4; ++it) orow_l[it] = rt[quad * 32 + it * 8 + (lane >> 2)];
+      for (int it = 0; it < 4; ++it) orow_l[it] = __shfl_sync(0xffffffffu, orow, it * 8 + (lane >> 2));
       float4 res[2][4];
       auto load_res = [&](int cb, float4 (&dst)[4]) {
 #pragma unroll
@@ -468,15 +310,23 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
                         ? __ldg(reinterpret_cast<const float4*>(p.residual + orow_l[it] * D + cb + c4))
                         : make_float4(0.f, 0.f, 0.f, 0.f);
       };
-      load_res(0, res[0]);
-      PWAIT(P_OF, &o_full[ob], oph);
+      load_res(32 * kc, res[0]);
+      const bool two = L::CAT && (e ? p.np1 : p.np0) == 3;   // dense d = 32: two partial sums
+      PW(S_OF, &o_full[ob], oph);
       tc_fence_after();
+      const uint32_t acc = tmem + lane_base + L::T_ACC2 + uint32_t(ob) * L::ACC2C;
 #pragma unroll
-      for (int cb = 0; cb < D; cb += 16) {
+      for (int cb = 32 * kc; cb < 32 * kc + 32; cb += 16) {
         const int rb = (cb >> 4) & 1;
-        if (cb + 16 < D) load_res(cb + 16, res[rb ^ 1]);
+        if (cb + 16 < 32 * kc + 32) load_res(cb + 16, res[rb ^ 1]);
         float v[16];
-        tmem_ld16(tmem + (uint32_t(quad * 32) << 16) + L::T_ACC2 + uint32_t(ob * D + cb), v);
+        tmem_ld16(acc + uint32_t(cb), v);
+        if (two) {
+          float w[16];
+          tmem_ld16(acc + 32u + uint32_t(cb), w);
+#pragma unroll
+          for (int t = 0; t < 16; ++t) v[t] = v[t] + w[t];
+        }
 #pragma unroll
         for (int t = 0; t < 16; t += 4)
           *reinterpret_cast<float4*>(xb + lane * kXPitch + t) =
@@ -498,38 +348,391 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(MlpParams p) {
         __syncwarp();
       }
       tc_fence_before();
-      mbar_arrive(&o_empty[ob]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[ob]);
+    };
+    // the NA previous tiles (their acc2 is drained NA tiles later)
+    int pe1 = 0, pe2 = 0;
+    int64_t pa1 = 0, pb1 = 0, pa2 = 0, pb2 = 0;
+    int64_t j = 0;
+    int ab = 0;
+    uint32_t pab = 0u;
+    for (int64_t m = blockIdx.x; m < ntile; m += gridDim.x) {
+      int e;
+      int64_t r0, r1;
+      if (!mlp_tile(p, c0, m, e, r0, r1)) continue;
+      const int64_t row = r0 + ptid;
+      float4 v[8];
+      if (row < r1 && !(kDbg && (p.dbg & 2))) {
+        const float* src = p.x + (p.perm ? int64_t(__ldg(p.perm + row)) : row) * D + 32 * kc;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = __ldg(reinterpret_cast<const float4*>(src) + i);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      PW(S_A1E, &a1_empty[ab], pab ^ 1u);
+      tc_fence_after();
+      if (!(kDbg && (p.dbg & 2))) {
+        const uint32_t a1 = tmem + lane_base + L::T_A1 + uint32_t(ab) * L::A1COLS;
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {   // 16 channels (8 bf16 pairs) at a time
+            uint32_t hp[8], mp[8], lp[8];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float4 q = v[sub * 4 + t];
+              const Split3 a = split3x2(q.x, q.y);
+              const Split3 b = split3x2(q.z, q.w);
+              hp[2 * t] = bf2_bits(a.h);
+              hp[2 * t + 1] = bf2_bits(b.h);
+              mp[2 * t] = bf2_bits(a.m);
+              mp[2 * t + 1] = bf2_bits(b.m);
+              lp[2 * t] = bf2_bits(a.l);
+              lp[2 * t + 1] = bf2_bits(b.l);
+            }
+            const uint32_t col = a1 + kc * 3 * kPlaneCols + sub * 8;
+            tmem_st8(col, hp);
+            tmem_st8(col + kPlaneCols, mp);
+            tmem_st8(col + 2 * kPlaneCols, lp);
+          }
+        tmem_st_wait();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a1_full[ab]);
+      if (++ab == L::NA) { ab = 0; pab ^= 1u; }
+      // then drain tile j - NA (its fc2 ends while fc1 works on the tiles between)
+      if (L::NA == 1 && j >= 1) drain(j - 1, pe1, pa1, pb1);
+      if (L::NA == 2 && j >= 2) drain(j - 2, pe2, pa2, pb2);
+      pe2 = pe1; pa2 = pa1; pb2 = pb1;
+      pe1 = e; pa1 = r0; pb1 = r1;
+      ++j;
+    }
+    if (L::NA == 2 && j >= 2) drain(j - 2, pe2, pa2, pb2);
+    if (j >= 1) drain(j - 1, pe1, pa1, pb1);
+  } else if (warp == kWld) {
+    // ---------------- weights ----------------
+    if (lane == 0) {
+      if (RES) {
+        const int ne = p.counts ? 2 : 1;
+        uint32_t total = 0;
+        for (int e = 0; e < ne; ++e)
+          total += uint32_t(e ? p.np1 : p.np0) * uint32_t(p.hidden) * 64u * uint32_t(L::KC1 + D / 32);
+        mbar_expect_tx(wres, total);
+        for (int e = 0; e < ne; ++e) {
+          const int np = e ? p.np1 : p.np0;
+          const uint32_t b1 = uint32_t(L::KC1 * np) * uint32_t(p.hidden) * 64u;
+          const uint32_t b2 = uint32_t(np) * uint32_t(p.hidden / 32) * uint32_t(D * 64);
+          bulk_g2s(smem + L::r_w1(e), e ? p.w1[1] : p.w1[0], b1, wres);
+          bulk_g2s(smem + L::r_w2(e), e ? p.w2[1] : p.w2[0], b2, wres);
+        }
+      } else {
+        // W1 and W2 chunk rings, filled in chunk order (W1(q), W2(q), W1(q+1) ...)
+        int s = 0;
+        uint32_t ph = 0u;
+        for (int64_t m = blockIdx.x; m < ntile; m += gridDim.x) {
+          int e;
+          int64_t r0, r1;
+          if (!mlp_tile(p, c0, m, e, r0, r1)) continue;
+          const int np = e ? p.np1 : p.np0;
+          const uint32_t by1 = uint32_t(L::KC1 * np) * (HC * 32 * 2);
+          const uint32_t by2 = uint32_t((HC / 32) * np) * (D * 32 * 2);
+          const uint8_t* s1 = reinterpret_cast<const uint8_t*>(e ? p.w1[1] : p.w1[0]);
+          const uint8_t* s2 = reinterpret_cast<const uint8_t*>(e ? p.w2[1] : p.w2[0]);
+          for (int c = 0; c < nchunk; ++c) {
+            PW(S_WR, &w1_empty[s], ph ^ 1u);
+            mbar_expect_tx(&w1_full[s], by1);
+            bulk_g2s(smem + s * L::W1C, s1 + size_t(c) * by1, by1, &w1_full[s]);
+            PW(S_WR, &w2_empty[s], ph ^ 1u);
+            mbar_expect_tx(&w2_full[s], by2);
+            bulk_g2s(smem + L::NW * L::W1C + s * L::W2C, s2 + size_t(c) * by2, by2, &w2_full[s]);
+            if (++s == L::NW) { s = 0; ph ^= 1u; }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kMma1) {
+    // ---------------- fc1 issuer: x planes (A1) · W1 chunk → acc1 buffer ----------------
+    constexpr uint32_t id1 = idesc_bf16_m128(HC);
+    constexpr uint64_t BP = (HC * 64) >> 4;   // W1 plane stride (descriptor units)
+    const uint32_t sbase = smem_u32(smem);
+    if (RES) PW(S_W, wres, 0);
+    int b = 0, ab = 0, s = 0, qq = 0;
+    uint32_t pb = 0u, pab = 0u, ps = 0u;
+    for (int64_t m = blockIdx.x; m < ntile; m += gridDim.x) {
+      int e;
+      int64_t r0, r1;
+      if (!mlp_tile(p, c0, m, e, r0, r1)) continue;
+      const bool shift = (e ? p.np1 : p.np0) == 1;
+      const uint32_t cstride = uint32_t(L::KC1 * (shift ? 1 : 3) * HC * 64);
+      uint32_t wrow = sbase + L::r_w1(e);
+      PW(S_A1F, &a1_full[ab], pab);
+      const uint32_t a1 = tmem + L::T_A1 + uint32_t(ab) * L::A1COLS;
+      for (int c = 0; c < nchunk; ++c, ++qq) {
+        if (!RES) PW(S_W, &w1_full[s], ps);
+        PW(S_BF, &buf_free[b], pb ^ 1u);   // fc2(q - 3) released the buffer
+        TL(0, qq);
+        tc_fence_after();
+        const uint32_t d1 = tmem + L::T_BUF + uint32_t(b) * kBufCols;
+        const uint64_t bd0 = smem_desc(RES ? wrow : sbase + uint32_t(s) * L::W1C);
+        if (!(kDbg && (p.dbg & 4))) {
+#pragma unroll
+          for (int kc = 0; kc < L::KC1; ++kc)
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+              const uint32_t ah = a1 + kc * 3 * kPlaneCols + ks * 8;
+              const uint32_t acc = (kc | ks) ? 1u : 0u;
+              if (shift) {
+                mma3(d1, ah, ah + kPlaneCols, ah + 2 * kPlaneCols,
+                     bd0 + uint64_t((kc * (HC * 64) + ks * 256) >> 4), id1, acc);
+              } else {
+                const uint64_t bd = bd0 + uint64_t((kc * (3 * HC * 64) + ks * 256) >> 4);
+                mma6(d1, ah, ah + kPlaneCols, ah + 2 * kPlaneCols, bd, bd + BP, bd + 2 * BP, id1, acc);
+              }
+            }
+        }
+        commit_w(&h_full[b]);
+        TL(1, qq);
+        if (!RES) commit_w(&w1_empty[s]);
+        if (++b == L::NB) { b = 0; pb ^= 1u; }
+        if (++s == L::NW) { s = 0; ps ^= 1u; }
+        wrow += cstride;
+      }
+      commit_w(&a1_empty[ab]);   // A1 fully consumed
+      if (++ab == L::NA) { ab = 0; pab ^= 1u; }
+    }
+  } else if (warp == kMma2) {
+    // ---------------- fc2 issuer: GELU planes (A2) · W2 chunk → acc2 ----------------
+    constexpr uint32_t id64 = idesc_bf16_m128(64);
+    constexpr uint32_t id32 = idesc_bf16_m128(32);
+    constexpr uint32_t id2 = idesc_bf16_m128(D);
+    constexpr uint64_t BP = (D * 64) >> 4;    // W2 plane stride (descriptor units)
+    const uint32_t sbase = smem_u32(smem);
+    if (RES) PW(S_W, wres, 0);
+    int b = 0, ob = 0, s = 0, qq = 0;
+    uint32_t pb = 0u, pob = 0u, ps = 0u;
+    for (int64_t m = blockIdx.x; m < ntile; m += gridDim.x) {
+      int e;
+      int64_t r0, r1;
+      if (!mlp_tile(p, c0, m, e, r0, r1)) continue;
+      const bool shift = (e ? p.np1 : p.np0) == 1;
+      const uint32_t cstride = uint32_t((HC / 32) * (shift ? 1 : 3) * D * 64);
+      uint32_t wrow = sbase + L::r_w2(e);
+      PW(S_OE, &o_empty[ob], pob ^ 1u);   // acc2[ob] drained
+      const uint32_t d2 = tmem + L::T_ACC2 + uint32_t(ob) * L::ACC2C;
+      for (int c = 0; c < nchunk; ++c, ++qq) {
+        if (!RES) PW(S_W, &w2_full[s], ps);
+        PW(S_HE, &h_empty[b], pb);        // GELU(q) wrote A2[b]
+        TL(4, qq);
+        tc_fence_after();
+        const uint32_t bb = tmem + L::T_BUF + uint32_t(b) * kBufCols;
+        const uint64_t bd0 = smem_desc(RES ? wrow : sbase + L::NW * L::W1C + uint32_t(s) * L::W2C);
+        const uint32_t a0 = c != 0 ? 1u : 0u;
+        if (!(kDbg && (p.dbg & 4))) {
+#pragma unroll
+          for (int ks = 0; ks < HC / 16; ++ks) {
+            // A2 planes of K step ks: kGeluAlt: hi at 32(ks/2) + 8(ks%2), mid 16
+            // further, lo at 64 + 16(ks/2) + 8(ks%2); else hi at 16ks, mid at
+            // 16ks + 8, lo at 64 + 8ks
+            const uint32_t ah = kGeluAlt ? bb + (ks >> 1) * 32u + (ks & 1) * 8u : bb + ks * 16u;
+            const uint32_t am = ah + (kGeluAlt ? 16u : 8u);
+            const uint32_t al = kGeluAlt ? bb + 64u + (ks >> 1) * 16u + (ks & 1) * 8u : bb + 64u + ks * 8u;
+            const uint32_t acc = ks ? 1u : a0;
+            if (shift) {
+              mma3(d2, ah, am, al, bd0 + uint64_t(((ks >> 1) * (D * 64) + (ks & 1) * 256) >> 4),
+                   id2, acc);
+            } else {
+              const uint64_t bd = bd0 + uint64_t(((ks >> 1) * (3 * D * 64) + (ks & 1) * 256) >> 4);
+              if (L::CAT)
+                mma_cat4(d2, ah, am, al, bd, bd + 2 * BP, id64, id32, acc);
+              else
+                mma6(d2, ah, am, al, bd, bd + BP, bd + 2 * BP, id2, acc);
+            }
+          }
+        }
+        commit_w(&buf_free[b]);
+        TL(5, qq);
+        if (!RES) commit_w(&w2_empty[s]);
+        if (++b == L::NB) { b = 0; pb ^= 1u; }
+        if (++s == L::NW) { s = 0; ps ^= 1u; }
+        wrow += cstride;
+      }
+      commit_w(&o_full[ob]);
+      if (++ob == 2) { ob = 0; pob ^= 1u; }
+    }
+  } else if (warp < kGelu && kGeluAlt) {
+    // ------- GELU: group gs = warp / 8 takes chunks q % 2 == gs; warp (h, quad)
+    // of the group takes hidden columns [32h, 32h + 32) = fc2 K steps 2h, 2h+1.
+    // Its planes go over its own consumed accumulator columns (hi [32h, 32h+16),
+    // mid [32h+16, 32h+32)) and the free columns [64 + 16h, 80 + 16h) (lo) -------
+    const int gs = warp >> 3, h = (warp >> 2) & 1, quad = warp & 3;
+    const uint32_t lb = tmem + (uint32_t(quad * 32) << 16) + L::T_BUF;
+    int nt = 0;
+    for (int64_t m = blockIdx.x; m < ntile; m += gridDim.x) {
+      int e;
+      int64_t r0, r1;
+      if (mlp_tile(p, c0, m, e, r0, r1)) ++nt;
+    }
+    const int total_q = nt * nchunk;
+    for (int q = gs; q < total_q; q += 2) {
+      const int b = q % L::NB;
+      const uint32_t ph = uint32_t(q / L::NB) & 1u;
+      PW(S_HF, &h_full[b], ph);             // fc1(q) done
+      if (warp == 0) TL(2, q);
+      tc_fence_after();
+      const uint32_t bb = lb + uint32_t(b) * kBufCols;
+      if (!(kDbg && (p.dbg & 1))) {
+        uint32_t r[32];
+        tmem_ld32_nowait(bb + uint32_t(32 * h), r);
+        tmem_ld_wait();
+        uint32_t hp[16], mp[16], lp[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          float g0 = __uint_as_float(r[2 * t]), g1 = __uint_as_float(r[2 * t + 1]);
+          if (kDbg && (p.dbg & 64)) {   // debug: no GELU math
+          } else if (t < 2 * NF) {
+            gelu_pair<true>(g0, g1);
+          } else {
+            gelu_pair<false>(g0, g1);
+          }
+          const Split3 sp = split3x2(g0, g1);
+          hp[t] = bf2_bits(sp.h);
+          mp[t] = bf2_bits(sp.m);
+          lp[t] = bf2_bits(sp.l);
+        }
+        tmem_st16(bb + uint32_t(32 * h), hp);
+        tmem_st16(bb + uint32_t(32 * h + 16), mp);
+        tmem_st16(bb + uint32_t(64 + 16 * h), lp);
+        tmem_st_wait();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&h_empty[b]);
+      if (warp == 0) TL(3, q);
+      if (warp == kGelu - 1) TL(6, q);
+    }
+  } else if (warp < kGelu) {
+    // ------- GELU (kGeluAlt = false): warp (k, quad) takes hidden columns [16k, 16k + 16) of every
+    // chunk = K step k of fc2; its planes go over its own consumed accumulator
+    // columns (hi [16k, 16k + 8), mid [16k + 8, 16k + 16)) and the free
+    // columns [64 + 8k, 72 + 8k) (lo) -------
+    const int k = warp >> 2, quad = warp & 3;
+    const uint32_t lb = tmem + (uint32_t(quad * 32) << 16) + L::T_BUF;
+    int nt = 0;
+    for (int64_t m = blockIdx.x; m < ntile; m += gridDim.x) {
+      int e;
+      int64_t r0, r1;
+      if (mlp_tile(p, c0, m, e, r0, r1)) ++nt;
+    }
+    const int total_q = nt * nchunk;
+    int b = 0;
+    uint32_t ph = 0u;
+    for (int q = 0; q < total_q; ++q) {
+      PW(S_HF, &h_full[b], ph);             // fc1(q) done
+      if (warp == 0) TL(2, q);
+      tc_fence_after();
+      const uint32_t bb = lb + uint32_t(b) * kBufCols;
+      if (!(kDbg && (p.dbg & 1))) {
+        float r[16];
+        if (kDbg && (p.dbg & 128)) {   // debug: no TMEM traffic (synthetic inputs, no stores)
+#pragma unroll
+          for (int t = 0; t < 16; ++t) r[t] = float(t + q) * 0.01f;
+        } else {
+          tmem_ld16(bb + uint32_t(16 * k), r);
+        }
+        uint32_t hp[8], mp[8], lp[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          float g0 = r[2 * t], g1 = r[2 * t + 1];
+          if (kDbg && (p.dbg & 64)) {   // debug: no GELU math
+          } else if (t < NF) {
+            gelu_pair<true>(g0, g1);
+          } else {
+            gelu_pair<false>(g0, g1);
+          }
+          const Split3 sp = split3x2(g0, g1);
+          hp[t] = bf2_bits(sp.h);
+          mp[t] = bf2_bits(sp.m);
+          lp[t] = bf2_bits(sp.l);
+        }
+        if (kDbg && (p.dbg & 128)) {
+          if (hp[0] == 0x12345u && mp[1] == 7u && lp[2] == 9u) mbar_arrive(&h_empty[b]);   // keep the math live
+        } else {
+          tmem_st8(bb + uint32_t(16 * k), hp);
+          tmem_st8(bb + uint32_t(16 * k + 8), mp);
+          tmem_st8(bb + uint32_t(64 + 8 * k), lp);
+          tmem_st_wait();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&h_empty[b]);
+      if (warp == 0) TL(3, q);
+      if (warp == kGelu - 1) TL(6, q);
+      if (++b == L::NB) { b = 0; ph ^= 1u; }
     }
   }
-  if (DBG && p.prof && lane == 0) {
-    const int site = warp < 8 ? P_T_GELU : (warp < 12 ? P_T_PROD : (warp == kMma ? P_T_MMA : -1));
+#ifdef SA_DEBUG
+  if (p.prof && lane == 0) {
+    const int site = warp < kGelu ? T_GELU
+                     : (warp < kMma1 ? T_PROD : (warp == kMma1 ? T_MMA1 : (warp == kMma2 ? T_MMA2 : -1)));
     if (site >= 0) atomicAdd(&sprof[site], (unsigned long long)(clock64() - t_start));
   }
-#undef PWAIT
+#endif
+#undef PW
+#undef TL
   tc_fence_before();
   __syncthreads();
-  if (DBG && p.prof && tid < P_NSITE) atomicAdd(p.prof + tid, sprof[tid]);
-  if (warp == kMma) tmem_dealloc<L::TCOLS>(tmem);
+#ifdef SA_DEBUG
+  if (p.prof && tid < S_N) atomicAdd(p.prof + tid, sprof[tid]);
+#endif
+  if (warp == kMma1) tmem_dealloc<L::TCOLS>(tmem);
 }
 
 }  // namespace tcm
 
+// GELU pairs (of 8 per thread and chunk) whose reciprocal runs on the FMA pipe
+SA_DEBUG_SWITCH(int, g_mlp_gelu_fma, 0, sa_debug_mlp_mode)
+SA_DEBUG_SWITCH(int, g_mlp_dbg, 0, sa_debug_mlp_roles)
 #ifdef SA_DEBUG
 static unsigned long long* g_mlp_prof = nullptr;
 extern "C" void sa_debug_mlp_profile(void* dev_buf) {
   g_mlp_prof = static_cast<unsigned long long*>(dev_buf);
 }
+static long long* g_mlp_tl = nullptr;
+extern "C" void sa_debug_mlp_timeline(void* dev_buf) { g_mlp_tl = static_cast<long long*>(dev_buf); }
 #else
 static constexpr unsigned long long* g_mlp_prof = nullptr;
+static constexpr long long* g_mlp_tl = nullptr;
 #endif
-SA_DEBUG_SWITCH(int, g_mlp_dbg, 0, sa_debug_mlp_mode)
 
 static int g_sms_mlp = 0;
+
+template <int D, bool RES, int NF>
+static void mlp_launch_one(const tcm::MlpParams& p, int grid, cudaStream_t s) {
+  const int smem = int(tcm::Layout<D, RES>::TOTAL);
+  cudaFuncSetAttribute(tcm::mlp_kernel<D, RES, NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       smem);
+  tcm::mlp_kernel<D, RES, NF><<<grid, tcm::Roles<D>::kThreads, smem, s>>>(p);
+}
+
+template <int D, bool RES>
+static void mlp_launch_nf(const tcm::MlpParams& p, int grid, cudaStream_t s) {
+  switch (g_mlp_gelu_fma) {
+#ifdef SA_DEBUG
+    case 2: mlp_launch_one<D, RES, 2>(p, grid, s); break;
+    case 4: mlp_launch_one<D, RES, 4>(p, grid, s); break;
+#endif
+    default: mlp_launch_one<D, RES, 0>(p, grid, s); break;
+  }
+}
 
 static int mlp_launch(tcm::MlpParams& p, int d, cudaStream_t s) {
   using namespace tcm;
   if (p.M == 0) return SA_OK;
   p.prof = g_mlp_prof;
+  p.tl = g_mlp_tl;
   p.dbg = g_mlp_dbg;
   if (g_sms_mlp == 0) {
     int dev = 0;
@@ -538,19 +741,14 @@ static int mlp_launch(tcm::MlpParams& p, int d, cudaStream_t s) {
   }
   const int64_t tiles = cdiv(p.M, 128) + (p.counts ? 1 : 0);
   const int grid = int(tiles < g_sms_mlp ? tiles : g_sms_mlp);
-  const bool dbg = p.prof != nullptr || p.dbg != 0;
-#define SA_MLP_LAUNCH(DV, DB)                                                               \
-  {                                                                                         \
-    const int smem = int(Layout<DV>::TOTAL);                                                \
-    cudaFuncSetAttribute(mlp_kernel<DV, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-    mlp_kernel<DV, DB><<<grid, tcm::kThreads, smem, s>>>(p);                                \
-  }
   if (d == 32) {
-    if (dbg) SA_MLP_LAUNCH(32, true) else SA_MLP_LAUNCH(32, false)
+    if (p.hidden <= kResHidden)
+      mlp_launch_nf<32, true>(p, grid, s);
+    else
+      mlp_launch_nf<32, false>(p, grid, s);
   } else {
-    if (dbg) SA_MLP_LAUNCH(64, true) else SA_MLP_LAUNCH(64, false)
+    mlp_launch_nf<64, false>(p, grid, s);
   }
-#undef SA_MLP_LAUNCH
   count_launch(1);
   SA_LAUNCH_CHECK("mlp_kernel");
   return SA_OK;
@@ -560,11 +758,13 @@ static int mlp_launch(tcm::MlpParams& p, int d, cudaStream_t s) {
 
 using namespace sa;
 
-/* The fused kernels read W1 packed with bn = 32 (hidden chunks) and W2 packed
+/* The fused kernels read W1 packed with bn = 64 (hidden chunks) and W2 packed
  * with bn = d; see sa_weight_pack. */
 extern "C" int sa_tc_fused_mlp_ok(int64_t d, int64_t hidden) {
-  return (d == 32 || d == 64) && hidden % tcm::HC == 0 && hidden > 0;
+  return (d == 32 || d == 64) && hidden % tcm::HC == 0 && hidden > 0 && hidden <= 8192;
 }
+
+extern "C" int sa_tc_fused_mlp_w1_bn(void) { return tcm::HC; }
 
 extern "C" int sa_tc_moe_mlp_fused(const float* x, const int32_t* perm, const int32_t* counts,
                                    const float* gate, const void* w1_dense, const void* w2_dense,
@@ -588,8 +788,8 @@ extern "C" int sa_tc_moe_mlp_fused(const float* x, const int32_t* perm, const in
   p.w2[0] = static_cast<const uint16_t*>(w2_dense);
   p.w1[1] = static_cast<const uint16_t*>(w1_shift);
   p.w2[1] = static_cast<const uint16_t*>(w2_shift);
-  p.np[0] = 3;
-  p.np[1] = 1;
+  p.np0 = 3;
+  p.np1 = 1;
   p.M = M;
   p.hidden = int(hidden);
   return mlp_launch(p, int(d), as_stream(stream));
@@ -610,7 +810,8 @@ extern "C" int sa_tc_mlp_fused(const float* x, const void* w1pack, int w1_kind,
   p.y = y;
   p.w1[0] = static_cast<const uint16_t*>(w1pack);
   p.w2[0] = static_cast<const uint16_t*>(w2pack);
-  p.np[0] = w1_kind == SA_W_SHIFT ? 1 : 3;
+  p.np0 = w1_kind == SA_W_SHIFT ? 1 : 3;
+  p.np1 = p.np0;
   p.M = M;
   p.hidden = int(hidden);
   return mlp_launch(p, int(d), as_stream(stream));

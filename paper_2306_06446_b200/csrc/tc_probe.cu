@@ -92,13 +92,6 @@ namespace sa {
 namespace tcp {
 using namespace tc;
 
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-      : "memory");
-  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
                                             uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -139,6 +132,7 @@ __global__ void __launch_bounds__(128, 1) mma_ts_probe_kernel(int n, int iters,
     for (int c = 0; c < 8; ++c)
       r[c] = uint32_t(a_in[tid * 16 + 2 * c]) | (uint32_t(a_in[tid * 16 + 2 * c + 1]) << 16);
     tmem_st8(tmem + (uint32_t(warp * 32) << 16) + a_col, r);
+    tmem_st_wait();
   }
   tc_fence_before();
   __syncthreads();
@@ -271,5 +265,267 @@ extern "C" int sa_probe_mma_mlp(int chunks, int np, int variant, unsigned long l
   // variant bit 3: one CTA per SM (full chip)
   sa::tcp::mma_mlp_probe_kernel<<<(variant & 8) ? 148 : 1, 128, smem, sa::as_stream(stream)>>>(
       chunks, np, variant, out);
+  return cudaGetLastError() == cudaSuccess ? SA_OK : SA_ERR_CUDA;
+}
+
+// ---- operand-pattern probe (diagnostics only) ---------------------------------
+// cycles per M=128 K=16 bf16 MMA (N = n) for the operand patterns the fused MLP
+// issues: mode 0 one A (TMEM) / one B; 1: A cycles over three TMEM planes;
+// 2: A and B cycle over three planes; 3: A from shared memory, cycling;
+// 4: as 2, D alternates between two accumulators. rnd: pseudo-random bf16
+// operands instead of ones. grid: CTAs (one per SM).
+namespace sa {
+namespace tcp {
+__global__ void __launch_bounds__(128, 1) mma_seq_probe_kernel(int n, int iters, int mode, int rnd,
+                                                               unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < (6 * 16384) / 4; i += 128)
+    reinterpret_cast<uint32_t*>(smem)[i] =
+        rnd ? ((uint32_t(i) * 2654435761u) & 0xbfffbfffu) | 0x3c003c00u : 0x3f803f80u;
+  if (warp == 0) tmem_alloc<512>(&slot);
+  if (tid == 0) {
+    mbar_init(&bar, (mode == 16 || mode == 18) ? 2 : 1);
+    fence_barrier_init();
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  {
+    uint32_t r[16];
+    for (int c = 0; c < 16; ++c)
+      r[c] = rnd ? ((uint32_t(tid * 16 + c) * 2246822519u) & 0xbfffbfffu) | 0x3c003c00u : 0x3f803f80u;
+    for (int col = 384; col < 512; col += 16) tmem_st16(tmem + (uint32_t(warp * 32) << 16) + col, r);
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (mode == 19 || mode == 20) {
+    // mode 19: warp 0 issues the mode-12 MMA stream while warps 1-3 stream
+    // tcgen05.ld / st over TMEM columns 256-383 (the GELU pattern); mode 20:
+    // the loads / stores alone (warps 1-3), reported as cycles per MMA-slot
+    const uint32_t idesc = idesc_bf16_m128(n);
+    const uint32_t id32 = idesc_bf16_m128(32);
+    const uint32_t sb = smem_u32(smem);
+    const uint64_t bpd = (uint32_t(n) * 64) >> 4;
+    const long long t0 = clock64();
+    if (warp == 0 && mode == 19) {
+      for (int i = 0; i < iters; i += 12) {
+        const uint64_t b0 = smem_desc(sb + 3 * 16384 + (i & 4) * 64);
+        const uint32_t a0 = tmem + 384 + (i & 4) * 2;
+        const bool odd = (i / 12) & 1;
+#pragma unroll
+        for (int u = 0; u < 12; ++u)
+          mma_ts_w(tmem + (odd ? 192u : 0u), a0 + uint32_t(u % 3) * 16, b0 + uint64_t(u / 6) * bpd,
+                   odd ? id32 : idesc, (i | u) ? 1u : 0u);
+      }
+      commit_w(&bar);
+      mbar_wait(&bar, 0);
+    } else if (warp > 0) {
+      const uint32_t base = tmem + (uint32_t(warp * 32) << 16) + 256;
+      for (int i = 0; i < iters / 4; ++i) {
+        float v[16];
+        tmem_ld16(base + (i & 3) * 16, v);
+        uint32_t r[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) r[t] = __float_as_uint(v[2 * t] + v[2 * t + 1]);
+        tmem_st8(base + 64 + (i & 7) * 8, r);
+        tmem_st8(base + 96 + (i & 3) * 8, r);
+        tmem_st_wait();
+      }
+    }
+    const long long t2 = clock64();
+    if (blockIdx.x == 0 && tid == (mode == 19 ? 0 : 32)) {
+      out[0] = (unsigned long long)(t2 - t0);
+      out[1] = (unsigned long long)(t2 - t0);
+    }
+  } else if (mode >= 16 && warp < 2) {
+    // mode 16: two warps issue concurrently (each 12 MMAs N = n into its own
+    // D, then a commit); mode 17: one warp, same stream with the commit;
+    // mode 18: two warps, no commits
+    const uint32_t idesc = idesc_bf16_m128(n);
+    const uint32_t sb = smem_u32(smem);
+    const uint64_t bpd = (uint32_t(n) * 64) >> 4;
+    __shared__ __align__(8) uint64_t cbar[2];
+    if (mode != 17 || warp == 0) {
+      const long long t0 = clock64();
+      for (int i = 0; i < iters; i += 12) {
+        const uint64_t b0 = smem_desc(sb + 3 * 16384 + (i & 4) * 64);
+        const uint32_t a0 = tmem + 384 + (i & 4) * 2 + warp * 48;
+        const uint32_t d = tmem + warp * 192;
+#pragma unroll
+        for (int u = 0; u < 12; ++u)
+          mma_ts_w(d, a0 + uint32_t(u % 3) * 16, b0 + uint64_t(u / 6) * bpd, idesc, (i | u) ? 1u : 0u);
+        if (mode != 18) commit_w(&cbar[warp]);
+      }
+      const long long t1 = clock64();
+      commit_w(&bar);
+      if (warp == 0) mbar_wait(&bar, 0);
+      const long long t2 = clock64();
+      if (blockIdx.x == 0 && tid == 0) {
+        out[0] = (unsigned long long)(t1 - t0);
+        out[1] = (unsigned long long)(t2 - t0);
+      }
+    }
+  } else if (mode >= 8 && mode < 16 && warp == 0) {
+    // warp-wide issue (elect inside the asm), per-MMA operands from the loop
+    // counter: mode 8 A / B cycle over three planes; mode 9 + D alternates;
+    // mode 10: the same, unrolled x6 from per-iteration base addresses
+    const uint32_t idesc = idesc_bf16_m128(n);
+    const uint32_t sb = smem_u32(smem);
+    const uint32_t bplane = uint32_t(n) * 64;
+    const long long t0 = clock64();
+    if (mode == 13 || mode == 14 || mode == 15) {
+      // mode 12's pattern at the fused MLP's TMEM columns: 13 D = 96 / 288, A at
+      // 416 (x planes); 14 D = 0 / 256, A at 416; 15 D = 96 / 288, A at 384
+      const uint32_t id32 = idesc_bf16_m128(32);
+      const uint32_t dd0 = mode == 14 ? 0u : 96u, dd1 = mode == 14 ? 256u : 288u;
+      const uint32_t abase = mode == 15 ? 384u : 416u;
+      for (int i = 0; i < iters; i += 12) {
+        const uint64_t b0 = smem_desc(sb + 3 * 16384 + (i & 4) * 64);
+        const uint32_t a0 = tmem + abase + (i & 4) * 2;
+        const uint64_t bpd = bplane >> 4;
+#pragma unroll
+        for (int u = 0; u < 12; ++u) {
+          const bool odd = (i / 12) & 1;
+          mma_ts_w(tmem + (odd ? dd1 : dd0), a0 + uint32_t(u % 3) * 16, b0 + uint64_t(u / 6) * bpd,
+                   odd ? id32 : idesc, (i | u) ? 1u : 0u);
+        }
+      }
+    } else if (mode == 11 || mode == 12) {
+      // mode 11: the same, N alternating n / 32 every MMA; mode 12: 12 MMAs into
+      // D0 (N = n) then 12 into D1 (N = 32), as fc1 / fc2 chunks alternate
+      const uint32_t id32 = idesc_bf16_m128(32);
+      for (int i = 0; i < iters; i += 12) {
+        const uint64_t b0 = smem_desc(sb + 3 * 16384 + (i & 4) * 64);
+        const uint32_t a0 = tmem + 384 + (i & 4) * 2;
+        const uint64_t bpd = bplane >> 4;
+#pragma unroll
+        for (int u = 0; u < 12; ++u) {
+          const bool odd = mode == 11 ? (u & 1) : ((i / 12) & 1);
+          mma_ts_w(tmem + (odd ? 192u : 0u), a0 + uint32_t(u % 3) * 16, b0 + uint64_t(u / 6) * bpd,
+                   odd ? id32 : idesc, (i | u) ? 1u : 0u);
+        }
+      }
+    } else if (mode == 10) {
+      for (int i = 0; i < iters; i += 6) {
+        const uint64_t b0 = smem_desc(sb + 3 * 16384 + (i & 2) * 128);
+        const uint32_t a0 = tmem + 384 + (i & 2) * 4;
+        const uint32_t d = tmem + ((i & 4) ? 192u : 0u);
+        const uint64_t bpd = bplane >> 4;
+#pragma unroll
+        for (int u = 0; u < 6; ++u)
+          mma_ts_w(d, a0 + uint32_t(u % 3) * 16, b0 + uint64_t(u / 3) * bpd, idesc, (i | u) ? 1u : 0u);
+      }
+    } else {
+      for (int i = 0; i < iters; ++i) {
+        const int pa = i % 3, pb = (i / 3) % 3;
+        const uint32_t d = tmem + ((mode == 9 && (i & 1)) ? 192u : 0u);
+        const uint64_t bd = smem_desc(sb + 3 * 16384 + uint32_t(pb) * bplane + (i & 1) * 256);
+        mma_ts_w(d, tmem + 384 + uint32_t(pa) * 16 + (i & 1) * 8, bd, idesc, i > 0 ? 1u : 0u);
+      }
+    }
+    const long long t1 = clock64();
+    commit_w(&bar);
+    mbar_wait(&bar, 0);
+    const long long t2 = clock64();
+    if (blockIdx.x == 0 && (tid & 31) == 0) {
+      out[0] = (unsigned long long)(t1 - t0);
+      out[1] = (unsigned long long)(t2 - t0);
+    }
+  } else if (mode < 8 && tid == 0) {
+    const uint32_t idesc = idesc_bf16_m128(n);
+    const uint32_t sb = smem_u32(smem);
+    const uint32_t bplane = uint32_t(n) * 64;   // B plane bytes (n rows x 32 k)
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      const int pa = (mode >= 1) ? i % 3 : 0;
+      const int pb = (mode == 2 || mode == 4) ? (i / 3) % 3 : 0;
+      const uint32_t d = tmem + ((mode == 4 && (i & 1)) ? 192u : 0u);
+      const uint64_t bd = smem_desc(sb + 3 * 16384 + uint32_t(pb) * bplane + (i & 1) * 256);
+      if (mode == 3) {
+        const uint64_t ad = smem_desc(sb + uint32_t(pa) * 16384 + (i & 1) * 256);
+        mma_bf16(d, ad, bd, idesc, i > 0 ? 1u : 0u);
+      } else {
+        mma_bf16_ts(d, tmem + 384 + uint32_t(pa) * 16 + (i & 1) * 8, bd, idesc, i > 0 ? 1u : 0u);
+      }
+    }
+    const long long t1 = clock64();
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    const long long t2 = clock64();
+    if (blockIdx.x == 0) {
+      out[0] = (unsigned long long)(t1 - t0);
+      out[1] = (unsigned long long)(t2 - t0);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+}  // namespace tcp
+}  // namespace sa
+
+extern "C" int sa_probe_mma_seq(int n, int iters, int mode, int rnd, int grid,
+                                unsigned long long* out, void* stream) {
+  const int smem = 6 * 16384 + 1024;
+  cudaFuncSetAttribute(sa::tcp::mma_seq_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       smem);
+  sa::tcp::mma_seq_probe_kernel<<<grid, 128, smem, sa::as_stream(stream)>>>(n, iters, mode, rnd, out);
+  return cudaGetLastError() == cudaSuccess ? SA_OK : SA_ERR_CUDA;
+}
+
+// ---- GELU + split throughput probe (diagnostics only) --------------------------
+// every thread runs `iters` rounds of 8 GELU pairs (nf of them with the FMA-pipe
+// reciprocal) + the bf16 plane split on register data; mode bit 0: skip the
+// split, bit 1: skip the GELU. Returns clock cycles of CTA 0.
+#include "tc_gemm_kernel.cuh"
+namespace sa {
+namespace tcp {
+template <int NF>
+__global__ void __launch_bounds__(512) gelu_probe_kernel(int iters, int mode, float* sink,
+                                                         unsigned long long* out) {
+  float v[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) v[t] = float(threadIdx.x + t) * 0.001f - 0.3f;
+  uint32_t acc = 0;
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      float g0 = v[2 * t], g1 = v[2 * t + 1];
+      if (!(mode & 2)) {
+        if (t < NF) tc::gelu_pair<true>(g0, g1);
+        else tc::gelu_pair<false>(g0, g1);
+      }
+      if (!(mode & 1)) {
+        const tc::Split3 sp = tc::split3x2(g0, g1);
+        acc += tc::bf2_bits(sp.h) ^ tc::bf2_bits(sp.m) ^ tc::bf2_bits(sp.l);
+      } else {
+        acc += __float_as_uint(g0) ^ __float_as_uint(g1);
+      }
+      v[2 * t] = g0 + 1e-3f;
+      v[2 * t + 1] = g1 - 1e-3f;
+    }
+  }
+  const long long t1 = clock64();
+  if (acc == 0x12345678u) sink[0] = v[0];
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = (unsigned long long)(t1 - t0);
+}
+}  // namespace tcp
+}  // namespace sa
+
+extern "C" int sa_probe_gelu(int iters, int mode, int nf, int threads, float* sink,
+                             unsigned long long* out, void* stream) {
+  auto s = sa::as_stream(stream);
+  if (nf == 0) sa::tcp::gelu_probe_kernel<0><<<148, threads, 0, s>>>(iters, mode, sink, out);
+  else if (nf == 4) sa::tcp::gelu_probe_kernel<4><<<148, threads, 0, s>>>(iters, mode, sink, out);
+  else sa::tcp::gelu_probe_kernel<8><<<148, threads, 0, s>>>(iters, mode, sink, out);
   return cudaGetLastError() == cudaSuccess ? SA_OK : SA_ERR_CUDA;
 }

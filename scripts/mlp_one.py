@@ -1,8 +1,7 @@
 #!/usr/bin/env python3
-"""Fused MoE MLP event timeline of CTA 0 (debug build): per hidden chunk q the
-clock of fc1 issue start / commit, GELU warp 0 start / done, GELU warp 15 done,
-fc2 issue start / commit, relative to fc1(0)."""
-import ctypes
+"""One fused MoE MLP call at the PVTv2-B0 stage-1 (or, with argv[1] == 64,
+stage-2) shape inside a profiler range, after a warm-up (for ncu
+--profile-from-start off -k regex:mlp_kernel)."""
 import os
 import sys
 
@@ -10,10 +9,8 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2306_06446_b200 import _lib, model as MD, moe as MOE  # noqa: E402
+from paper_2306_06446_b200 import model as MD, moe as MOE  # noqa: E402
 
-lib = _lib._lib = _lib._open(_lib.DEBUG_LIB_PATH)
-lib.sa_debug_mlp_timeline.argtypes = [ctypes.c_void_p]
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 hidden, M = (256, 802816) if d == 32 else (512, 200704)
 g = np.random.default_rng(0)
@@ -27,15 +24,8 @@ x = torch.from_numpy(g.standard_normal((M, d)).astype(np.float32)).cuda()
 res = torch.from_numpy(g.standard_normal((M, d)).astype(np.float32)).cuda()
 plan, _ = MOE.route_plan(x, mod.wg.value)
 mod.forward(x, plan=plan, residual=res)
-tl = torch.zeros(8 * 64, dtype=torch.int64, device="cuda")
-lib.sa_debug_mlp_timeline(tl.data_ptr())
+torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStart()
 mod.forward(x, plan=plan, residual=res)
 torch.cuda.synchronize()
-lib.sa_debug_mlp_timeline(None)
-t = tl.view(8, 64).cpu().numpy()
-t0 = t[0, 0]
-names = ["f1 start", "f1 commit", "gelu0 go", "gelu0 done", "f2 start", "f2 commit", "gelu15 done"]
-print("q   " + " ".join(f"{n:>11s}" for n in names))
-for q in range(40):
-    print(f"{q:2d}  " + " ".join(f"{(t[e, q] - t0):11d}" for e in range(7)))
-print("per-chunk period (f2 start):", np.diff(t[4, 8:40]).mean())
+torch.cuda.cudart().cudaProfilerStop()

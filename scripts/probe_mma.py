@@ -11,11 +11,11 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2306_06446_b200 import _lib  # noqa: E402
 
-lib = _lib.debug_library().__enter__()   # the whole script runs on the debug build
+lib = _lib._lib = _lib._open(_lib.DEBUG_LIB_PATH)   # the debug build, loaded alone
 lib.sa_probe_mma.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
 out = torch.zeros(2, dtype=torch.int64, device="cuda")
-for layout in (2, 3, 4, 5, 6):
-    for n in (32,):
+for layout in (0, 2, 10, 12):
+    for n in (32, 64, 96, 128, 256):
         iters = 4800
         lib.sa_probe_mma(n, iters, layout, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()

@@ -10,11 +10,11 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2306_06446_b200 import _lib  # noqa: E402
 
-lib = _lib.debug_library().__enter__()   # the whole script runs on the debug build
+lib = _lib._lib = _lib._open(_lib.DEBUG_LIB_PATH)   # the debug build, loaded alone
 lib.sa_probe_mma_ts.argtypes = [ctypes.c_int, ctypes.c_int] + [ctypes.c_void_p] * 5
 torch.manual_seed(0)
 out = torch.zeros(2, dtype=torch.int64, device="cuda")
-for n in (32, 64, 128, 256):
+for n in (32, 64, 96, 128, 256):
     a = torch.randint(-4, 5, (128, 16), device="cuda").to(torch.bfloat16)
     b = torch.randint(-4, 5, (n, 16), device="cuda").to(torch.bfloat16)
     d = torch.zeros(128, n, device="cuda")

@@ -355,6 +355,58 @@ def test_moe_module_vs_oracle(M, d, hidden):
     assert rel_err(y, res + ref) < 1e-5
 
 
+@pytest.mark.parametrize("M,d,hidden,scale,force", [
+    (5, 32, 256, 1.0, None), (129, 32, 512, 1.0, None), (1000, 64, 256, 1.0, None),
+    (3000, 32, 128, 1.0, None), (2000, 32, 256, 8.0, None), (777, 64, 512, 6.0, None),
+    (1500, 32, 256, 1.0, 0), (1500, 32, 256, 1.0, 1), (640, 64, 512, 1.0, 1)])
+def test_fused_moe_mlp_edges(M, d, hidden, scale, force):
+    """Fused MoE MLP kernel: ragged and tiny M, resident (d = 32, hidden <= 256)
+    and streamed weights, hidden pre-activations spanning the GELU's saturated
+    tails (scale), every token on one expert (force) — routes bit-exact and
+    y within 1e-5 of the oracle."""
+    mod, L = _moe_layers(d, d, hidden, seed=M + d)
+    if force is not None:   # positive inputs, router +1 / -1 columns: one expert wins everywhere
+        wg = np.zeros((d, 2), F32)
+        wg[:, force] = 1.0
+        wg[:, 1 - force] = -1.0
+        mod.wg.value.copy_(torch.from_numpy(wg))
+        L["wg"] = wg
+        x = np.abs(ops.rng(M).standard_normal((M, d))).astype(F32) * scale + 0.01
+    else:
+        x = (ops.rng(M).standard_normal((M, d)) * scale).astype(F32)
+    res = ops.rng(M + 1).standard_normal((M, d)).astype(F32)
+    y = host(mod.forward(dev(x), residual=dev(res)))
+    tr = nets.Trace()
+    ref = nets.moe_fwd(L, x, "m", tr)
+    assert np.array_equal(mod.last_plan.expert_of, tr.moe[0]["expert_of"])
+    if force is not None:
+        assert mod.last_plan.share(force) == 1.0
+    assert rel_err(y - res, ref) < 1e-5
+
+
+@pytest.mark.parametrize("d,hidden,shift", [(32, 256, False), (32, 256, True), (64, 512, False),
+                                           (64, 512, True), (32, 512, False)])
+def test_fused_mlp_plain_vs_oracle(d, hidden, shift):
+    """Single-expert fused MLP (sa_tc_mlp_fused) for dense and shift layers."""
+    from paper_2306_06446_b200 import model as MD
+    g = ops.rng(d + hidden)
+    M = 2049
+    x = (g.standard_normal((M, d)) * 2).astype(F32)
+    w1 = (g.standard_normal((d, hidden)) / np.sqrt(d)).astype(F32)
+    w2 = (g.standard_normal((hidden, d)) / np.sqrt(hidden)).astype(F32)
+    mk = MD.ShiftLinearLayer if shift else MD.Linear
+    mlp = MD.Mlp(mk(w1), mk(w2))
+    assert MD.fused_mlp_ok(d, hidden)
+    y = host(mlp.forward(dev(x)))
+    if shift:
+        L1 = dict(zip(("kind", "s", "p"), ("shift",) + ops.shift_quantize(w1)))
+        L2 = dict(zip(("kind", "s", "p"), ("shift",) + ops.shift_quantize(w2)))
+    else:
+        L1, L2 = {"kind": "dense", "w": w1}, {"kind": "dense", "w": w2}
+    ref = nets.linear_fwd({"kind": "mlp", "fc1": L1, "fc2": L2}, x)
+    assert rel_err(y, ref) < 1e-5
+
+
 def test_moe_golden(golden):
     from paper_2306_06446_b200 import model as MD
     k = golden("kat")
