@@ -253,24 +253,34 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
-    def _run(self):
-        # NVML polls in microseconds, so the ~100 ms timed region gets many
-        # samples; nvidia-smi (one subprocess per sample) is the fallback.
-        try:
+    def _nvml(self):
+        # NVML is initialised before the timed region starts (its first init
+        # can take longer than a short timed region)
+        if getattr(self, "_h", None) is None:
             import pynvml
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            bits = (pynvml.nvmlClocksThrottleReasonHwSlowdown,
-                    pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
-                    pynvml.nvmlClocksThrottleReasonSwThermalSlowdown,
-                    pynvml.nvmlClocksThrottleReasonSwPowerCap)
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._pynvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._mx = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        return self._pynvml, self._h
+
+    def _sample(self):
+        pynvml, h = self._nvml()
+        bits = (pynvml.nvmlClocksThrottleReasonHwSlowdown,
+                pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
+                pynvml.nvmlClocksThrottleReasonSwThermalSlowdown,
+                pynvml.nvmlClocksThrottleReasonSwPowerCap)
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.rows.append([str(sm), str(self._mx)] + ["Active" if r & b else "Not Active" for b in bits])
+
+    def _run(self):
+        # NVML polls in microseconds, so the timed region gets many samples;
+        # nvidia-smi (one subprocess per sample) is the fallback.
+        try:
             while not self._stop.is_set():
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                self.rows.append([str(sm), str(mx)] +
-                                 ["Active" if r & b else "Not Active" for b in bits])
-                self._stop.wait(0.005)
+                self._sample()
+                self._stop.wait(0.002)
             return
         except Exception:
             pass
@@ -286,12 +296,21 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def __enter__(self):
+        try:
+            self._nvml()
+        except Exception:
+            pass
         self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=6)
+        if not self.rows:   # a timed region shorter than one polling interval
+            try:
+                self._sample()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.rows:

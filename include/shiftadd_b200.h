@@ -105,6 +105,13 @@ int sa_quantize_shift(const float* w, int64_t count, int p_min, int p_max, uint8
 int sa_shift_linear(const float* x, const uint8_t* packed, float* y, int64_t M, int64_t K,
                     int64_t N, int p_min, int variant, void* stream);
 
+/* sa_add_linear replaces quantize.add_matmul (quantize.py:143-160) for an
+ * AddLinear(b, gamma) layer (quantize.py:62-75): y = gamma * (x @ b) with b in
+ * {-1, +1}, computed by signed fp64 accumulation (adds and subtracts only)
+ * and one multiply by gamma. signs: K x N bytes, bit 7 set where b < 0. */
+int sa_add_linear(const float* x, const uint8_t* signs, double gamma, float* y, int64_t M,
+                  int64_t K, int64_t N, void* stream);
+
 /* ---- dense / shift linear with fused epilogue: replaces Linear.forward
  * (model.py:104-107) and ShiftLinearLayer.forward; y = [residual +] act(x @ W).
  * act: 0 none, 1 gelu (tanh form). residual may be NULL. */

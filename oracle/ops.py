@@ -220,3 +220,19 @@ def numpy_exp_tie_threshold() -> np.float32:
         else:
             hi = mid - 1
     return np.array([lo], np.uint32).view(np.float32)[0]
+
+
+# ---------------------------------------------------------------------------
+# MatAdd (AddLinear)
+
+
+def add_matmul(x: np.ndarray, b: np.ndarray, gamma: float) -> np.ndarray:
+    """Signed accumulation of x's columns under b in float64, scaled once by
+    gamma, rounded to the input dtype (ref quantize.py:143-160)."""
+    x64 = np.asarray(x, dtype=np.float64)
+    out = np.empty((x.shape[0], b.shape[1]), dtype=np.float64)
+    for j in range(b.shape[1]):
+        pos = b[:, j] > 0
+        out[:, j] = x64[:, pos].sum(axis=1) - x64[:, ~pos].sum(axis=1)
+    out *= gamma
+    return out.astype(x.dtype, copy=False)

@@ -49,6 +49,7 @@ _SIGS = {
     "sa_dwconv_tokens": (_I32, [_P, _P, _P, _I64, _I64, _I64, _I32, _P]),
     "sa_quantize_shift": (_I32, [_P, _I64, _I32, _I32, _P, _P, _P, _P]),
     "sa_shift_linear": (_I32, [_P, _P, _P, _I64, _I64, _I64, _I32, _I32, _P]),
+    "sa_add_linear": (_I32, [_P, _P, C.c_double, _P, _I64, _I64, _I64, _P]),
     "sa_linear": (_I32, [_P, _P, _I32, _P, _I64, _I64, _I64, _I32, _P, _I32, _P]),
     "sa_mlp_workspace": (_SZ, [_I64, _I64]),
     "sa_mlp": (_I32, [_P, _P, _I32, _P, _I32, _P, _I64, _I64, _I64, _I32, _P, _P, _SZ, _P]),

@@ -16,7 +16,7 @@ from typing import Optional, Union
 import torch
 
 from . import _lib
-from .quantize import ShiftLinear, shift_forward, sign_hash
+from .quantize import AddLinear, ShiftLinear, add_matmul, shift_forward, sign_hash
 from .tensor import ShapeError, matmul, to_device
 
 MODES = ("softmax", "linear", "linear-binary")   # ref attention.py:28
@@ -24,7 +24,7 @@ ORDERS = ("auto", "linear", "quadratic")
 PHI_EPS = 1e-6
 EPS_NORM = 1e-6                                  # ref attention.py:32
 
-Projection = Union[torch.Tensor, ShiftLinear]
+Projection = Union[torch.Tensor, ShiftLinear, AddLinear]
 
 
 @dataclass
@@ -66,6 +66,8 @@ def project(x, w: Projection) -> torch.Tensor:
     """ref attention.py:66-71"""
     if isinstance(w, ShiftLinear):
         return shift_forward(x, w)
+    if isinstance(w, AddLinear):
+        return add_matmul(x, w)
     return matmul(x, w)
 
 

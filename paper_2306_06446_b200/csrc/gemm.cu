@@ -366,6 +366,58 @@ __global__ void __launch_bounds__(256) matshift_kernel(const float* __restrict__
   }
 }
 
+// ---- MatAdd (AddLinear): signed accumulation under binary weights ----------
+// y[m][n] = gamma · sum_k (b[k][n] < 0 ? -x[m][k] : x[m][k]): adds and subtracts
+// only, one multiply by gamma at the end (ref quantize.py:143-160). The sum runs
+// in fp64 like the reference (fp64 sums of fp32 terms, exact whenever the
+// terms' exponents span < 29 bits), then one fp64 product and one rounding to
+// fp32, so results are bit-identical to the reference in that regime.
+// signs: one byte per weight, bit 7 set = negative (the shift-code sign bit).
+__global__ void __launch_bounds__(256) matadd_kernel(const float* __restrict__ x,
+                                                     const uint8_t* __restrict__ signs,
+                                                     double gamma, float* __restrict__ y, int64_t M,
+                                                     int64_t K, int64_t N) {
+  __shared__ float xs[kMsBK][kMsBM + 1];
+  __shared__ uint8_t ws[kMsBK][kMsBN];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;  // 4x4 outputs per thread
+  const int64_t m0 = int64_t(blockIdx.x) * kMsBM, n0 = int64_t(blockIdx.y) * kMsBN;
+  double acc[4][4] = {};
+  for (int64_t k0 = 0; k0 < K; k0 += kMsBK) {
+    for (int idx = tid; idx < kMsBM * kMsBK; idx += 256) {
+      const int mm = idx / kMsBK, kk = idx % kMsBK;
+      const int64_t gm = m0 + mm, gk = k0 + kk;
+      xs[kk][mm] = (gm < M && gk < K) ? x[gm * K + gk] : 0.f;
+    }
+    for (int idx = tid; idx < kMsBK * kMsBN; idx += 256) {
+      const int kk = idx / kMsBN, nn = idx % kMsBN;
+      const int64_t gk = k0 + kk, gn = n0 + nn;
+      ws[kk][nn] = (gk < K && gn < N) ? signs[gk * N + gn] : uint8_t(0);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < kMsBK; ++kk) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double xv = double(xs[kk][ty * 4 + i]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += (ws[kk][tx * 4 + j] & 0x80u) ? -xv : xv;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t gm = m0 + ty * 4 + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gn = n0 + tx * 4 + j;
+      if (gn < N) y[gm * N + gn] = float(acc[i][j] * gamma);
+    }
+  }
+}
+
 static int check_k4(const char* who, int64_t K) {
   SA_REQUIRE(K % 4 == 0, SA_ERR_SHAPE, "%s: inner extent %lld must be a multiple of 4", who,
              (long long)K);
@@ -422,6 +474,19 @@ extern "C" int sa_shift_linear(const float* x, const uint8_t* packed, float* y, 
   matshift_kernel<<<grid, 256, 0, as_stream(stream)>>>(x, packed, y, M, K, N, p_min);
   count_launch(1);
   SA_LAUNCH_CHECK("sa_shift_linear");
+  return SA_OK;
+}
+
+extern "C" int sa_add_linear(const float* x, const uint8_t* signs, double gamma, float* y,
+                             int64_t M, int64_t K, int64_t N, void* stream) {
+  SA_REQUIRE(M >= 0 && K > 0 && N > 0, SA_ERR_SHAPE, "sa_add_linear: bad extents");
+  SA_REQUIRE(cdiv(M, kMsBM) < (int64_t(1) << 31) && cdiv(N, kMsBN) < 65536, SA_ERR_SHAPE,
+             "sa_add_linear: extents too large");
+  if (M == 0) return SA_OK;
+  dim3 grid(unsigned(cdiv(M, kMsBM)), unsigned(cdiv(N, kMsBN)));
+  matadd_kernel<<<grid, 256, 0, as_stream(stream)>>>(x, signs, gamma, y, M, K, N);
+  count_launch(1);
+  SA_LAUNCH_CHECK("sa_add_linear");
   return SA_OK;
 }
 

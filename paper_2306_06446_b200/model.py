@@ -203,7 +203,7 @@ class Linear:
         return ()
 
     def post_step(self):
-        pass
+        self._tc = {}   # the packed tensor-core planes follow the (possibly reloaded) weights
 
 
 class ShiftLinearLayer:
@@ -825,6 +825,40 @@ class Network:
                 if isinstance(blk.mlp, MoeModule):
                     yield f"{pre}.mlp", blk.mlp
 
+    def named_params(self):
+        """(name, GradPair) of every parameter (ref Model.named_params,
+        model.py:592-598, generalised to several stages: prefix s<i>.)."""
+        for si, S in enumerate(self.stages):
+            pre = f"s{si}"
+            yield f"{pre}.patch_embed.w", S.patch_embed.w
+            if S.cls is not None:
+                yield f"{pre}.cls", S.cls
+            if S.pos is not None:
+                yield f"{pre}.pos", S.pos
+            if S.embed_ln is not None:
+                yield from S.embed_ln.named_params(f"{pre}.embed_ln")
+            for bi, blk in enumerate(S.blocks):
+                yield from blk.named_params(f"{pre}.block{bi}")
+            if S.stage_ln is not None:
+                yield from S.stage_ln.named_params(f"{pre}.final_ln")
+        yield "head.w", self.head.w
+
+    def extra_blobs(self):
+        """Shift-layer sign / exponent blobs (ref model.py:600-602)."""
+        for si, S in enumerate(self.stages):
+            for bi, blk in enumerate(S.blocks):
+                yield from blk.extra_blobs(f"s{si}.block{bi}")
+
+    def post_step(self):
+        """Re-derive every layer's device state from its (re)loaded values:
+        shift codes from the shadows, packed tensor-core planes (ref
+        model.py:604-606)."""
+        for S in self.stages:
+            S.patch_embed.post_step()
+            for blk in S.blocks:
+                blk.post_step()
+        self.head.post_step()
+
     def named_weights(self):
         """(name, device tensor) in oracle.nets.iter_weights order."""
         for si, S in enumerate(self.stages):
@@ -933,6 +967,29 @@ class Model(Network):
         self.cfg = cfg
         super().__init__(_model_cfg_to_spec(cfg, quant_cfg), dtype, moe_cfg, quant_cfg)
 
+    def named_params(self):
+        """The reference Model's parameter names (ref model.py:592-598)."""
+        S = self.stages[0]
+        yield "patch_embed.w", S.patch_embed.w
+        yield "pos", S.pos
+        for i, blk in enumerate(S.blocks):
+            yield from blk.named_params(f"block{i}")
+        yield from S.stage_ln.named_params("final_ln")
+        yield "head.w", self.head.w
+
+    def extra_blobs(self):
+        for i, blk in enumerate(self.stages[0].blocks):
+            yield from blk.extra_blobs(f"block{i}")
+
+    def moe_modules(self):
+        """ref model.py:608-615 (names and order)."""
+        for i, blk in enumerate(self.stages[0].blocks):
+            if isinstance(blk.mlp, MoeModule):
+                yield f"block{i}.mlp", blk.mlp
+            for key in ("q", "k", "v", "o"):
+                if isinstance(blk.attn.proj[key], MoeModule):
+                    yield f"block{i}.attn.{key}", blk.attn.proj[key]
+
     @property
     def patch_embed(self):
         return self.stages[0].patch_embed
@@ -944,6 +1001,66 @@ class Model(Network):
     @property
     def final_ln(self):
         return self.stages[0].stage_ln
+
+
+@dataclass
+class EvalResult:
+    """ref model.py:738-742"""
+
+    accuracy: float
+    expert_shares: dict
+    dispatch_maps: dict        # layer -> (N, tokens) winning expert per token
+
+
+def evaluate(model: Network, dataset, batch_size: int = 64) -> EvalResult:
+    """Accuracy, per-layer expert shares and dispatch maps over a dataset
+    (anything with `.images` (N, H, W, C) and `.labels` (N,)) (ref
+    model.py:745-765): the forward runs on the device batch by batch; each MoE
+    layer's winning experts come from its last DispatchPlan (one D2H copy per
+    layer and batch)."""
+    images, labels = dataset.images, np.asarray(dataset.labels)
+    n = labels.shape[0]
+    correct = 0
+    names = [name for name, _ in model.moe_modules()]
+    maps = {name: [] for name in names}
+    for start in range(0, n, batch_size):
+        batch = images[start:start + batch_size]
+        logits = model.forward(batch).cpu().numpy()
+        correct += int((np.argmax(logits, axis=1) == labels[start:start + batch_size]).sum())
+        b = logits.shape[0]
+        for name, module in model.moe_modules():
+            maps[name].append(module.last_plan.expert_of.reshape(b, -1))
+    dispatch_maps = {name: np.concatenate(chunks, axis=0) for name, chunks in maps.items() if chunks}
+    shares = {}
+    for name, arr in dispatch_maps.items():
+        counts = np.bincount(arr.ravel(), minlength=2).astype(np.float64)
+        shares[name] = (counts / counts.sum()).tolist()
+    return EvalResult(accuracy=correct / n, expert_shares=shares, dispatch_maps=dispatch_maps)
+
+
+def write_dispatch_map(result: EvalResult, layer: str, out_dir) -> str:
+    """The reference's dispatch-map export (ref cli.py:233-265,
+    docs/formats.md "dispatch_<layer>.csv"): one row per image, `image,
+    token0..tokenN-1` with the winning expert (0 = mult, 1 = shift), plus
+    dispatch_summary.json with the aggregate shares. Returns the CSV path."""
+    import csv
+    import json
+    if layer not in result.dispatch_maps:
+        raise KeyError(f"no MoE layer named {layer!r}; available: {sorted(result.dispatch_maps)}")
+    dmap = result.dispatch_maps[layer]
+    os.makedirs(out_dir, exist_ok=True)
+    grid_csv = os.path.join(out_dir, f"dispatch_{layer.replace('.', '_')}.csv")
+    with open(grid_csv, "w", newline="") as fh:
+        writer = csv.writer(fh)
+        writer.writerow(["image"] + [f"token{t}" for t in range(dmap.shape[1])])
+        for i in range(dmap.shape[0]):
+            writer.writerow([i] + dmap[i].tolist())
+    summary = {"layer": layer, "expert_shares": result.expert_shares,
+               "tokens_per_image": int(dmap.shape[1]), "images": int(dmap.shape[0]),
+               "accuracy": result.accuracy}
+    with open(os.path.join(out_dir, "dispatch_summary.json"), "w") as fh:
+        fh.write(json.dumps(summary, indent=2, sort_keys=True) + "\n")
+    return grid_csv
 
 
 def build_model(spec: dict, **kw) -> Network:

@@ -77,6 +77,32 @@ class ShiftLinear:
         return self.s.shape[1]
 
 
+@dataclass
+class AddLinear:
+    """Binarized weights plus one trailing scale (ref quantize.py:62-75); the
+    device keeps one sign byte per weight (bit 7 = b < 0) for sa_add_linear."""
+
+    b: torch.Tensor          # {-1,+1} float32, (in_dim, out_dim)
+    gamma: float
+    signs: torch.Tensor = field(default=None, repr=False)  # uint8, same shape
+
+    def __post_init__(self):
+        self.b = to_device(self.b, torch.float32)
+        if self.b.ndim != 2:
+            raise ShapeError(f"AddLinear needs a 2-D sign matrix, got {tuple(self.b.shape)}")
+        self.gamma = float(self.gamma)
+        if self.signs is None:
+            self.signs = ((self.b < 0).to(torch.uint8) << 7).contiguous()
+
+    @property
+    def in_dim(self) -> int:
+        return self.b.shape[0]
+
+    @property
+    def out_dim(self) -> int:
+        return self.b.shape[1]
+
+
 def sign_unit(x) -> torch.Tensor:
     """Sign with sign(0) := +1 (so -0.0 and NaN map to +1) (ref quantize.py:78-80)."""
     x = to_device(x, None)
@@ -159,8 +185,12 @@ def binarize(x, scale_mode: str = "per-matrix"):
     flat = x.reshape(lead, -1)
     per = flat.shape[1]
     d = 32 if per % 32 == 0 else (16 if per % 16 == 0 else None)
-    if d is None:
-        raise ShapeError("device binarize needs a multiple of 16 elements per scale group")
+    if d is None:   # ragged groups (weight matrices): device torch reductions, fp64 mean
+        b = sign_unit(x).to(torch.float32)
+        g = flat.abs().to(torch.float64).mean(dim=1).to(torch.float32)
+        if scale_mode == "per-matrix":
+            return b, float(g[0])
+        return b, g.reshape((lead,) + (1,) * (x.ndim - 1))
     rows = flat.reshape(lead * (per // d), d)
     codes, gamma = sign_hash(rows, heads=1, batch=lead)
     bits = unpack_codes(codes.reshape(-1, 1), d).reshape(x.shape)
@@ -168,3 +198,43 @@ def binarize(x, scale_mode: str = "per-matrix"):
     if scale_mode == "per-matrix":
         return b, float(gamma.reshape(-1)[0])
     return b, gamma.reshape((lead,) + (1,) * (x.ndim - 1))
+
+
+def add_matmul(x, layer: AddLinear) -> torch.Tensor:
+    """Signed accumulation of x's columns under b, scaled once by gamma (ref
+    quantize.py:143-160): sa_add_linear adds / subtracts in fp64 and multiplies
+    by gamma once, then rounds to float32 — the reference's arithmetic."""
+    x = to_device(x)
+    if x.ndim != 2:
+        raise ShapeError(f"add_matmul expects a 2-D input, got {tuple(x.shape)}")
+    if x.shape[1] != layer.in_dim:
+        raise ShapeError(f"input extent {x.shape[1]} != layer in_dim {layer.in_dim}")
+    y = torch.empty((x.shape[0], layer.out_dim), dtype=torch.float32, device=x.device)
+    _lib.call("sa_add_linear", _lib.ptr(x), _lib.ptr(layer.signs), float(layer.gamma),
+              _lib.ptr(y), x.shape[0], layer.in_dim, layer.out_dim, _lib.stream())
+    return y
+
+
+def reconstruct_add(layer: AddLinear, dtype=torch.float32) -> torch.Tensor:
+    """gamma·b (ref quantize.py:188-189)."""
+    return (layer.gamma * layer.b.to(torch.float64)).to(dtype)
+
+
+@dataclass
+class ReparamResult:
+    """ref quantize.py:171-174"""
+
+    layer: object                  # ShiftLinear or AddLinear
+    shadow: torch.Tensor           # dense copy of the source weights
+
+
+def reparam_linear(dense_w, target: str, cfg: QuantConfig = QuantConfig()) -> ReparamResult:
+    """Convert a dense matrix into a shift or add layer plus its shadow (ref
+    quantize.py:177-185)."""
+    w = to_device(dense_w)
+    if target == "shift":
+        return ReparamResult(layer=quantize_shift(w, cfg), shadow=w.clone())
+    if target == "add":
+        b, gamma = binarize(w, scale_mode="per-matrix")
+        return ReparamResult(layer=AddLinear(b=b, gamma=gamma), shadow=w.clone())
+    raise ValueError(f"unknown reparameterization target {target!r}")

@@ -8,7 +8,8 @@ Run in the build container only (it imports the unmodified reference from
     python tests/golden/make_golden.py
 
 Outputs (committed): tests/golden/{kat,toy_c1,toy_c1_moe,pvt_small,deit_small,pvt_b0_full,
-    pvt_v1_tiny_full,deit_tiny_full,pvt_v2_b2_full,apply_stage}.npz
+    pvt_v1_tiny_full,deit_tiny_full,pvt_v2_b2_full,apply_stage,checkpoint,addlinear}.npz and
+    tests/golden/toy_moe.saddckpt (a reference-written checkpoint)
 
 Every model here is composed from the reference's own classes (Linear,
 ShiftLinearLayer, MoeModule, Mlp, AttentionLayer, Block, LayerNorm and the
@@ -428,12 +429,71 @@ def make_apply_stage():
     return out
 
 
+def make_addlinear():
+    """MatAdd KATs from the reference (ref quantize.py:143-160, 177-185 and
+    tests/test_quantize.py:150-171): the hand case, the all-plus-one row sum and
+    binarized random layers (reparam_linear(w, "add"))."""
+    out = {}
+    layer = Q.AddLinear(b=T.tensor([[1.0], [-1.0]]), gamma=1.0)
+    out["hand_x"] = T.tensor([[1.0, 2.0]])
+    out["hand_b"] = layer.b
+    out["hand_y"] = Q.add_matmul(out["hand_x"], layer)
+    g = T.make_rng(31)
+    for i, (m, k, n) in enumerate(((4, 6, 3), (8, 8, 8), (100, 64, 48), (1000, 96, 80))):
+        x = g.uniform(-1, 1, (m, k)).astype(F32)
+        if i == 0:
+            b, gamma = np.ones((k, n), F32), 1.0
+        else:
+            rr = Q.reparam_linear(g.uniform(-1, 1, (k, n)).astype(F32), "add")
+            b, gamma = rr.layer.b, rr.layer.gamma
+            out[f"w{i}"] = rr.shadow
+        out[f"x{i}"], out[f"b{i}"], out[f"g{i}"] = x, b.astype(F32), np.array(gamma)
+        out[f"y{i}"] = Q.add_matmul(x, Q.AddLinear(b=b, gamma=gamma))
+    return out
+
+
+def make_checkpoint():
+    """A SADDCKPT container written by the reference (ref checkpoint.py:64-97)
+    for a toy MoE Model whose weights were perturbed away from the init (so a
+    loader must really read them), plus the reference forward logits and
+    `evaluate` dispatch maps / shares (ref model.py:745-765) over 5 images in
+    batches of 3."""
+    from shiftadd import checkpoint as CK
+    from shiftadd import data as DATA
+    bcs = [MD.BlockConfig(d=32, h=2, mlp_ratio=2.0, attn_mode="linear-binary", mlp_mode="moe",
+                          attn_linear_mode="moe"),
+           MD.BlockConfig(d=32, h=2, mlp_ratio=2.0, attn_mode="linear-binary", mlp_mode="shift",
+                          attn_linear_mode="moe")]
+    m = MD.Model(MD.ModelConfig(blocks=bcs, patch=4, img=16, classes=5, seed=3))
+    g = T.make_rng(11)
+    for _, p in m.named_params():
+        p.value[...] = (p.value + g.standard_normal(p.value.shape) * 0.05).astype(F32)
+    m.post_step()
+    CK.save_checkpoint(os.path.join(HERE, "toy_moe.saddckpt"), m, step=42,
+                       extra_meta={"note": "golden fixture"})
+    images = T.make_rng(12).uniform(0, 1, (5, 16, 16, 3)).astype(F32)
+    labels = T.make_rng(13).integers(0, 5, 5).astype(np.int64)
+    out = {"images": images, "labels": labels, "logits": m.forward(images)}
+    res = MD.evaluate(m, DATA.Dataset(images=images, labels=labels), batch_size=3)
+    out["accuracy"] = np.array(res.accuracy)
+    for name, arr in res.dispatch_maps.items():
+        out["map:" + name] = arr.astype(np.int32)
+        out["share:" + name] = np.array(res.expert_shares[name])
+    return out
+
+
 def main():
     only = sys.argv[1:]
     if only:   # e.g. `make_golden.py pvt_v1_tiny_full` regenerates just that fixture
         for name in only:
             if name == "apply_stage":
                 np.savez_compressed(os.path.join(HERE, "apply_stage.npz"), **make_apply_stage())
+                continue
+            if name == "checkpoint":
+                np.savez_compressed(os.path.join(HERE, "checkpoint.npz"), **make_checkpoint())
+                continue
+            if name == "addlinear":
+                np.savez_compressed(os.path.join(HERE, "addlinear.npz"), **make_addlinear())
                 continue
             fn, b, seed = FULL_224[name]
             np.savez_compressed(os.path.join(HERE, name + ".npz"),
@@ -456,6 +516,8 @@ def main():
         np.savez_compressed(os.path.join(HERE, name + ".npz"),
                             **make_model_fixture(fn(), b, seed, full=False))
     np.savez_compressed(os.path.join(HERE, "apply_stage.npz"), **make_apply_stage())
+    np.savez_compressed(os.path.join(HERE, "checkpoint.npz"), **make_checkpoint())
+    np.savez_compressed(os.path.join(HERE, "addlinear.npz"), **make_addlinear())
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -747,3 +747,55 @@ def ctypes_i64(v):
 def ctypes_p(v):
     import ctypes
     return ctypes.c_void_p(v)
+
+
+# ------------------------------------------------------------------ MatAdd
+
+
+def test_add_matmul_golden_bit_exact(golden):
+    """sa_add_linear (signed fp64 accumulation, one gamma multiply) against the
+    reference's add_matmul outputs: bit-exact (ref quantize.py:143-160)."""
+    from paper_2306_06446_b200 import quantize as Q
+    k = golden("addlinear")
+    y = host(Q.add_matmul(dev(k["hand_x"]), Q.AddLinear(b=dev(k["hand_b"]), gamma=1.0)))
+    assert np.array_equal(y, k["hand_y"])
+    for i in range(4):
+        layer = Q.AddLinear(b=dev(k[f"b{i}"]), gamma=float(k[f"g{i}"]))
+        y = host(Q.add_matmul(dev(k[f"x{i}"]), layer))
+        assert np.array_equal(y, k[f"y{i}"]), i
+
+
+def test_reparam_add_and_project(golden):
+    """reparam_linear(w, "add") reproduces the reference's signs (gamma to
+    1 ulp: fp64 vs numpy float32 mean) and attention.project dispatches an
+    AddLinear to add_matmul (ref attention.py:66-71, quantize.py:177-189)."""
+    from paper_2306_06446_b200 import attention as A
+    from paper_2306_06446_b200 import quantize as Q
+    k = golden("addlinear")
+    for i in (1, 2, 3):
+        rr = Q.reparam_linear(dev(k[f"w{i}"]), "add")
+        assert np.array_equal(host(rr.layer.b), k[f"b{i}"])
+        assert abs(rr.layer.gamma - float(k[f"g{i}"])) <= 2 * np.spacing(np.float32(k[f"g{i}"]))
+        assert np.array_equal(host(rr.shadow), k[f"w{i}"])
+        y = host(A.project(dev(k[f"x{i}"]), rr.layer))
+        ref = ops.add_matmul(k[f"x{i}"], host(rr.layer.b), rr.layer.gamma)
+        assert np.array_equal(y, ref)
+        rec = host(Q.reconstruct_add(rr.layer))
+        assert np.array_equal(rec, (rr.layer.gamma * host(rr.layer.b).astype(np.float64)).astype(F32))
+    with pytest.raises(ValueError):
+        Q.reparam_linear(dev(k["w1"]), "mult")
+
+
+def test_add_matmul_shapes_and_errors():
+    from paper_2306_06446_b200 import quantize as Q
+    from paper_2306_06446_b200.tensor import ShapeError
+    g = ops.rng(5)
+    b = np.where(g.standard_normal((37, 29)) < 0, -1.0, 1.0).astype(F32)
+    x = g.standard_normal((131, 37)).astype(F32)
+    layer = Q.AddLinear(b=dev(b), gamma=0.37)
+    assert np.array_equal(host(Q.add_matmul(dev(x), layer)), ops.add_matmul(x, b, 0.37))
+    assert host(Q.add_matmul(dev(x[:0]), layer)).shape == (0, 29)
+    with pytest.raises(ShapeError):
+        Q.add_matmul(dev(x[:, :36]), layer)
+    with pytest.raises(ShapeError):
+        Q.add_matmul(dev(x.reshape(-1)), layer)

@@ -171,3 +171,13 @@ def test_balanced_router_set_matches_model_layout():
         assert rs.weights[k].shape == shape and rs.weights[k].dtype == np.float32
     near = [k for k, s in rs.train_shares.items() if abs(s - 0.75) <= 0.10]
     assert len(near) >= len(names) // 2
+
+
+def test_oracle_add_matmul_golden(golden):
+    """MatAdd restatement = the reference's add_matmul bit for bit (ref
+    quantize.py:143-160) on its own KATs and binarized random layers."""
+    k = golden("addlinear")
+    assert np.array_equal(ops.add_matmul(k["hand_x"], k["hand_b"], 1.0), k["hand_y"])
+    for i in range(4):
+        y = ops.add_matmul(k[f"x{i}"], k[f"b{i}"], float(k[f"g{i}"]))
+        assert np.array_equal(y, k[f"y{i}"]), i
