@@ -27,7 +27,8 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libshiftadd_b200.so")
 DEBUG_LIB = os.path.join(HERE, "libshiftadd_b200_debug.so")
-DEBUG_ONLY = ("tc_probe.cu",)   # diagnostics kernels: never in the product library
+# diagnostics kernels and measured-and-reverted variants: never in the product library
+DEBUG_ONLY = ("tc_probe.cu", "binattn_stream.cu")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -99,7 +100,9 @@ def _build_one(force: bool, verbose: bool, debug: bool) -> str:
             print(log, file=sys.stderr)
     objs = [o for o, _ in results]
     tmp = lib_path + ".tmp"
-    cmd = [cc, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
+    # -Bsymbolic: the product and debug libraries define the same template
+    # kernels; each must launch its own (a test process loads both)
+    cmd = [cc, *ARCH, "-shared", "-Xlinker", "-Bsymbolic", "-o", tmp, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -472,11 +472,16 @@ int binattn_split_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
                          const float* v, const float* dw, float* out, int64_t B, int64_t n,
                          int64_t d, int64_t heads, float eps, void* ws, size_t ws_bytes,
                          cudaStream_t s);
+int binattn_stream_launch(const uint32_t* cq, const uint32_t* ck, const float* gq, const float* gk,
+                          const float* v, const float* dw, float* out, int64_t B, int64_t n,
+                          int64_t d, int64_t heads, float eps, cudaStream_t s);
 // 0: product choice — dk = 64: tensor-core cluster kernel (binattn_tc.cu);
 // dk = 32: CUDA-core single-pass cluster kernel (binattn_fused.cu), measured
 // faster at dk = 32 (profiles/r2_attn_bench.txt); 1: multi-kernel; 2: split
 // two-kernel form of the CUDA-core fused kernel (bit-identical to it); 3: the
-// tensor-core kernel at any dk it supports
+// tensor-core cluster kernel at any dk it supports; 4: = 0; 5 (debug build
+// only): the streaming tensor-core kernel (binattn_stream.cu, measured slower:
+// DESIGN.md §5)
 
 }  // namespace sa
 
@@ -511,17 +516,24 @@ extern "C" int sa_linear_binary_attn(const uint32_t* codes_q, const uint32_t* co
   SA_REQUIRE(ws_bytes >= sa_linear_binary_attn_workspace(B, n, d, heads), SA_ERR_VALUE,
              "sa_linear_binary_attn: workspace too small");
   const int64_t dk = d / heads;
+#ifdef SA_DEBUG
+  if (g_attn_mode == 5) {
+    st = binattn_stream_launch(codes_q, codes_k, gamma_q, gamma_k, v, dw, out, B, n, d, heads, eps,
+                               as_stream(stream));
+    if (st != SA_ERR_VALUE) return st;
+  }
+#endif
   if (dk == 32 && g_attn_mode == 2) {
     st = binattn_split_launch(codes_q, codes_k, gamma_q, gamma_k, v, dw, out, B, n, d, heads, eps,
                               ws, ws_bytes, as_stream(stream));
     if (st != SA_ERR_VALUE) return st;
   }
-  if ((dk == 64 && g_attn_mode == 0) || g_attn_mode == 3) {
+  if ((dk == 64 && (g_attn_mode == 0 || g_attn_mode == 4)) || g_attn_mode == 3) {
     st = binattn_tc_launch(codes_q, codes_k, gamma_q, gamma_k, v, dw, out, B, n, d, heads, eps,
                            as_stream(stream));
     if (st != SA_ERR_VALUE) return st;
   }
-  if (dk == 32 && g_attn_mode == 0) {
+  if (dk == 32 && (g_attn_mode == 0 || g_attn_mode == 4)) {
     st = binattn_fused_launch(codes_q, codes_k, gamma_q, gamma_k, v, dw, out, B, n, d, heads, eps,
                               as_stream(stream));
     if (st != SA_ERR_VALUE) return st;

@@ -84,6 +84,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// the same on a shared-space address, with a suspend-time hint: a waiting
+// thread sleeps until the phase completes (or the hint elapses) instead of
+// spinning through issue slots its neighbours need
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity, uint32_t hint_ns = 0x100000u) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity), "r"(hint_ns)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_s(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }

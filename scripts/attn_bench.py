@@ -79,7 +79,7 @@ def main():
                     order, lib.sa_debug_attn_mode)
                 setm.argtypes = [ctypes.c_int]
                 modes = {"quadratic": ((1, "cuda_core"),), "softmax": ((1, "cuda_core"),)}.get(
-                    order, ((3, "tc"), (1, "multi")))
+                    order, ((3, "tc_cluster"), (5, "stream"), (1, "multi")))
                 for mode, name in modes:
                     setm(mode)
                     us = time_it(f)

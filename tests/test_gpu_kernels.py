@@ -609,9 +609,10 @@ def test_ln_route_wide_matches_unfused(M, d, nr):
                                              (2, 197, 192, 3, True), (1, 5, 64, 1, True),
                                              (2, 1000, 128, 2, False)])
 def test_tc_binary_attention_vs_oracle_and_cuda_core(B, n, d, h, with_dw, debug_lib):
-    """The tensor-core cluster kernel (product path, dk = 32 and 64) against the
-    oracle and the CUDA-core kernels (single-pass fused dk = 32 and the
-    three-kernel path), on square and non-square token grids with partial last
+    """The product kernels (dk = 32: CUDA-core single-pass cluster kernel; 64:
+    tensor-core cluster kernel) against the oracle, the tensor-core cluster
+    kernel at every dk, the streaming tensor-core kernel (debug build) and the
+    three-kernel path, on square and non-square token grids with partial last
     rows; the split two-kernel form is bit-identical to the fused CUDA-core one."""
     import ctypes
     from paper_2306_06446_b200 import attention as A
@@ -630,7 +631,10 @@ def test_tc_binary_attention_vs_oracle_and_cuda_core(B, n, d, h, with_dw, debug_
             lib.sa_debug_attn_mode(0)
     prod = host(A.binary_core(*args))        # default path (dk 32: CUDA-core fused, 64: tc)
     assert np.array_equal(run(0), prod)
-    tc = run(3)                              # the tensor-core kernel at every dk
+    tc = run(3)                              # the tensor-core cluster kernel at every dk
+    prev = run(4)                            # = the product choice
+    stream = run(5)                          # the streaming tensor-core kernel
+    assert np.array_equal(run(5), stream)    # deterministic
     legacy = run(1)
     fold = lambda t: ops.heads_split(t.reshape(B, n, d), h).reshape(B * h, n, d // h)  # noqa
     qf, _ = ops.binary_features(fold(q))
@@ -644,11 +648,16 @@ def test_tc_binary_attention_vs_oracle_and_cuda_core(B, n, d, h, with_dw, debug_
     assert rel_err(legacy, merged) < 2e-5
     assert rel_err(tc, legacy) < 2e-5
     assert rel_err(prod, merged) < 2e-5
+    assert rel_err(prod, tc) < 2e-5
+    assert np.array_equal(prev, prod)
+    if d // h in (32, 64):
+        assert rel_err(stream, merged) < 2e-5
+        assert rel_err(stream, tc) < 2e-5
     if d // h == 32:
-        assert rel_err(prod, legacy) < 2e-6   # CUDA-core fused vs three-kernel path
-        assert np.array_equal(run(2), prod)   # split form: same arithmetic
+        assert rel_err(prev, legacy) < 2e-6   # CUDA-core fused vs three-kernel path
+        assert np.array_equal(run(2), prev)   # split form: same arithmetic
     else:
-        assert np.array_equal(prod, tc)
+        assert np.array_equal(prev, tc)
     # all-negative query rows give exactly the DWConv term (zero attention part)
     q2 = q.copy()
     q2[0, :] = -np.abs(q2[0, :]) - 1.0

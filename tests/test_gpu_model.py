@@ -382,7 +382,10 @@ def test_apply_stage_matches_reference(golden):
     MD.apply_stage(m, 2, mlp_target="moe", attn_target="moe")
     assert digest(m.named_weights()) == str(fx["sha2"])
     assert rel_err(host(m.forward(x)), fx["logits2"]) < LOGIT_TOL
-    for lname, mod in m.moe_modules():
-        assert np.array_equal(mod.last_plan.expert_of, fx["route:" + lname]), lname
+    names = [lname for lname, _ in m.moe_modules()]
+    assert names[:2] == ["block0.mlp", "block0.attn.q"]   # the reference's names and order
+    for lname, mod in m.moe_modules():   # fixture keys use the s<stage>.b<block> form
+        key = "route:" + lname.replace("block", "s0.b", 1)
+        assert np.array_equal(mod.last_plan.expert_of, fx[key]), lname
     with pytest.raises(ValueError):
         MD.apply_stage(m, 3)
