@@ -303,6 +303,12 @@ __device__ __forceinline__ void gelu_pair(float& x0, float& x1) {
   }
 }
 
+__device__ __forceinline__ float gelu_one(float x) {
+  float y = 0.f;
+  gelu_pair<false>(x, y);
+  return x;
+}
+
 __host__ __device__ inline size_t tc_fixed_smem() {
   return size_t(8) * kWarpSlot + 1024             // epilogue slots (+ 1 KB alignment)
          + 2 * 128 * sizeof(int64_t)                // per-group row tables
@@ -798,8 +804,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
             float4 o = make_float4(__uint_as_float(raw[4 * c]), __uint_as_float(raw[4 * c + 1]),
                                    __uint_as_float(raw[4 * c + 2]), __uint_as_float(raw[4 * c + 3]));
             if (p.act == 1) {
-              gelu_fast2(o.x, o.y);
-              gelu_fast2(o.z, o.w);
+              gelu_pair<false>(o.x, o.y);
+              gelu_pair<false>(o.z, o.w);
             }
             if (p.gate) { o.x *= gt; o.y *= gt; o.z *= gt; o.w *= gt; }
             if (LNE) {
@@ -843,7 +849,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             float e = o[q];
-            if (p.act == 1) e = gelu_fast(e);
+            if (p.act == 1) e = gelu_one(e);
             if (p.gate) e = e * gt;
             o[q] = e;
           }
@@ -888,8 +894,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
             float4 o = make_float4(__uint_as_float(raw[q]), __uint_as_float(raw[q + 1]),
                                    __uint_as_float(raw[q + 2]), __uint_as_float(raw[q + 3]));
             if (p.act == 1) {
-              gelu_fast2(o.x, o.y);
-              gelu_fast2(o.z, o.w);
+              gelu_pair<false>(o.x, o.y);
+              gelu_pair<false>(o.z, o.w);
             }
             if (p.gate) { o.x *= gt; o.y *= gt; o.z *= gt; o.w *= gt; }
             *reinterpret_cast<float4*>(xb + lane * kXPitchW + q) = o;
@@ -971,7 +977,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
           float o = v[q];
-          if (p.act == 1) o = gelu_fast(o);
+          if (p.act == 1) o = gelu_one(o);
           if (p.gate) o = o * gt;
           v[q] = o;
         }
