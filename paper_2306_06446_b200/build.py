@@ -102,7 +102,8 @@ def _build_one(force: bool, verbose: bool, debug: bool) -> str:
     tmp = lib_path + ".tmp"
     # -Bsymbolic: the product and debug libraries define the same template
     # kernels; each must launch its own (a test process loads both)
-    cmd = [cc, *ARCH, "-shared", "-Xlinker", "-Bsymbolic", "-o", tmp, *objs, "-lcudart"]
+    cmd = [cc, *ARCH, "-shared", "-Xlinker", "-Bsymbolic", "-Xlinker", "--no-undefined", "-o", tmp,
+           *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

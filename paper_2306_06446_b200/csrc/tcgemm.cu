@@ -403,6 +403,14 @@ static int tc_patch_embed_impl(const float* grid, int64_t B, int64_t H, int64_t 
                                int64_t patch, float sub, const void* wpack, int bn, int64_t d,
                                const float* cls, const float* pos, float* y, const float* ln_g,
                                const float* ln_b, float ln_eps, void* stream);
+namespace sa {
+int embed_ln_launch(const float* grid, int64_t B, int64_t H, int64_t W, int64_t C, int64_t patch,
+                    float sub, const void* wpack, int bn, int64_t d, const float* gain,
+                    const float* bias, float eps, float* y, cudaStream_t s);
+}
+// patch embed + LN: 0 = the dedicated kernel (embed_tc.cu) when the shape
+// allows, 1 = the GEMM path's LNE epilogue (bit-identical)
+SA_DEBUG_SWITCH(int, g_embed_mode, 0, sa_debug_embed_mode)
 
 extern "C" int sa_tc_patch_embed(const float* grid, int64_t B, int64_t H, int64_t W, int64_t C,
                                  int64_t patch, float sub, const void* wpack, int bn, int64_t d,
@@ -421,6 +429,12 @@ extern "C" int sa_tc_patch_embed_ln(const float* grid, int64_t B, int64_t H, int
                                     void* stream) {
   SA_REQUIRE(gain != nullptr && bias != nullptr && sa_tc_patch_embed_ln_ok(d, 0, 0), SA_ERR_VALUE,
              "sa_tc_patch_embed_ln: d=%lld unsupported (32 or 64)", (long long)d);
+  if (g_embed_mode == 0 && B > 0 && H > 0 && W > 0 && C > 0 && patch > 0 && H % patch == 0 &&
+      B * (H / patch) * (W / patch) < (int64_t(1) << 31)) {
+    const int st = embed_ln_launch(grid, B, H, W, C, patch, sub, wpack, bn, d, gain, bias, eps, y,
+                                   as_stream(stream));
+    if (st != SA_ERR_VALUE) return st;
+  }
   return tc_patch_embed_impl(grid, B, H, W, C, patch, sub, wpack, bn, d, nullptr, nullptr, y, gain,
                              bias, eps, stream);
 }

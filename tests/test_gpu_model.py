@@ -389,3 +389,44 @@ def test_apply_stage_matches_reference(golden):
         assert np.array_equal(mod.last_plan.expert_of, fx[key]), lname
     with pytest.raises(ValueError):
         MD.apply_stage(m, 3)
+
+
+@pytest.mark.parametrize("B,H,C,patch,d", [(3, 224, 3, 4, 32), (2, 56, 32, 2, 64), (1, 8, 3, 4, 32),
+                                           (5, 28, 32, 2, 64), (2, 16, 8, 2, 32)])
+def test_embed_ln_kernel_bit_identical_to_gemm_path(B, H, C, patch, d, debug_lib):
+    """The dedicated patch-embed + LayerNorm kernel (embed_tc.cu) against the
+    GEMM path's LNE epilogue (sa_debug_embed_mode(1)): bit-identical tokens,
+    ragged last tiles included, and the oracle's embed + LayerNorm within fp32
+    tolerance."""
+    import ctypes
+    from paper_2306_06446_b200 import _lib
+    from paper_2306_06446_b200 import model as MD
+    lib = debug_lib
+    lib.sa_debug_embed_mode.argtypes = [ctypes.c_int]
+    g = ops.rng(B * H + C)
+    grid = g.uniform(0, 1, (B, H, H, C)).astype(F32)
+    K = patch * patch * C
+    w = (g.standard_normal((K, d)) / np.sqrt(K)).astype(F32)
+    gain = (1 + 0.1 * g.standard_normal(d)).astype(F32)
+    bias = (0.1 * g.standard_normal(d)).astype(F32)
+    lay = MD.Linear(w)
+    pk, bn, _ = lay.tc_pack()
+    side = H // patch
+    out = {}
+    grid_d, gain_d, bias_d = dev(grid), dev(gain), dev(bias)   # alive until the kernels ran
+    for mode in (0, 1):
+        y = torch.empty((B * side * side, d), dtype=torch.float32, device="cuda")
+        lib.sa_debug_embed_mode(mode)
+        try:
+            _lib.call("sa_tc_patch_embed_ln", _lib.ptr(grid_d), B, H, H, C, patch, 0.5,
+                      _lib.ptr(pk), bn, d, _lib.ptr(gain_d), _lib.ptr(bias_d), 1e-5,
+                      _lib.ptr(y), _lib.stream())
+            torch.cuda.synchronize()
+        finally:
+            lib.sa_debug_embed_mode(0)
+        out[mode] = host(y)
+    assert np.array_equal(out[0], out[1])
+    patches = (grid - 0.5).reshape(B, side, patch, side, patch, C).transpose(0, 1, 3, 2, 4, 5)
+    tok = ops.mm(patches.reshape(B * side * side, K), w)
+    ref = ops.layer_norm(tok, gain, bias)
+    assert rel_err(out[0], ref) < 1e-5
