@@ -38,28 +38,41 @@ namespace qkv {
 
 using namespace tc;
 
-// warps 0-3 epilogue, then Cfg::PG producer groups of 4 warps (alternate
-// tiles, one A buffer each), then the MMA issuer (Cfg::MMA_WARP, Cfg::THREADS)
-constexpr int kEpi = 0, kProd = 4;
+// Warp roles: Cfg::EG epilogue groups of 4 warps (warps 0 .. 4·EG-1), then
+// Cfg::PG producer groups of 4 warps, then the MMA issuer (Cfg::MMA_WARP).
+// Producer group g takes the CTA's tiles j = g, g + PG, ...; the A-operand
+// buffers (NA) are a ring over tiles; the accumulators are a ring of NACC
+// "units" — one (tile, projection) pair for the q/k/v form (both experts,
+// 2·D columns), one tile for W_O — and epilogue group e takes units
+// u = e, e + EG, ... All handshakes are mbarrier rings whose waiters can be at
+// most one phase ahead (EG <= NACC, producer lag bounded by the A ring; see
+// the wait sites).
 constexpr uint32_t kPlaneCols = 16;
-constexpr int kRT = 4;           // route-table ring slots
+constexpr int kRT = 8;           // route-table ring slots (tiles)
+constexpr int kAD = 8;           // "A buffer consumed" barrier ring (tiles)
 
 template <int D, int NP>   // NP projections: 3 (q, k, v with LN1 + hash) or 1 (W_O)
 struct Cfg {
   static constexpr int KC1 = D / 32;                // K stages of 32
   static constexpr int H = D / 32;                  // heads (dk = 32)
-  static constexpr int NA = (NP == 3 && D == 64) ? 1 : 2;          // A buffers in TMEM
-  static constexpr int NACC = NP == 3 ? (D == 32 ? 2 : 1) : (D == 32 ? 4 : 2);
-  // two producer groups for the d = 32 q/k/v form (its LN + three interleaved
-  // fp64 router chains per row pace the tile); one elsewhere (register budget)
-  static constexpr int PG = (NP == 3 && D == 32) ? 2 : 1;
-  static constexpr int MMA_WARP = kProd + 4 * PG;
+  // the q/k/v form is CUDA-core bound (LN, three fp64 router dots per row,
+  // sign-hash / γ epilogue): several groups per role keep enough warps in
+  // flight to hide their dependent chains
+  static constexpr int PG = NP == 3 ? (D == 32 ? 3 : 2) : 1;
+  static constexpr int EG = NP == 3 ? (D == 32 ? 3 : 2) : 1;
+  static constexpr int NA = 2;                      // A buffers in TMEM
+  static constexpr uint32_t ACC_COLS = 2 * D;       // one unit: dense | shift expert
+  static constexpr int NACC = D == 32 ? 4 : 2;
+  static constexpr int PROD0 = 4 * EG;
+  static constexpr int MMA_WARP = PROD0 + 4 * PG;
   static constexpr int THREADS = (MMA_WARP + 1) * 32;
+  static constexpr bool PREFETCH = PG <= 2 && (D == 32 || NP == 1);   // register budget
   static constexpr uint32_t A_COLS = KC1 * 3 * kPlaneCols;
   static constexpr uint32_t T_A = 0;
-  static constexpr uint32_t T_ACC = (NA * A_COLS + 31) / 32 * 32;  // 2·NP parts of D columns
-  static constexpr uint32_t ACC_COLS = 2 * NP * D;
+  static constexpr uint32_t T_ACC = (NA * A_COLS + 31) / 32 * 32;
   static_assert(T_ACC + NACC * ACC_COLS <= 512, "TMEM budget");
+  static_assert(EG <= NACC, "epilogue groups may run at most one accumulator phase ahead");
+  static_assert(PG <= 4, "route-table / A-ring phase bound");
   // resident weights: per projection dense (3 planes) then shift (1 plane)
   static constexpr uint32_t WD = uint32_t(D) * D * 2 * 3;
   static constexpr uint32_t WS = uint32_t(D) * D * 2;
@@ -80,22 +93,31 @@ struct Params {
   int32_t* expert_of;         // [3][M]
   float* gate;                // [3][M]
   uint32_t* codes[2];         // q, k: [B][H][n]
-  double* gpart;              // [2][M/32 segments][H][2]
-  int nseg;
+  float* rsum;                // [2][H][M] per-row Σ|y| (fp32 pairwise over the head's 32 columns)
   const float* residual;      // NP = 1: out = residual + gate · expert(x)
+  int dbg;                    // debug builds: 1 producers skip LN / routers, 2 epilogue skips
+                              // its work (handshakes only), 4 no MMAs, 8 producers skip loads,
+                              // 32 skip routers only, 64 skip LN only
 };
+#ifdef SA_DEBUG
+constexpr bool kQDbg = true;
+#else
+constexpr bool kQDbg = false;
+#endif
 
 // smem layout (bytes)
 template <int D, int NP>
 struct Smem {
+  using C = Cfg<D, NP>;
   static constexpr uint32_t W = 0;
-  static constexpr uint32_t WG = Cfg<D, NP>::W_BYTES;              // [NP][2D] double
+  static constexpr uint32_t WG = C::W_BYTES;                       // [NP][D][2] double
   static constexpr uint32_t RT_E = WG + NP * 2 * D * 8;            // [kRT][NP][128] int
   static constexpr uint32_t RT_G = RT_E + kRT * NP * 128 * 4;      // [kRT][NP][128] float
-  static constexpr uint32_t BOX = (RT_G + kRT * NP * 128 * 4 + 1023) & ~1023u;  // [4 warps][H][4 KB]
-  static constexpr uint32_t BAR = BOX + 4 * Cfg<D, NP>::H * 4096;
-  static constexpr uint32_t NBAR = 2 * Cfg<D, NP>::NA + 2 * Cfg<D, NP>::NACC + 2 * kRT + 1;
+  static constexpr uint32_t BOX = (RT_G + kRT * NP * 128 * 4 + 1023) & ~1023u;  // [4·EG warps][H][4 KB]
+  static constexpr uint32_t BAR = BOX + 4 * C::EG * C::H * 4096;
+  static constexpr uint32_t NBAR = C::NA + kAD + 2 * C::NACC + 2 * kRT + 1;
   static constexpr uint32_t TOTAL = BAR + NBAR * 8 + 16 + 1024;    // + alignment slack
+  static_assert(TOTAL <= 227 * 1024, "shared memory budget");
 };
 
 __device__ __forceinline__ int decide2(float l0, float l1, float tie_thresh, float& gate) {
@@ -107,6 +129,16 @@ __device__ __forceinline__ int decide2(float l0, float l1, float tie_thresh, flo
   const float e1 = (sh1 >= -tie_thresh) ? 1.f : expf(sh1);
   gate = (e ? e1 : e0) / (e0 + e1);
   return e;
+}
+
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
 }
 
 template <int D, int NP>
@@ -121,8 +153,8 @@ __global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, c
   float* rt_g = reinterpret_cast<float*>(smem + S::RT_G);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::BAR);
   uint64_t* a_full = bar;
-  uint64_t* a_empty = a_full + C::NA;
-  uint64_t* acc_full = a_empty + C::NA;
+  uint64_t* a_done = a_full + C::NA;
+  uint64_t* acc_full = a_done + kAD;
   uint64_t* acc_empty = acc_full + C::NACC;
   uint64_t* rt_full = acc_empty + C::NACC;
   uint64_t* rt_empty = rt_full + kRT;
@@ -132,17 +164,15 @@ __global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, c
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == kMma) tmem_alloc<512>(tmem_slot);
   if (tid == 0) {
-    for (int i = 0; i < C::NA; ++i) {
-      mbar_init(&a_full[i], 4);
-      mbar_init(&a_empty[i], 1);
-    }
+    for (int i = 0; i < C::NA; ++i) mbar_init(&a_full[i], 4);
+    for (int i = 0; i < kAD; ++i) mbar_init(&a_done[i], 1);
     for (int i = 0; i < C::NACC; ++i) {
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], 128);
     }
     for (int i = 0; i < kRT; ++i) {
       mbar_init(&rt_full[i], 4);
-      mbar_init(&rt_empty[i], 4);
+      mbar_init(&rt_empty[i], 4 * NP);   // every unit of the tile reads its route
     }
     mbar_init(wbar, 1);
     fence_barrier_init();
@@ -160,35 +190,41 @@ __global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, c
   const uint32_t tmem = *tmem_slot;
   const int ntile = int((p.M + 127) / 128);
 
-  if (warp >= kProd && warp < kMma) {
+  if (warp >= C::PROD0 && warp < kMma) {
     // ---------------- producers: LN + routers + A planes ----------------
-    // PG groups of 4 warps take alternate tiles (group g: the CTA's tiles
-    // j = g, g + PG, ...; with PG = 2 each group owns one of the two A buffers)
     constexpr int NPG = C::PG;
-    const int pg = (warp - kProd) >> 2, pw = (warp - kProd) & 3;
+    const int pg = (warp - C::PROD0) >> 2, pw = (warp - C::PROD0) & 3;
     const int rl = pw * 32 + lane;
     const uint32_t lane_base = uint32_t(pw * 32) << 16;
-    int j = pg;
-    // the group's next tile row is loaded while this tile is normalised / routed
-    float4 xn[D / 4];
-    auto load_row = [&](int mm) {
+    float4 xn[C::PREFETCH ? D / 4 : 1];
+    auto load_row = [&](int mm, float4* dst) {
       const int64_t rr = int64_t(mm) * 128 + rl;
       const float4* xr = reinterpret_cast<const float4*>(p.x + rr * D);
 #pragma unroll
       for (int i = 0; i < D / 4; ++i)
-        xn[i] = (mm < ntile && rr < p.M) ? __ldg(xr + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        dst[i] = (mm < ntile && rr < p.M && !(kQDbg && (p.dbg & 8))) ? __ldg(xr + i)
+                                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
     };
-    load_row(blockIdx.x + pg * gridDim.x);
+    if (C::PREFETCH) load_row(blockIdx.x + pg * gridDim.x, xn);
+    int j = pg;
     for (int m = blockIdx.x + pg * gridDim.x; m < ntile; m += NPG * gridDim.x, j += NPG) {
       const int64_t row = int64_t(m) * 128 + rl;
       const bool ok = row < p.M;
       float v[D];
+      {
+        float4 xc[C::PREFETCH ? 1 : D / 4];
+        const float4* src = xn;
+        if (!C::PREFETCH) {
+          load_row(m, xc);
+          src = xc;
+        }
 #pragma unroll
-      for (int i = 0; i < D / 4; ++i) {
-        v[4 * i] = xn[i].x; v[4 * i + 1] = xn[i].y; v[4 * i + 2] = xn[i].z; v[4 * i + 3] = xn[i].w;
+        for (int i = 0; i < D / 4; ++i) {
+          v[4 * i] = src[i].x; v[4 * i + 1] = src[i].y; v[4 * i + 2] = src[i].z; v[4 * i + 3] = src[i].w;
+        }
       }
-      load_row(m + NPG * gridDim.x);
-      if (NP == 3 && ok) {
+      if (C::PREFETCH) load_row(m + NPG * gridDim.x, xn);
+      if (NP == 3 && ok && !(kQDbg && (p.dbg & 65))) {
         // LayerNorm: the exact operation sequence of ln_route_kernel (moe.cu)
         float s = 0.f;
 #pragma unroll
@@ -211,30 +247,49 @@ __global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, c
           v[4 * i + 3] = v[4 * i + 3] * inv * g.w + b.w;
         }
       }
-      // routers (fp64 dots in channel order, as ln_route_kernel / route_kernel)
+      // routers (fp64 dots in channel order, as ln_route_kernel / route_kernel).
+      // Slot rs was last used by tile j - kRT; this group's previous tile
+      // passed its A-ring wait, so tile j - kRT's release is the only
+      // outstanding phase (one-phase-ahead bound).
       const int rs = j % kRT;
       mbar_wait(&rt_empty[rs], (uint32_t(j / kRT) & 1u) ^ 1u);
-      // d = 32: the NP routers' chains are interleaved (2·NP independent fp64
-      // chains in flight, each in channel order, so the logits are unchanged);
-      // d = 64 keeps one router at a time (register budget)
-      constexpr int RI = D == 32 ? NP : 1;
-#pragma unroll 1
-      for (int r0 = 0; r0 < NP; r0 += RI) {
+      // the NP routers' chains are interleaved (2·NP independent fp64 chains
+      // in flight, each in channel order, so the logits are unchanged)
+      constexpr int RI = NP;
+      {
+        constexpr int r0 = 0;
+        if (kQDbg && (p.dbg & 33)) {   // debug: no router dots (route table: expert 0, gate 1)
+#pragma unroll
+          for (int i = 0; i < RI; ++i) {
+            rt_e[(rs * NP + r0 + i) * 128 + rl] = 0;
+            rt_g[(rs * NP + r0 + i) * 128 + rl] = 1.f;
+          }
+        } else {
         double s0[RI], s1[RI];
 #pragma unroll
         for (int i = 0; i < RI; ++i) {
           s0[i] = 0.0;
           s1[i] = 0.0;
         }
+        // weights of channel c + 1 are loaded while channel c's DFMAs run
+        // (warp-uniform shared-memory broadcasts)
+        const double2* wrow = reinterpret_cast<const double2*>(swg);
+        double2 wc[RI];
+#pragma unroll
+        for (int i = 0; i < RI; ++i) wc[i] = wrow[i * D];
 #pragma unroll
         for (int c = 0; c < D; ++c) {
+          double2 wn[RI];
+#pragma unroll
+          for (int i = 0; i < RI; ++i) wn[i] = wrow[i * D + (c + 1 < D ? c + 1 : c)];
           const double vc = double(v[c]);
 #pragma unroll
           for (int i = 0; i < RI; ++i) {
-            const double2 w = *reinterpret_cast<const double2*>(swg + (r0 + i) * 2 * D + 2 * c);
-            s0[i] = fma(vc, w.x, s0[i]);
-            s1[i] = fma(vc, w.y, s1[i]);
+            s0[i] = fma(vc, wc[i].x, s0[i]);
+            s1[i] = fma(vc, wc[i].y, s1[i]);
           }
+#pragma unroll
+          for (int i = 0; i < RI; ++i) wc[i] = wn[i];
         }
 #pragma unroll
         for (int i = 0; i < RI; ++i) {
@@ -249,12 +304,13 @@ __global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, c
           rt_e[(rs * NP + r) * 128 + rl] = e;
           rt_g[(rs * NP + r) * 128 + rl] = g;
         }
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&rt_full[rs]);
-      // A planes → TMEM
+      // A planes → TMEM: buffer ab was last read by tile j - NA's MMAs
       const int ab = j % C::NA;
-      mbar_wait(&a_empty[ab], (uint32_t(j / C::NA) & 1u) ^ 1u);
+      if (j >= C::NA) mbar_wait(&a_done[(j - C::NA) % kAD], uint32_t((j - C::NA) / kAD) & 1u);
       tc_fence_after();
       const uint32_t a1 = tmem + lane_base + C::T_A + uint32_t(ab) * C::A_COLS;
 #pragma unroll
@@ -281,53 +337,56 @@ __global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, c
     mbar_wait(wbar, 0);   // resident weights landed
     constexpr uint32_t idesc = idesc_bf16_m128(D);
     const uint32_t wbase = smem_u32(smem + S::W);
+    int u = 0;
     int j = 0;
     for (int m = blockIdx.x; m < ntile; m += gridDim.x, ++j) {
-      const int ab = j % C::NA, cb = j % C::NACC;
+      const int ab = j % C::NA;
       mbar_wait(&a_full[ab], uint32_t(j / C::NA) & 1u);
-      mbar_wait(&acc_empty[cb], (uint32_t(j / C::NACC) & 1u) ^ 1u);
       tc_fence_after();
       const uint32_t a0 = tmem + C::T_A + uint32_t(ab) * C::A_COLS;
-      const uint32_t acc = tmem + C::T_ACC + uint32_t(cb) * C::ACC_COLS;
 #pragma unroll
-      for (int r = 0; r < NP; ++r) {
-        const uint32_t wd = wbase + r * (C::WD + C::WS);
-        const uint32_t ws = wd + C::WD;
+      for (int r = 0; r < NP; ++r, ++u) {
+        const int cb = u % C::NACC;
+        mbar_wait(&acc_empty[cb], (uint32_t(u / C::NACC) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t acc = tmem + C::T_ACC + uint32_t(cb) * C::ACC_COLS;
+        if (!(kQDbg && (p.dbg & 4))) {
+          const uint32_t wd = wbase + r * (C::WD + C::WS);
+          const uint32_t ws = wd + C::WD;
 #pragma unroll
-        for (int kc = 0; kc < C::KC1; ++kc)
+          for (int kc = 0; kc < C::KC1; ++kc)
 #pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            const uint32_t ad = a0 + kc * 3 * kPlaneCols + ks * 8;
-            const uint32_t accf = (kc | ks) != 0;
-            mma_chain6_ts_w(acc + uint32_t(2 * r) * D, ad,
-                            smem_desc(wd + kc * 3 * (D * 32 * 2) + ks * 256), kPlaneCols,
-                            (D * 32 * 2) >> 4, idesc, accf);
-            mma_chain3_ts_w(acc + uint32_t(2 * r + 1) * D, ad,
-                            smem_desc(ws + kc * (D * 32 * 2) + ks * 256), kPlaneCols, idesc, accf);
-          }
+            for (int ks = 0; ks < 2; ++ks) {
+              const uint32_t ad = a0 + kc * 3 * kPlaneCols + ks * 8;
+              const uint32_t accf = (kc | ks) != 0;
+              mma_chain6_ts_w(acc, ad, smem_desc(wd + kc * 3 * (D * 32 * 2) + ks * 256), kPlaneCols,
+                              (D * 32 * 2) >> 4, idesc, accf);
+              mma_chain3_ts_w(acc + uint32_t(D), ad, smem_desc(ws + kc * (D * 32 * 2) + ks * 256),
+                              kPlaneCols, idesc, accf);
+            }
+        }
+        commit_w(&acc_full[cb]);
       }
-      commit_w(&a_empty[ab]);
-      commit_w(&acc_full[cb]);
+      commit_w(&a_done[j % kAD]);
     }
-  } else if (warp < kEpi + 4) {
-    // ---------------- epilogue (thread = row) ----------------
-    const int quad = warp - kEpi;
+  } else if (warp < C::PROD0) {
+    // ---------------- epilogue (thread = row), group eg takes units eg, eg + EG, ... ----------------
+    const int eg = warp >> 2, quad = warp & 3;
     const int rl = quad * 32 + lane;
     const uint32_t lane_base = uint32_t(quad * 32) << 16;
-    uint8_t* box = smem + S::BOX + quad * C::H * 4096;
-    int j = 0;
-    for (int m = blockIdx.x; m < ntile; m += gridDim.x, ++j) {
+    uint8_t* box = smem + S::BOX + (eg * 4 + quad) * C::H * 4096;
+    const int nunit = ((ntile - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x)) * NP;
+    for (int u = eg; u < nunit; u += C::EG) {
+      const int j = u / NP, r = u % NP;
+      const int m = int(blockIdx.x) + j * int(gridDim.x);
       const int64_t row = int64_t(m) * 128 + rl;
       const bool ok = row < p.M;
-      const int rs = j % kRT, cb = j % C::NACC;
+      const int rs = j % kRT, cb = u % C::NACC;
+      // one-phase-ahead: this group's previous unit u - EG >= u - NACC was
+      // already committed, and tile j - 1's route (or older) was already read
       mbar_wait(&rt_full[rs], uint32_t(j / kRT) & 1u);
-      int e[NP];
-      float g[NP];
-#pragma unroll
-      for (int r = 0; r < NP; ++r) {
-        e[r] = rt_e[(rs * NP + r) * 128 + rl];
-        g[r] = rt_g[(rs * NP + r) * 128 + rl];
-      }
+      const int e = rt_e[(rs * NP + r) * 128 + rl];
+      const float g = rt_g[(rs * NP + r) * 128 + rl];
       // W_O: the residual row is loaded before the accumulator wait
       float4 res[NP == 1 ? D / 4 : 1];
       if (NP == 1) {
@@ -338,75 +397,87 @@ __global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, c
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&rt_empty[rs]);
-      mbar_wait(&acc_full[cb], uint32_t(j / C::NACC) & 1u);
+      mbar_wait(&acc_full[cb], uint32_t(u / C::NACC) & 1u);
       tc_fence_after();
+      if (kQDbg && (p.dbg & 2)) {
+        tc_fence_before();
+        mbar_arrive(&acc_empty[cb]);
+        continue;
+      }
       const uint32_t acc = tmem + lane_base + C::T_ACC + uint32_t(cb) * C::ACC_COLS;
       // image / segment bookkeeping of this warp's 32 rows
       const int64_t wrow0 = int64_t(m) * 128 + quad * 32;
       const int b = int(row / p.n), t = int(row - int64_t(b) * p.n);
-      const int b0 = int(wrow0 / p.n);
-      const int seg = int(wrow0 >> 5);
-#pragma unroll 1
-      for (int r = 0; r < NP; ++r) {
+      const float2 g2 = make_float2(g, g);
 #pragma unroll
-        for (int hh = 0; hh < C::H; ++hh) {
-          uint32_t rd[32], rsft[32];
-          tmem_ld32_nowait(acc + uint32_t(2 * r) * D + hh * 32, rd);
-          tmem_ld32_nowait(acc + uint32_t(2 * r + 1) * D + hh * 32, rsft);
+      for (int hh = 0; hh < C::H; ++hh) {
+        uint32_t code = 0u;
+        float hs[2];
+        uint8_t* bx = box + hh * 4096;
+        if (!(NP == 3 && r < 2)) {   // v / W_O: the box is free once its last TMA store read it
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+        }
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          uint32_t rd[16], rsft[16];
+          tmem_ld16_nowait(acc + hh * 32 + half * 16, rd);
+          tmem_ld16_nowait(acc + uint32_t(D) + hh * 32 + half * 16, rsft);
           tmem_ld_wait();
-          float y[32];
           // gate and residual are two float32 roundings, as the reference's
           // y * gate then residual + y (no FMA contraction)
+          float y[16];
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            y[c] = __fmul_rn(g[r], __uint_as_float(e[r] ? rsft[c] : rd[c]));
+          for (int c = 0; c < 16; c += 2) {
+            const float2 a2 = make_float2(__uint_as_float(e ? rsft[c] : rd[c]),
+                                          __uint_as_float(e ? rsft[c + 1] : rd[c + 1]));
+            const float2 y2 = __fmul2_rn(g2, a2);
+            y[c] = y2.x;
+            y[c + 1] = y2.y;
+          }
           if (NP == 1) {   // W_O: + residual
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const float4 q4 = res[(NP == 1 ? (hh * 32 + c) / 4 : 0)];
+            for (int c = 0; c < 16; ++c) {
+              const int cc = hh * 32 + half * 16 + c;
+              const float4 q4 = res[NP == 1 ? cc / 4 : 0];
               const float rv = (c & 3) == 0 ? q4.x : (c & 3) == 1 ? q4.y : (c & 3) == 2 ? q4.z : q4.w;
               y[c] = __fadd_rn(rv, y[c]);
             }
           }
           if (NP == 3 && r < 2) {
-            uint32_t code = 0u;
-            double asum = 0.0;
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              code |= (y[c] < 0.f ? 0u : 1u) << c;
-              asum += double(fabsf(y[c]));
-            }
-            if (!ok) asum = 0.0;
-            if (ok) p.codes[r][(int64_t(b) * C::H + hh) * p.n + t] = code;
-            // fp64 |y| partials of this 32-row segment, split by image (the
-            // segment may straddle one image boundary; n >= 32 is required)
-            double s0 = (ok && b == b0) ? asum : 0.0;
-            double s1 = (ok && b != b0) ? asum : 0.0;
+            for (int c = 0; c < 16; ++c) code |= (y[c] < 0.f ? 0u : 1u) << (half * 16 + c);
+            // |y| row sum: fixed pairwise fp32 tree over the 32 columns
+            // (error <= 5 ulp of the row sum), fp64 across rows below
+            float tsum[8];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-              s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-            }
-            if (lane == 0 && wrow0 < p.M) {
-              double* gp = p.gpart + ((int64_t(r) * p.nseg + seg) * C::H + hh) * 2;
-              gp[0] = s0;
-              gp[1] = s1;
-            }
+            for (int c = 0; c < 8; ++c) tsum[c] = fabsf(y[2 * c]) + fabsf(y[2 * c + 1]);
+#pragma unroll
+            for (int w = 4; w > 0; w >>= 1)
+#pragma unroll
+              for (int c = 0; c < w; ++c) tsum[c] += tsum[c + w];
+            hs[half] = tsum[0];
           } else {
-            // v: 32 x 32 box (128-byte swizzle) → TMA store
-            uint8_t* bx = box + hh * 4096;
-            if (lane == 0) bulk_wait_read0();
-            __syncwarp();
+            // v / W_O: half of a 32 x 32 box (128-byte swizzle) → TMA store
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-              *reinterpret_cast<float4*>(bx + lane * 128 + ((c ^ (lane & 7)) * 16)) =
+            for (int c = 0; c < 4; ++c) {
+              const int ch = half * 4 + c;
+              *reinterpret_cast<float4*>(bx + lane * 128 + ((ch ^ (lane & 7)) * 16)) =
                   make_float4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]);
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&tmV, bx, hh * 32, int(wrow0));
-              bulk_commit();
             }
+          }
+        }
+        if (NP == 3 && r < 2) {
+          if (ok) {
+            p.codes[r][(int64_t(b) * C::H + hh) * p.n + t] = code;
+            p.rsum[(int64_t(r) * C::H + hh) * p.M + row] = hs[0] + hs[1];
+          }
+        } else {
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmV, bx, hh * 32, int(wrow0));
+            bulk_commit();
           }
         }
       }
@@ -421,9 +492,10 @@ __global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, c
 }
 
 // γ[r][b·H + h] = Σ |y| over image b's rows of head h / (n · 32): one warp per
-// (r, b, h); lane l sums the segments l, l + 32, ... of the image in order and
-// the lanes meet in a fixed xor tree (deterministic, no atomics).
-__global__ void gamma_finalize_qkv(const double* __restrict__ gpart, int nseg, int H, int64_t B,
+// (r, b, h); lane l sums the per-row fp32 sums of rows l, l + 32, ... of the
+// image in fp64, and the lanes meet in a fixed xor tree (deterministic, no
+// atomics).
+__global__ void gamma_finalize_qkv(const float* __restrict__ rsum, int64_t M, int H, int64_t B,
                                    int n, float* __restrict__ gq, float* __restrict__ gk) {
   const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -432,13 +504,9 @@ __global__ void gamma_finalize_qkv(const double* __restrict__ gpart, int nseg, i
   const int64_t bh = i % (B * H);
   const int64_t b = bh / H;
   const int h = int(bh % H);
-  const int64_t lo = b * n, hi = (b + 1) * n;   // rows of image b
+  const float* src = rsum + (int64_t(r) * H + h) * M + b * n;
   double s = 0.0;
-  for (int64_t sg = (lo >> 5) + lane; sg <= (hi - 1) >> 5; sg += 32) {
-    const int64_t b0 = (sg * 32) / n;             // image of the segment's first row
-    const double* gp = gpart + ((int64_t(r) * nseg + sg) * H + h) * 2;
-    s += (b0 == b) ? gp[0] : gp[1];
-  }
+  for (int t = lane; t < n; t += 32) s += double(__ldg(src + t));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) (r == 0 ? gq : gk)[bh] = float(s / (double(n) * 32.0));
@@ -449,14 +517,16 @@ __global__ void gamma_finalize_qkv(const double* __restrict__ gpart, int nseg, i
 
 using namespace sa;
 
+SA_DEBUG_SWITCH(int, g_qkv_dbg, 0, sa_debug_qkv_mode)
+
+
 extern "C" int sa_ln_qkv_hash_ok(int64_t d, int64_t n) {
   return (d == 32 || d == 64) && n >= 32;
 }
 
 extern "C" size_t sa_ln_qkv_hash_workspace(int64_t B, int64_t n, int64_t d) {
   const int64_t M = B * n;
-  const int64_t nseg = (M + 31) / 32;
-  return size_t(2 * nseg * (d / 32) * 2) * sizeof(double) + 256;
+  return size_t(2 * M * (d / 32)) * sizeof(float) + 256;
 }
 
 extern "C" int sa_ln_qkv_hash(const float* x, const float* gain, const float* bias, float eps,
@@ -477,6 +547,7 @@ extern "C" int sa_ln_qkv_hash(const float* x, const float* gain, const float* bi
   const int64_t M = B * n;
   Params p;
   memset(&p, 0, sizeof(p));
+  p.dbg = g_qkv_dbg;
   p.x = x;
   p.gain = gain;
   p.bias = bias;
@@ -495,8 +566,7 @@ extern "C" int sa_ln_qkv_hash(const float* x, const float* gain, const float* bi
   p.gate = gate;
   p.codes[0] = codes_q;
   p.codes[1] = codes_k;
-  p.gpart = static_cast<double*>(ws);
-  p.nseg = int((M + 31) / 32);
+  p.rsum = static_cast<float*>(ws);
   CUtensorMap tmV;
   memset(&tmV, 0, sizeof(tmV));
   {
@@ -525,7 +595,7 @@ extern "C" int sa_ln_qkv_hash(const float* x, const float* gain, const float* bi
     qkv_kernel<64, 3><<<grid, qkv::Cfg<64, 3>::THREADS, smem, s>>>(p, tmV);
   }
   const int64_t H = d / 32;
-  gamma_finalize_qkv<<<unsigned(cdiv(2 * B * H, 8)), 256, 0, s>>>(p.gpart, p.nseg, int(H), B,
+  gamma_finalize_qkv<<<unsigned(cdiv(2 * B * H, 8)), 256, 0, s>>>(p.rsum, M, int(H), B,
                                                                  int(n), gamma_q, gamma_k);
   count_launch(2);
   SA_LAUNCH_CHECK("sa_ln_qkv_hash");
@@ -550,6 +620,7 @@ extern "C" int sa_fused_moe_linear(const float* x, const float* wg, const void* 
   cudaStream_t s = as_stream(stream);
   Params p;
   memset(&p, 0, sizeof(p));
+  p.dbg = g_qkv_dbg;
   p.x = x;
   p.wg[0] = wg;
   p.wd[0] = static_cast<const uint16_t*>(w_dense);
