@@ -214,10 +214,13 @@ int sa_tc_moe_mlp(const float* x, const int32_t* perm, const int32_t* counts, co
                   const void* w2_shift, int bn1, int bn2, float* y, const float* residual,
                   int64_t M, int64_t d, int64_t hidden, void* ws, size_t ws_bytes, void* stream);
 /* Fused MLP on the tensor cores: fc1 → GELU → fc2 in ONE kernel, the hidden
- * activations stay on chip (TMEM → registers → TMEM); d = 32 or 64,
- * hidden % 64 == 0. W1 must be packed with bn = sa_tc_fused_mlp_w1_bn(), W2
- * with bn = d. */
+ * activations stay on chip (TMEM → registers → TMEM); d = 32, 64 (hidden
+ * chunks of 64) or d = 128, 160 (chunks of 32), hidden a multiple of the
+ * chunk. W1 must be packed with bn = sa_tc_fused_mlp_chunk(d), W2 with bn = d.
+ * sa_tc_fused_mlp_w1_bn() is the d <= 64 chunk (64), kept for callers of the
+ * narrow form. */
 int sa_tc_fused_mlp_ok(int64_t d, int64_t hidden);
+int sa_tc_fused_mlp_chunk(int64_t d);
 int sa_tc_fused_mlp_w1_bn(void);
 int sa_tc_moe_mlp_fused(const float* x, const int32_t* perm, const int32_t* counts,
                         const float* gate, const void* w1_dense, const void* w2_dense,

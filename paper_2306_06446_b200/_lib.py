@@ -88,6 +88,7 @@ _SIGS = {
                                     _P, _F32, _P, _P]),
     "sa_tc_fused_mlp_ok": (_I32, [_I64, _I64]),
     "sa_tc_fused_mlp_w1_bn": (_I32, []),
+    "sa_tc_fused_mlp_chunk": (_I32, [_I64]),
     "sa_tc_moe_mlp_fused": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64,
                                    _P]),
     "sa_tc_mlp_fused": (_I32, [_P, _P, _I32, _P, _I32, _P, _I64, _I64, _I64, _P, _P]),

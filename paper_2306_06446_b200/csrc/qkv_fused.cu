@@ -51,6 +51,12 @@ constexpr uint32_t kPlaneCols = 16;
 constexpr int kRT = 8;           // route-table ring slots (tiles)
 constexpr int kAD = 8;           // "A buffer consumed" barrier ring (tiles)
 
+#ifndef QKV_WO_PG
+#define QKV_WO_PG 1
+#endif
+#ifndef QKV_WO_EG
+#define QKV_WO_EG 1
+#endif
 template <int D, int NP>   // NP projections: 3 (q, k, v with LN1 + hash) or 1 (W_O)
 struct Cfg {
   static constexpr int KC1 = D / 32;                // K stages of 32
@@ -58,8 +64,8 @@ struct Cfg {
   // the q/k/v form is CUDA-core bound (LN, three fp64 router dots per row,
   // sign-hash / γ epilogue): several groups per role keep enough warps in
   // flight to hide their dependent chains
-  static constexpr int PG = NP == 3 ? (D == 32 ? 3 : 2) : 1;
-  static constexpr int EG = NP == 3 ? (D == 32 ? 3 : 2) : 1;
+  static constexpr int PG = NP == 3 ? (D == 32 ? 3 : 2) : QKV_WO_PG;
+  static constexpr int EG = NP == 3 ? (D == 32 ? 3 : 2) : QKV_WO_EG;
   static constexpr int NA = 2;                      // A buffers in TMEM
   static constexpr uint32_t ACC_COLS = 2 * D;       // one unit: dense | shift expert
   static constexpr int NACC = D == 32 ? 4 : 2;

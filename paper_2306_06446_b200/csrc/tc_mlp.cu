@@ -49,9 +49,17 @@ constexpr int kGelu = 16;              // GELU warps 0-15 (column group x lane q
 constexpr bool kGeluAlt = false;
 constexpr int kGeluPerChunk = kGeluAlt ? 8 : 16;
 constexpr int kProd = 16;              // producers: warps 16 .. 16 + 4·(d/32) - 1
+// wide form (d = 128 / 160): hidden chunks of 32, one A1 buffer, a single
+// acc2 of d columns, GELU in two groups of 8 warps on alternate chunks, one
+// producer warp per TMEM lane quarter walking every K stage
+template <int D>
+struct Wide {
+  static constexpr bool W = D > 64;
+  static constexpr int HC = W ? 32 : 64;
+};
 template <int D>
 struct Roles {
-  static constexpr int NPW = 4 * (D / 32);        // producer warps (one 32-channel stage each)
+  static constexpr int NPW = Wide<D>::W ? 4 : 4 * (D / 32);   // producer warps
   static constexpr int kMma1 = kProd + NPW, kMma2 = kMma1 + 1, kWld = kMma1 + 2;
   static constexpr int kThreads = (kWld + 1) * 32;
 };
@@ -88,11 +96,16 @@ enum { S_OF = 0, S_A1E, S_WR, S_OE, S_HE, S_A1F, S_BF, S_HF, S_W, T_PROD, T_MMA1
 
 template <int D, bool RES>
 struct Layout {
+  static constexpr bool W = Wide<D>::W;
+  static constexpr int HC = Wide<D>::HC;                      // hidden chunk (fc1 N, fc2 K)
   static constexpr int KC1 = D / 32;                          // fc1 K stages
   static constexpr int NA = D == 32 ? 2 : 1;                  // A1 buffers (TMEM)
-  static constexpr int NB = 3;                                // acc1 / A2 buffers (TMEM)
+  static constexpr int NB = W ? 2 : 3;                        // acc1 / A2 buffers (TMEM)
+  static constexpr uint32_t BUFC = HC + HC / 2;               // acc1 (HC fp32) | A2 (3 planes)
+  static constexpr int NO = W ? 1 : 2;                        // acc2 buffers
+  static constexpr int GPC = W ? 8 : kGeluPerChunk;           // GELU warps per chunk
   static constexpr bool CAT = D == 32;                        // N-concatenated dense fc2
-  static constexpr int NW = 4;                                // ring slots (RES = false)
+  static constexpr int NW = W ? 3 : 4;                        // ring slots (RES = false)
   static constexpr uint32_t W1C = KC1 * 3 * (HC * 32 * 2);    // dense W1 chunk bytes
   static constexpr uint32_t W2C = (HC / 32) * 3 * (D * 32 * 2);
   static constexpr uint32_t RW1 = (kResHidden / HC) * W1C;    // resident dense W1
@@ -102,17 +115,17 @@ struct Layout {
   __device__ static constexpr uint32_t r_w2(int e) { return RW1 + RW1 / 3 + (e ? RW2 : 0u); }
   static constexpr uint32_t WBYTES = RES ? (RW1 + RW1 / 3 + RW2 + RW2 / 3) : NW * (W1C + W2C);
   static constexpr uint32_t OFF_XB = WBYTES;
-  static constexpr uint32_t XB = 4 * KC1 * 32 * kXPitch * 4; // producer transpose slots
+  static constexpr uint32_t XB = Roles<D>::NPW * 32 * kXPitch * 4;   // producer transpose slots
   static constexpr uint32_t OFF_BAR = OFF_XB + XB;
   // barriers: a1 full/empty[NA], w1 full/empty[NW], w2 full/empty[NW],
-  //           h_full/h_empty/buf_free[NB], o_full/o_empty[2], wres
-  static constexpr uint32_t NBAR = 2 * NA + 4 * NW + 3 * NB + 4 + 1;
+  //           h_full/h_empty/buf_free[NB], o_full/o_empty[NO], wres
+  static constexpr uint32_t NBAR = 2 * NA + 4 * NW + 3 * NB + 2 * NO + 1;
   static constexpr uint32_t TOTAL = OFF_BAR + NBAR * 8 + 16 + 1024;  // + alignment slack
   // TMEM columns: buffers[NB] (acc1 | A2) | acc2[2] | A1[NA] (KC1 x 3 planes)
   static constexpr uint32_t T_BUF = 0;
-  static constexpr uint32_t T_ACC2 = NB * kBufCols;
-  static constexpr uint32_t ACC2C = 64;
-  static constexpr uint32_t T_A1 = T_ACC2 + 2 * ACC2C;
+  static constexpr uint32_t T_ACC2 = NB * BUFC;
+  static constexpr uint32_t ACC2C = W ? D : 64;
+  static constexpr uint32_t T_A1 = T_ACC2 + NO * ACC2C;
   static constexpr uint32_t A1COLS = KC1 * 3 * kPlaneCols;
   static constexpr uint32_t TCOLS = 512;
   static_assert(T_A1 + NA * A1COLS <= TCOLS, "TMEM budget");
@@ -210,9 +223,9 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
   uint64_t* h_full = w2_empty + L::NW;      // fc1(q) done
   uint64_t* h_empty = h_full + L::NB;       // GELU(q) wrote A2 (16 warps)
   uint64_t* buf_free = h_empty + L::NB;     // fc2(q) done reading A2: buffer reusable
-  uint64_t* o_full = buf_free + L::NB;      // [2] acc2 ready
-  uint64_t* o_empty = o_full + 2;           // [2] acc2 drained (producer warps)
-  uint64_t* wres = o_empty + 2;             // resident weights landed
+  uint64_t* o_full = buf_free + L::NB;      // [NO] acc2 ready
+  uint64_t* o_empty = o_full + L::NO;       // [NO] acc2 drained (producer warps)
+  uint64_t* wres = o_empty + L::NO;         // resident weights landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_BAR + L::NBAR * 8);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -253,10 +266,10 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
     }
     for (int i = 0; i < L::NB; ++i) {
       mbar_init(&h_full[i], 1);
-      mbar_init(&h_empty[i], kGeluPerChunk);
+      mbar_init(&h_empty[i], L::GPC);
       mbar_init(&buf_free[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < L::NO; ++i) {
       mbar_init(&o_full[i], 1);
       mbar_init(&o_empty[i], NPW);
     }
@@ -269,20 +282,27 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
   const uint32_t tmem = *tmem_slot;
   const int64_t c0 = p.counts ? int64_t(p.counts[0]) : 0;
   const int64_t ntile = mlp_tiles(p, c0);
+  constexpr int HC = L::HC;
   const int nchunk = p.hidden / HC;
 
   if (kDbg && (p.dbg & 8) && warp != kMma1 && warp != kMma2) {
     // debug: the MMA issuers alone, no waits (raw instruction-stream rate)
   } else if (warp >= kProd && warp < kMma1) {
     // ------- producers: x rows → A1 planes (TMEM); drain acc2 -------
-    // warp (quad, kc): rows quad·32 + lane (= TMEM lanes), channels [32kc, 32kc + 32)
-    const int quad = (warp - kProd) & 3, kc = (warp - kProd) >> 2;
+    // warp (quad, kc0): rows quad·32 + lane (= TMEM lanes), K stages / output
+    // channel blocks kc0, kc0 + KST, ... (narrow: one stage per warp; wide: one
+    // warp per lane quarter walks every stage)
+    constexpr int KST = NPW / 4;
+    const int quad = (warp - kProd) & 3, kc0 = (warp - kProd) >> 2;
     const int ptid = quad * 32 + lane;
     const uint32_t lane_base = uint32_t(quad * 32) << 16;
     float* xb = reinterpret_cast<float*>(smem + L::OFF_XB) + (warp - kProd) * 32 * kXPitch;
+    // the warp's 16-column output blocks: 2 per owned K stage
+    constexpr int NBLK = 2 * (L::KC1 / KST);
+    auto blk_col = [&](int bi) { return 32 * (kc0 + (bi >> 1) * KST) + 16 * (bi & 1); };
     auto drain = [&](int64_t jt, int e, int64_t r0, int64_t r1) {
-      const int ob = int(jt & 1);
-      const uint32_t oph = uint32_t(jt >> 1) & 1u;
+      const int ob = int(jt % L::NO);
+      const uint32_t oph = uint32_t(jt / L::NO) & 1u;
       if (kDbg && (p.dbg & 2)) {
         PW(S_OF, &o_full[ob], oph);
         __syncwarp();
@@ -310,15 +330,16 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
                         ? __ldg(reinterpret_cast<const float4*>(p.residual + orow_l[it] * D + cb + c4))
                         : make_float4(0.f, 0.f, 0.f, 0.f);
       };
-      load_res(32 * kc, res[0]);
+      load_res(blk_col(0), res[0]);
       const bool two = L::CAT && (e ? p.np1 : p.np0) == 3;   // dense d = 32: two partial sums
       PW(S_OF, &o_full[ob], oph);
       tc_fence_after();
       const uint32_t acc = tmem + lane_base + L::T_ACC2 + uint32_t(ob) * L::ACC2C;
 #pragma unroll
-      for (int cb = 32 * kc; cb < 32 * kc + 32; cb += 16) {
-        const int rb = (cb >> 4) & 1;
-        if (cb + 16 < 32 * kc + 32) load_res(cb + 16, res[rb ^ 1]);
+      for (int bi = 0; bi < NBLK; ++bi) {
+        const int cb = blk_col(bi);
+        const int rb = bi & 1;
+        if (bi + 1 < NBLK) load_res(blk_col(bi + 1), res[rb ^ 1]);
         float v[16];
         tmem_ld16(acc + uint32_t(cb), v);
         if (two) {
@@ -362,19 +383,23 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
       int64_t r0, r1;
       if (!mlp_tile(p, c0, m, e, r0, r1)) continue;
       const int64_t row = r0 + ptid;
+      const bool live = row < r1 && !(kDbg && (p.dbg & 2));
+      const float* xrow = live ? p.x + (p.perm ? int64_t(__ldg(p.perm + row)) : row) * D : nullptr;
       float4 v[8];
-      if (row < r1 && !(kDbg && (p.dbg & 2))) {
-        const float* src = p.x + (p.perm ? int64_t(__ldg(p.perm + row)) : row) * D + 32 * kc;
+      auto load_stage = [&](int kc) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = __ldg(reinterpret_cast<const float4*>(src) + i);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+        for (int i = 0; i < 8; ++i)
+          v[i] = live ? __ldg(reinterpret_cast<const float4*>(xrow + 32 * kc) + i)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      };
+      load_stage(kc0);
       PW(S_A1E, &a1_empty[ab], pab ^ 1u);
       tc_fence_after();
-      if (!(kDbg && (p.dbg & 2))) {
-        const uint32_t a1 = tmem + lane_base + L::T_A1 + uint32_t(ab) * L::A1COLS;
+      const uint32_t a1 = tmem + lane_base + L::T_A1 + uint32_t(ab) * L::A1COLS;
+#pragma unroll 1
+      for (int kc = kc0; kc < L::KC1; kc += KST) {
+        if (kc != kc0) load_stage(kc);
+        if (!(kDbg && (p.dbg & 2))) {
 #pragma unroll
           for (int sub = 0; sub < 2; ++sub) {   // 16 channels (8 bf16 pairs) at a time
             uint32_t hp[8], mp[8], lp[8];
@@ -395,8 +420,9 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
             tmem_st8(col + kPlaneCols, mp);
             tmem_st8(col + 2 * kPlaneCols, lp);
           }
-        tmem_st_wait();
+        }
       }
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&a1_full[ab]);
@@ -474,7 +500,7 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
         PW(S_BF, &buf_free[b], pb ^ 1u);   // fc2(q - 3) released the buffer
         TL(0, qq);
         tc_fence_after();
-        const uint32_t d1 = tmem + L::T_BUF + uint32_t(b) * kBufCols;
+        const uint32_t d1 = tmem + L::T_BUF + uint32_t(b) * L::BUFC;
         const uint64_t bd0 = smem_desc(RES ? wrow : sbase + uint32_t(s) * L::W1C);
         if (!(kDbg && (p.dbg & 4))) {
 #pragma unroll
@@ -526,7 +552,7 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
         PW(S_HE, &h_empty[b], pb);        // GELU(q) wrote A2[b]
         TL(4, qq);
         tc_fence_after();
-        const uint32_t bb = tmem + L::T_BUF + uint32_t(b) * kBufCols;
+        const uint32_t bb = tmem + L::T_BUF + uint32_t(b) * L::BUFC;
         const uint64_t bd0 = smem_desc(RES ? wrow : sbase + L::NW * L::W1C + uint32_t(s) * L::W2C);
         const uint32_t a0 = c != 0 ? 1u : 0u;
         if (!(kDbg && (p.dbg & 4))) {
@@ -537,7 +563,8 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
             // 16ks + 8, lo at 64 + 8ks
             const uint32_t ah = kGeluAlt ? bb + (ks >> 1) * 32u + (ks & 1) * 8u : bb + ks * 16u;
             const uint32_t am = ah + (kGeluAlt ? 16u : 8u);
-            const uint32_t al = kGeluAlt ? bb + 64u + (ks >> 1) * 16u + (ks & 1) * 8u : bb + 64u + ks * 8u;
+            const uint32_t al = kGeluAlt ? bb + 64u + (ks >> 1) * 16u + (ks & 1) * 8u
+                                         : bb + uint32_t(HC) + ks * 8u;
             const uint32_t acc = ks ? 1u : a0;
             if (shift) {
               mma3(d2, ah, am, al, bd0 + uint64_t(((ks >> 1) * (D * 64) + (ks & 1) * 256) >> 4),
@@ -559,9 +586,9 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
         wrow += cstride;
       }
       commit_w(&o_full[ob]);
-      if (++ob == 2) { ob = 0; pob ^= 1u; }
+      if (++ob == L::NO) { ob = 0; pob ^= 1u; }
     }
-  } else if (warp < kGelu && kGeluAlt) {
+  } else if (warp < kGelu && kGeluAlt && !L::W) {
     // ------- GELU: group gs = warp / 8 takes chunks q % 2 == gs; warp (h, quad)
     // of the group takes hidden columns [32h, 32h + 32) = fc2 K steps 2h, 2h+1.
     // Its planes go over its own consumed accumulator columns (hi [32h, 32h+16),
@@ -613,11 +640,15 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
       if (warp == kGelu - 1) TL(6, q);
     }
   } else if (warp < kGelu) {
-    // ------- GELU (kGeluAlt = false): warp (k, quad) takes hidden columns [16k, 16k + 16) of every
+    // ------- GELU (kGeluAlt = false): warp (k, quad) takes hidden columns [16k, 16k + 16) of a
     // chunk = K step k of fc2; its planes go over its own consumed accumulator
     // columns (hi [16k, 16k + 8), mid [16k + 8, 16k + 16)) and the free
-    // columns [64 + 8k, 72 + 8k) (lo) -------
-    const int k = warp >> 2, quad = warp & 3;
+    // columns [HC + 8k, HC + 8k + 8) (lo). Narrow (HC = 64): all 16 warps on
+    // every chunk; wide (HC = 32): groups of 8 warps (gs = warp / 8) on
+    // alternate chunks -------
+    const int gs = L::W ? warp >> 3 : 0;
+    const int k = L::W ? (warp >> 2) & 1 : warp >> 2, quad = warp & 3;
+    constexpr int QS = L::W ? 2 : 1;
     const uint32_t lb = tmem + (uint32_t(quad * 32) << 16) + L::T_BUF;
     int nt = 0;
     for (int64_t m = blockIdx.x; m < ntile; m += gridDim.x) {
@@ -626,13 +657,13 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
       if (mlp_tile(p, c0, m, e, r0, r1)) ++nt;
     }
     const int total_q = nt * nchunk;
-    int b = 0;
-    uint32_t ph = 0u;
-    for (int q = 0; q < total_q; ++q) {
+    for (int q = gs; q < total_q; q += QS) {
+      const int b = q % L::NB;
+      const uint32_t ph = uint32_t(q / L::NB) & 1u;
       PW(S_HF, &h_full[b], ph);             // fc1(q) done
       if (warp == 0) TL(2, q);
       tc_fence_after();
-      const uint32_t bb = lb + uint32_t(b) * kBufCols;
+      const uint32_t bb = lb + uint32_t(b) * L::BUFC;
       if (!(kDbg && (p.dbg & 1))) {
         float r[16];
         if (kDbg && (p.dbg & 128)) {   // debug: no TMEM traffic (synthetic inputs, no stores)
@@ -661,7 +692,7 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
         } else {
           tmem_st8(bb + uint32_t(16 * k), hp);
           tmem_st8(bb + uint32_t(16 * k + 8), mp);
-          tmem_st8(bb + uint32_t(64 + 8 * k), lp);
+          tmem_st8(bb + uint32_t(HC + 8 * k), lp);
           tmem_st_wait();
         }
       }
@@ -670,7 +701,6 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
       if (lane == 0) mbar_arrive(&h_empty[b]);
       if (warp == 0) TL(3, q);
       if (warp == kGelu - 1) TL(6, q);
-      if (++b == L::NB) { b = 0; ph ^= 1u; }
     }
   }
 #ifdef SA_DEBUG
@@ -746,8 +776,12 @@ static int mlp_launch(tcm::MlpParams& p, int d, cudaStream_t s) {
       mlp_launch_nf<32, true>(p, grid, s);
     else
       mlp_launch_nf<32, false>(p, grid, s);
-  } else {
+  } else if (d == 64) {
     mlp_launch_nf<64, false>(p, grid, s);
+  } else if (d == 128) {
+    mlp_launch_nf<128, false>(p, grid, s);
+  } else {
+    mlp_launch_nf<160, false>(p, grid, s);
   }
   count_launch(1);
   SA_LAUNCH_CHECK("mlp_kernel");
@@ -758,10 +792,16 @@ static int mlp_launch(tcm::MlpParams& p, int d, cudaStream_t s) {
 
 using namespace sa;
 
-/* The fused kernels read W1 packed with bn = 64 (hidden chunks) and W2 packed
- * with bn = d; see sa_weight_pack. */
+/* The fused kernels read W1 packed with bn = sa_tc_fused_mlp_chunk(d) (the
+ * hidden chunk: 64 for d = 32 / 64, 32 for d = 128 / 160) and W2 packed with
+ * bn = d; see sa_weight_pack. */
+extern "C" int sa_tc_fused_mlp_chunk(int64_t d) {
+  return (d == 32 || d == 64) ? 64 : (d == 128 || d == 160) ? 32 : 0;
+}
+
 extern "C" int sa_tc_fused_mlp_ok(int64_t d, int64_t hidden) {
-  return (d == 32 || d == 64) && hidden % tcm::HC == 0 && hidden > 0 && hidden <= 8192;
+  const int hc = sa_tc_fused_mlp_chunk(d);
+  return hc > 0 && hidden % hc == 0 && hidden > 0 && hidden <= 8192;
 }
 
 extern "C" int sa_tc_fused_mlp_w1_bn(void) { return tcm::HC; }

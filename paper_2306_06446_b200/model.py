@@ -138,9 +138,9 @@ def _dual_expert_linear(m) -> bool:
             and m.experts[0].in_dim == m.experts[0].out_dim)
 
 
-def fused_mlp_w1_bn() -> int:
-    """Hidden-chunk width the fused MLP kernel reads W1 packed with."""
-    return int(_lib.load().sa_tc_fused_mlp_w1_bn())
+def fused_mlp_w1_bn(d: int = 32) -> int:
+    """Hidden-chunk width the fused MLP kernel reads W1 packed with at model dim d."""
+    return int(_lib.load().sa_tc_fused_mlp_chunk(d))
 
 
 def fused_mlp_ok(d, hidden) -> bool:
@@ -328,7 +328,7 @@ class Mlp:
         y = torch.empty((M, self.fc2.out_dim), dtype=torch.float32, device=x.device)
         res = residual.reshape(y.shape) if residual is not None else None
         if fused_mlp_ok(d, hidden) and k1 == k2:
-            p1, _, _ = self.fc1.tc_pack(fused_mlp_w1_bn())
+            p1, _, _ = self.fc1.tc_pack(fused_mlp_w1_bn(d))
             p2, _, _ = self.fc2.tc_pack()
             _lib.call("sa_tc_mlp_fused", _lib.ptr(x2), _lib.ptr(p1), k1, _lib.ptr(p2), k2,
                       _lib.ptr(y), M, d, hidden, _lib.ptr(res), _stream())
@@ -392,9 +392,9 @@ def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None):
             return None
         y = torch.empty((M, d), dtype=torch.float32, device=x.device)
         if fused_mlp_ok(d, hidden):
-            p1d, _, _ = e0.fc1.tc_pack(fused_mlp_w1_bn())
+            p1d, _, _ = e0.fc1.tc_pack(fused_mlp_w1_bn(d))
             p2d, _, _ = e0.fc2.tc_pack()
-            p1s, _, _ = e1.fc1.tc_pack(fused_mlp_w1_bn())
+            p1s, _, _ = e1.fc1.tc_pack(fused_mlp_w1_bn(d))
             p2s, _, _ = e1.fc2.tc_pack()
             _lib.call("sa_tc_moe_mlp_fused", _lib.ptr(x), _lib.ptr(plan.perm_dev),
                       _lib.ptr(plan.counts_dev), _lib.ptr(plan.gate_dev), _lib.ptr(p1d),

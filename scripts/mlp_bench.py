@@ -42,7 +42,10 @@ def timed(fn, reps=10):
     b.record()
     torch.cuda.synchronize()
     return [a.elapsed_time(b) * 1e3 / reps]
-for d, hidden, M in ((32, 256, 802816), (64, 512, 200704)):
+SHAPES = ((32, 256, 802816), (64, 512, 200704))
+if os.environ.get("MLP_SHAPES"):   # e.g. "160,640,50176;128,1024,200704"
+    SHAPES = tuple(tuple(int(v) for v in t.split(",")) for t in os.environ["MLP_SHAPES"].split(";"))
+for d, hidden, M in SHAPES:
     g = np.random.default_rng(0)
     w1 = (g.standard_normal((d, hidden)) / np.sqrt(d)).astype(np.float32)
     w2 = (g.standard_normal((hidden, d)) / np.sqrt(hidden)).astype(np.float32)

@@ -358,7 +358,11 @@ def test_moe_module_vs_oracle(M, d, hidden):
 @pytest.mark.parametrize("M,d,hidden,scale,force", [
     (5, 32, 256, 1.0, None), (129, 32, 512, 1.0, None), (1000, 64, 256, 1.0, None),
     (3000, 32, 128, 1.0, None), (2000, 32, 256, 8.0, None), (777, 64, 512, 6.0, None),
-    (1500, 32, 256, 1.0, 0), (1500, 32, 256, 1.0, 1), (640, 64, 512, 1.0, 1)])
+    (1500, 32, 256, 1.0, 0), (1500, 32, 256, 1.0, 1), (640, 64, 512, 1.0, 1),
+    # wide form (d = 128 / 160: hidden chunks of 32, single acc2, streamed weights)
+    (5, 160, 640, 1.0, None), (1000, 160, 640, 1.0, None), (777, 160, 640, 6.0, None),
+    (1500, 160, 640, 1.0, 0), (1500, 160, 640, 1.0, 1), (3001, 128, 512, 1.0, None),
+    (700, 128, 1024, 1.0, None)])
 def test_fused_moe_mlp_edges(M, d, hidden, scale, force):
     """Fused MoE MLP kernel: ragged and tiny M, resident (d = 32, hidden <= 256)
     and streamed weights, hidden pre-activations spanning the GELU's saturated
@@ -385,7 +389,8 @@ def test_fused_moe_mlp_edges(M, d, hidden, scale, force):
 
 
 @pytest.mark.parametrize("d,hidden,shift", [(32, 256, False), (32, 256, True), (64, 512, False),
-                                           (64, 512, True), (32, 512, False)])
+                                           (64, 512, True), (32, 512, False), (160, 640, False),
+                                           (160, 640, True), (128, 1024, False)])
 def test_fused_mlp_plain_vs_oracle(d, hidden, shift):
     """Single-expert fused MLP (sa_tc_mlp_fused) for dense and shift layers."""
     from paper_2306_06446_b200 import model as MD
