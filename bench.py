@@ -411,6 +411,15 @@ def op_bytes(name, args):
     return None
 
 
+def op_key(name, args):
+    """Row of the per-op table: the fused MoE MLP runs two kernels — the
+    narrow form (d = 32 / 64, HBM-bound) and the wide form (d = 128 / 160,
+    tensor-bound) — so its calls are split by model dim."""
+    if name == "sa_tc_moe_mlp_fused":
+        return f"{name}[d={args[11]}]"
+    return name
+
+
 def kernel_microbench(torch, hbm_peak, iters=20):
     """Standalone timings of the hot-path kernels at the PVTv2-B0 stage-1 shape
     (B=256, n=3136, d=32; hidden 256): K1 sign-hash, K2a binary attention,
@@ -655,7 +664,7 @@ def main():
         torch.cuda._sleep(int(3e8))
         with timer.record():
             m.forward(images)
-    summ = timer.summary()
+    summ = timer.summary(op_key)
     peaks = {}
     pk_path = os.path.join(REPO, "MEASURED_PEAKS.json")
     if os.path.exists(pk_path):
@@ -664,7 +673,7 @@ def main():
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     ops_rows = []
     for name, r in summ.items():
-        nbytes = [op_bytes(name, a) for a in r["args"]]
+        nbytes = [op_bytes(name.split("[")[0], a) for a in r["args"]]
         total_b = sum(b for b in nbytes if b) if all(b is not None for b in nbytes) else None
         ach = (total_b / 1e9) / (r["ms"] / 1e3) if total_b else None
         ops_rows.append({"op": name, "calls_per_fwd": r["calls"] // 3, "ms_per_fwd": r["ms"] / 3,

@@ -43,11 +43,13 @@ class OpTimer:
         finally:
             _lib.call = orig
 
-    def summary(self):
+    def summary(self, key=None):
+        """Per-op totals; `key(name, args)` may split an entry point into rows
+        (e.g. one per model dim when the shapes run different kernels)."""
         torch.cuda.synchronize()
         out = defaultdict(lambda: {"calls": 0, "ms": 0.0, "args": []})
         for name, s, e, args in self.events:
-            r = out[name]
+            r = out[key(name, args) if key else name]
             r["calls"] += 1
             r["ms"] += s.elapsed_time(e)
             r["args"].append(args)

@@ -23,6 +23,13 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --skip-cpu > gpurun_out/launches_bench.log 2>&1
 timeout 600 python scripts/attn_bench.py --debug > gpurun_out/attn_bench.txt 2>&1
 timeout 300 python scripts/mlp_bench.py 0 > gpurun_out/mlp_bench.txt 2>&1
+MLP_SHAPES="160,640,50176" timeout 300 python scripts/mlp_bench.py 0 r4 r8 >> gpurun_out/mlp_bench.txt 2>&1
+QKV_PRODUCT=1 timeout 300 python scripts/qkv_roles.py > gpurun_out/qkv_bench.txt 2>&1
+timeout 300 python scripts/qkv_roles.py 0 1 2 34 >> gpurun_out/qkv_bench.txt 2>&1
+timeout 300 python scripts/gemm_roles.py 0 >> gpurun_out/qkv_bench.txt 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/fwd_launches.csv python scripts/fwd_launches.py > /dev/null 2>&1
+python scripts/launch_summary.py gpurun_out/fwd_launches.csv > gpurun_out/fwd_summary.txt 2>&1
 timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_c2.log 2>&1
 head -c 300 gpurun_out/bench_c2.log; echo
 for c in c3 c4 c5; do

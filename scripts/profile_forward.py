@@ -29,12 +29,13 @@ for _ in range(a.warm):
 torch.cuda.synchronize()
 calls = []
 if a.record:
+    from bench import op_key   # the bench's per-op rows (MLP split by model dim)
     orig = _lib.call
 
     def rec(name, *args):
         c0 = _lib.launch_count()
         r = orig(name, *args)
-        calls.append([name, _lib.launch_count() - c0])
+        calls.append([op_key(name, args), _lib.launch_count() - c0])
         return r
     _lib.call = rec
 torch.cuda.cudart().cudaProfilerStart()
