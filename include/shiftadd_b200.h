@@ -258,6 +258,16 @@ int sa_fused_moe_linear_ok(int64_t d);
 int sa_fused_moe_linear(const float* x, const float* wg, const void* w_dense, const void* w_shift,
                         const float* residual, float tie_thresh, int64_t M, int64_t d,
                         int32_t* expert_of, float* gate, float* y, void* stream);
+/* sa_fused_moe_linear with the block's second LayerNorm and the MLP router in
+ * the epilogue (Block.forward, model.py:454-459; moe.py:81-92): y = the block
+ * residual stream h, y2 = LN2(h) and the MLP's (expert, gate) per row, each
+ * bit-identical to sa_ln_route on h; d = 32 or 64. */
+int sa_fused_moe_linear_ln_route(const float* x, const float* wg, const void* w_dense,
+                                 const void* w_shift, const float* residual, float tie_thresh,
+                                 int64_t M, int64_t d, int32_t* expert_of, float* gate, float* y,
+                                 const float* ln_gain, const float* ln_bias, float eps,
+                                 const float* wg2, float* y2, int32_t* expert_of2, float* gate2,
+                                 void* stream);
 
 /* patchify (model.py:557-563) + patch-embed Linear on the tensor cores */
 int sa_tc_patch_embed(const float* grid, int64_t B, int64_t H, int64_t W, int64_t C,

@@ -97,6 +97,8 @@ _SIGS = {
     "sa_ln_qkv_hash_ok": (_I32, [_I64, _I64]),
     "sa_fused_moe_linear_ok": (_I32, [_I64]),
     "sa_fused_moe_linear": (_I32, [_P, _P, _P, _P, _P, _F32, _I64, _I64, _P, _P, _P, _P]),
+    "sa_fused_moe_linear_ln_route": (_I32, [_P, _P, _P, _P, _P, _F32, _I64, _I64, _P, _P, _P, _P,
+                                            _P, _F32, _P, _P, _P, _P, _P]),
     "sa_ln_qkv_hash_workspace": (_SZ, [_I64, _I64, _I64]),
     "sa_ln_qkv_hash": (_I32, [_P, _P, _P, _F32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F32, _I64,
                               _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),

@@ -57,7 +57,7 @@ constexpr int kAD = 8;           // "A buffer consumed" barrier ring (tiles)
 #ifndef QKV_WO_EG
 #define QKV_WO_EG 1
 #endif
-template <int D, int NP>   // NP projections: 3 (q, k, v with LN1 + hash) or 1 (W_O)
+template <int D, int NP, bool LNR = false>   // NP projections: 3 (q, k, v with LN1 + hash) or 1 (W_O)
 struct Cfg {
   static constexpr int KC1 = D / 32;                // K stages of 32
   static constexpr int H = D / 32;                  // heads (dk = 32)
@@ -65,7 +65,8 @@ struct Cfg {
   // sign-hash / γ epilogue): several groups per role keep enough warps in
   // flight to hide their dependent chains
   static constexpr int PG = NP == 3 ? (D == 32 ? 3 : 2) : QKV_WO_PG;
-  static constexpr int EG = NP == 3 ? (D == 32 ? 3 : 2) : QKV_WO_EG;
+  // (LNR: the W_O epilogue also runs the LayerNorm + fp64 router: two groups)
+  static constexpr int EG = NP == 3 ? (D == 32 ? 3 : 2) : (LNR ? 2 : QKV_WO_EG);
   static constexpr int NA = 2;                      // A buffers in TMEM
   static constexpr uint32_t ACC_COLS = 2 * D;       // one unit: dense | shift expert
   static constexpr int NACC = D == 32 ? 4 : 2;
@@ -101,6 +102,14 @@ struct Params {
   uint32_t* codes[2];         // q, k: [B][H][n]
   float* rsum;                // [2][H][M] per-row Σ|y| (fp32 pairwise over the head's 32 columns)
   const float* residual;      // NP = 1: out = residual + gate · expert(x)
+  // W_O form with the next LayerNorm + router in the epilogue (LNR): y2 =
+  // LN2(out) (tmV2), the MLP router's (expert, gate) per row
+  const float* ln_g;
+  const float* ln_b;
+  float ln_eps;
+  const float* wg2;
+  int32_t* expert_of2;
+  float* gate2;
   int dbg;                    // debug builds: 1 producers skip LN / routers, 2 epilogue skips
                               // its work (handshakes only), 4 no MMAs, 8 producers skip loads,
                               // 32 skip routers only, 64 skip LN only
@@ -112,15 +121,16 @@ constexpr bool kQDbg = false;
 #endif
 
 // smem layout (bytes)
-template <int D, int NP>
+template <int D, int NP, bool LNR = false>
 struct Smem {
-  using C = Cfg<D, NP>;
+  using C = Cfg<D, NP, LNR>;
   static constexpr uint32_t W = 0;
-  static constexpr uint32_t WG = C::W_BYTES;                       // [NP][D][2] double
-  static constexpr uint32_t RT_E = WG + NP * 2 * D * 8;            // [kRT][NP][128] int
+  static constexpr uint32_t WG = C::W_BYTES;                       // [NP (+1)][D][2] double
+  static constexpr uint32_t RT_E = WG + (NP + (LNR ? 1 : 0)) * 2 * D * 8;   // [kRT][NP][128] int
   static constexpr uint32_t RT_G = RT_E + kRT * NP * 128 * 4;      // [kRT][NP][128] float
   static constexpr uint32_t BOX = (RT_G + kRT * NP * 128 * 4 + 1023) & ~1023u;  // [4·EG warps][H][4 KB]
-  static constexpr uint32_t BAR = BOX + 4 * C::EG * C::H * 4096;
+  static constexpr uint32_t BOX2 = BOX + 4 * C::EG * C::H * 4096;   // LNR: y2 boxes
+  static constexpr uint32_t BAR = BOX2 + (LNR ? 4 * C::EG * C::H * 4096 : 0);
   static constexpr uint32_t NBAR = C::NA + kAD + 2 * C::NACC + 2 * kRT + 1;
   static constexpr uint32_t TOTAL = BAR + NBAR * 8 + 16 + 1024;    // + alignment slack
   static_assert(TOTAL <= 227 * 1024, "shared memory budget");
@@ -147,10 +157,12 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[1
       : "r"(taddr));
 }
 
-template <int D, int NP>
-__global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, const __grid_constant__ CUtensorMap tmV) {
-  using C = Cfg<D, NP>;
-  using S = Smem<D, NP>;
+template <int D, int NP, bool LNR = false>
+__global__ void __launch_bounds__(Cfg<D, NP, LNR>::THREADS, 1) qkv_kernel(Params p, const __grid_constant__ CUtensorMap tmV,
+                                                                         const __grid_constant__ CUtensorMap tmV2) {
+  static_assert(!LNR || NP == 1, "LN + router epilogue: W_O form only");
+  using C = Cfg<D, NP, LNR>;
+  using S = Smem<D, NP, LNR>;
   constexpr int kMma = C::MMA_WARP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -190,6 +202,8 @@ __global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, c
     }
   }
   for (int i = tid; i < NP * 2 * D; i += C::THREADS) swg[i] = double(p.wg[i / (2 * D)][i % (2 * D)]);
+  if (LNR)
+    for (int i = tid; i < 2 * D; i += C::THREADS) swg[NP * 2 * D + i] = double(p.wg2[i]);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -415,6 +429,7 @@ __global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, c
       const int64_t wrow0 = int64_t(m) * 128 + quad * 32;
       const int b = int(row / p.n), t = int(row - int64_t(b) * p.n);
       const float2 g2 = make_float2(g, g);
+      float hrow[LNR ? D : 1];   // LNR: the output row, for the LayerNorm + router below
 #pragma unroll
       for (int hh = 0; hh < C::H; ++hh) {
         uint32_t code = 0u;
@@ -448,6 +463,7 @@ __global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, c
               const float4 q4 = res[NP == 1 ? cc / 4 : 0];
               const float rv = (c & 3) == 0 ? q4.x : (c & 3) == 1 ? q4.y : (c & 3) == 2 ? q4.z : q4.w;
               y[c] = __fadd_rn(rv, y[c]);
+              if (LNR) hrow[LNR ? cc : 0] = y[c];
             }
           }
           if (NP == 3 && r < 2) {
@@ -489,6 +505,75 @@ __global__ void __launch_bounds__(Cfg<D, NP>::THREADS, 1) qkv_kernel(Params p, c
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[cb]);
+      if (LNR) {
+        // LayerNorm of the output row + the next MoE router on it: the exact
+        // operation sequence of ln_route_kernel (moe.cu), so y2 and the route
+        // are bit-identical to sa_ln_route on the stored output
+        if (ok) {
+          float s = 0.f;
+#pragma unroll
+          for (int i = 0; i < D / 4; ++i)
+            s += (hrow[4 * i] + hrow[4 * i + 1]) + (hrow[4 * i + 2] + hrow[4 * i + 3]);
+          const float mean = s / float(D);
+          float q2 = 0.f;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            hrow[i] -= mean;
+            q2 += hrow[i] * hrow[i];
+          }
+          const float inv = 1.0f / sqrtf(q2 / float(D) + p.ln_eps);
+#pragma unroll
+          for (int i = 0; i < D / 4; ++i) {
+            const float4 g4 = __ldg(reinterpret_cast<const float4*>(p.ln_g) + i);
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.ln_b) + i);
+            hrow[4 * i] = hrow[4 * i] * inv * g4.x + b4.x;
+            hrow[4 * i + 1] = hrow[4 * i + 1] * inv * g4.y + b4.y;
+            hrow[4 * i + 2] = hrow[4 * i + 2] * inv * g4.z + b4.z;
+            hrow[4 * i + 3] = hrow[4 * i + 3] * inv * g4.w + b4.w;
+          }
+          const double2* w2r = reinterpret_cast<const double2*>(swg + NP * 2 * D);
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            const double2 w = w2r[c];
+            const double vc = double(hrow[c]);
+            s0 = fma(vc, w.x, s0);
+            s1 = fma(vc, w.y, s1);
+          }
+          float g2v;
+          const int e2 = decide2(float(s0), float(s1), p.tie, g2v);
+          p.expert_of2[row] = e2;
+          p.gate2[row] = g2v;
+        }
+        // y2 boxes: free once their previous stores (issued before this
+        // unit's H output-box stores) were read
+        uint8_t* box2 = smem + S::BOX2 + (eg * 4 + quad) * C::H * 4096;
+        if (lane == 0) {
+          if (C::H == 1)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else
+            asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
+        }
+        __syncwarp();
+#pragma unroll
+        for (int hh = 0; hh < C::H; ++hh)
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<float4*>(box2 + hh * 4096 + lane * 128 + ((c ^ (lane & 7)) * 16)) =
+                make_float4(hrow[(hh * 32 + 4 * c) % (LNR ? D : 1)],
+                            hrow[(hh * 32 + 4 * c + 1) % (LNR ? D : 1)],
+                            hrow[(hh * 32 + 4 * c + 2) % (LNR ? D : 1)],
+                            hrow[(hh * 32 + 4 * c + 3) % (LNR ? D : 1)]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int hh = 0; hh < C::H; ++hh) {
+            tma_store_2d(&tmV2, box2 + hh * 4096, hh * 32, int(wrow0));
+            bulk_commit();
+          }
+        }
+      }
     }
     if (lane == 0) bulk_wait0();
   }
@@ -594,11 +679,11 @@ extern "C" int sa_ln_qkv_hash(const float* x, const float* gain, const float* bi
   if (d == 32) {
     const int smem = int(Smem<32, 3>::TOTAL);
     cudaFuncSetAttribute(qkv_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    qkv_kernel<32, 3><<<grid, qkv::Cfg<32, 3>::THREADS, smem, s>>>(p, tmV);
+    qkv_kernel<32, 3><<<grid, qkv::Cfg<32, 3>::THREADS, smem, s>>>(p, tmV, tmV);
   } else {
     const int smem = int(Smem<64, 3>::TOTAL);
     cudaFuncSetAttribute(qkv_kernel<64, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    qkv_kernel<64, 3><<<grid, qkv::Cfg<64, 3>::THREADS, smem, s>>>(p, tmV);
+    qkv_kernel<64, 3><<<grid, qkv::Cfg<64, 3>::THREADS, smem, s>>>(p, tmV, tmV);
   }
   const int64_t H = d / 32;
   gamma_finalize_qkv<<<unsigned(cdiv(2 * B * H, 8)), 256, 0, s>>>(p.rsum, M, int(H), B,
@@ -614,15 +699,41 @@ extern "C" int sa_ln_qkv_hash(const float* x, const float* gain, const float* bi
  * out = residual + gate · expert(x); expert_of / gate [M] for the lazy plan. */
 extern "C" int sa_fused_moe_linear_ok(int64_t d) { return d == 32 || d == 64; }
 
-extern "C" int sa_fused_moe_linear(const float* x, const float* wg, const void* w_dense,
-                                   const void* w_shift, const float* residual, float tie_thresh,
-                                   int64_t M, int64_t d, int32_t* expert_of, float* gate,
-                                   float* y, void* stream) {
+namespace {
+
+int encode_rows_map(CUtensorMap* tm, float* base, int64_t M, int64_t d) {
+  memset(tm, 0, sizeof(*tm));
+  const cuuint64_t dims[2] = {cuuint64_t(d), cuuint64_t(M)};
+  const cuuint64_t strides[1] = {cuuint64_t(d) * 4};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  return int(encode_tmap_tiled(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+}
+
+template <int D, bool LNR>
+void launch_wo(const qkv::Params& p, const CUtensorMap& tmY, const CUtensorMap& tmY2, int grid,
+               cudaStream_t s) {
   using namespace qkv;
-  SA_REQUIRE(sa_fused_moe_linear_ok(d), SA_ERR_SHAPE, "sa_fused_moe_linear: d=%lld unsupported",
-             (long long)d);
-  SA_REQUIRE(M > 0 && M < (int64_t(1) << 31), SA_ERR_SHAPE, "sa_fused_moe_linear: bad M");
-  SA_REQUIRE(residual != nullptr, SA_ERR_VALUE, "sa_fused_moe_linear: residual required");
+  const int smem = int(Smem<D, 1, LNR>::TOTAL);
+  cudaFuncSetAttribute(qkv_kernel<D, 1, LNR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  qkv_kernel<D, 1, LNR><<<grid, Cfg<D, 1, LNR>::THREADS, smem, s>>>(p, tmY, tmY2);
+}
+
+int fused_moe_linear_impl(const char* who, const float* x, const float* wg, const void* w_dense,
+                          const void* w_shift, const float* residual, float tie_thresh, int64_t M,
+                          int64_t d, int32_t* expert_of, float* gate, float* y,
+                          const float* ln_gain, const float* ln_bias, float eps,
+                          const float* wg2, float* y2, int32_t* expert_of2, float* gate2,
+                          void* stream) {
+  using namespace qkv;
+  SA_REQUIRE(sa_fused_moe_linear_ok(d), SA_ERR_SHAPE, "%s: d=%lld unsupported", who, (long long)d);
+  SA_REQUIRE(M > 0 && M < (int64_t(1) << 31), SA_ERR_SHAPE, "%s: bad M", who);
+  SA_REQUIRE(residual != nullptr, SA_ERR_VALUE, "%s: residual required", who);
+  const bool lnr = y2 != nullptr;
+  SA_REQUIRE(!lnr || (ln_gain && ln_bias && wg2 && expert_of2 && gate2), SA_ERR_VALUE,
+             "%s: LayerNorm / router outputs need gain, bias, router weights and route arrays", who);
   cudaStream_t s = as_stream(stream);
   Params p;
   memset(&p, 0, sizeof(p));
@@ -637,18 +748,20 @@ extern "C" int sa_fused_moe_linear(const float* x, const float* wg, const void* 
   p.expert_of = expert_of;
   p.gate = gate;
   p.residual = residual;
-  CUtensorMap tmY;
-  memset(&tmY, 0, sizeof(tmY));
-  {
-    const cuuint64_t dims[2] = {cuuint64_t(d), cuuint64_t(M)};
-    const cuuint64_t strides[1] = {cuuint64_t(d) * 4};
-    const cuuint32_t box[2] = {32, 32};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode_tmap_tiled(
-        &tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, y, dims, strides, box, estr,
-        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    SA_REQUIRE(r == CUDA_SUCCESS, SA_ERR_CUDA, "sa_fused_moe_linear: tensor map failed (%d)", int(r));
+  p.ln_g = ln_gain;
+  p.ln_b = ln_bias;
+  p.ln_eps = eps;
+  p.wg2 = wg2;
+  p.expert_of2 = expert_of2;
+  p.gate2 = gate2;
+  CUtensorMap tmY, tmY2;
+  int r = encode_rows_map(&tmY, y, M, d);
+  SA_REQUIRE(r == CUDA_SUCCESS, SA_ERR_CUDA, "%s: tensor map failed (%d)", who, r);
+  if (lnr) {
+    r = encode_rows_map(&tmY2, y2, M, d);
+    SA_REQUIRE(r == CUDA_SUCCESS, SA_ERR_CUDA, "%s: tensor map for y2 failed (%d)", who, r);
+  } else {
+    tmY2 = tmY;
   }
   int sms = 0, dev = 0;
   cudaGetDevice(&dev);
@@ -656,15 +769,42 @@ extern "C" int sa_fused_moe_linear(const float* x, const float* wg, const void* 
   const int64_t tiles = (M + 127) / 128;
   const int grid = int(tiles < sms ? tiles : sms);
   if (d == 32) {
-    const int smem = int(Smem<32, 1>::TOTAL);
-    cudaFuncSetAttribute(qkv_kernel<32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    qkv_kernel<32, 1><<<grid, qkv::Cfg<32, 1>::THREADS, smem, s>>>(p, tmY);
+    if (lnr) launch_wo<32, true>(p, tmY, tmY2, grid, s);
+    else launch_wo<32, false>(p, tmY, tmY2, grid, s);
   } else {
-    const int smem = int(Smem<64, 1>::TOTAL);
-    cudaFuncSetAttribute(qkv_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    qkv_kernel<64, 1><<<grid, qkv::Cfg<64, 1>::THREADS, smem, s>>>(p, tmY);
+    if (lnr) launch_wo<64, true>(p, tmY, tmY2, grid, s);
+    else launch_wo<64, false>(p, tmY, tmY2, grid, s);
   }
   count_launch(1);
-  SA_LAUNCH_CHECK("sa_fused_moe_linear");
+  SA_LAUNCH_CHECK(who);
   return SA_OK;
+}
+
+}  // namespace
+
+extern "C" int sa_fused_moe_linear(const float* x, const float* wg, const void* w_dense,
+                                   const void* w_shift, const float* residual, float tie_thresh,
+                                   int64_t M, int64_t d, int32_t* expert_of, float* gate,
+                                   float* y, void* stream) {
+  return fused_moe_linear_impl("sa_fused_moe_linear", x, wg, w_dense, w_shift, residual,
+                               tie_thresh, M, d, expert_of, gate, y, nullptr, nullptr, 0.f,
+                               nullptr, nullptr, nullptr, nullptr, stream);
+}
+
+/* The same W_O kernel with the block's second LayerNorm and the MLP router in
+ * its epilogue (Block.forward, model.py:454-459: h = x + attn(LN1 x); the MLP
+ * input LN2(h) and its route, moe.py:81-92): y = h, y2 = LN2(h) and the MLP's
+ * (expert, gate) per row — what sa_ln_route computes from h, bit for bit,
+ * without re-reading h. */
+extern "C" int sa_fused_moe_linear_ln_route(const float* x, const float* wg, const void* w_dense,
+                                            const void* w_shift, const float* residual,
+                                            float tie_thresh, int64_t M, int64_t d,
+                                            int32_t* expert_of, float* gate, float* y,
+                                            const float* ln_gain, const float* ln_bias, float eps,
+                                            const float* wg2, float* y2, int32_t* expert_of2,
+                                            float* gate2, void* stream) {
+  SA_REQUIRE(y2 != nullptr, SA_ERR_VALUE, "sa_fused_moe_linear_ln_route: y2 required");
+  return fused_moe_linear_impl("sa_fused_moe_linear_ln_route", x, wg, w_dense, w_shift, residual,
+                               tie_thresh, M, d, expert_of, gate, y, ln_gain, ln_bias, eps, wg2,
+                               y2, expert_of2, gate2, stream);
 }

@@ -124,6 +124,8 @@ FUSE_QKV = os.environ.get("SA_FUSE_QKV", "1") == "1"
 
 
 FUSE_O = os.environ.get("SA_FUSE_O", "1") == "1"
+# the block's LN2 + MLP router in the W_O kernel's epilogue (sa_fused_moe_linear_ln_route)
+FUSE_LN2 = os.environ.get("SA_FUSE_LN2", "1") == "1"
 
 
 def _fused_o_ok(mod, x2) -> bool:
@@ -624,8 +626,10 @@ class Block:
         x2 = x.reshape(batch * n, d)
         fuse = FUSE_LN_ROUTE and d % 32 == 0 and d <= 256
         qkv = [self.attn.proj[k] for k in ("q", "k", "v")]
+        pre = None   # (LN2(h), MLP plan) from the W_O epilogue
         if self._fused_qkv_ok(d, n, qkv):
-            h = self._fused_attention(x2, batch, n, d, qkv).reshape(batch, n, d)
+            h, pre = self._fused_attention(x2, batch, n, d, qkv)
+            h = h.reshape(batch, n, d)
         elif fuse and all(isinstance(p, MoeModule) for p in qkv):
             y, plans = MOE.ln_route_plans(x2, self.ln1.gain.value, self.ln1.bias.value,
                                           [p.wg.value for p in qkv])
@@ -633,7 +637,9 @@ class Block:
         else:
             h = self.attn.forward(self.ln1.forward(x), residual=x)
         h2 = h.reshape(batch * n, d)
-        if fuse and isinstance(self.mlp, MoeModule):
+        if pre is not None:
+            y = self.mlp.forward(pre[0], residual=h2, plan=pre[1])
+        elif fuse and isinstance(self.mlp, MoeModule):
             flat, (plan,) = MOE.ln_route_plans(h2, self.ln2.gain.value, self.ln2.bias.value,
                                                [self.mlp.wg.value])
             y = self.mlp.forward(flat, residual=h2, plan=plan)
@@ -677,7 +683,24 @@ class Block:
             proj.last_plan = MOE.LazyDispatchPlan(expert_of[r], gate[r])
         dw = self.attn.dw.value if self.attn.dw is not None else None
         merged = A.binary_core_codes(cq, ck, gq, gk, v, batch, H, dw, A.EPS_NORM, "linear")
-        return self.attn.proj["o"].forward(merged, residual=x2)
+        o = self.attn.proj["o"]
+        if FUSE_LN2 and FUSE_LN_ROUTE and isinstance(self.mlp, MoeModule) and _fused_o_ok(o, merged):
+            # W_O + residual, then LN2 and the MLP router on the result, in one kernel
+            expert_of = torch.empty(M, dtype=torch.int32, device=dev)
+            gate_o = torch.empty(M, dtype=torch.float32, device=dev)
+            h = torch.empty_like(x2)
+            y2 = torch.empty_like(x2)
+            expert_of2 = torch.empty(M, dtype=torch.int32, device=dev)
+            gate2 = torch.empty(M, dtype=torch.float32, device=dev)
+            _lib.call("sa_fused_moe_linear_ln_route", _lib.ptr(merged), _lib.ptr(o.wg.value),
+                      _lib.ptr(o.experts[0].tc_pack(d)[0]), _lib.ptr(o.experts[1].tc_pack(d)[0]),
+                      _lib.ptr(x2), MOE.tie_threshold(), M, d, _lib.ptr(expert_of),
+                      _lib.ptr(gate_o), _lib.ptr(h), _lib.ptr(self.ln2.gain.value),
+                      _lib.ptr(self.ln2.bias.value), 1e-5, _lib.ptr(self.mlp.wg.value),
+                      _lib.ptr(y2), _lib.ptr(expert_of2), _lib.ptr(gate2), _stream())
+            o.last_plan = MOE.LazyDispatchPlan(expert_of, gate_o)
+            return h, (y2, MOE.LazyDispatchPlan(expert_of2, gate2))
+        return o.forward(merged, residual=x2), None
 
     def named_params(self, prefix):
         yield from self.ln1.named_params(prefix + ".ln1")

@@ -291,6 +291,39 @@ def test_fused_qkv_matches_unfused(golden, name):
     assert rel_err(got, fx["logits"]) < LOGIT_TOL
 
 
+@pytest.mark.parametrize("name", ["toy_c1_moe", "pvt_small", "pvt_b0_full"])
+def test_fused_wo_ln2_route_bit_identical(golden, name):
+    """sa_fused_moe_linear_ln_route (W_O + residual, then LN2 and the MLP
+    router in the same kernel's epilogue) reproduces sa_fused_moe_linear +
+    sa_ln_route exactly: identical logits and identical routes of every MoE
+    layer."""
+    from paper_2306_06446_b200 import model as MD
+    fx = golden(name)
+    spec = FIXTURES[name]()
+    m = MD.Network(spec)
+    b = min(int(fx["batch"]), 4)
+    images = fx["images"][:b] if "images" in fx else ops.rng(int(fx["images_seed"])).uniform(
+        0, 1, (b, spec["img"], spec["img"], 3)).astype(F32)
+    x = dev(images)
+    old = MD.FUSE_LN2
+    try:
+        MD.FUSE_LN2 = False
+        ref = host(m.forward(x))
+        plans_ref = [mod.last_plan.expert_of.copy() for _, mod in m.moe_modules()]
+        MD.FUSE_LN2 = True
+        got = host(m.forward(x))
+        plans = [mod.last_plan.expert_of.copy() for _, mod in m.moe_modules()]
+        perms = [(mod.last_plan.expert_of.copy(), mod.last_plan.index_of) for _, mod in m.moe_modules()]
+    finally:
+        MD.FUSE_LN2 = old
+    assert np.array_equal(got, ref)
+    for a, c in zip(plans, plans_ref):
+        assert np.array_equal(a, c)
+    for e, ix in perms:   # the lazily built stable partition of the fused routes
+        assert np.array_equal(ix[0], np.flatnonzero(e == 0))
+        assert np.array_equal(ix[1], np.flatnonzero(e == 1))
+
+
 @pytest.mark.parametrize("name", ["pvt_small", "pvt_b0_full"])
 def test_fused_embed_layernorm_bit_identical(golden, name):
     """sa_tc_patch_embed_ln (embedding LayerNorm in the patch GEMM's epilogue)
