@@ -65,7 +65,7 @@ struct Params {
 
 struct Smem {
   // byte offsets into the dynamic shared memory carve-out
-  uint32_t v, cq, ck, part, cntp, cntw, tab, tcb, mt, bar, total;
+  uint32_t v, cq, ck, part, cntp, cntw, tab, tcb, mt, cb, bar, total;
 };
 
 __host__ __device__ inline Smem smem_layout(int d, int heads, int side, int band_rows) {
@@ -93,8 +93,10 @@ __host__ __device__ inline Smem smem_layout(int d, int heads, int side, int band
   o += heads * 4 * 256 * 4;
   s.mt = o;                                    // [256][8] float: 0/1 masks of a code byte
   o += 256 * 8 * 4;
-  s.bar = o;                                   // one mbarrier per smem row (+ codes)
-  o += (band_rows + 3) * 8;
+  s.cb = o;                                    // [kMaxCluster][DK] int: pushed band counts
+  o += kMaxCluster * DK * 4;
+  s.bar = o;                                   // one mbarrier per smem row (+ codes), then
+  o += (band_rows + 3) * 8 + 16;               // the two exchange barriers (xbar, tbar)
   s.total = o;
   return s;
 }
@@ -181,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
                          (reinterpret_cast<uintptr_t>(p.ck) & 15) == 0 &&
                          (su32(cqs) & 15u) == 0 && (su32(cks) & 15u) == 0;
   if (tid == 0) {
-    for (int R = 0; R < BR + 3; ++R)
+    for (int R = 0; R < BR + 5; ++R)   // rows, codes, xbar, tbar
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + R)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (code_bulk) {
@@ -220,6 +222,10 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
   for (int i = tid; i < 256 * 8; i += kThreads)          // byte → 8 masks
     mt[i] = ((i >> 3) >> (i & 7)) & 1 ? 1.0f : 0.0f;
   __syncthreads();  // barrier init, codes, masks visible
+  // push exchange (below): every CTA's exchange barriers must be initialised
+  // before a peer's first remote store; the matching wait sits just before it
+  const bool push = HEADS == 1 && (kMaxCluster % CL) == 0;
+  if (push) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   auto wait_row = [&](int R) {
     asm volatile(
         "{\n\t.reg .pred q;\n\tW_%=:\n\t"
@@ -352,6 +358,113 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
   }
 
   // ---- 3. exchange band partials across the cluster (rank order) -------------
+  if (push) {
+    // Push form (one head per CTA, CL | 8): CTA o owns nibble groups
+    // [o·G, o·G + G) (G = 8 / CL, 4 kv rows each). Every CTA stores its band
+    // partial rows into the owners' receive slots and its counts into every
+    // CTA (st.async, completing on the receiver's xbar); each owner sums its
+    // rows in rank order, builds its groups' nibble tables and stores them
+    // into every peer's table region (completing on tbar). No cluster-wide
+    // barrier and no remote loads: each CTA only waits for the bytes it needs.
+    const int G = kMaxCluster / CL;
+    uint64_t* xbar = bar + BR + 3;
+    uint64_t* tbar = bar + BR + 4;
+    float* rbuf = tcb;                                   // [CL][G][4][DK] (tcb is built after)
+    int* cbuf = reinterpret_cast<int*>(smem + L.cb);     // [CL][DK]
+    if (tid == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(xbar)),
+                   "r"(uint32_t(CL * G * 4 * DK * 4 + CL * DK * 4))
+                   : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(tbar)),
+                   "r"(uint32_t((CL - 1) * G * 16 * DK * 4))
+                   : "memory");
+    }
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    auto remote = [&](const void* local, int r) {
+      uint32_t a;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(su32(local)), "r"(r));
+      return a;
+    };
+    auto st_async4 = [&](uint32_t raddr, uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3,
+                         uint32_t rbar) {
+      asm volatile(
+          "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+              raddr),
+          "r"(x0), "r"(x1), "r"(x2), "r"(x3), "r"(rbar)
+          : "memory");
+    };
+    {   // thread → kv row tid / 8, columns 4 (tid % 8) .. + 3 of this band's partial
+      const int row = tid >> 3, q = tid & 7;
+      const uint4 v4 = *reinterpret_cast<const uint4*>(part + row * DK + 4 * q);
+      const int grp = row >> 2, o = grp / G, gi = grp - o * G;
+      const float* slot = rbuf + ((rank * G + gi) * 4 + (row & 3)) * DK + 4 * q;
+      st_async4(remote(slot, o), v4.x, v4.y, v4.z, v4.w, remote(xbar, o));
+      if (tid < CL * (DK / 4)) {   // counts → every CTA: thread → (rank dr, 4 counts)
+        const int dr = tid / (DK / 4), k = tid % (DK / 4);
+        const uint4 c4 = *reinterpret_cast<const uint4*>(cntp + 4 * k);
+        st_async4(remote(cbuf + rank * DK + 4 * k, dr), c4.x, c4.y, c4.z, c4.w, remote(xbar, dr));
+      }
+    }
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tWX_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 q, [%0], 0;\n\t"
+        "@!q bra WX_%=;\n\t}" ::"r"(su32(xbar))
+        : "memory");
+    if (tid < G * DK) {   // owner: thread = (own group, column)
+      const float g = __ldg(p.gk + b * H + hz);
+      const int gi = tid / DK, c = tid % DK, grp = rank * G + gi;
+      float row[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int r = 0; r < CL; ++r) {   // rank order, as the pull form
+        const float* pr = rbuf + ((r * G + gi) * 4) * DK + c;
+        row[0] += pr[0];
+        row[1] += pr[DK];
+        row[2] += pr[2 * DK];
+        row[3] += pr[3 * DK];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) row[i] = __fmul_rn(row[i], g);   // not contracted into the table sums
+      float val[16];
+      val[0] = 0.f;
+      val[1] = row[0];
+      val[2] = row[1];
+      val[4] = row[2];
+      val[8] = row[3];
+#pragma unroll
+      for (int m = 3; m < 16; ++m)
+        if (m & (m - 1)) val[m] = val[m & (m - 1)] + val[m & -m];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) tab[(grp * 16 + m) * DK + c] = val[m];
+    }
+    if (tid < DK) {   // total counts (rank order)
+      int sc = 0;
+      for (int r = 0; r < CL; ++r) sc += cbuf[r * DK + tid];
+      cntw[tid] = sc;
+    }
+    __syncthreads();
+    // this CTA's table groups → every peer (G × 16 × DK floats, contiguous)
+    const float* mine = tab + rank * G * 16 * DK;
+    for (int i = tid; i < (CL - 1) * G * 4 * DK; i += kThreads) {
+      const int pr = i / (G * 4 * DK), k = i - pr * (G * 4 * DK);
+      const int dr = pr < rank ? pr : pr + 1;
+      const uint4 v4 = *reinterpret_cast<const uint4*>(mine + 4 * k);
+      st_async4(remote(mine + 4 * k, dr), v4.x, v4.y, v4.z, v4.w, remote(tbar, dr));
+    }
+    // byte tables of the counts as exact floats: tcb[g][m] = sum_{i in m} cnt[8g+i]
+    for (int e = tid; e < 4 * 256; e += kThreads) {
+      const int g8 = e >> 8, m = e & 255;
+      int sc = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if ((m >> i) & 1) sc += cntw[8 * g8 + i];
+      tcb[e] = float(sc);
+    }
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tWT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 q, [%0], 0;\n\t"
+        "@!q bra WT_%=;\n\t}" ::"r"(su32(tbar))
+        : "memory");
+    __syncthreads();
+  } else {
   cluster.sync();
 #pragma unroll 1
   for (int h = 0; h < HEADS; ++h) {
@@ -413,6 +526,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
   // does not touch), so an early CTA goes straight on to its outputs
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 
+  }
   // ---- 4. pass 2: outputs ------------------------------------------------------
   wait_row(0);
   wait_row(BR + 1);
@@ -509,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
       *reinterpret_cast<float4*>(ob + size_t(t) * ld) = o;
     }
   }
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (!push) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------

@@ -33,7 +33,11 @@ def timed(fn, reps=10):
 
 MODES = [int(a) for a in sys.argv[1:]] or [0, 1, 2, 4, 5, 32, 33, 36, 37]
 g = np.random.default_rng(0)
-for label, d, hidden, M, moe in (("s3-moe", 160, 640, 50176, True), ("s4-dense", 256, 1024, 12544, False)):
+SHAPES = (("s3-moe", 160, 640, 50176, True), ("s4-dense", 256, 1024, 12544, False))
+if os.environ.get("GEMM_SHAPES"):   # e.g. "deit-moe,192,768,100864,1"
+    SHAPES = tuple((t.split(",")[0], *[int(v) for v in t.split(",")[1:4]], t.split(",")[4] == "1")
+                   for t in os.environ["GEMM_SHAPES"].split(";"))
+for label, d, hidden, M, moe in SHAPES:
     w1 = (g.standard_normal((d, hidden)) / np.sqrt(d)).astype(np.float32)
     w2 = (g.standard_normal((hidden, d)) / np.sqrt(hidden)).astype(np.float32)
     x = torch.from_numpy(g.standard_normal((M, d)).astype(np.float32)).cuda()
