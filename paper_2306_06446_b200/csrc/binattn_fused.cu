@@ -61,6 +61,7 @@ struct Params {
   int n, d, heads, side, rows_total, band_rows;
   float eps;
   int ld;     // global row stride of V / out in floats (= model dim); head = blockIdx.z
+  int pull;   // debug builds: 1 = the pull exchange (cluster barrier + DSMEM loads)
 };
 
 struct Smem {
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
   __syncthreads();  // barrier init, codes, masks visible
   // push exchange (below): every CTA's exchange barriers must be initialised
   // before a peer's first remote store; the matching wait sits just before it
-  const bool push = HEADS == 1 && (kMaxCluster % CL) == 0;
+  const bool push = HEADS == 1 && (kMaxCluster % CL) == 0 && !p.pull;
   if (push) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   auto wait_row = [&](int R) {
     asm volatile(
@@ -1111,6 +1112,8 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_out_kernel(Params p, cons
 // Host side: picks the cluster geometry and launches; returns SA_ERR_VALUE when
 // the shape is outside this kernel's envelope (the caller then uses the
 // multi-kernel path of binattn.cu).
+SA_DEBUG_SWITCH(int, g_attn_pull, 0, sa_debug_attn_pull)
+
 int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq, const float* gk,
                          const float* v, const float* dw, float* out, int64_t B, int64_t n,
                          int64_t d, int64_t heads, float eps, cudaStream_t s) {
@@ -1130,7 +1133,8 @@ int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
   const Smem L = smem_layout(DK, 1, side, br);
   if (L.total > 220 * 1024) return SA_ERR_VALUE;
   if (br * side > 32 * 63) return SA_ERR_VALUE;   // bit-sliced counters hold 63 tokens/lane
-  Params p{cq, ck, gq, gk, v, dw, out, int(n), DK, int(heads), side, rows_total, br, eps, int(d)};
+  Params p{cq, ck, gq, gk, v, dw, out, int(n), DK, int(heads), side, rows_total, br, eps, int(d),
+           g_attn_pull};
   void (*kern)(Params, CUtensorMap) = nullptr;
   switch (side) {
     case 56: kern = binattn_fused_kernel<DK, 56>; break;
@@ -1216,7 +1220,8 @@ int binattn_split_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
   const int g1 = g_kv_persistent ? (items < sms ? items : sms) : items;
   const KvSmem L = kv_smem_layout(side, br, g1 >= items ? 1 : 2);
   if (L.total > 220 * 1024) return SA_ERR_VALUE;
-  Params p{cq, ck, gq, gk, v, dw, out, int(n), DK, int(heads), side, rows_total, br, eps, int(d)};
+  Params p{cq, ck, gq, gk, v, dw, out, int(n), DK, int(heads), side, rows_total, br, eps, int(d),
+           g_attn_pull};
   float* part = static_cast<float*>(ws);
   int* cntp = reinterpret_cast<int*>(part + size_t(B * heads * cl) * DK * DK);
   if (br > kMaxBandRows) return SA_ERR_VALUE;
