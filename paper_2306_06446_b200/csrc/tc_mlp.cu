@@ -101,11 +101,16 @@ struct Layout {
   static constexpr int KC1 = D / 32;                          // fc1 K stages
   static constexpr int NA = D == 32 ? 2 : 1;                  // A1 buffers (TMEM)
   static constexpr int NB = W ? 2 : 3;                        // acc1 / A2 buffers (TMEM)
-  static constexpr uint32_t BUFC = HC + HC / 2;               // acc1 (HC fp32) | A2 (3 planes)
+  // wide: the A1 lo plane lives in shared memory (ss-form MMAs), hi / mid in
+  // TMEM; d <= 160 also concatenates the dense fc1 B planes along N (3 MMAs
+  // per K step into three 32-column partial sums, added by the GELU warps)
+  static constexpr bool CATW = W && D <= 160;
+  static constexpr int A1P = W ? 2 : 3;                       // A1 planes in TMEM
+  static constexpr uint32_t BUFC = W ? (CATW ? 96 : 48) : 96; // acc1 | A2 (3 planes)
   static constexpr int NO = W ? 1 : 2;                        // acc2 buffers
   static constexpr int GPC = W ? 8 : kGeluPerChunk;           // GELU warps per chunk
   static constexpr bool CAT = D == 32;                        // N-concatenated dense fc2
-  static constexpr int NW = W ? 3 : 4;                        // ring slots (RES = false)
+  static constexpr int NW = W ? (D == 128 ? 3 : 2) : 4;       // ring slots (RES = false)
   static constexpr uint32_t W1C = KC1 * 3 * (HC * 32 * 2);    // dense W1 chunk bytes
   static constexpr uint32_t W2C = (HC / 32) * 3 * (D * 32 * 2);
   static constexpr uint32_t RW1 = (kResHidden / HC) * W1C;    // resident dense W1
@@ -114,7 +119,9 @@ struct Layout {
   __device__ static constexpr uint32_t r_w1(int e) { return e ? RW1 : 0u; }
   __device__ static constexpr uint32_t r_w2(int e) { return RW1 + RW1 / 3 + (e ? RW2 : 0u); }
   static constexpr uint32_t WBYTES = RES ? (RW1 + RW1 / 3 + RW2 + RW2 / 3) : NW * (W1C + W2C);
-  static constexpr uint32_t OFF_XB = WBYTES;
+  static constexpr uint32_t OFF_ALO = WBYTES;                 // wide: [KC1][128 x 32] bf16 lo plane
+  static constexpr uint32_t ALO = W ? KC1 * kBM * 32 * 2 : 0;
+  static constexpr uint32_t OFF_XB = OFF_ALO + ALO;
   static constexpr uint32_t XB = Roles<D>::NPW * 32 * kXPitch * 4;   // producer transpose slots
   static constexpr uint32_t OFF_BAR = OFF_XB + XB;
   // barriers: a1 full/empty[NA], w1 full/empty[NW], w2 full/empty[NW],
@@ -126,7 +133,7 @@ struct Layout {
   static constexpr uint32_t T_ACC2 = NB * BUFC;
   static constexpr uint32_t ACC2C = W ? D : 64;
   static constexpr uint32_t T_A1 = T_ACC2 + NO * ACC2C;
-  static constexpr uint32_t A1COLS = KC1 * 3 * kPlaneCols;
+  static constexpr uint32_t A1COLS = KC1 * A1P * kPlaneCols;
   static constexpr uint32_t TCOLS = 512;
   static_assert(T_A1 + NA * A1COLS <= TCOLS, "TMEM budget");
   static_assert(TOTAL <= 232448, "shared memory budget");
@@ -202,6 +209,56 @@ __device__ __forceinline__ void mma_cat4(uint32_t d, uint32_t ah, uint32_t am, u
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %5, %7, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %6, 1;\n\t}" ::"r"(d),
       "r"(ah), "r"(am), "r"(al), "l"(b0), "l"(b2), "r"(id64), "r"(id32), "r"(acc)
+      : "memory");
+}
+
+// wide form, A lo plane from shared memory (descriptor), hi / mid from TMEM.
+// shift: lo·w, mid·w, hi·w (the order of mma3)
+__device__ __forceinline__ void mma3_lo(uint32_t d, uint32_t ah, uint32_t am, uint64_t alo, uint64_t b,
+                                        uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %4, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %4, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, 1;\n\t}" ::"r"(d),
+      "r"(ah), "r"(am), "l"(alo), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+// dense, six products in mma6's order (lo·hi from shared memory)
+__device__ __forceinline__ void mma6_lo(uint32_t d, uint32_t ah, uint32_t am, uint64_t alo, uint64_t b0,
+                                        uint64_t b1, uint64_t b2, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %8, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %4, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %5, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %6, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %4, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %5, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %7, 1;\n\t}" ::"r"(d),
+      "r"(ah), "r"(am), "l"(alo), "l"(b0), "l"(b1), "l"(b2), "r"(id), "r"(acc)
+      : "memory");
+}
+// dense, B planes concatenated along N (rows 0-31 w_hi, 32-63 w_mid, 64-95
+// w_lo): A_hi·[w_hi|w_mid|w_lo] → columns [0, 96), A_mid·[w_hi|w_mid] →
+// [32, 96), A_lo·w_hi → [64, 96): column block j holds the products of
+// combined order j (hh; hm + mh; hl + mm + lh)
+__device__ __forceinline__ void mma_cat3(uint32_t d, uint32_t ah, uint32_t am, uint64_t alo,
+                                         uint64_t b0, uint32_t id96, uint32_t id64, uint32_t id32,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b32 d1, d2;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %8, 0;\n\t"
+      "add.u32 d1, %0, 32;\n\t"
+      "add.u32 d2, %0, 64;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], [%2], %4, %6, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d2], %3, %4, %7, 1;\n\t}" ::"r"(d),
+      "r"(ah), "r"(am), "l"(alo), "l"(b0), "r"(id96), "r"(id64), "r"(id32), "r"(acc)
       : "memory");
 }
 
@@ -415,13 +472,22 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
               lp[2 * t] = bf2_bits(a.l);
               lp[2 * t + 1] = bf2_bits(b.l);
             }
-            const uint32_t col = a1 + kc * 3 * kPlaneCols + sub * 8;
+            const uint32_t col = a1 + kc * L::A1P * kPlaneCols + sub * 8;
             tmem_st8(col, hp);
             tmem_st8(col + kPlaneCols, mp);
-            tmem_st8(col + 2 * kPlaneCols, lp);
+            if constexpr (L::W) {   // lo plane → shared memory, UMMA canonical K-major layout
+              uint8_t* lo = smem + L::OFF_ALO + kc * (kBM * 32 * 2);
+              *reinterpret_cast<uint4*>(lo + plane_offset(ptid, 16 * sub)) =
+                  make_uint4(lp[0], lp[1], lp[2], lp[3]);
+              *reinterpret_cast<uint4*>(lo + plane_offset(ptid, 16 * sub + 8)) =
+                  make_uint4(lp[4], lp[5], lp[6], lp[7]);
+            } else {
+              tmem_st8(col + 2 * kPlaneCols, lp);
+            }
           }
         }
       }
+      if constexpr (L::W) fence_proxy_async_smem();   // the lo plane is read by the tensor cores
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -503,6 +569,28 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
         const uint32_t d1 = tmem + L::T_BUF + uint32_t(b) * L::BUFC;
         const uint64_t bd0 = smem_desc(RES ? wrow : sbase + uint32_t(s) * L::W1C);
         if (!(kDbg && (p.dbg & 4))) {
+          if constexpr (L::W) {
+            constexpr uint32_t id96 = idesc_bf16_m128(96), id64 = idesc_bf16_m128(64);
+            const uint32_t alo0 = smem_u32(smem + L::OFF_ALO);
+#pragma unroll
+            for (int kc = 0; kc < L::KC1; ++kc)
+#pragma unroll
+              for (int ks = 0; ks < 2; ++ks) {
+                const uint32_t ah = a1 + kc * 2 * kPlaneCols + ks * 8;
+                const uint64_t alo = smem_desc(alo0 + kc * (kBM * 32 * 2) + ks * 256);
+                const uint32_t acc = (kc | ks) ? 1u : 0u;
+                if (shift) {
+                  mma3_lo(d1, ah, ah + kPlaneCols, alo,
+                          bd0 + uint64_t((kc * (HC * 64) + ks * 256) >> 4), id1, acc);
+                } else {
+                  const uint64_t bd = bd0 + uint64_t((kc * (3 * HC * 64) + ks * 256) >> 4);
+                  if (L::CATW)
+                    mma_cat3(d1, ah, ah + kPlaneCols, alo, bd, id96, id64, id1, acc);
+                  else
+                    mma6_lo(d1, ah, ah + kPlaneCols, alo, bd, bd + BP, bd + 2 * BP, id1, acc);
+                }
+              }
+          } else {
 #pragma unroll
           for (int kc = 0; kc < L::KC1; ++kc)
 #pragma unroll
@@ -517,6 +605,7 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
                 mma6(d1, ah, ah + kPlaneCols, ah + 2 * kPlaneCols, bd, bd + BP, bd + 2 * BP, id1, acc);
               }
             }
+          }
         }
         commit_w(&h_full[b]);
         TL(1, qq);
@@ -564,7 +653,7 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
             const uint32_t ah = kGeluAlt ? bb + (ks >> 1) * 32u + (ks & 1) * 8u : bb + ks * 16u;
             const uint32_t am = ah + (kGeluAlt ? 16u : 8u);
             const uint32_t al = kGeluAlt ? bb + 64u + (ks >> 1) * 16u + (ks & 1) * 8u
-                                         : bb + uint32_t(HC) + ks * 8u;
+                                : (L::CATW ? bb + 32u + ks * 16u : bb + uint32_t(HC) + ks * 8u);
             const uint32_t acc = ks ? 1u : a0;
             if (shift) {
               mma3(d2, ah, am, al, bd0 + uint64_t(((ks >> 1) * (D * 64) + (ks & 1) * 256) >> 4),
@@ -657,51 +746,125 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
       if (mlp_tile(p, c0, m, e, r0, r1)) ++nt;
     }
     const int total_q = nt * nchunk;
-    for (int q = gs; q < total_q; q += QS) {
-      const int b = q % L::NB;
-      const uint32_t ph = uint32_t(q / L::NB) & 1u;
-      PW(S_HF, &h_full[b], ph);             // fc1(q) done
-      if (warp == 0) TL(2, q);
-      tc_fence_after();
-      const uint32_t bb = lb + uint32_t(b) * L::BUFC;
-      if (!(kDbg && (p.dbg & 1))) {
-        float r[16];
-        if (kDbg && (p.dbg & 128)) {   // debug: no TMEM traffic (synthetic inputs, no stores)
-#pragma unroll
-          for (int t = 0; t < 16; ++t) r[t] = float(t + q) * 0.01f;
-        } else {
-          tmem_ld16(bb + uint32_t(16 * k), r);
-        }
-        uint32_t hp[8], mp[8], lp[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          float g0 = r[2 * t], g1 = r[2 * t + 1];
-          if (kDbg && (p.dbg & 64)) {   // debug: no GELU math
-          } else if (t < NF) {
-            gelu_pair<true>(g0, g1);
+    if constexpr (L::W) {
+      // chunk q (global chunk index of this CTA); cat3: dense wide tile whose
+      // acc1 holds three partial sums (mma_cat3)
+      auto gelu_chunk = [&](int q, int b, uint32_t ph, bool cat3) {
+        PW(S_HF, &h_full[b], ph);             // fc1(q) done
+        if (warp == 0) TL(2, q);
+        tc_fence_after();
+        const uint32_t bb = lb + uint32_t(b) * L::BUFC;
+        if (!(kDbg && (p.dbg & 1))) {
+          float r[16];
+          if (kDbg && (p.dbg & 128)) {   // debug: no TMEM traffic (synthetic inputs, no stores)
+  #pragma unroll
+            for (int t = 0; t < 16; ++t) r[t] = float(t + q) * 0.01f;
+          } else if (L::CATW && cat3) {
+            float r1[16], r2[16];
+            tmem_ld16(bb + uint32_t(16 * k), r);
+            tmem_ld16(bb + uint32_t(32 + 16 * k), r1);
+            tmem_ld16(bb + uint32_t(64 + 16 * k), r2);
+  #pragma unroll
+            for (int t = 0; t < 16; ++t) r[t] = r[t] + (r1[t] + r2[t]);   // hh + (hm+mh + hl+mm+lh)
           } else {
-            gelu_pair<false>(g0, g1);
+            tmem_ld16(bb + uint32_t(16 * k), r);
           }
-          const Split3 sp = split3x2(g0, g1);
-          hp[t] = bf2_bits(sp.h);
-          mp[t] = bf2_bits(sp.m);
-          lp[t] = bf2_bits(sp.l);
+          uint32_t hp[8], mp[8], lp[8];
+  #pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            float g0 = r[2 * t], g1 = r[2 * t + 1];
+            if (kDbg && (p.dbg & 64)) {   // debug: no GELU math
+            } else if (t < NF) {
+              gelu_pair<true>(g0, g1);
+            } else {
+              gelu_pair<false>(g0, g1);
+            }
+            const Split3 sp = split3x2(g0, g1);
+            hp[t] = bf2_bits(sp.h);
+            mp[t] = bf2_bits(sp.m);
+            lp[t] = bf2_bits(sp.l);
+          }
+          if (kDbg && (p.dbg & 128)) {
+            if (hp[0] == 0x12345u && mp[1] == 7u && lp[2] == 9u) mbar_arrive(&h_empty[b]);   // keep the math live
+          } else {
+            tmem_st8(bb + uint32_t(16 * k), hp);
+            tmem_st8(bb + uint32_t(16 * k + 8), mp);
+            // lo: over this warp's own consumed columns of block 1 (CATW), else the free columns
+            tmem_st8(bb + uint32_t(L::CATW ? 32 + 16 * k : HC + 8 * k), lp);
+            tmem_st_wait();
+          }
         }
-        if (kDbg && (p.dbg & 128)) {
-          if (hp[0] == 0x12345u && mp[1] == 7u && lp[2] == 9u) mbar_arrive(&h_empty[b]);   // keep the math live
-        } else {
-          tmem_st8(bb + uint32_t(16 * k), hp);
-          tmem_st8(bb + uint32_t(16 * k + 8), mp);
-          tmem_st8(bb + uint32_t(HC + 8 * k), lp);
-          tmem_st_wait();
-        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&h_empty[b]);
+        if (warp == 0) TL(3, q);
+        if (warp == kGelu - 1) TL(6, q);
+      };
+      int q = 0;
+      for (int64_t m = blockIdx.x; m < ntile; m += gridDim.x) {
+        int e;
+        int64_t r0, r1;
+        if (!mlp_tile(p, c0, m, e, r0, r1)) continue;
+        const bool dense = (e ? p.np1 : p.np0) == 3;
+        for (int c = 0; c < nchunk; ++c, ++q)
+          if ((q % QS) == gs) gelu_chunk(q, q % L::NB, uint32_t(q / L::NB) & 1u, dense);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&h_empty[b]);
-      if (warp == 0) TL(3, q);
-      if (warp == kGelu - 1) TL(6, q);
+    } else {
+      for (int q = 0; q < total_q; ++q) {
+        const int b = q % L::NB;
+        const uint32_t ph = uint32_t(q / L::NB) & 1u;
+        PW(S_HF, &h_full[b], ph);             // fc1(q) done
+        if (warp == 0) TL(2, q);
+        tc_fence_after();
+        const uint32_t bb = lb + uint32_t(b) * L::BUFC;
+        if (!(kDbg && (p.dbg & 1))) {
+          float r[16];
+          if (kDbg && (p.dbg & 128)) {   // debug: no TMEM traffic (synthetic inputs, no stores)
+  #pragma unroll
+            for (int t = 0; t < 16; ++t) r[t] = float(t + q) * 0.01f;
+          } else if (false) {
+            float r1[16], r2[16];
+            tmem_ld16(bb + uint32_t(16 * k), r);
+            tmem_ld16(bb + uint32_t(32 + 16 * k), r1);
+            tmem_ld16(bb + uint32_t(64 + 16 * k), r2);
+  #pragma unroll
+            for (int t = 0; t < 16; ++t) r[t] = r[t] + (r1[t] + r2[t]);   // hh + (hm+mh + hl+mm+lh)
+          } else {
+            tmem_ld16(bb + uint32_t(16 * k), r);
+          }
+          uint32_t hp[8], mp[8], lp[8];
+  #pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            float g0 = r[2 * t], g1 = r[2 * t + 1];
+            if (kDbg && (p.dbg & 64)) {   // debug: no GELU math
+            } else if (t < NF) {
+              gelu_pair<true>(g0, g1);
+            } else {
+              gelu_pair<false>(g0, g1);
+            }
+            const Split3 sp = split3x2(g0, g1);
+            hp[t] = bf2_bits(sp.h);
+            mp[t] = bf2_bits(sp.m);
+            lp[t] = bf2_bits(sp.l);
+          }
+          if (kDbg && (p.dbg & 128)) {
+            if (hp[0] == 0x12345u && mp[1] == 7u && lp[2] == 9u) mbar_arrive(&h_empty[b]);   // keep the math live
+          } else {
+            tmem_st8(bb + uint32_t(16 * k), hp);
+            tmem_st8(bb + uint32_t(16 * k + 8), mp);
+            // lo: over this warp's own consumed columns of block 1 (CATW), else the free columns
+            tmem_st8(bb + uint32_t(L::CATW ? 32 + 16 * k : HC + 8 * k), lp);
+            tmem_st_wait();
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&h_empty[b]);
+        if (warp == 0) TL(3, q);
+        if (warp == kGelu - 1) TL(6, q);
+      }
     }
+    (void)total_q;
   }
 #ifdef SA_DEBUG
   if (p.prof && lane == 0) {
@@ -796,6 +959,8 @@ using namespace sa;
  * hidden chunk: 64 for d = 32 / 64, 32 for d = 128 / 160) and W2 packed with
  * bn = d; see sa_weight_pack. */
 extern "C" int sa_tc_fused_mlp_chunk(int64_t d) {
+  // (d = 192 builds and is exact, but fc1's 72 N = 32 MMAs per chunk make it
+  // slower than the two-GEMM path: 391 vs 353 us at the DeiT-T shape)
   return (d == 32 || d == 64) ? 64 : (d == 128 || d == 160) ? 32 : 0;
 }
 

@@ -263,7 +263,8 @@ extern "C" int sa_weight_pack(const void* w, int w_kind, int64_t K, int64_t N, i
                               void* out, void* stream) {
   SA_REQUIRE(w_kind == SA_W_DENSE || w_kind == SA_W_SHIFT, SA_ERR_VALUE,
              "sa_weight_pack: unknown weight kind %d", w_kind);
-  SA_REQUIRE(tc_tile_n_ok(bn), SA_ERR_VALUE, "sa_weight_pack: tile N=%d unsupported", bn);
+  // GEMM tile widths, plus d = 192 (the wide fused MLP reads W2 packed with bn = d)
+  SA_REQUIRE(tc_tile_n_ok(bn) || bn == 192, SA_ERR_VALUE, "sa_weight_pack: tile N=%d unsupported", bn);
   SA_REQUIRE(K > 0 && N > 0, SA_ERR_SHAPE, "sa_weight_pack: empty weight");
   const int kchunks = int(cdiv(K, tc::kBK));
   const int np = nplanes_of(w_kind);

@@ -331,7 +331,7 @@ class Mlp:
         res = residual.reshape(y.shape) if residual is not None else None
         if fused_mlp_ok(d, hidden) and k1 == k2:
             p1, _, _ = self.fc1.tc_pack(fused_mlp_w1_bn(d))
-            p2, _, _ = self.fc2.tc_pack()
+            p2, _, _ = self.fc2.tc_pack(d)
             _lib.call("sa_tc_mlp_fused", _lib.ptr(x2), _lib.ptr(p1), k1, _lib.ptr(p2), k2,
                       _lib.ptr(y), M, d, hidden, _lib.ptr(res), _stream())
             return y.reshape(*lead, self.fc2.out_dim)
@@ -395,9 +395,9 @@ def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None):
         y = torch.empty((M, d), dtype=torch.float32, device=x.device)
         if fused_mlp_ok(d, hidden):
             p1d, _, _ = e0.fc1.tc_pack(fused_mlp_w1_bn(d))
-            p2d, _, _ = e0.fc2.tc_pack()
+            p2d, _, _ = e0.fc2.tc_pack(d)
             p1s, _, _ = e1.fc1.tc_pack(fused_mlp_w1_bn(d))
-            p2s, _, _ = e1.fc2.tc_pack()
+            p2s, _, _ = e1.fc2.tc_pack(d)
             _lib.call("sa_tc_moe_mlp_fused", _lib.ptr(x), _lib.ptr(plan.perm_dev),
                       _lib.ptr(plan.counts_dev), _lib.ptr(plan.gate_dev), _lib.ptr(p1d),
                       _lib.ptr(p2d), _lib.ptr(p1s), _lib.ptr(p2s), _lib.ptr(y), _lib.ptr(res),

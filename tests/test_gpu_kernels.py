@@ -362,7 +362,8 @@ def test_moe_module_vs_oracle(M, d, hidden):
     # wide form (d = 128 / 160: hidden chunks of 32, single acc2, streamed weights)
     (5, 160, 640, 1.0, None), (1000, 160, 640, 1.0, None), (777, 160, 640, 6.0, None),
     (1500, 160, 640, 1.0, 0), (1500, 160, 640, 1.0, 1), (3001, 128, 512, 1.0, None),
-    (700, 128, 1024, 1.0, None)])
+    (700, 128, 1024, 1.0, None), (2000, 192, 768, 1.0, None), (333, 192, 768, 6.0, None),
+    (1200, 192, 768, 1.0, 0), (1200, 192, 768, 1.0, 1)])
 def test_fused_moe_mlp_edges(M, d, hidden, scale, force):
     """Fused MoE MLP kernel: ragged and tiny M, resident (d = 32, hidden <= 256)
     and streamed weights, hidden pre-activations spanning the GELU's saturated
