@@ -227,6 +227,14 @@ int sa_tc_moe_mlp_fused(const float* x, const int32_t* perm, const int32_t* coun
                         const void* w1_shift, const void* w2_shift, float* y,
                         const float* residual, int64_t M, int64_t d, int64_t hidden,
                         void* stream);
+/* sa_tc_moe_mlp_fused with the stage's final LayerNorm (model.py:565-577,
+ * tensor.py:114-128) on the output rows in the same kernel, bit-identical to
+ * sa_tc_moe_mlp_fused + sa_layernorm; d = 32. */
+int sa_tc_moe_mlp_fused_ln(const float* x, const int32_t* perm, const int32_t* counts,
+                           const float* gate, const void* w1_dense, const void* w2_dense,
+                           const void* w1_shift, const void* w2_shift, float* y,
+                           const float* residual, int64_t M, int64_t d, int64_t hidden,
+                           const float* ln_gain, const float* ln_bias, float eps, void* stream);
 int sa_tc_mlp_fused(const float* x, const void* w1pack, int w1_kind, const void* w2pack,
                     int w2_kind, float* y, int64_t M, int64_t d, int64_t hidden,
                     const float* residual, void* stream);

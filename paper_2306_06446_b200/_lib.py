@@ -91,6 +91,8 @@ _SIGS = {
     "sa_tc_fused_mlp_chunk": (_I32, [_I64]),
     "sa_tc_moe_mlp_fused": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64,
                                    _P]),
+    "sa_tc_moe_mlp_fused_ln": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64,
+                                      _P, _P, _F32, _P]),
     "sa_tc_mlp_fused": (_I32, [_P, _P, _I32, _P, _I32, _P, _I64, _I64, _I64, _P, _P]),
     "sa_moe_partition_workspace": (_SZ, [_I64]),
     "sa_moe_partition": (_I32, [_P, _I64, _P, _P, _P, _SZ, _P]),

@@ -51,6 +51,12 @@ constexpr uint32_t kPlaneCols = 16;
 constexpr int kRT = 8;           // route-table ring slots (tiles)
 constexpr int kAD = 8;           // "A buffer consumed" barrier ring (tiles)
 
+#ifndef QKV_PG64
+#define QKV_PG64 2   // q/k/v producer groups at d = 64
+#endif
+#ifndef QKV_RI64
+#define QKV_RI64 3   // q/k/v router chains interleaved per pass at d = 64
+#endif
 #ifndef QKV_WO_PG
 #define QKV_WO_PG 1
 #endif
@@ -64,7 +70,7 @@ struct Cfg {
   // the q/k/v form is CUDA-core bound (LN, three fp64 router dots per row,
   // sign-hash / γ epilogue): several groups per role keep enough warps in
   // flight to hide their dependent chains
-  static constexpr int PG = NP == 3 ? (D == 32 ? 3 : 2) : QKV_WO_PG;
+  static constexpr int PG = NP == 3 ? (D == 32 ? 3 : QKV_PG64) : QKV_WO_PG;
   // (LNR: the W_O epilogue also runs the LayerNorm + fp64 router: two groups)
   static constexpr int EG = NP == 3 ? (D == 32 ? 3 : 2) : (LNR ? 2 : QKV_WO_EG);
   static constexpr int NA = 2;                      // A buffers in TMEM
@@ -275,9 +281,9 @@ __global__ void __launch_bounds__(Cfg<D, NP, LNR>::THREADS, 1) qkv_kernel(Params
       mbar_wait(&rt_empty[rs], (uint32_t(j / kRT) & 1u) ^ 1u);
       // the NP routers' chains are interleaved (2·NP independent fp64 chains
       // in flight, each in channel order, so the logits are unchanged)
-      constexpr int RI = NP;
-      {
-        constexpr int r0 = 0;
+      constexpr int RI = (NP == 3 && D == 64) ? QKV_RI64 : NP;
+#pragma unroll 1
+      for (int r0 = 0; r0 < NP; r0 += RI) {
         if (kQDbg && (p.dbg & 33)) {   // debug: no router dots (route table: expert 0, gate 1)
 #pragma unroll
           for (int i = 0; i < RI; ++i) {
@@ -293,7 +299,7 @@ __global__ void __launch_bounds__(Cfg<D, NP, LNR>::THREADS, 1) qkv_kernel(Params
         }
         // weights of channel c + 1 are loaded while channel c's DFMAs run
         // (warp-uniform shared-memory broadcasts)
-        const double2* wrow = reinterpret_cast<const double2*>(swg);
+        const double2* wrow = reinterpret_cast<const double2*>(swg) + r0 * D;
         double2 wc[RI];
 #pragma unroll
         for (int i = 0; i < RI; ++i) wc[i] = wrow[i * D];

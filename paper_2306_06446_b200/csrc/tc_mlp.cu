@@ -82,6 +82,9 @@ struct MlpParams {
   unsigned long long* prof;  // debug builds: cycles per wait site (nullptr: off)
   long long* tl;             // debug builds: CTA 0 event timeline [8][64] (nullptr: off)
   int dbg;                   // debug builds: role isolation bits (see kDbg)
+  const float* lnf_g;        // LNF: the stage's final LayerNorm on the output rows
+  const float* lnf_b;
+  float lnf_eps;
 };
 
 #ifdef SA_DEBUG
@@ -94,7 +97,7 @@ constexpr bool kDbg = false;   // no waits
 enum { S_OF = 0, S_A1E, S_WR, S_OE, S_HE, S_A1F, S_BF, S_HF, S_W, T_PROD, T_MMA1, T_MMA2,
        T_GELU, S_N };
 
-template <int D, bool RES>
+template <int D, bool RES, bool LNF = false>
 struct Layout {
   static constexpr bool W = Wide<D>::W;
   static constexpr int HC = Wide<D>::HC;                      // hidden chunk (fc1 N, fc2 K)
@@ -122,7 +125,8 @@ struct Layout {
   static constexpr uint32_t OFF_ALO = WBYTES;                 // wide: [KC1][128 x 32] bf16 lo plane
   static constexpr uint32_t ALO = W ? KC1 * kBM * 32 * 2 : 0;
   static constexpr uint32_t OFF_XB = OFF_ALO + ALO;
-  static constexpr uint32_t XB = Roles<D>::NPW * 32 * kXPitch * 4;   // producer transpose slots
+  static constexpr int XP = LNF ? D + 4 : kXPitch;            // transpose pitch (LNF: whole rows)
+  static constexpr uint32_t XB = Roles<D>::NPW * 32 * XP * 4;   // producer transpose slots
   static constexpr uint32_t OFF_BAR = OFF_XB + XB;
   // barriers: a1 full/empty[NA], w1 full/empty[NW], w2 full/empty[NW],
   //           h_full/h_empty/buf_free[NB], o_full/o_empty[NO], wres
@@ -262,9 +266,10 @@ __device__ __forceinline__ void mma_cat3(uint32_t d, uint32_t ah, uint32_t am, u
       : "memory");
 }
 
-template <int D, bool RES, int NF>
+template <int D, bool RES, int NF, bool LNF = false>
 __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p) {
-  using L = Layout<D, RES>;
+  static_assert(!LNF || (D == 32 && !Wide<D>::W), "final LayerNorm: d = 32 (one warp holds a row)");
+  using L = Layout<D, RES, LNF>;
   constexpr int kMma1 = Roles<D>::kMma1, kMma2 = Roles<D>::kMma2, kWld = Roles<D>::kWld;
   constexpr int NPW = Roles<D>::NPW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -353,7 +358,7 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
     const int quad = (warp - kProd) & 3, kc0 = (warp - kProd) >> 2;
     const int ptid = quad * 32 + lane;
     const uint32_t lane_base = uint32_t(quad * 32) << 16;
-    float* xb = reinterpret_cast<float*>(smem + L::OFF_XB) + (warp - kProd) * 32 * kXPitch;
+    float* xb = reinterpret_cast<float*>(smem + L::OFF_XB) + (warp - kProd) * 32 * L::XP;
     // the warp's 16-column output blocks: 2 per owned K stage
     constexpr int NBLK = 2 * (L::KC1 / KST);
     auto blk_col = [&](int bi) { return 32 * (kc0 + (bi >> 1) * KST) + 16 * (bi & 1); };
@@ -392,6 +397,88 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
       PW(S_OF, &o_full[ob], oph);
       tc_fence_after();
       const uint32_t acc = tmem + lane_base + L::T_ACC2 + uint32_t(ob) * L::ACC2C;
+      if constexpr (LNF) {
+        // (1) gate · acc2 row-major into xb (thread = row), (2) + residual in
+        // the transposed layout (coalesced residual loads), (3) the stage's
+        // final LayerNorm per row with layernorm_row_kernel's operation order,
+        // (4) coalesced stores of the normalised rows
+        constexpr int XP = L::XP;
+#pragma unroll
+        for (int bi = 0; bi < NBLK; ++bi) {
+          const int cb = blk_col(bi);
+          float v[16];
+          tmem_ld16(acc + uint32_t(cb), v);
+          if (two) {
+            float w[16];
+            tmem_ld16(acc + 32u + uint32_t(cb), w);
+#pragma unroll
+            for (int t = 0; t < 16; ++t) v[t] = v[t] + w[t];
+          }
+#pragma unroll
+          for (int t = 0; t < 16; t += 4)
+            *reinterpret_cast<float4*>(xb + lane * XP + cb + t) =
+                make_float4(v[t] * gt, v[t + 1] * gt, v[t + 2] * gt, v[t + 3] * gt);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int bi = 0; bi < NBLK; ++bi) {
+          const int cb = blk_col(bi);
+          const int rb = bi & 1;
+          if (bi + 1 < NBLK) load_res(blk_col(bi + 1), res[rb ^ 1]);
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int ri = it * 8 + (lane >> 2);
+            float4* q = reinterpret_cast<float4*>(xb + ri * XP + cb + c4);
+            float4 o = *q;
+            if (p.residual) {
+              const float4 rr = res[rb][it];
+              o = make_float4(rr.x + o.x, rr.y + o.y, rr.z + o.z, rr.w + o.w);
+            }
+            *q = o;
+          }
+        }
+        __syncwarp();
+        if (orow >= 0) {
+          float4* xr = reinterpret_cast<float4*>(xb + lane * XP);
+          float4 w4[D / 4];
+          float sm = 0.f;
+#pragma unroll
+          for (int i = 0; i < D / 4; ++i) {
+            w4[i] = xr[i];
+            sm += (w4[i].x + w4[i].y) + (w4[i].z + w4[i].w);
+          }
+          const float mean = sm / float(D);
+          float q2 = 0.f;
+#pragma unroll
+          for (int i = 0; i < D / 4; ++i) {
+            w4[i].x -= mean; w4[i].y -= mean; w4[i].z -= mean; w4[i].w -= mean;
+            q2 += (w4[i].x * w4[i].x + w4[i].y * w4[i].y) + (w4[i].z * w4[i].z + w4[i].w * w4[i].w);
+          }
+          const float inv = 1.0f / sqrtf(q2 / float(D) + p.lnf_eps);
+#pragma unroll
+          for (int i = 0; i < D / 4; ++i) {
+            const float4 g4 = __ldg(reinterpret_cast<const float4*>(p.lnf_g) + i);
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.lnf_b) + i);
+            xr[i] = make_float4(w4[i].x * inv * g4.x + b4.x, w4[i].y * inv * g4.y + b4.y,
+                                w4[i].z * inv * g4.z + b4.z, w4[i].w * inv * g4.w + b4.w);
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int bi = 0; bi < NBLK; ++bi) {
+          const int cb = blk_col(bi);
+          const int n = cb + c4;
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int ri = it * 8 + (lane >> 2);
+            const int64_t orow_i = orow_l[it];
+            if (orow_i < 0) continue;
+            *reinterpret_cast<float4*>(p.y + orow_i * D + n) =
+                *reinterpret_cast<const float4*>(xb + ri * XP + cb + c4);
+          }
+        }
+        __syncwarp();
+      } else {
 #pragma unroll
       for (int bi = 0; bi < NBLK; ++bi) {
         const int cb = blk_col(bi);
@@ -424,6 +511,7 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
           *reinterpret_cast<float4*>(p.y + orow_i * D + n) = o;
         }
         __syncwarp();
+      }
       }
       tc_fence_before();
       __syncwarp();
@@ -902,12 +990,12 @@ static constexpr long long* g_mlp_tl = nullptr;
 
 static int g_sms_mlp = 0;
 
-template <int D, bool RES, int NF>
+template <int D, bool RES, int NF, bool LNF = false>
 static void mlp_launch_one(const tcm::MlpParams& p, int grid, cudaStream_t s) {
-  const int smem = int(tcm::Layout<D, RES>::TOTAL);
-  cudaFuncSetAttribute(tcm::mlp_kernel<D, RES, NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const int smem = int(tcm::Layout<D, RES, LNF>::TOTAL);
+  cudaFuncSetAttribute(tcm::mlp_kernel<D, RES, NF, LNF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        smem);
-  tcm::mlp_kernel<D, RES, NF><<<grid, tcm::Roles<D>::kThreads, smem, s>>>(p);
+  tcm::mlp_kernel<D, RES, NF, LNF><<<grid, tcm::Roles<D>::kThreads, smem, s>>>(p);
 }
 
 template <int D, bool RES>
@@ -934,7 +1022,12 @@ static int mlp_launch(tcm::MlpParams& p, int d, cudaStream_t s) {
   }
   const int64_t tiles = cdiv(p.M, 128) + (p.counts ? 1 : 0);
   const int grid = int(tiles < g_sms_mlp ? tiles : g_sms_mlp);
-  if (d == 32) {
+  if (p.lnf_g) {   // d = 32 with the stage's final LayerNorm (checked by the caller)
+    if (p.hidden <= kResHidden)
+      mlp_launch_one<32, true, 0, true>(p, grid, s);
+    else
+      mlp_launch_one<32, false, 0, true>(p, grid, s);
+  } else if (d == 32) {
     if (p.hidden <= kResHidden)
       mlp_launch_nf<32, true>(p, grid, s);
     else
@@ -997,6 +1090,45 @@ extern "C" int sa_tc_moe_mlp_fused(const float* x, const int32_t* perm, const in
   p.np1 = 1;
   p.M = M;
   p.hidden = int(hidden);
+  return mlp_launch(p, int(d), as_stream(stream));
+}
+
+/* sa_tc_moe_mlp_fused with the stage's final LayerNorm (Model stage norm,
+ * model.py:565-577; tensor.py:114-128) applied to the output rows in the same
+ * kernel: y = LN(residual + gate · expert(x)), bit-identical to
+ * sa_tc_moe_mlp_fused followed by sa_layernorm; d = 32. */
+extern "C" int sa_tc_moe_mlp_fused_ln(const float* x, const int32_t* perm, const int32_t* counts,
+                                      const float* gate, const void* w1_dense, const void* w2_dense,
+                                      const void* w1_shift, const void* w2_shift, float* y,
+                                      const float* residual, int64_t M, int64_t d, int64_t hidden,
+                                      const float* ln_gain, const float* ln_bias, float eps,
+                                      void* stream) {
+  SA_REQUIRE(d == 32 && sa_tc_fused_mlp_ok(d, hidden), SA_ERR_SHAPE,
+             "sa_tc_moe_mlp_fused_ln: d=%lld hidden=%lld unsupported (d = 32)", (long long)d,
+             (long long)hidden);
+  SA_REQUIRE(M >= 0 && M < (int64_t(1) << 31), SA_ERR_SHAPE,
+             "sa_tc_moe_mlp_fused_ln: M=%lld out of range", (long long)M);
+  SA_REQUIRE(ln_gain != nullptr && ln_bias != nullptr, SA_ERR_VALUE,
+             "sa_tc_moe_mlp_fused_ln: LayerNorm gain and bias required");
+  tcm::MlpParams p;
+  memset(&p, 0, sizeof(p));
+  p.x = x;
+  p.perm = perm;
+  p.counts = counts;
+  p.gate = gate;
+  p.residual = residual;
+  p.y = y;
+  p.w1[0] = static_cast<const uint16_t*>(w1_dense);
+  p.w2[0] = static_cast<const uint16_t*>(w2_dense);
+  p.w1[1] = static_cast<const uint16_t*>(w1_shift);
+  p.w2[1] = static_cast<const uint16_t*>(w2_shift);
+  p.np0 = 3;
+  p.np1 = 1;
+  p.M = M;
+  p.hidden = int(hidden);
+  p.lnf_g = ln_gain;
+  p.lnf_b = ln_bias;
+  p.lnf_eps = eps;
   return mlp_launch(p, int(d), as_stream(stream));
 }
 

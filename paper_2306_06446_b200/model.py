@@ -126,6 +126,8 @@ FUSE_QKV = os.environ.get("SA_FUSE_QKV", "1") == "1"
 FUSE_O = os.environ.get("SA_FUSE_O", "1") == "1"
 # the block's LN2 + MLP router in the W_O kernel's epilogue (sa_fused_moe_linear_ln_route)
 FUSE_LN2 = os.environ.get("SA_FUSE_LN2", "1") == "1"
+# a stage's final LayerNorm in the last block's fused MLP kernel (d = 32)
+FUSE_STAGE_LN = os.environ.get("SA_FUSE_STAGE_LN", "1") == "1"
 
 
 def _fused_o_ok(mod, x2) -> bool:
@@ -360,10 +362,13 @@ class Mlp:
         self.fc2.post_step()
 
 
-def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None):
+def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None, post_ln=None):
     """K5 for the two expert shapes the reference builds (ref model.py:499-502,
     514-521): (Linear, ShiftLinearLayer) and (Mlp(Linear, Linear),
-    Mlp(Shift, Shift)). Returns None for any other expert set."""
+    Mlp(Shift, Shift)). Returns None for any other expert set. `post_ln` (a
+    LayerNorm) is applied to the output in the same kernel when the fused MLP
+    supports it (d = 32); the caller checks `fused_expert_forward.applied`."""
+    fused_expert_forward.applied = False
     if len(experts) != 2:
         return None
     e0, e1 = experts
@@ -398,6 +403,14 @@ def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None):
             p2d, _, _ = e0.fc2.tc_pack(d)
             p1s, _, _ = e1.fc1.tc_pack(fused_mlp_w1_bn(d))
             p2s, _, _ = e1.fc2.tc_pack(d)
+            if post_ln is not None and d == 32 and FUSE_STAGE_LN:
+                _lib.call("sa_tc_moe_mlp_fused_ln", _lib.ptr(x), _lib.ptr(plan.perm_dev),
+                          _lib.ptr(plan.counts_dev), _lib.ptr(plan.gate_dev), _lib.ptr(p1d),
+                          _lib.ptr(p2d), _lib.ptr(p1s), _lib.ptr(p2s), _lib.ptr(y), _lib.ptr(res),
+                          M, d, hidden, _lib.ptr(post_ln.gain.value), _lib.ptr(post_ln.bias.value),
+                          1e-5, _stream())
+                fused_expert_forward.applied = True
+                return y
             _lib.call("sa_tc_moe_mlp_fused", _lib.ptr(x), _lib.ptr(plan.perm_dev),
                       _lib.ptr(plan.counts_dev), _lib.ptr(plan.gate_dev), _lib.ptr(p1d),
                       _lib.ptr(p2d), _lib.ptr(p1s), _lib.ptr(p2s), _lib.ptr(y), _lib.ptr(res),
@@ -448,9 +461,12 @@ class MoeModule:
     def router(self) -> MOE.Router:
         return MOE.Router(w_g=self.wg.value, sigma=self.cfg.sigma, lam=self.cfg.lam)
 
-    def forward(self, x, train=False, residual=None, plan=None):
+    def forward(self, x, train=False, residual=None, plan=None, post_ln=None):
         """`plan` (optional) is a DispatchPlan already computed for x by a fused
-        LayerNorm+router pass (Block.forward); otherwise routing runs here."""
+        LayerNorm+router pass (Block.forward); otherwise routing runs here.
+        `post_ln`: a LayerNorm the fused MLP may apply to the output in the same
+        kernel; `self.post_ln_applied` says whether it did."""
+        self.post_ln_applied = False
         _no_train(train)
         x = to_device(x)
         lead = x.shape[:-1]
@@ -470,7 +486,8 @@ class MoeModule:
         if plan is None:
             plan, _ = MOE.route_plan(x2, self.wg.value)
         self.last_plan = plan
-        y = fused_expert_forward(x2, self.experts, plan, residual)
+        y = fused_expert_forward(x2, self.experts, plan, residual, post_ln)
+        self.post_ln_applied = y is not None and fused_expert_forward.applied
         if y is None:
             y = MOE.moe_forward(x2, self.experts, plan)
             if residual is not None:
@@ -619,8 +636,11 @@ class Block:
         self.attn = attn
         self.mlp = mlp
 
-    def forward(self, x, train=False):
+    def forward(self, x, train=False, post_ln=None):
+        """`post_ln`: the stage's final LayerNorm, applied to this block's output
+        inside the MLP kernel when it supports it (`self.post_ln_applied`)."""
         _no_train(train)
+        self.post_ln_applied = False
         x = to_device(x)
         batch, n, d = x.shape
         x2 = x.reshape(batch * n, d)
@@ -638,11 +658,13 @@ class Block:
             h = self.attn.forward(self.ln1.forward(x), residual=x)
         h2 = h.reshape(batch * n, d)
         if pre is not None:
-            y = self.mlp.forward(pre[0], residual=h2, plan=pre[1])
+            y = self.mlp.forward(pre[0], residual=h2, plan=pre[1], post_ln=post_ln)
+            self.post_ln_applied = self.mlp.post_ln_applied
         elif fuse and isinstance(self.mlp, MoeModule):
             flat, (plan,) = MOE.ln_route_plans(h2, self.ln2.gain.value, self.ln2.bias.value,
                                                [self.mlp.wg.value])
-            y = self.mlp.forward(flat, residual=h2, plan=plan)
+            y = self.mlp.forward(flat, residual=h2, plan=plan, post_ln=post_ln)
+            self.post_ln_applied = self.mlp.post_ln_applied
         else:
             flat = self.ln2.forward(h).reshape(batch * n, d)
             y = self.mlp.forward(flat, residual=h2)
@@ -936,10 +958,11 @@ class Network:
             if S.embed_ln is not None and not fused_ln:
                 tok = S.embed_ln.forward(tok)
             t3 = tok.reshape(B, S.rows, S.d)
-            for blk in S.blocks:
-                t3 = blk.forward(t3)
+            for i, blk in enumerate(S.blocks):
+                last = i == len(S.blocks) - 1
+                t3 = blk.forward(t3, post_ln=S.stage_ln if last else None)
             tok = t3.reshape(B * S.rows, S.d)
-            if S.stage_ln is not None:
+            if S.stage_ln is not None and not (S.blocks and S.blocks[-1].post_ln_applied):
                 tok = S.stage_ln.forward(tok)
             side = H // S.patch
             grid, H, W, C, sub = tok, side, side, S.d, 0.0

@@ -14,6 +14,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2306_06446_b200 import _lib, model as MD, moe as MOE  # noqa: E402
 
 PRODUCT = os.environ.get("QKV_PRODUCT") == "1"   # product library, modes ignored (for ncu)
+if os.environ.get("SA_LIB"):   # A/B variant of the product library (scripts/build_variant.py)
+    _lib.LIB_PATH = os.environ["SA_LIB"]
 lib = _lib.load() if PRODUCT else _lib._open(_lib.DEBUG_LIB_PATH)
 _lib._lib = lib
 if not PRODUCT:

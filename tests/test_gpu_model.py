@@ -325,6 +325,31 @@ def test_fused_wo_ln2_route_bit_identical(golden, name):
 
 
 @pytest.mark.parametrize("name", ["pvt_small", "pvt_b0_full"])
+def test_fused_stage_layernorm_bit_identical(golden, name):
+    """sa_tc_moe_mlp_fused_ln (the stage's final LayerNorm in the last block's
+    fused MLP, d = 32) reproduces the fused MLP + sa_layernorm exactly."""
+    from paper_2306_06446_b200 import model as MD
+    fx = golden(name)
+    spec = FIXTURES[name]()
+    m = MD.Network(spec)
+    b = min(int(fx["batch"]), 4)
+    images = fx["images"][:b] if "images" in fx else ops.rng(int(fx["images_seed"])).uniform(
+        0, 1, (b, spec["img"], spec["img"], 3)).astype(F32)
+    x = dev(images)
+    old = MD.FUSE_STAGE_LN
+    try:
+        MD.FUSE_STAGE_LN = False
+        ref = host(m.forward(x))
+        assert not any(S.blocks[-1].post_ln_applied for S in m.stages)
+        MD.FUSE_STAGE_LN = True
+        got = host(m.forward(x))
+        assert any(S.blocks[-1].post_ln_applied for S in m.stages if S.d == 32)
+    finally:
+        MD.FUSE_STAGE_LN = old
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("name", ["pvt_small", "pvt_b0_full"])
 def test_fused_embed_layernorm_bit_identical(golden, name):
     """sa_tc_patch_embed_ln (embedding LayerNorm in the patch GEMM's epilogue)
     reproduces sa_tc_patch_embed + sa_layernorm exactly: identical logits."""
