@@ -372,8 +372,8 @@ def op_bytes(name, args):
     if name == "sa_tc_moe_linear":
         M, K, N, res = args[9], args[10], args[11], args[8]
         return M * K * A + M * N * A + K * N * 8 + (M * N * A if res else 0) + M * 8
-    if name in ("sa_tc_moe_mlp_fused", "sa_tc_moe_mlp"):
-        if name == "sa_tc_moe_mlp_fused":
+    if name in ("sa_tc_moe_mlp_fused", "sa_tc_moe_mlp", "sa_tc_moe_mlp_fused_ln"):
+        if name in ("sa_tc_moe_mlp_fused", "sa_tc_moe_mlp_fused_ln"):
             res, M, d, hidden = args[9], args[10], args[11], args[12]
         else:
             res, M, d, hidden = args[11], args[12], args[13], args[14]
@@ -405,6 +405,10 @@ def op_bytes(name, args):
         # x, residual in; y out; (expert, gate) dispatch array
         M, d = args[6], args[7]
         return 3 * M * d * A + M * 8
+    if name == "sa_fused_moe_linear_ln_route":
+        # x, residual in; h and LN2(h) out; two (expert, gate) dispatch arrays
+        M, d = args[6], args[7]
+        return 4 * M * d * A + 2 * M * 8
     if name == "sa_pool":
         B, n, d = args[2], args[3], args[4]
         return B * n * d * A
