@@ -432,6 +432,28 @@ __device__ __forceinline__ Split3 split3x2(float a, float b) {
   s.l = __floats2bfloat162_rn(l.x, l.y);
   return s;
 }
+// The same exact three-plane split by TRUNCATION, with integer / fp32-add
+// instructions only: hi = the upper 16 bits of x, mid = the upper 16 bits of
+// r = x - hi (exact), lo = r - mid (exact; <= 8 significant bits, so its
+// upper 16 bits are the whole value). hi + mid + lo == x as the RN split, but
+// no F2FP conversion: those issue on the same 16-lane pipe as MUFU, which the
+// GELU already saturates. Returns the three packed bf16x2 words.
+struct Split3u {
+  uint32_t h, m, l;
+};
+__device__ __forceinline__ Split3u split3x2_trunc(float a, float b) {
+  Split3u s;
+  const uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
+  s.h = __byte_perm(ua, ub, 0x7632);
+  const float2 r = sub2(make_float2(a, b), make_float2(__uint_as_float(ua & 0xffff0000u),
+                                                       __uint_as_float(ub & 0xffff0000u)));
+  const uint32_t ra = __float_as_uint(r.x), rb = __float_as_uint(r.y);
+  s.m = __byte_perm(ra, rb, 0x7632);
+  const float2 l = sub2(r, make_float2(__uint_as_float(ra & 0xffff0000u),
+                                       __uint_as_float(rb & 0xffff0000u)));
+  s.l = __byte_perm(__float_as_uint(l.x), __float_as_uint(l.y), 0x7632);
+  return s;
+}
 __device__ __forceinline__ uint32_t bf2_bits(__nv_bfloat162 v) {
   return *reinterpret_cast<uint32_t*>(&v);
 }

@@ -800,10 +800,10 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
           } else {
             gelu_pair<false>(g0, g1);
           }
-          const Split3 sp = split3x2(g0, g1);
-          hp[t] = bf2_bits(sp.h);
-          mp[t] = bf2_bits(sp.m);
-          lp[t] = bf2_bits(sp.l);
+          const Split3u sp = split3x2_trunc(g0, g1);   // no F2FP: the MUFU pipe is the GELU's
+          hp[t] = sp.h;
+          mp[t] = sp.m;
+          lp[t] = sp.l;
         }
         tmem_st16(bb + uint32_t(32 * h), hp);
         tmem_st16(bb + uint32_t(32 * h + 16), mp);
@@ -867,10 +867,10 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
             } else {
               gelu_pair<false>(g0, g1);
             }
-            const Split3 sp = split3x2(g0, g1);
-            hp[t] = bf2_bits(sp.h);
-            mp[t] = bf2_bits(sp.m);
-            lp[t] = bf2_bits(sp.l);
+            const Split3u sp = split3x2_trunc(g0, g1);   // no F2FP: the MUFU pipe is the GELU's
+            hp[t] = sp.h;
+            mp[t] = sp.m;
+            lp[t] = sp.l;
           }
           if (kDbg && (p.dbg & 128)) {
             if (hp[0] == 0x12345u && mp[1] == 7u && lp[2] == 9u) mbar_arrive(&h_empty[b]);   // keep the math live
@@ -930,10 +930,10 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
             } else {
               gelu_pair<false>(g0, g1);
             }
-            const Split3 sp = split3x2(g0, g1);
-            hp[t] = bf2_bits(sp.h);
-            mp[t] = bf2_bits(sp.m);
-            lp[t] = bf2_bits(sp.l);
+            const Split3u sp = split3x2_trunc(g0, g1);   // no F2FP: the MUFU pipe is the GELU's
+            hp[t] = sp.h;
+            mp[t] = sp.m;
+            lp[t] = sp.l;
           }
           if (kDbg && (p.dbg & 128)) {
             if (hp[0] == 0x12345u && mp[1] == 7u && lp[2] == 9u) mbar_arrive(&h_empty[b]);   // keep the math live

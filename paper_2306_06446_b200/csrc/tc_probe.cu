@@ -504,7 +504,10 @@ __global__ void __launch_bounds__(512) gelu_probe_kernel(int iters, int mode, fl
         if (t < NF) tc::gelu_pair<true>(g0, g1);
         else tc::gelu_pair<false>(g0, g1);
       }
-      if (!(mode & 1)) {
+      if (!(mode & 1) && (mode & 4)) {   // truncation split (no F2FP)
+        const tc::Split3u sp = tc::split3x2_trunc(g0, g1);
+        acc += sp.h ^ sp.m ^ sp.l;
+      } else if (!(mode & 1)) {
         const tc::Split3 sp = tc::split3x2(g0, g1);
         acc += tc::bf2_bits(sp.h) ^ tc::bf2_bits(sp.m) ^ tc::bf2_bits(sp.l);
       } else {

@@ -16,7 +16,8 @@ lib.sa_probe_gelu.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p, ctypes.c_voi
 out = torch.zeros(1, dtype=torch.int64, device="cuda")
 sink = torch.zeros(1, device="cuda")
 iters = 400
-for mode, name in ((0, "gelu+split"), (1, "gelu only"), (2, "split only")):
+for mode, name in ((0, "gelu+split"), (4, "gelu+tsplit"), (1, "gelu only"), (2, "split only"),
+                   (6, "tsplit only")):
     for nf in (0, 4, 8):
         row = []
         for threads in (128, 256, 512):
