@@ -551,14 +551,14 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
               const float4 q = v[sub * 4 + t];
-              const Split3 a = split3x2(q.x, q.y);
-              const Split3 b = split3x2(q.z, q.w);
-              hp[2 * t] = bf2_bits(a.h);
-              hp[2 * t + 1] = bf2_bits(b.h);
-              mp[2 * t] = bf2_bits(a.m);
-              mp[2 * t + 1] = bf2_bits(b.m);
-              lp[2 * t] = bf2_bits(a.l);
-              lp[2 * t + 1] = bf2_bits(b.l);
+              const Split3u a = split3x2_trunc(q.x, q.y);   // (no F2FP, as the GELU planes)
+              const Split3u b = split3x2_trunc(q.z, q.w);
+              hp[2 * t] = a.h;
+              hp[2 * t + 1] = b.h;
+              mp[2 * t] = a.m;
+              mp[2 * t + 1] = b.m;
+              lp[2 * t] = a.l;
+              lp[2 * t + 1] = b.l;
             }
             const uint32_t col = a1 + kc * L::A1P * kPlaneCols + sub * 8;
             tmem_st8(col, hp);
