@@ -148,14 +148,14 @@ __global__ void __launch_bounds__(Cfg<D, KC>::THREADS, 1) embed_ln_kernel(Params
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const float4 q = v[kcl * 8 + sub * 4 + i];
-            const Split3 a = split3x2(q.x, q.y);
-            const Split3 c = split3x2(q.z, q.w);
-            hp[2 * i] = bf2_bits(a.h);
-            hp[2 * i + 1] = bf2_bits(c.h);
-            mp[2 * i] = bf2_bits(a.m);
-            mp[2 * i + 1] = bf2_bits(c.m);
-            lp[2 * i] = bf2_bits(a.l);
-            lp[2 * i + 1] = bf2_bits(c.l);
+            const Split3u a = split3x2_trunc(q.x, q.y);
+            const Split3u c = split3x2_trunc(q.z, q.w);
+            hp[2 * i] = a.h;
+            hp[2 * i + 1] = c.h;
+            mp[2 * i] = a.m;
+            mp[2 * i + 1] = c.m;
+            lp[2 * i] = a.l;
+            lp[2 * i + 1] = c.l;
           }
           const uint32_t col = a1 + kc * 3 * kPlaneCols + sub * 8;
           tmem_st8(col, hp);

@@ -344,10 +344,10 @@ __global__ void __launch_bounds__(Cfg<D, NP, LNR>::THREADS, 1) qkv_kernel(Params
         uint32_t hp[16], mp[16], lp[16];
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
-          const Split3 sp = split3x2(v[kc * 32 + 2 * t], v[kc * 32 + 2 * t + 1]);
-          hp[t] = bf2_bits(sp.h);
-          mp[t] = bf2_bits(sp.m);
-          lp[t] = bf2_bits(sp.l);
+          const Split3u sp = split3x2_trunc(v[kc * 32 + 2 * t], v[kc * 32 + 2 * t + 1]);
+          hp[t] = sp.h;
+          mp[t] = sp.m;
+          lp[t] = sp.l;
         }
         tmem_st16(a1 + kc * 3 * kPlaneCols, hp);
         tmem_st16(a1 + kc * 3 * kPlaneCols + kPlaneCols, mp);

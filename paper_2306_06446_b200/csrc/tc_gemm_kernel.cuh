@@ -521,13 +521,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcParams p,
           if (AM == A_PATCH && rowp[i] != nullptr && k < p.K) {
             v[i].x -= p.sub; v[i].y -= p.sub; v[i].z -= p.sub; v[i].w -= p.sub;
           }
-          const Split3 a = split3x2(v[i].x, v[i].y);
-          const Split3 b = split3x2(v[i].z, v[i].w);
+          const Split3u a = split3x2_trunc(v[i].x, v[i].y);   // (no F2FP, see split3x2_trunc)
+          const Split3u b = split3x2_trunc(v[i].z, v[i].w);
           const uint32_t off = plane_offset(rsub + 16 * i, k4);
-          *reinterpret_cast<uint2*>(st + off) = make_uint2(bf2_bits(a.h), bf2_bits(b.h));
-          *reinterpret_cast<uint2*>(st + kPlaneA + off) = make_uint2(bf2_bits(a.m), bf2_bits(b.m));
-          *reinterpret_cast<uint2*>(st + 2 * kPlaneA + off) =
-              make_uint2(bf2_bits(a.l), bf2_bits(b.l));
+          *reinterpret_cast<uint2*>(st + off) = make_uint2(a.h, b.h);
+          *reinterpret_cast<uint2*>(st + kPlaneA + off) = make_uint2(a.m, b.m);
+          *reinterpret_cast<uint2*>(st + 2 * kPlaneA + off) = make_uint2(a.l, b.l);
         }
         if (!(p.dbg & 8)) fence_proxy_async_smem();
         __syncwarp();
