@@ -32,12 +32,16 @@ using namespace tc;
 
 constexpr uint32_t kPlaneCols = 16;
 
+#ifndef EMB_SPLIT_PG
+#define EMB_SPLIT_PG 4   // split-K producer groups (each converts KC / PG stages of every tile)
+#endif
 template <int D, int KC>
 struct Cfg {
   // producer groups: K <= 64: two groups on alternate tiles (two tiles' image
   // loads in flight); deeper K: two groups splitting each row's K stages
   static constexpr bool SPLITK = KC > 2;
-  static constexpr int PG = SPLITK ? 2 : 4;
+  static constexpr int PG = SPLITK ? EMB_SPLIT_PG : 4;
+  static_assert(!SPLITK || KC % EMB_SPLIT_PG == 0, "split K: whole K stages per group");
   static constexpr int MMA_WARP = 4 + 4 * PG;
   static constexpr int THREADS = (MMA_WARP + 1) * 32;
   static constexpr int NA = SPLITK ? 2 : 4, NACC = 2;
@@ -86,7 +90,7 @@ __global__ void __launch_bounds__(Cfg<D, KC>::THREADS, 1) embed_ln_kernel(Params
   if (warp == kMma) tmem_alloc<CF::TCOLS>(tmem_slot);
   if (tid == 0) {
     for (int i = 0; i < CF::NA; ++i) {
-      mbar_init(&a_full[i], CF::SPLITK ? 8 : 4);
+      mbar_init(&a_full[i], CF::SPLITK ? 4 * CF::PG : 4);
       mbar_init(&a_empty[i], 1);
     }
     for (int i = 0; i < CF::NACC; ++i) {
@@ -110,7 +114,7 @@ __global__ void __launch_bounds__(Cfg<D, KC>::THREADS, 1) embed_ln_kernel(Params
     const int rl = pw * 32 + lane;
     const uint32_t lane_base = uint32_t(pw * 32) << 16;
     const int rowf4 = int(p.patch * p.C) / 4;   // float4 per image row of the patch
-    constexpr int KCG = CF::SPLITK ? KC / 2 : KC;   // K stages this group converts
+    constexpr int KCG = CF::SPLITK ? KC / CF::PG : KC;   // K stages this group converts
     const int kc0 = CF::SPLITK ? pg * KCG : 0;
     const int mstep = CF::SPLITK ? gridDim.x : CF::PG * gridDim.x;
     int j = CF::SPLITK ? 0 : pg;
