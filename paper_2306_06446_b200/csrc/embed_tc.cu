@@ -32,6 +32,9 @@ using namespace tc;
 
 constexpr uint32_t kPlaneCols = 16;
 
+#ifndef EMB_SPLIT_MINKC
+#define EMB_SPLIT_MINKC 2   // K stages above which the producers split K instead of alternating tiles
+#endif
 #ifndef EMB_SPLIT_PG
 #define EMB_SPLIT_PG 4   // split-K producer groups (each converts KC / PG stages of every tile)
 #endif
@@ -39,9 +42,9 @@ template <int D, int KC>
 struct Cfg {
   // producer groups: K <= 64: two groups on alternate tiles (two tiles' image
   // loads in flight); deeper K: two groups splitting each row's K stages
-  static constexpr bool SPLITK = KC > 2;
-  static constexpr int PG = SPLITK ? EMB_SPLIT_PG : 4;
-  static_assert(!SPLITK || KC % EMB_SPLIT_PG == 0, "split K: whole K stages per group");
+  static constexpr bool SPLITK = KC > EMB_SPLIT_MINKC;
+  static constexpr int PG = SPLITK ? (KC < EMB_SPLIT_PG ? KC : EMB_SPLIT_PG) : 4;
+  static_assert(!SPLITK || KC % PG == 0, "split K: whole K stages per group");
   static constexpr int MMA_WARP = 4 + 4 * PG;
   static constexpr int THREADS = (MMA_WARP + 1) * 32;
   static constexpr int NA = SPLITK ? 2 : 4, NACC = 2;
@@ -50,7 +53,6 @@ struct Cfg {
   static constexpr uint32_t T_ACC = NA * A_COLS;
   static constexpr uint32_t TCOLS = 512;
   static_assert(T_ACC + NACC * D <= TCOLS, "TMEM budget");
-  static_assert(!SPLITK || KC % 2 == 0, "split K needs an even number of K stages");
   static constexpr uint32_t W_BYTES = uint32_t(KC) * 3 * D * 64;   // resident packed weights
   static constexpr uint32_t XB = W_BYTES;                          // [4 warps][32][kXPitch] fp32
   static constexpr uint32_t BAR = XB + 4 * 32 * kXPitch * 4;
