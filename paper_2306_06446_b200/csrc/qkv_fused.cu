@@ -51,6 +51,12 @@ constexpr uint32_t kPlaneCols = 16;
 constexpr int kRT = 8;           // route-table ring slots (tiles)
 constexpr int kAD = 8;           // "A buffer consumed" barrier ring (tiles)
 
+#ifndef QKV_PG32
+#define QKV_PG32 3   // q/k/v producer groups at d = 32
+#endif
+#ifndef QKV_EG32
+#define QKV_EG32 2   // q/k/v epilogue groups at d = 32 (3: 107.0 vs 104.8 us)
+#endif
 #ifndef QKV_PG64
 #define QKV_PG64 2   // q/k/v producer groups at d = 64
 #endif
@@ -70,9 +76,9 @@ struct Cfg {
   // the q/k/v form is CUDA-core bound (LN, three fp64 router dots per row,
   // sign-hash / γ epilogue): several groups per role keep enough warps in
   // flight to hide their dependent chains
-  static constexpr int PG = NP == 3 ? (D == 32 ? 3 : QKV_PG64) : QKV_WO_PG;
+  static constexpr int PG = NP == 3 ? (D == 32 ? QKV_PG32 : QKV_PG64) : QKV_WO_PG;
   // (LNR: the W_O epilogue also runs the LayerNorm + fp64 router: two groups)
-  static constexpr int EG = NP == 3 ? (D == 32 ? 3 : 2) : (LNR ? 2 : QKV_WO_EG);
+  static constexpr int EG = NP == 3 ? (D == 32 ? QKV_EG32 : 2) : (LNR ? 2 : QKV_WO_EG);
   static constexpr int NA = 2;                      // A buffers in TMEM
   static constexpr uint32_t ACC_COLS = 2 * D;       // one unit: dense | shift expert
   static constexpr int NACC = D == 32 ? 4 : 2;
