@@ -522,6 +522,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     from paper_2306_06446_b200 import specs
+    if os.environ.get("SA_LIB"):   # A/B runs of a library variant (scripts/build_variant.py)
+        from paper_2306_06446_b200 import _lib
+        _lib.LIB_PATH = os.environ["SA_LIB"]
     spec_name, _, _, METRIC, _ = CONFIGS[args.config]
     spec = specs.BUILDERS[spec_name](variant=args.variant)
     router = load_router(args, spec_name)
