@@ -229,7 +229,7 @@ int sa_tc_moe_mlp_fused(const float* x, const int32_t* perm, const int32_t* coun
                         void* stream);
 /* sa_tc_moe_mlp_fused with the stage's final LayerNorm (model.py:565-577,
  * tensor.py:114-128) on the output rows in the same kernel, bit-identical to
- * sa_tc_moe_mlp_fused + sa_layernorm; d = 32. */
+ * sa_tc_moe_mlp_fused + sa_layernorm; d = 32 or 64. */
 int sa_tc_moe_mlp_fused_ln(const float* x, const int32_t* perm, const int32_t* counts,
                            const float* gate, const void* w1_dense, const void* w2_dense,
                            const void* w1_shift, const void* w2_shift, float* y,

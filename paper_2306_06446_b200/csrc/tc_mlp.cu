@@ -113,7 +113,7 @@ struct Layout {
   static constexpr int NO = W ? 1 : 2;                        // acc2 buffers
   static constexpr int GPC = W ? 8 : kGeluPerChunk;           // GELU warps per chunk
   static constexpr bool CAT = D == 32;                        // N-concatenated dense fc2
-  static constexpr int NW = W ? (D == 128 ? 3 : 2) : 4;       // ring slots (RES = false)
+  static constexpr int NW = W ? (D == 128 ? 3 : 2) : (LNF && D == 64 ? 3 : 4);   // ring slots (RES = false)
   static constexpr uint32_t W1C = KC1 * 3 * (HC * 32 * 2);    // dense W1 chunk bytes
   static constexpr uint32_t W2C = (HC / 32) * 3 * (D * 32 * 2);
   static constexpr uint32_t RW1 = (kResHidden / HC) * W1C;    // resident dense W1
@@ -126,7 +126,9 @@ struct Layout {
   static constexpr uint32_t ALO = W ? KC1 * kBM * 32 * 2 : 0;
   static constexpr uint32_t OFF_XB = OFF_ALO + ALO;
   static constexpr int XP = LNF ? D + 4 : kXPitch;            // transpose pitch (LNF: whole rows)
-  static constexpr uint32_t XB = Roles<D>::NPW * 32 * XP * 4;   // producer transpose slots
+  // producer transpose slots (LNF: one whole-row buffer per TMEM lane quarter,
+  // shared by the quarter's producer warps)
+  static constexpr uint32_t XB = (LNF ? 4 : Roles<D>::NPW) * 32 * XP * 4;
   static constexpr uint32_t OFF_BAR = OFF_XB + XB;
   // barriers: a1 full/empty[NA], w1 full/empty[NW], w2 full/empty[NW],
   //           h_full/h_empty/buf_free[NB], o_full/o_empty[NO], wres
@@ -268,7 +270,7 @@ __device__ __forceinline__ void mma_cat3(uint32_t d, uint32_t ah, uint32_t am, u
 
 template <int D, bool RES, int NF, bool LNF = false>
 __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p) {
-  static_assert(!LNF || (D == 32 && !Wide<D>::W), "final LayerNorm: d = 32 (one warp holds a row)");
+  static_assert(!LNF || D == 32 || D == 64, "final LayerNorm: narrow form (d = 32 / 64)");
   using L = Layout<D, RES, LNF>;
   constexpr int kMma1 = Roles<D>::kMma1, kMma2 = Roles<D>::kMma2, kWld = Roles<D>::kWld;
   constexpr int NPW = Roles<D>::NPW;
@@ -358,7 +360,7 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
     const int quad = (warp - kProd) & 3, kc0 = (warp - kProd) >> 2;
     const int ptid = quad * 32 + lane;
     const uint32_t lane_base = uint32_t(quad * 32) << 16;
-    float* xb = reinterpret_cast<float*>(smem + L::OFF_XB) + (warp - kProd) * 32 * L::XP;
+    float* xb = reinterpret_cast<float*>(smem + L::OFF_XB) + (LNF ? quad : warp - kProd) * 32 * L::XP;
     // the warp's 16-column output blocks: 2 per owned K stage
     constexpr int NBLK = 2 * (L::KC1 / KST);
     auto blk_col = [&](int bi) { return 32 * (kc0 + (bi >> 1) * KST) + 16 * (bi & 1); };
@@ -437,30 +439,48 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
             *q = o;
           }
         }
-        __syncwarp();
-        if (orow >= 0) {
-          float4* xr = reinterpret_cast<float4*>(xb + lane * XP);
-          float4 w4[D / 4];
+        // d = 64: the lane quarter's two producer warps hold half a row each;
+        // named barrier (id 1 + quad, 64 threads) before the statistics read
+        // the other warp's columns, and again before either overwrites its own
+        auto quad_sync = [&]() {
+          if (KST > 1) asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
+          else __syncwarp();
+        };
+        quad_sync();
+        float mean = 0.f, inv = 0.f;
+        const float4* xr = reinterpret_cast<const float4*>(xb + lane * XP);
+        if (orow >= 0) {   // layernorm_row_kernel's operation order over the whole row
           float sm = 0.f;
 #pragma unroll
           for (int i = 0; i < D / 4; ++i) {
-            w4[i] = xr[i];
-            sm += (w4[i].x + w4[i].y) + (w4[i].z + w4[i].w);
+            const float4 w = xr[i];
+            sm += (w.x + w.y) + (w.z + w.w);
           }
-          const float mean = sm / float(D);
+          mean = sm / float(D);
           float q2 = 0.f;
 #pragma unroll
           for (int i = 0; i < D / 4; ++i) {
-            w4[i].x -= mean; w4[i].y -= mean; w4[i].z -= mean; w4[i].w -= mean;
-            q2 += (w4[i].x * w4[i].x + w4[i].y * w4[i].y) + (w4[i].z * w4[i].z + w4[i].w * w4[i].w);
+            float4 w = xr[i];
+            w.x -= mean; w.y -= mean; w.z -= mean; w.w -= mean;
+            q2 += (w.x * w.x + w.y * w.y) + (w.z * w.z + w.w * w.w);
           }
-          const float inv = 1.0f / sqrtf(q2 / float(D) + p.lnf_eps);
+          inv = 1.0f / sqrtf(q2 / float(D) + p.lnf_eps);
+        }
+        quad_sync();
+        if (orow >= 0) {   // this warp's columns
 #pragma unroll
-          for (int i = 0; i < D / 4; ++i) {
-            const float4 g4 = __ldg(reinterpret_cast<const float4*>(p.lnf_g) + i);
-            const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.lnf_b) + i);
-            xr[i] = make_float4(w4[i].x * inv * g4.x + b4.x, w4[i].y * inv * g4.y + b4.y,
-                                w4[i].z * inv * g4.z + b4.z, w4[i].w * inv * g4.w + b4.w);
+          for (int bi = 0; bi < NBLK; bi += 2) {
+            const int c0 = blk_col(bi) / 4;
+#pragma unroll
+            for (int i = c0; i < c0 + 8; ++i) {
+              float4 w = xr[i];
+              w.x -= mean; w.y -= mean; w.z -= mean; w.w -= mean;
+              const float4 g4 = __ldg(reinterpret_cast<const float4*>(p.lnf_g) + i);
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.lnf_b) + i);
+              reinterpret_cast<float4*>(xb + lane * XP)[i] =
+                  make_float4(w.x * inv * g4.x + b4.x, w.y * inv * g4.y + b4.y,
+                              w.z * inv * g4.z + b4.z, w.w * inv * g4.w + b4.w);
+            }
           }
         }
         __syncwarp();
@@ -1022,8 +1042,10 @@ static int mlp_launch(tcm::MlpParams& p, int d, cudaStream_t s) {
   }
   const int64_t tiles = cdiv(p.M, 128) + (p.counts ? 1 : 0);
   const int grid = int(tiles < g_sms_mlp ? tiles : g_sms_mlp);
-  if (p.lnf_g) {   // d = 32 with the stage's final LayerNorm (checked by the caller)
-    if (p.hidden <= kResHidden)
+  if (p.lnf_g) {   // the stage's final LayerNorm (d = 32 / 64, checked by the caller)
+    if (d == 64)
+      mlp_launch_one<64, false, 0, true>(p, grid, s);
+    else if (p.hidden <= kResHidden)
       mlp_launch_one<32, true, 0, true>(p, grid, s);
     else
       mlp_launch_one<32, false, 0, true>(p, grid, s);
@@ -1103,8 +1125,8 @@ extern "C" int sa_tc_moe_mlp_fused_ln(const float* x, const int32_t* perm, const
                                       const float* residual, int64_t M, int64_t d, int64_t hidden,
                                       const float* ln_gain, const float* ln_bias, float eps,
                                       void* stream) {
-  SA_REQUIRE(d == 32 && sa_tc_fused_mlp_ok(d, hidden), SA_ERR_SHAPE,
-             "sa_tc_moe_mlp_fused_ln: d=%lld hidden=%lld unsupported (d = 32)", (long long)d,
+  SA_REQUIRE((d == 32 || d == 64) && sa_tc_fused_mlp_ok(d, hidden), SA_ERR_SHAPE,
+             "sa_tc_moe_mlp_fused_ln: d=%lld hidden=%lld unsupported (d = 32 / 64)", (long long)d,
              (long long)hidden);
   SA_REQUIRE(M >= 0 && M < (int64_t(1) << 31), SA_ERR_SHAPE,
              "sa_tc_moe_mlp_fused_ln: M=%lld out of range", (long long)M);

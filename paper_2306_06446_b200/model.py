@@ -128,6 +128,7 @@ FUSE_O = os.environ.get("SA_FUSE_O", "1") == "1"
 FUSE_LN2 = os.environ.get("SA_FUSE_LN2", "1") == "1"
 # a stage's final LayerNorm in the last block's fused MLP kernel (d = 32)
 FUSE_STAGE_LN = os.environ.get("SA_FUSE_STAGE_LN", "1") == "1"
+FUSE_STAGE_LN64 = os.environ.get("SA_FUSE_STAGE_LN64", "1") == "1"
 
 
 def _fused_o_ok(mod, x2) -> bool:
@@ -403,7 +404,7 @@ def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None, post
             p2d, _, _ = e0.fc2.tc_pack(d)
             p1s, _, _ = e1.fc1.tc_pack(fused_mlp_w1_bn(d))
             p2s, _, _ = e1.fc2.tc_pack(d)
-            if post_ln is not None and d == 32 and FUSE_STAGE_LN:
+            if post_ln is not None and FUSE_STAGE_LN and (d == 32 or (d == 64 and FUSE_STAGE_LN64)):
                 _lib.call("sa_tc_moe_mlp_fused_ln", _lib.ptr(x), _lib.ptr(plan.perm_dev),
                           _lib.ptr(plan.counts_dev), _lib.ptr(plan.gate_dev), _lib.ptr(p1d),
                           _lib.ptr(p2d), _lib.ptr(p1s), _lib.ptr(p2s), _lib.ptr(y), _lib.ptr(res),
