@@ -594,25 +594,42 @@ __global__ void __launch_bounds__(Cfg<D, NP, LNR>::THREADS, 1) qkv_kernel(Params
   if (warp == kMma) tmem_dealloc<512>(tmem);
 }
 
-// γ[r][b·H + h] = Σ |y| over image b's rows of head h / (n · 32): one warp per
-// (r, b, h); lane l sums the per-row fp32 sums of rows l, l + 32, ... of the
-// image in fp64, and the lanes meet in a fixed xor tree (deterministic, no
-// atomics).
-__global__ void gamma_finalize_qkv(const float* __restrict__ rsum, int64_t M, int H, int64_t B,
-                                   int n, float* __restrict__ gq, float* __restrict__ gk) {
-  const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (i >= 2 * B * H) return;   // warp-uniform
+// γ[r][b·H + h] = Σ |y| over image b's rows of head h / (n · 32): one
+// 128-thread CTA per (r, b, h); thread t sums the per-row fp32 sums of rows
+// t, t + 128, ... in fp64 (four independent loads in flight), each warp meets
+// in a fixed xor tree and thread 0 adds the four warp sums in order
+// (deterministic, no atomics).
+constexpr int kGfThreads = 128;
+__global__ void __launch_bounds__(kGfThreads) gamma_finalize_qkv(const float* __restrict__ rsum,
+                                                               int64_t M, int H, int64_t B, int n,
+                                                               float* __restrict__ gq,
+                                                               float* __restrict__ gk) {
+  __shared__ double ws[kGfThreads / 32];
+  const int64_t i = blockIdx.x;   // (r, b, h)
+  const int tid = threadIdx.x, lane = tid & 31;
   const int r = int(i / (B * H));
   const int64_t bh = i % (B * H);
   const int64_t b = bh / H;
   const int h = int(bh % H);
   const float* src = rsum + (int64_t(r) * H + h) * M + b * n;
-  double s = 0.0;
-  for (int t = lane; t < n; t += 32) s += double(__ldg(src + t));
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int t = tid;
+  for (; t + 3 * kGfThreads < n; t += 4 * kGfThreads) {
+    s0 += double(__ldg(src + t));
+    s1 += double(__ldg(src + t + kGfThreads));
+    s2 += double(__ldg(src + t + 2 * kGfThreads));
+    s3 += double(__ldg(src + t + 3 * kGfThreads));
+  }
+  for (; t < n; t += kGfThreads) s0 += double(__ldg(src + t));
+  double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) (r == 0 ? gq : gk)[bh] = float(s / (double(n) * 32.0));
+  if (lane == 0) ws[tid >> 5] = s;
+  __syncthreads();
+  if (tid == 0) {
+    const double tot = (ws[0] + ws[1]) + (ws[2] + ws[3]);
+    (r == 0 ? gq : gk)[bh] = float(tot / (double(n) * 32.0));
+  }
 }
 
 }  // namespace qkv
@@ -698,7 +715,7 @@ extern "C" int sa_ln_qkv_hash(const float* x, const float* gain, const float* bi
     qkv_kernel<64, 3><<<grid, qkv::Cfg<64, 3>::THREADS, smem, s>>>(p, tmV, tmV);
   }
   const int64_t H = d / 32;
-  gamma_finalize_qkv<<<unsigned(cdiv(2 * B * H, 8)), 256, 0, s>>>(p.rsum, M, int(H), B,
+  gamma_finalize_qkv<<<unsigned(2 * B * H), kGfThreads, 0, s>>>(p.rsum, M, int(H), B,
                                                                  int(n), gamma_q, gamma_k);
   count_launch(2);
   SA_LAUNCH_CHECK("sa_ln_qkv_hash");
