@@ -489,3 +489,65 @@ def test_embed_ln_kernel_bit_identical_to_gemm_path(B, H, C, patch, d, debug_lib
     tok = ops.mm(patches.reshape(B * side * side, K), w)
     ref = ops.layer_norm(tok, gain, bias)
     assert rel_err(out[0], ref) < 1e-5
+
+
+@pytest.mark.parametrize("M,d", [(1, 32), (127, 32), (129, 64), (1000, 32), (4097, 64)])
+def test_wo_ln2_route_kernel_ragged(M, d):
+    """sa_fused_moe_linear_ln_route on ragged row counts equals
+    sa_fused_moe_linear followed by sa_ln_route on its output, bit for bit
+    (h, LN2(h), the MLP routes and gates)."""
+    from paper_2306_06446_b200 import _lib
+    from paper_2306_06446_b200 import model as MD
+    from paper_2306_06446_b200 import moe as MOE
+    g = ops.rng(M + d)
+    w = (g.standard_normal((d, d)) / np.sqrt(d)).astype(F32)
+    o = MD.MoeModule((g.standard_normal((d, 2)) * 0.5).astype(F32),
+                     [MD.Linear(w), MD.ShiftLinearLayer(w.copy())], MD.MoeConfig())
+    ln = MD.LayerNorm(d)
+    ln.gain.value.copy_(torch.from_numpy((1 + 0.1 * g.standard_normal(d)).astype(F32)))
+    ln.bias.value.copy_(torch.from_numpy((0.1 * g.standard_normal(d)).astype(F32)))
+    wg2 = dev((g.standard_normal((d, 2)) * 0.5).astype(F32))
+    x = dev(g.standard_normal((M, d)).astype(F32))
+    res = dev(g.standard_normal((M, d)).astype(F32))
+    h_ref = o.forward(x, residual=res)
+    y_ref, (plan,) = MOE.ln_route_plans(h_ref, ln.gain.value, ln.bias.value, [wg2])
+    e1, g1 = torch.empty(M, dtype=torch.int32, device="cuda"), torch.empty(M, device="cuda")
+    h, y2 = torch.empty_like(x), torch.empty_like(x)
+    e2, g2 = torch.empty(M, dtype=torch.int32, device="cuda"), torch.empty(M, device="cuda")
+    _lib.call("sa_fused_moe_linear_ln_route", _lib.ptr(x), _lib.ptr(o.wg.value),
+              _lib.ptr(o.experts[0].tc_pack(d)[0]), _lib.ptr(o.experts[1].tc_pack(d)[0]),
+              _lib.ptr(res), MOE.tie_threshold(), M, d, _lib.ptr(e1), _lib.ptr(g1), _lib.ptr(h),
+              _lib.ptr(ln.gain.value), _lib.ptr(ln.bias.value), 1e-5, _lib.ptr(wg2), _lib.ptr(y2),
+              _lib.ptr(e2), _lib.ptr(g2), _lib.stream())
+    assert np.array_equal(host(h), host(h_ref))
+    assert np.array_equal(host(y2), host(y_ref))
+    assert np.array_equal(host(e2), plan.expert_of)
+    assert np.array_equal(host(g2), plan.gate_of)
+
+
+@pytest.mark.parametrize("M,d,hidden", [(1, 32, 256), (130, 32, 256), (777, 64, 512),
+                                        (5000, 32, 512)])
+def test_mlp_stage_ln_kernel_ragged(M, d, hidden):
+    """sa_tc_moe_mlp_fused_ln on ragged row counts equals the fused MoE MLP
+    followed by sa_layernorm, bit for bit."""
+    from paper_2306_06446_b200 import model as MD
+    from paper_2306_06446_b200 import moe as MOE
+    from paper_2306_06446_b200 import tensor as T
+    g = ops.rng(M * 3 + d)
+    w1 = (g.standard_normal((d, hidden)) / np.sqrt(d)).astype(F32)
+    w2 = (g.standard_normal((hidden, d)) / np.sqrt(hidden)).astype(F32)
+    mod = MD.MoeModule((g.standard_normal((d, 2)) * 0.5).astype(F32),
+                       [MD.Mlp(MD.Linear(w1), MD.Linear(w2)),
+                        MD.Mlp(MD.ShiftLinearLayer(w1.copy()), MD.ShiftLinearLayer(w2.copy()))],
+                       MD.MoeConfig())
+    ln = MD.LayerNorm(d)
+    ln.gain.value.copy_(torch.from_numpy((1 + 0.1 * g.standard_normal(d)).astype(F32)))
+    ln.bias.value.copy_(torch.from_numpy((0.1 * g.standard_normal(d)).astype(F32)))
+    x = dev(g.standard_normal((M, d)).astype(F32))
+    res = dev(g.standard_normal((M, d)).astype(F32))
+    plan, _ = MOE.route_plan(x, mod.wg.value)
+    y = mod.forward(x, plan=plan, residual=res)
+    ref, _ = T.layernorm(y, ln.gain.value, ln.bias.value)
+    got = mod.forward(x, plan=plan, residual=res, post_ln=ln)
+    assert mod.post_ln_applied
+    assert np.array_equal(host(got), host(ref))
