@@ -226,7 +226,10 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
   // push exchange (below): every CTA's exchange barriers must be initialised
   // before a peer's first remote store; the matching wait sits just before it
   const bool push = HEADS == 1 && (kMaxCluster % CL) == 0 && !p.pull;
-  if (push) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  // a one-CTA cluster exchanges nothing: plain shared-memory stores (st.async
+  // into the cluster window needs a cluster of at least two CTAs)
+  const bool solo = CL == 1;
+  if (push && !solo) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   auto wait_row = [&](int R) {
     asm volatile(
         "{\n\t.reg .pred q;\n\tW_%=:\n\t"
@@ -372,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
     uint64_t* tbar = bar + BR + 4;
     float* rbuf = tcb;                                   // [CL][G][4][DK] (tcb is built after)
     int* cbuf = reinterpret_cast<int*>(smem + L.cb);     // [CL][DK]
-    if (tid == 0) {
+    if (tid == 0 && !solo) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(xbar)),
                    "r"(uint32_t(CL * G * 4 * DK * 4 + CL * DK * 4))
                    : "memory");
@@ -380,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
                    "r"(uint32_t((CL - 1) * G * 16 * DK * 4))
                    : "memory");
     }
-    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    if (!solo) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     auto remote = [&](const void* local, int r) {
       uint32_t a;
       asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(su32(local)), "r"(r));
@@ -399,18 +402,24 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
       const uint4 v4 = *reinterpret_cast<const uint4*>(part + row * DK + 4 * q);
       const int grp = row >> 2, o = grp / G, gi = grp - o * G;
       const float* slot = rbuf + ((rank * G + gi) * 4 + (row & 3)) * DK + 4 * q;
-      st_async4(remote(slot, o), v4.x, v4.y, v4.z, v4.w, remote(xbar, o));
+      if (solo) *reinterpret_cast<uint4*>(const_cast<float*>(slot)) = v4;
+      else st_async4(remote(slot, o), v4.x, v4.y, v4.z, v4.w, remote(xbar, o));
       if (tid < CL * (DK / 4)) {   // counts → every CTA: thread → (rank dr, 4 counts)
         const int dr = tid / (DK / 4), k = tid % (DK / 4);
         const uint4 c4 = *reinterpret_cast<const uint4*>(cntp + 4 * k);
-        st_async4(remote(cbuf + rank * DK + 4 * k, dr), c4.x, c4.y, c4.z, c4.w, remote(xbar, dr));
+        if (solo) *reinterpret_cast<uint4*>(cbuf + rank * DK + 4 * k) = c4;
+        else st_async4(remote(cbuf + rank * DK + 4 * k, dr), c4.x, c4.y, c4.z, c4.w, remote(xbar, dr));
       }
     }
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tWX_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 q, [%0], 0;\n\t"
-        "@!q bra WX_%=;\n\t}" ::"r"(su32(xbar))
-        : "memory");
+    if (solo) {
+      __syncthreads();
+    } else {
+      asm volatile(
+          "{\n\t.reg .pred q;\n\tWX_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 q, [%0], 0;\n\t"
+          "@!q bra WX_%=;\n\t}" ::"r"(su32(xbar))
+          : "memory");
+    }
     if (tid < G * DK) {   // owner: thread = (own group, column)
       const float g = __ldg(p.gk + b * H + hz);
       const int gi = tid / DK, c = tid % DK, grp = rank * G + gi;
@@ -459,11 +468,12 @@ __global__ void __launch_bounds__(kThreads, 2) binattn_fused_kernel(Params p,
         if ((m >> i) & 1) sc += cntw[8 * g8 + i];
       tcb[e] = float(sc);
     }
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tWT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 q, [%0], 0;\n\t"
-        "@!q bra WT_%=;\n\t}" ::"r"(su32(tbar))
-        : "memory");
+    if (!solo)
+      asm volatile(
+          "{\n\t.reg .pred q;\n\tWT_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 q, [%0], 0;\n\t"
+          "@!q bra WT_%=;\n\t}" ::"r"(su32(tbar))
+          : "memory");
     __syncthreads();
   } else {
   cluster.sync();
