@@ -274,12 +274,18 @@ __global__ void __launch_bounds__(kRouteTok) partition_scan_kernel(
 SA_DEBUG_SWITCH(int, g_fused_partition, 1, sa_debug_fused_partition)
 
 // scan + partition of nr stacked plans
+#ifndef SA_FUSED_PARTITION_MAX_NB
+#define SA_FUSED_PARTITION_MAX_NB 1024
+#endif
+// block counts up to which each partition CTA folds the scan of all block
+// counts itself (nb reads per CTA) instead of a separate scan kernel
+constexpr int kFusedPartitionMaxNb = SA_FUSED_PARTITION_MAX_NB;
 static void launch_partition(const int32_t* expert_of, int32_t* block_cnt1, int32_t* block_off1,
                              int32_t* counts, int32_t* perm, int64_t M, int nb, int nr,
                              cudaStream_t s) {
   // each folded-scan CTA reads all nb block counts (nb² work): only for
   // moderate block counts; large M keeps the single-CTA scan kernel
-  if (g_fused_partition && nb <= 1024) {
+  if (g_fused_partition && nb <= kFusedPartitionMaxNb) {
     partition_scan_kernel<<<dim3(nb, nr), kRouteTok, 0, s>>>(expert_of, block_cnt1, M, counts, perm);
   } else {
     route_scan_kernel<<<nr, 1024, 0, s>>>(block_cnt1, nb, M, block_off1, counts);
@@ -790,7 +796,7 @@ extern "C" int sa_ln_route(const float* x, const float* gain, const float* bias,
 #undef SA_LNRW
   }
   launch_partition(expert_of, block_cnt1, block_off1, counts, perm, M, nb, nr, s);
-  count_launch(g_fused_partition && nb <= 1024 ? 2 : 3);
+  count_launch(g_fused_partition && nb <= kFusedPartitionMaxNb ? 2 : 3);
   SA_LAUNCH_CHECK("sa_ln_route");
   return SA_OK;
 }
@@ -853,7 +859,7 @@ extern "C" int sa_moe_route(const float* x, const float* wg, int64_t M, int64_t 
                                        block_cnt1);
   }
   launch_partition(expert_of, block_cnt1, block_off1, counts, perm, M, nb, 1, s);
-  count_launch(g_fused_partition && nb <= 1024 ? 2 : 3);
+  count_launch(g_fused_partition && nb <= kFusedPartitionMaxNb ? 2 : 3);
   SA_LAUNCH_CHECK("sa_moe_route");
   return SA_OK;
 }
@@ -874,7 +880,7 @@ extern "C" int sa_moe_dispatch(const float* logits, int64_t M, float tie_thresh,
   int32_t* block_off1 = block_cnt1 + nb;
   dispatch_kernel<<<nb, kRouteTok, 0, s>>>(logits, M, tie_thresh, expert_of, gate, block_cnt1);
   launch_partition(expert_of, block_cnt1, block_off1, counts, perm, M, nb, 1, s);
-  count_launch(g_fused_partition && nb <= 1024 ? 2 : 3);
+  count_launch(g_fused_partition && nb <= kFusedPartitionMaxNb ? 2 : 3);
   SA_LAUNCH_CHECK("sa_moe_dispatch");
   return SA_OK;
 }
@@ -912,7 +918,7 @@ extern "C" int sa_moe_partition(const int32_t* expert_of, int64_t M, int32_t* co
   int32_t* block_off1 = block_cnt1 + nb;
   count_kernel<<<nb, kRouteTok, 0, s>>>(expert_of, M, block_cnt1);
   launch_partition(expert_of, block_cnt1, block_off1, counts, perm, M, nb, 1, s);
-  count_launch(g_fused_partition && nb <= 1024 ? 2 : 3);
+  count_launch(g_fused_partition && nb <= kFusedPartitionMaxNb ? 2 : 3);
   SA_LAUNCH_CHECK("sa_moe_partition");
   return SA_OK;
 }
