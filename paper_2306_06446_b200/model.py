@@ -363,22 +363,25 @@ class Mlp:
         self.fc2.post_step()
 
 
-def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None, post_ln=None):
+def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None):
     """K5 for the two expert shapes the reference builds (ref model.py:499-502,
     514-521): (Linear, ShiftLinearLayer) and (Mlp(Linear, Linear),
-    Mlp(Shift, Shift)). Returns None for any other expert set. `post_ln` (a
-    LayerNorm) is applied to the output in the same kernel when the fused MLP
-    supports it (d = 32); the caller checks `fused_expert_forward.applied`."""
-    fused_expert_forward.applied = False
+    Mlp(Shift, Shift)). Returns None for any other expert set."""
+    return _fused_expert_forward(x, experts, plan, residual)[0]
+
+
+def _fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None, post_ln=None):
+    """(y, post_ln applied): `post_ln` (a LayerNorm) is applied to the output
+    in the same kernel when the fused MLP supports it (d = 32 / 64)."""
     if len(experts) != 2:
-        return None
+        return None, False
     e0, e1 = experts
     M = x.shape[0]
     res = residual.reshape(M, -1) if residual is not None else None
     if isinstance(e0, Linear) and isinstance(e1, ShiftLinearLayer):
         K, N = e0.in_dim, e0.out_dim
         if (e1.in_dim, e1.out_dim) != (K, N):
-            return None
+            return None, False
         y = torch.empty((M, N), dtype=torch.float32, device=x.device)
         if tc_enabled():
             pd, bn, _ = e0.tc_pack()
@@ -387,17 +390,17 @@ def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None, post
             _lib.call("sa_tc_moe_linear", _lib.ptr(x), _lib.ptr(plan.perm_dev),
                       _lib.ptr(plan.counts_dev), _lib.ptr(plan.gate_dev), _lib.ptr(pd), _lib.ptr(ps),
                       bn, _lib.ptr(y), _lib.ptr(res), M, K, N, _stream())
-            return y
+            return y, False
         _lib.call("sa_moe_linear", _lib.ptr(x), _lib.ptr(plan.perm_dev), _lib.ptr(plan.counts_dev),
                   _lib.ptr(plan.gate_dev), _lib.ptr(e0.w.value), _lib.ptr(e1.quant.packed),
                   e1.quant.p_min, _lib.ptr(y), _lib.ptr(res), M, K, N, _stream())
-        return y
+        return y, False
     if (isinstance(e0, Mlp) and isinstance(e1, Mlp) and isinstance(e0.fc1, Linear)
             and isinstance(e0.fc2, Linear) and isinstance(e1.fc1, ShiftLinearLayer)
             and isinstance(e1.fc2, ShiftLinearLayer)):
         d, hidden = e0.fc1.in_dim, e0.fc1.out_dim
         if e1.fc1.quant.p_min != e1.fc2.quant.p_min:
-            return None
+            return None, False
         y = torch.empty((M, d), dtype=torch.float32, device=x.device)
         if fused_mlp_ok(d, hidden):
             p1d, _, _ = e0.fc1.tc_pack(fused_mlp_w1_bn(d))
@@ -410,13 +413,12 @@ def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None, post
                           _lib.ptr(p2d), _lib.ptr(p1s), _lib.ptr(p2s), _lib.ptr(y), _lib.ptr(res),
                           M, d, hidden, _lib.ptr(post_ln.gain.value), _lib.ptr(post_ln.bias.value),
                           1e-5, _stream())
-                fused_expert_forward.applied = True
-                return y
+                return y, True
             _lib.call("sa_tc_moe_mlp_fused", _lib.ptr(x), _lib.ptr(plan.perm_dev),
                       _lib.ptr(plan.counts_dev), _lib.ptr(plan.gate_dev), _lib.ptr(p1d),
                       _lib.ptr(p2d), _lib.ptr(p1s), _lib.ptr(p2s), _lib.ptr(y), _lib.ptr(res),
                       M, d, hidden, _stream())
-            return y
+            return y, False
         if tc_enabled():
             p1d, bn1, _ = e0.fc1.tc_pack()
             p2d, bn2, _ = e0.fc2.tc_pack()
@@ -427,15 +429,15 @@ def fused_expert_forward(x, experts, plan: MOE.DispatchPlan, residual=None, post
                       _lib.ptr(plan.counts_dev), _lib.ptr(plan.gate_dev), _lib.ptr(p1d),
                       _lib.ptr(p2d), _lib.ptr(p1s), _lib.ptr(p2s), bn1, bn2, _lib.ptr(y),
                       _lib.ptr(res), M, d, hidden, _lib.ptr(ws), ws.numel(), _stream())
-            return y
+            return y, False
         ws = _lib.Workspace.get(_lib.load().sa_moe_mlp_workspace(M, hidden), slot=3)
         _lib.call("sa_moe_mlp", _lib.ptr(x), _lib.ptr(plan.perm_dev), _lib.ptr(plan.counts_dev),
                   _lib.ptr(plan.gate_dev), _lib.ptr(e0.fc1.w.value), _lib.ptr(e0.fc2.w.value),
                   _lib.ptr(e1.fc1.quant.packed), _lib.ptr(e1.fc2.quant.packed),
                   e1.fc1.quant.p_min, _lib.ptr(y), _lib.ptr(res), M, d, hidden, _lib.ptr(ws),
                   ws.numel(), _stream())
-        return y
-    return None
+        return y, False
+    return None, False
 
 
 class MoeModule:
@@ -487,8 +489,7 @@ class MoeModule:
         if plan is None:
             plan, _ = MOE.route_plan(x2, self.wg.value)
         self.last_plan = plan
-        y = fused_expert_forward(x2, self.experts, plan, residual, post_ln)
-        self.post_ln_applied = y is not None and fused_expert_forward.applied
+        y, self.post_ln_applied = _fused_expert_forward(x2, self.experts, plan, residual, post_ln)
         if y is None:
             y = MOE.moe_forward(x2, self.experts, plan)
             if residual is not None:
