@@ -15,6 +15,9 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2306_06446_b200 import _lib, attention as A, quantize as Q  # noqa: E402
 
+if os.environ.get("SA_LIB"):   # A/B variant library (scripts/build_variant.py)
+    _lib.LIB_PATH = os.environ["SA_LIB"]
+
 SHAPES = [  # (label, B, n, d, heads)
     ("b0-s1", 256, 3136, 32, 1), ("b0-s2", 256, 784, 64, 2), ("b0-s3", 256, 196, 160, 5),
     ("t-s1", 256, 3136, 64, 1), ("t-s2", 256, 784, 128, 2), ("t-s3", 256, 196, 320, 5),
