@@ -40,6 +40,9 @@ namespace baf {
 
 constexpr int DK = 32;
 constexpr int kThreads = 256;
+#ifndef K2A_BAND_TOKENS
+#define K2A_BAND_TOKENS 400   // ~tokens per cluster CTA (sets the cluster size)
+#endif
 constexpr int kStreams = 16;        // pass-1 token streams (16 threads each)
 constexpr int kMaxCluster = 8;
 // pass-2 tokens per row segment (a multiple of 3: the window ring), chosen per
@@ -1135,7 +1138,7 @@ int binattn_fused_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
   // one CTA per (band, image, head): bands of ~400 tokens amortise the table
   // work; a head slice of a wider model is a strided view (row stride d)
   // (16-CTA non-portable clusters measured 1.8x slower: GPC packing)
-  int cl = int((n + 399) / 400);
+  int cl = int((n + K2A_BAND_TOKENS - 1) / K2A_BAND_TOKENS);
   cl = cl < 1 ? 1 : (cl > kMaxCluster ? kMaxCluster : cl);
   cl = cl > rows_total ? rows_total : cl;
   const int br = (rows_total + cl - 1) / cl;
@@ -1215,7 +1218,7 @@ int binattn_split_launch(const uint32_t* cq, const uint32_t* ck, const float* gq
   int side = 0;
   while (int64_t(side) * side < n) ++side;
   const int rows_total = int((n + side - 1) / side);
-  int cl = int((n + 399) / 400);
+  int cl = int((n + K2A_BAND_TOKENS - 1) / K2A_BAND_TOKENS);
   cl = cl < 1 ? 1 : (cl > kMaxCluster ? kMaxCluster : cl);
   cl = cl > rows_total ? rows_total : cl;
   const int br = (rows_total + cl - 1) / cl;
