@@ -43,6 +43,9 @@ namespace tcm {
 using namespace tc;
 
 constexpr int HC = 64;                 // hidden chunk (fc1 N, fc2 K)
+#ifndef MLP_NF
+#define MLP_NF 0                       // GELU pairs (of 8) whose reciprocal runs on the FMA pipe
+#endif
 constexpr int kGelu = 16;              // GELU warps 0-15 (column group x lane quad)
 // GELU layout: true = two groups of 8 warps on alternate chunks, 32 columns per
 // warp; false = all 16 warps on every chunk, 16 columns per warp
@@ -1025,7 +1028,7 @@ static void mlp_launch_nf(const tcm::MlpParams& p, int grid, cudaStream_t s) {
     case 2: mlp_launch_one<D, RES, 2>(p, grid, s); break;
     case 4: mlp_launch_one<D, RES, 4>(p, grid, s); break;
 #endif
-    default: mlp_launch_one<D, RES, 0>(p, grid, s); break;
+    default: mlp_launch_one<D, RES, MLP_NF>(p, grid, s); break;
   }
 }
 
