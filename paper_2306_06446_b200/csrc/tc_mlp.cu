@@ -60,9 +60,14 @@ struct Wide {
   static constexpr bool W = D > 64;
   static constexpr int HC = W ? 32 : 64;
 };
+#ifndef MLP_PG32
+#define MLP_PG32 1   // d = 32: producer groups on alternate tiles (A/B knob)
+#endif
 template <int D>
 struct Roles {
-  static constexpr int NPW = Wide<D>::W ? 4 : 4 * (D / 32);   // producer warps
+  static constexpr int PGN = D == 32 ? MLP_PG32 : 1;                // producer groups
+  static constexpr int PPG = Wide<D>::W ? 4 : 4 * (D / 32);         // warps per group
+  static constexpr int NPW = PGN * PPG;                             // producer warps
   static constexpr int kMma1 = kProd + NPW, kMma2 = kMma1 + 1, kWld = kMma1 + 2;
   static constexpr int kThreads = (kWld + 1) * 32;
 };
@@ -131,7 +136,7 @@ struct Layout {
   static constexpr int XP = LNF ? D + 4 : kXPitch;            // transpose pitch (LNF: whole rows)
   // producer transpose slots (LNF: one whole-row buffer per TMEM lane quarter,
   // shared by the quarter's producer warps)
-  static constexpr uint32_t XB = (LNF ? 4 : Roles<D>::NPW) * 32 * XP * 4;
+  static constexpr uint32_t XB = (LNF ? 4 * Roles<D>::PGN : Roles<D>::NPW) * 32 * XP * 4;
   static constexpr uint32_t OFF_BAR = OFF_XB + XB;
   // barriers: a1 full/empty[NA], w1 full/empty[NW], w2 full/empty[NW],
   //           h_full/h_empty/buf_free[NB], o_full/o_empty[NO], wres
@@ -322,7 +327,7 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
   if (warp == kMma1) tmem_alloc<L::TCOLS>(tmem_slot);
   if (tid == 0) {
     for (int i = 0; i < L::NA; ++i) {
-      mbar_init(&a1_full[i], NPW);
+      mbar_init(&a1_full[i], Roles<D>::PPG);
       mbar_init(&a1_empty[i], 1);
     }
     for (int i = 0; i < L::NW; ++i) {
@@ -338,7 +343,7 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
     }
     for (int i = 0; i < L::NO; ++i) {
       mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], NPW);
+      mbar_init(&o_empty[i], Roles<D>::PPG);
     }
     mbar_init(wres, 1);
     fence_barrier_init();
@@ -359,11 +364,17 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
     // warp (quad, kc0): rows quad·32 + lane (= TMEM lanes), K stages / output
     // channel blocks kc0, kc0 + KST, ... (narrow: one stage per warp; wide: one
     // warp per lane quarter walks every stage)
-    constexpr int KST = NPW / 4;
-    const int quad = (warp - kProd) & 3, kc0 = (warp - kProd) >> 2;
+    // (PGN > 1: groups of PPG warps take the CTA's tiles alternately; each
+    // group owns one A1 buffer and one acc2 buffer, NA = NO = PGN)
+    constexpr int PGN = Roles<D>::PGN, PPG = Roles<D>::PPG;
+    constexpr int KST = PPG / 4;
+    static_assert(PGN == 1 || (PGN == L::NA && PGN == L::NO), "a group per A1 / acc2 buffer");
+    const int pgi = (warp - kProd) / PPG, pwl = (warp - kProd) % PPG;
+    const int quad = pwl & 3, kc0 = pwl >> 2;
     const int ptid = quad * 32 + lane;
     const uint32_t lane_base = uint32_t(quad * 32) << 16;
-    float* xb = reinterpret_cast<float*>(smem + L::OFF_XB) + (LNF ? quad : warp - kProd) * 32 * L::XP;
+    float* xb = reinterpret_cast<float*>(smem + L::OFF_XB) +
+                (LNF ? pgi * 4 + quad : warp - kProd) * 32 * L::XP;
     // the warp's 16-column output blocks: 2 per owned K stage
     constexpr int NBLK = 2 * (L::KC1 / KST);
     auto blk_col = [&](int bi) { return 32 * (kc0 + (bi >> 1) * KST) + 16 * (bi & 1); };
@@ -543,13 +554,15 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
     // the NA previous tiles (their acc2 is drained NA tiles later)
     int pe1 = 0, pe2 = 0;
     int64_t pa1 = 0, pb1 = 0, pa2 = 0, pb2 = 0;
-    int64_t j = 0;
-    int ab = 0;
+    int64_t j = 0;   // this group's tile count
+    int ab = PGN > 1 ? pgi : 0;   // PGN > 1: the group's own A1 buffer
     uint32_t pab = 0u;
+    int64_t jall = 0;   // the CTA's valid-tile index (all groups)
     for (int64_t m = blockIdx.x; m < ntile; m += gridDim.x) {
       int e;
       int64_t r0, r1;
       if (!mlp_tile(p, c0, m, e, r0, r1)) continue;
+      if (PGN > 1 && (jall++ % PGN) != pgi) continue;
       const int64_t row = r0 + ptid;
       const bool live = row < r1 && !(kDbg && (p.dbg & 2));
       const float* xrow = live ? p.x + (p.perm ? int64_t(__ldg(p.perm + row)) : row) * D : nullptr;
@@ -603,6 +616,14 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&a1_full[ab]);
+      if (PGN > 1) {
+        // this group's previous tile (global index (j - 1)·PGN + group)
+        pab ^= 1u;
+        if (j >= 1) drain((j - 1) * PGN + pgi, pe1, pa1, pb1);
+        pe1 = e; pa1 = r0; pb1 = r1;
+        ++j;
+        continue;
+      }
       if (++ab == L::NA) { ab = 0; pab ^= 1u; }
       // then drain tile j - NA (its fc2 ends while fc1 works on the tiles between)
       if (L::NA == 1 && j >= 1) drain(j - 1, pe1, pa1, pb1);
@@ -611,8 +632,12 @@ __global__ void __launch_bounds__(Roles<D>::kThreads, 1) mlp_kernel(MlpParams p)
       pe1 = e; pa1 = r0; pb1 = r1;
       ++j;
     }
-    if (L::NA == 2 && j >= 2) drain(j - 2, pe2, pa2, pb2);
-    if (j >= 1) drain(j - 1, pe1, pa1, pb1);
+    if (PGN > 1) {
+      if (j >= 1) drain((j - 1) * PGN + pgi, pe1, pa1, pb1);
+    } else {
+      if (L::NA == 2 && j >= 2) drain(j - 2, pe2, pa2, pb2);
+      if (j >= 1) drain(j - 1, pe1, pa1, pb1);
+    }
   } else if (warp == kWld) {
     // ---------------- weights ----------------
     if (lane == 0) {
