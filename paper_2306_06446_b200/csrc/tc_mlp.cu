@@ -49,7 +49,10 @@ constexpr int HC = 64;                 // hidden chunk (fc1 N, fc2 K)
 constexpr int kGelu = 16;              // GELU warps 0-15 (column group x lane quad)
 // GELU layout: true = two groups of 8 warps on alternate chunks, 32 columns per
 // warp; false = all 16 warps on every chunk, 16 columns per warp
-constexpr bool kGeluAlt = false;
+#ifndef MLP_GELU_ALT
+#define MLP_GELU_ALT 0
+#endif
+constexpr bool kGeluAlt = MLP_GELU_ALT != 0;
 constexpr int kGeluPerChunk = kGeluAlt ? 8 : 16;
 constexpr int kProd = 16;              // producers: warps 16 .. 16 + 4·(d/32) - 1
 // wide form (d = 128 / 160): hidden chunks of 32, one A1 buffer, a single
