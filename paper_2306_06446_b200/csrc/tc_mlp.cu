@@ -63,6 +63,9 @@ struct Wide {
   static constexpr bool W = D > 64;
   static constexpr int HC = W ? 32 : 64;
 };
+#ifndef MLP_NA64
+#define MLP_NA64 1   // d = 64: A1 buffers (2 leaves two chunk buffers) (A/B knob)
+#endif
 #ifndef MLP_PG32
 #define MLP_PG32 1   // d = 32: producer groups on alternate tiles (A/B knob)
 #endif
@@ -113,8 +116,9 @@ struct Layout {
   static constexpr bool W = Wide<D>::W;
   static constexpr int HC = Wide<D>::HC;                      // hidden chunk (fc1 N, fc2 K)
   static constexpr int KC1 = D / 32;                          // fc1 K stages
-  static constexpr int NA = D == 32 ? 2 : 1;                  // A1 buffers (TMEM)
-  static constexpr int NB = W ? 2 : 3;                        // acc1 / A2 buffers (TMEM)
+  // A1 buffers (TMEM); d = 64 can trade a chunk buffer for a second A1
+  static constexpr int NA = D == 32 ? 2 : (D == 64 && MLP_NA64 == 2 ? 2 : 1);
+  static constexpr int NB = W ? 2 : (D == 64 && NA == 2 ? 2 : 3);   // acc1 / A2 buffers (TMEM)
   // wide: the A1 lo plane lives in shared memory (ss-form MMAs), hi / mid in
   // TMEM; d <= 160 also concatenates the dense fc1 B planes along N (3 MMAs
   // per K step into three 32-column partial sums, added by the GELU warps)
